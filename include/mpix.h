@@ -1,0 +1,275 @@
+/*
+ * mpix.h — C ABI of the B200-native MPIX-stream GPU-enqueue path
+ * (arXiv 2208.13707, "MPIX Stream: An Explicit Solution to Hybrid MPI+X
+ * Programming").
+ *
+ * This is the drop-in boundary. The reference (`/root/reference/proj`,
+ * "streamix") exposes the same operations as C++ methods on
+ * `streamix::Proc` (proj/include/streamix/world.hpp:35-92) returning
+ * `Result<T>` (proj/include/streamix/result.hpp:39-81). The paper gives the C
+ * signatures this header follows.
+ * Each declaration below cites the reference entry point it replaces.
+ *
+ * Plain C types only: no torch, no C++ in the signatures. Buffers are device
+ * pointers (any allocation visible to the rank's GPU through UVA; peer GPUs
+ * reach them over NVLink after MPIX_World_init enabled peer access).
+ *
+ * Rank model: one process hosts a world of N ranks, rank r bound to one GPU
+ * (several ranks may share a GPU). This mirrors the reference's
+ * `World(n)` + `run_ranks` (world.hpp:129-159): collective calls
+ * (communicator creation/free, barrier) are made once per member, normally
+ * from one host thread per rank. Every MPI_Comm handle is one rank's view of
+ * a communicator, so point-to-point and enqueue calls need no thread-bound
+ * rank.
+ */
+#ifndef MPIX_H
+#define MPIX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------------ */
+/* Handles                                                                   */
+/* ------------------------------------------------------------------------ */
+
+typedef struct mpix_info_s *MPI_Info;     /* streamix::Info   info.hpp:16-31   */
+typedef struct mpix_stream_s *MPIX_Stream; /* streamix::Stream stream.hpp:15-24 */
+typedef struct mpix_comm_s *MPI_Comm;     /* streamix::CommH  comm.hpp:38-41   */
+/* streamix::Req (request.hpp:52). Opaque 64-bit ticket; 0 = MPI_REQUEST_NULL. */
+typedef uint64_t MPI_Request;
+typedef int MPI_Datatype;
+typedef int MPI_Op;
+
+/* streamix::Status (request.hpp:13-19). Enqueue calls never surface a status
+ * in the reference (proc_enqueue.cpp:61,130-137); see MPIX_Wait_enqueue. */
+typedef struct {
+  int MPI_SOURCE;
+  int MPI_TAG;
+  int MPI_ERROR;
+  int source_index;
+  uint64_t count_bytes; /* UINT64_MAX when not known on the host */
+  int truncated;
+} MPI_Status;
+
+#define MPI_INFO_NULL ((MPI_Info)0)
+#define MPIX_STREAM_NULL ((MPIX_Stream)0) /* types.hpp:19 STREAM_NULL */
+#define MPI_COMM_NULL ((MPI_Comm)0)
+#define MPI_REQUEST_NULL ((MPI_Request)0)
+#define MPI_STATUS_IGNORE ((MPI_Status *)0)
+#define MPI_STATUSES_IGNORE ((MPI_Status *)0)
+#define MPI_IN_PLACE ((void *)1)
+
+#define MPI_ANY_SOURCE (-1) /* types.hpp:10 */
+#define MPI_ANY_TAG (-1)    /* types.hpp:11 */
+#define MPIX_ANY_INDEX (-1) /* types.hpp:12 */
+
+/* Datatypes. BYTE/INT/DOUBLE are the reference's Elem::{byte,i32,f64}
+ * (types.hpp:27-31); FLOAT and BFLOAT16 are added for Allreduce. */
+#define MPI_BYTE 1
+#define MPI_INT 2
+#define MPI_DOUBLE 3
+#define MPI_FLOAT 4
+#define MPIX_BFLOAT16 5
+
+/* Reduction ops for MPIX_Allreduce_enqueue (no reference: SPEC.md:19,443). */
+#define MPI_SUM 1
+#define MPI_MAX 2
+#define MPI_MIN 3
+
+/* ------------------------------------------------------------------------ */
+/* Error codes. 0..22 mirror streamix::Err in declaration order             */
+/* (result.hpp:9-33); names from MPIX_Error_string match to_string()         */
+/* (result.cpp:5-32). 100+ are conditions the simulation cannot have.        */
+/* ------------------------------------------------------------------------ */
+#define MPI_SUCCESS 0
+#define MPIX_ERR_POOL_EXHAUSTED 1
+#define MPIX_ERR_NO_EXPLICIT_POOL 2
+#define MPIX_ERR_PENDING_OPS 3
+#define MPIX_ERR_IN_USE 4
+#define MPIX_ERR_BAD_HINT 5
+#define MPIX_ERR_INVALID_STREAM 6
+#define MPIX_ERR_INVALID_COMM 7
+#define MPIX_ERR_INVALID_RANK 8
+#define MPIX_ERR_INVALID_COUNT 9
+#define MPIX_ERR_INVALID_TAG 10
+#define MPIX_ERR_INVALID_REQUEST 11
+#define MPIX_ERR_INVALID_INDEX 12
+#define MPIX_ERR_MULTIPLEX_COMM 13
+#define MPIX_ERR_NOT_MULTIPLEX 14
+#define MPIX_ERR_WILDCARD_DST 15
+#define MPIX_ERR_EMPTY_LIST 16
+#define MPIX_ERR_NOT_ENQUEUE_COMM 17
+#define MPIX_ERR_STREAM_MISMATCH 18
+#define MPIX_ERR_QUEUE_BUSY 19
+#define MPIX_ERR_CONFIG_INVALID 20
+#define MPIX_ERR_NOT_FOUND 21
+#define MPIX_ERR_BAD_ENCODING 22
+#define MPIX_ERR_CUDA 100          /* a CUDA runtime call failed            */
+#define MPIX_ERR_NOT_INITIALIZED 101
+#define MPIX_ERR_UNSUPPORTED 102   /* documented v1 divergence  */
+#define MPIX_ERR_INVALID_ARG 103
+#define MPIX_ERR_TYPE 104          /* unknown datatype                      */
+#define MPIX_ERR_OP 105            /* unknown / unsupported reduction op    */
+#define MPIX_ERR_NO_MEM 106
+
+/* Name of an error code, e.g. "NOT_ENQUEUE_COMM" (result.cpp:5-32). */
+const char *MPIX_Error_string(int code);
+
+/* ------------------------------------------------------------------------ */
+/* World bootstrap — replaces streamix::World(n) / run_ranks                 */
+/* (world.hpp:129-159, world.cpp:53-84). Not part of the paper's API: in    */
+/* MPI this is MPI_Init; here one process owns all ranks.                    */
+/* ------------------------------------------------------------------------ */
+
+/* Create the world: rank r runs on GPU devices[r] (devices may be NULL:
+ * rank r -> device r % device_count). Enables peer access between every
+ * pair of distinct devices. */
+int MPIX_World_init(int nranks, const int *devices);
+/* Destroy the world and every communicator. Caller synchronises its streams
+ * first. */
+int MPIX_World_finalize(void);
+int MPIX_World_size(int *nranks);
+/* Rank r's view of the bootstrap world communicator (ctx 0) —
+ * Proc::world_comm() (world.hpp:40). */
+int MPIX_World_comm(int rank, MPI_Comm *comm);
+/* Bind the calling host thread to a rank (optional; lets single-rank-per-
+ * thread code call MPIX_Comm_world_self). */
+int MPIX_Rank_bind(int rank);
+int MPIX_Comm_world_self(MPI_Comm *comm);
+
+int MPI_Comm_rank(MPI_Comm comm, int *rank);
+int MPI_Comm_size(MPI_Comm comm, int *size);
+/* Collective. Proc::barrier (proc_comm.cpp:31-46). Host-side barrier. */
+int MPI_Barrier(MPI_Comm comm);
+/* Collective. Proc::comm_free (proc_comm.cpp:178-194). Sets *comm to
+ * MPI_COMM_NULL. The world communicator cannot be freed (INVALID_COMM). */
+int MPI_Comm_free(MPI_Comm *comm);
+
+/* ------------------------------------------------------------------------ */
+/* Info hints — streamix::Info (info.hpp:16-31, info.cpp:17-59)             */
+/* ------------------------------------------------------------------------ */
+int MPI_Info_create(MPI_Info *info);
+int MPI_Info_free(MPI_Info *info);
+int MPI_Info_set(MPI_Info info, const char *key, const char *value);
+/* Copies the value (NUL-terminated) into value[0..valuelen); *flag = 0 when
+ * the key is absent. */
+int MPI_Info_get(MPI_Info info, const char *key, int valuelen, char *value,
+                 int *flag);
+/* PAPER.md:333. Lowercase hex, high nibble first (info.cpp:37-46). */
+int MPIX_Info_set_hex(MPI_Info info, const char *key, const void *value,
+                      int vallen);
+/* Info::get_hex (info.cpp:31-35, 48-59): NOT_FOUND / BAD_ENCODING.
+ * *outlen receives the decoded length; at most maxlen bytes are written. */
+int MPIX_Info_get_hex(MPI_Info info, const char *key, void *value, int maxlen,
+                      int *outlen);
+
+/* ------------------------------------------------------------------------ */
+/* Streams — Proc::stream_create / stream_free (proc_stream.cpp:7-60)       */
+/* ------------------------------------------------------------------------ */
+
+/* PAPER.md:310. info == MPI_INFO_NULL (or no "type" key): a serial-context
+ * (host thread) stream. info{type="cudaStream_t", value=hex(cudaStream_t)}:
+ * a GPU stream; the value must decode to exactly sizeof(cudaStream_t) bytes
+ * and name a live CUDA stream, else BAD_HINT (proc_stream.cpp:12-17). The
+ * optional key "endpoint_policy" accepts "shared"/"exclusive", anything else
+ * is BAD_HINT (proc_stream.cpp:27-33). */
+int MPIX_Stream_create(MPI_Info info, MPIX_Stream *stream);
+/* IN_USE while a communicator references the stream; INVALID_STREAM for
+ * MPIX_STREAM_NULL. Sets *stream to MPIX_STREAM_NULL on success. */
+int MPIX_Stream_free(MPIX_Stream *stream);
+/* The cudaStream_t a GPU stream wraps (NULL for serial-context streams). */
+int MPIX_Stream_get_cuda(MPIX_Stream stream, void **cuda_stream);
+
+/* ------------------------------------------------------------------------ */
+/* Communicators — Proc::stream_comm_create(_multiple)                      */
+/* (proc_comm.cpp:48-176). Collective over the parent's members.             */
+/* ------------------------------------------------------------------------ */
+
+/* PAPER.md:366. stream may be MPIX_STREAM_NULL (a member without a local
+ * stream; enqueue on that member gives NOT_ENQUEUE_COMM, A7). For a GPU
+ * stream, the CUDA stream's device must be the rank's device
+ * (INVALID_STREAM otherwise). */
+int MPIX_Stream_comm_create(MPI_Comm parent, MPIX_Stream stream,
+                            MPI_Comm *newcomm);
+/* PAPER.md:391 (named _multiple at PAPER.md:477). count == 0 gives
+ * EMPTY_LIST (proc_comm.cpp:55). Enqueue on a multiplex communicator gives
+ * NOT_ENQUEUE_COMM (proc_enqueue.cpp:24). */
+int MPIX_Stream_comm_create_multiplex(MPI_Comm parent, int count,
+                                      MPIX_Stream streams[], MPI_Comm *newcomm);
+int MPIX_Stream_comm_create_multiple(MPI_Comm parent, int count,
+                                     MPIX_Stream streams[], MPI_Comm *newcomm);
+
+/* ------------------------------------------------------------------------ */
+/* Enqueue operations — Proc::*_enqueue (proc_enqueue.cpp:30-141).          */
+/* Each call validates (NOT_ENQUEUE_COMM, then rank -> tag -> count,        */
+/* proc_enqueue.cpp:8-28), launches one sm_100a kernel into the comm's CUDA  */
+/* stream and returns; it never blocks on the peer.            */
+/* Matching is MPI non-overtaking per (comm, source, dest, tag).             */
+/* v1 divergence: MPI_ANY_SOURCE / MPI_ANY_TAG receives give UNSUPPORTED.    */
+/* ------------------------------------------------------------------------ */
+
+/* PAPER.md:427. Blocking in the stream: later work in the stream sees the
+ * send buffer reusable. Completes without the receiver (eager, like
+ * proc_p2p.cpp:60-62): small messages go into the receiver's eager ring,
+ * large ones are pushed zero-copy when the receive is already posted and
+ * staged in local HBM otherwise. */
+int MPIX_Send_enqueue(const void *buf, int count, MPI_Datatype datatype,
+                      int dest, int tag, MPI_Comm comm);
+/* PAPER.md:428. Blocking in the stream until the message has landed in buf.
+ * Delivers min(len, capacity) bytes (endpoint.cpp:17-24). */
+int MPIX_Recv_enqueue(void *buf, int count, MPI_Datatype datatype, int source,
+                      int tag, MPI_Comm comm, MPI_Status *status);
+/* PAPER.md:429-430. Non-blocking in the stream; buffer owned by the
+ * runtime until a Wait(all)_enqueue on the same stream. */
+int MPIX_Isend_enqueue(const void *buf, int count, MPI_Datatype datatype,
+                       int dest, int tag, MPI_Comm comm, MPI_Request *request);
+int MPIX_Irecv_enqueue(void *buf, int count, MPI_Datatype datatype, int source,
+                       int tag, MPI_Comm comm, MPI_Request *request);
+/* PAPER.md:431-432. Waitall: n == 0 is success with nothing enqueued; a
+ * MPI_REQUEST_NULL entry is INVALID_REQUEST; requests from different
+ * streams are STREAM_MISMATCH (proc_enqueue.cpp:120-126). The request stays
+ * valid afterwards (waiting twice is ok/ok, Appendix A9); release it with
+ * MPIX_Request_free. Statuses: only source/tag are filled (count_bytes =
+ * UINT64_MAX), the reference never surfaces enqueue statuses. */
+int MPIX_Wait_enqueue(MPI_Request *request, MPI_Status *status);
+int MPIX_Waitall_enqueue(int count, MPI_Request requests[],
+                         MPI_Status statuses[]);
+int MPIX_Request_free(MPI_Request *request);
+
+/* New (absent from the reference): in-stream sum/max/min
+ * allreduce over peer memory. sendbuf may be MPI_IN_PLACE. Every element is
+ * reduced in rank order 0..P-1 with an fp32 accumulator for bf16 (one final
+ * round-to-nearest-even), fp32/fp64 adds in that order, wrapping int32. */
+int MPIX_Allreduce_enqueue(const void *sendbuf, void *recvbuf, int count,
+                           MPI_Datatype datatype, MPI_Op op, MPI_Comm comm);
+
+/* ------------------------------------------------------------------------ */
+/* Introspection (tests / bench)                                             */
+/* ------------------------------------------------------------------------ */
+
+/* Number of runtime kernels launched so far (all ranks). */
+uint64_t MPIX_Launch_count(void);
+/* Effective configuration: eager bytes, ring slots, max CTAs per op,
+ * one-shot/two-shot crossover bytes. */
+int MPIX_Config_get(uint64_t *eager_bytes, int *ring_slots, int *max_ctas,
+                    uint64_t *oneshot_max_bytes);
+/* Communicator context id (equal on every member, recycled lowest-first,
+ * world.cpp:43-51). */
+int MPIX_Comm_get_ctx(MPI_Comm comm, uint32_t *ctx);
+/* 1 when enqueue calls are accepted on comm (single-stream comm with a GPU
+ * stream on this member), else 0. */
+int MPIX_Comm_is_enqueue(MPI_Comm comm, int *flag);
+/* Datatype width in bytes, or 0 if unknown. */
+int MPIX_Type_size(MPI_Datatype datatype);
+/* Library build string (arch, version). */
+const char *MPIX_Version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPIX_H */

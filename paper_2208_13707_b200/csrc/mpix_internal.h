@@ -1,0 +1,186 @@
+// mpix_internal.h — structures shared by the host runtime (mpix_runtime.cpp)
+// and the sm_100a kernels (mpix_kernels.cu).
+//
+// The reference moves a message through a loopback byte channel and a host
+// matching engine (proj/src/wire.cpp:53-73, proj/src/endpoint.cpp:15-69).
+// Here every rank owns, per communicator, one "region" of device memory on
+// its GPU. Peers reach it over NVLink (or directly when they share the GPU).
+// A message s->d meets its receive through two descriptor rings:
+//
+//   SR(s->d)  in d's region, written by s   send descriptors   (d scans it)
+//   RR(s->d)  in s's region, written by d   receive descriptors (s scans it)
+//
+// Both sides scan first, then post their own descriptor, fence, and rescan
+// (store-buffering / Dekker). The arbitration word is the send descriptor's
+// state: whoever moves it POSTED->TAKEN with a system-scope CAS is the
+// "second arriver" and performs the copy inside its own in-stream kernel —
+// push (sender) or pull (receiver). No host thread and no progress engine.
+#pragma once
+
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+namespace mpix {
+
+constexpr int kThreads = 512;          // threads per CTA for every op kernel
+constexpr int kMaxCollRanks = 16;      // max communicator size for Allreduce
+constexpr int kWaitBatch = 1024;       // requests per wait kernel launch
+constexpr uint64_t kOpRecords = 16384; // op-record ring entries per rank
+
+enum : uint64_t { ST_FREE = 0, ST_POSTED = 1, ST_TAKEN = 2 };
+
+__host__ __device__ inline uint64_t st_word(uint64_t pseq, uint64_t st) {
+  return (pseq << 8) | st;
+}
+
+// One ring slot. Mirrors the fields of the reference's Envelope/RecvDesc
+// (wire.hpp:13-21, endpoint.hpp:35-40) that matching needs: the (tag, seq)
+// key replaces (context, source, tag) because the ring is per (comm, pair).
+struct alignas(64) SlotDesc {
+  uint64_t state;      // (pair_seq << 8) | ST_*
+  uint64_t key;        // ((uint32)tag << 32) | per-(pair,tag) sequence
+  uint64_t addr;       // send: payload address; recv: destination buffer
+  uint64_t bytes;      // send: payload length; recv: capacity
+  uint64_t done_addr;  // poster's completion word (0 = none)
+  uint64_t done_val;   // value to store there
+  uint64_t pad[2];
+};
+static_assert(sizeof(SlotDesc) == 64, "slot is one 64-B line");
+
+struct alignas(32) CollSlot {
+  uint64_t flag;  // allreduce epoch this peer has entered
+  uint64_t sbuf;  // its send buffer
+  uint64_t rbuf;  // its receive buffer
+  uint64_t pad;
+};
+
+// Layout of one rank's per-communicator region.
+struct RegionLayout {
+  int P;       // communicator size
+  int R;       // ring slots per ordered pair
+  uint64_t E;  // eager bytes per slot
+
+  __host__ __device__ uint64_t ring_bytes() const {
+    return (uint64_t)R * sizeof(SlotDesc);
+  }
+  // send descriptors posted by peer q (messages q -> me)
+  __host__ __device__ uint64_t sr(int q) const { return (uint64_t)q * ring_bytes(); }
+  // receive descriptors posted by peer q (messages me -> q)
+  __host__ __device__ uint64_t rr(int q) const {
+    return (uint64_t)P * ring_bytes() + (uint64_t)q * ring_bytes();
+  }
+  // free-mirror of MY send slots inside q's SR(me->q) ring
+  __host__ __device__ uint64_t sr_free(int q) const {
+    return 2ull * P * ring_bytes() + (uint64_t)q * R * 8;
+  }
+  // free-mirror of MY receive slots inside q's RR(q->me) ring
+  __host__ __device__ uint64_t rr_free(int q) const {
+    return 2ull * P * ring_bytes() + (uint64_t)P * R * 8 + (uint64_t)q * R * 8;
+  }
+  __host__ __device__ uint64_t coll_in(int q) const {
+    return 2ull * P * ring_bytes() + 2ull * P * R * 8 + (uint64_t)q * sizeof(CollSlot);
+  }
+  __host__ __device__ uint64_t coll_exit(int q) const {
+    return coll_in(P) + (uint64_t)q * 8;
+  }
+  __host__ __device__ uint64_t eager_base() const {
+    return (coll_exit(P) + 255) & ~255ull;
+  }
+  // eager payload ring of messages q -> me
+  __host__ __device__ uint64_t eager(int q) const {
+    return eager_base() + (uint64_t)q * R * E;
+  }
+  __host__ __device__ uint64_t total() const { return eager(P); }
+};
+
+// Grid-wide decision record for multi-CTA operations (CTA 0 decides, the
+// others follow). One per launched multi-CTA op, in a per-rank ring.
+struct alignas(64) OpRecord {
+  uint64_t opid;     // published last (release) by CTA 0
+  uint64_t action;   // ACT_*
+  uint64_t src;
+  uint64_t dst;
+  uint64_t bytes;
+  uint32_t counter;  // CTAs finished copying
+  uint32_t nfin;
+  uint64_t fin_addr[6];  // completion stores, performed in order by the
+  uint64_t fin_val[6];   // last CTA with st.release.sys
+  uint64_t coll[2 * kMaxCollRanks];  // allreduce: peers' sbuf / rbuf
+  uint64_t flags;
+};
+
+enum : uint64_t { ACT_NONE = 0, ACT_COPY = 1, ACT_STAGE = 2 };
+
+enum SendMode : int { MODE_ISEND = 0, MODE_EAGER = 1, MODE_STAGED = 2 };
+
+struct P2PArgs {
+  int is_recv;
+  int mode;       // SendMode (send side)
+  int blocking;   // recv: the kernel waits for its own completion
+  int R;
+  uint64_t key;
+  uint64_t pseq;       // my pair sequence -> post slot pseq % R
+  SlotDesc* post_ring; // ring I post into (peer memory)
+  uint64_t* post_mirror;  // my free-mirror for that ring (local)
+  SlotDesc* scan_ring;    // ring I scan (local)
+  uint64_t* scan_mirror;  // peer's free-mirror for the scanned ring (peer)
+  uint8_t* eager_ring;    // send: SR's eager payload ring (peer memory)
+  uint64_t E;
+  uint8_t* buf;
+  uint64_t bytes;         // send: length; recv: capacity
+  uint8_t* staging;       // MODE_STAGED
+  uint64_t* my_done;      // my request's completion word (local)
+  uint64_t my_gen;
+  uint64_t* stage_done;   // MODE_STAGED: released by the consumer of staging
+  uint64_t stage_gen;
+  OpRecord* rec;
+  uint64_t opid;
+  uint64_t* err_word;     // per-rank error word (watchdog)
+  uint64_t spin_limit_ns; // 0 = wait forever
+};
+
+struct WaitEntry {
+  uint64_t* flag;
+  uint64_t gen;
+};
+
+struct WaitArgs {
+  int n;
+  uint64_t* err_word;
+  uint64_t spin_limit_ns;
+  WaitEntry e[kWaitBatch];
+};
+
+enum ARDtype : int { AR_I32 = 0, AR_F32 = 1, AR_BF16 = 2, AR_F64 = 3 };
+enum AROp : int { AR_SUM = 0, AR_MAX = 1, AR_MIN = 2 };
+enum ARAlgo : int { AR_ONESHOT = 0, AR_TWOSHOT = 1 };
+
+struct ARArgs {
+  const uint8_t* sbuf;
+  uint8_t* rbuf;
+  uint64_t count;   // elements
+  int esize;
+  int dtype;
+  int op;
+  int algo;
+  int P;
+  int me;
+  uint64_t epoch;
+  CollSlot* peer_in[kMaxCollRanks];   // region[q].coll_in[me]
+  uint64_t* peer_exit[kMaxCollRanks]; // region[q].coll_exit[me]
+  CollSlot* my_in;                    // region[me].coll_in[0..P)
+  uint64_t* my_exit;                  // region[me].coll_exit[0..P)
+  OpRecord* rec;
+  uint64_t opid;
+  uint64_t* err_word;
+  uint64_t spin_limit_ns;
+};
+
+// Launchers implemented in mpix_kernels.cu (host side).
+cudaError_t launch_p2p(const P2PArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_wait(const WaitArgs& a, cudaStream_t s);
+cudaError_t launch_allreduce(const ARArgs& a, int grid, cudaStream_t s);
+int p2p_occupancy();
+int allreduce_occupancy();
+
+}  // namespace mpix

@@ -1,0 +1,1124 @@
+// mpix_runtime.cpp — host runtime behind include/mpix.h.
+//
+// Replaces the reference's L1-L3 host layers: World/Proc
+// (proj/src/world.cpp), stream lifecycle (proj/src/proc_stream.cpp),
+// communicator rendezvous (proj/src/proc_comm.cpp), the enqueue engine
+// (proj/src/proc_enqueue.cpp) and the simulated GPU queue
+// (proj/src/exec_queue.cpp). The queue worker thread is gone: every enqueue
+// call validates, assigns matching sequence numbers, and launches one
+// sm_100a kernel (mpix_kernels.cu) into the user's cudaStream_t.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <queue>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "mpix.h"
+#include "mpix_internal.h"
+
+namespace mpix {
+
+// ---------------------------------------------------------------------------
+// Configuration (env knobs, SURVEY.md §5 "Config / flags")
+// ---------------------------------------------------------------------------
+struct Config {
+  uint64_t eager_bytes = 4096;       // MPIX_EAGER_BYTES
+  int ring_slots = 128;              // MPIX_RING_SLOTS
+  int max_ctas = 0;                  // MPIX_MAX_CTAS (0 = auto)
+  uint64_t bytes_per_cta = 65536;    // MPIX_BYTES_PER_CTA
+  uint64_t oneshot_max = 65536;      // MPIX_ALLREDUCE_ONESHOT_MAX (bytes)
+  uint64_t spin_limit_ns = 60ull * 1000 * 1000 * 1000;  // MPIX_SPIN_TIMEOUT_MS
+
+  static Config from_env() {
+    Config c;
+    auto geti = [](const char* n, uint64_t d) -> uint64_t {
+      const char* v = std::getenv(n);
+      if (!v || !*v) return d;
+      return std::strtoull(v, nullptr, 10);
+    };
+    c.eager_bytes = geti("MPIX_EAGER_BYTES", c.eager_bytes);
+    c.eager_bytes = (c.eager_bytes + 15) & ~15ull;
+    c.ring_slots = (int)geti("MPIX_RING_SLOTS", c.ring_slots);
+    if (c.ring_slots < 2) c.ring_slots = 2;
+    c.max_ctas = (int)geti("MPIX_MAX_CTAS", 0);
+    c.bytes_per_cta = geti("MPIX_BYTES_PER_CTA", c.bytes_per_cta);
+    if (c.bytes_per_cta < 4096) c.bytes_per_cta = 4096;
+    c.oneshot_max = geti("MPIX_ALLREDUCE_ONESHOT_MAX", c.oneshot_max);
+    c.spin_limit_ns = geti("MPIX_SPIN_TIMEOUT_MS", 60000) * 1000000ull;
+    return c;
+  }
+};
+
+constexpr uint64_t kReqSlots = 1ull << 20;  // completion words per rank
+
+std::atomic<uint64_t> g_launches{0};
+
+// ---------------------------------------------------------------------------
+// Host rendezvous for collective calls (replaces ctrl_send/ctrl_recv over the
+// collective wire context, proj/src/proc_comm.cpp:17-29).
+// ---------------------------------------------------------------------------
+struct CollMsg {
+  int64_t i0 = 0, i1 = 0;
+  uint64_t u0 = 0;
+  void* p0 = nullptr;
+  std::shared_ptr<void> sp;
+};
+
+class Rendezvous {
+ public:
+  std::vector<CollMsg> exchange(int P, int rank, uint64_t seq, CollMsg m) {
+    std::unique_lock<std::mutex> lk(mu_);
+    Round& r = rounds_[seq];
+    if (r.vals.empty()) r.vals.resize(P);
+    r.vals[rank] = std::move(m);
+    if (++r.arrived == P)
+      cv_.notify_all();
+    else
+      cv_.wait(lk, [&] { return r.arrived == P; });
+    std::vector<CollMsg> out = r.vals;
+    if (++r.left == P) rounds_.erase(seq);
+    return out;
+  }
+
+ private:
+  struct Round {
+    std::vector<CollMsg> vals;
+    int arrived = 0;
+    int left = 0;
+  };
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::map<uint64_t, Round> rounds_;
+};
+
+struct RankState {
+  int rank = 0;
+  int device = 0;
+  int sms = 148;
+  int per_device = 1;  // ranks sharing this GPU
+  uint64_t* d_done = nullptr;
+  std::atomic<uint64_t> req_next{0};
+  OpRecord* d_rec = nullptr;
+  std::atomic<uint64_t> op_next{1};
+  uint64_t* h_err = nullptr;  // host-mapped error word
+  uint64_t* d_err = nullptr;
+  cudaStream_t aux = nullptr;      // setup work
+  cudaStream_t reclaim = nullptr;  // staging release
+  cudaMemPool_t pool = nullptr;
+  int p2p_cap = 1;
+  int ar_cap = 1;
+  std::mutex mu;
+  // request table: slot -> issuing stream, for STREAM_MISMATCH
+  struct ReqInfo {
+    uint64_t gen = 0;
+    cudaStream_t stream = nullptr;
+    int source = -1, tag = -1;
+  };
+  std::vector<ReqInfo> reqs;
+};
+
+struct CommShared {
+  uint32_t ctx = 0;
+  int P = 0;
+  bool multiplex = false;
+  bool is_world = false;
+  RegionLayout L{};
+  std::vector<uint8_t*> base;  // per-rank region
+  std::vector<int> counts;     // per-rank stream count
+  Rendezvous rv;
+};
+
+}  // namespace mpix
+
+// Opaque handle types of mpix.h.
+struct mpix_info_s {
+  std::map<std::string, std::string> entries;
+};
+
+struct mpix_stream_s {
+  enum Kind { serial = 0, cuda = 1 } kind = serial;
+  cudaStream_t cu = nullptr;
+  int device = -1;
+  bool exclusive = true;
+  std::atomic<int> refcount{0};
+};
+
+struct mpix_comm_s {
+  std::shared_ptr<mpix::CommShared> sh;
+  int rank = 0;
+  std::vector<mpix_stream_s*> local_streams;
+  bool enqueue_ok = false;
+  cudaStream_t cu = nullptr;
+  std::vector<uint64_t> send_pseq, recv_pseq;
+  std::unordered_map<uint64_t, uint32_t> send_tagseq, recv_tagseq;
+  uint64_t coll_epoch = 0;
+  uint64_t rv_seq = 0;
+};
+
+namespace mpix {
+
+struct World {
+  Config cfg;
+  int n = 0;
+  std::vector<std::unique_ptr<RankState>> ranks;
+  std::vector<mpix_comm_s*> world_comms;
+  std::mutex ctx_mu;
+  uint32_t next_ctx = 1;
+  std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<>> retired;
+  std::mutex comms_mu;
+  std::vector<mpix_comm_s*> all_comms;
+
+  uint32_t alloc_ctx() {  // world.cpp:43-51: retired ids recycled lowest-first
+    std::lock_guard<std::mutex> lk(ctx_mu);
+    if (!retired.empty()) {
+      uint32_t c = retired.top();
+      retired.pop();
+      return c;
+    }
+    return next_ctx++;
+  }
+  void retire_ctx(uint32_t c) {
+    std::lock_guard<std::mutex> lk(ctx_mu);
+    retired.push(c);
+  }
+};
+
+std::mutex g_world_mu;
+World* g_world = nullptr;
+thread_local int t_bound_rank = -1;
+
+#define CK(call)                                 \
+  do {                                           \
+    cudaError_t e_ = (call);                     \
+    if (e_ != cudaSuccess) return MPIX_ERR_CUDA; \
+  } while (0)
+
+int type_size(MPI_Datatype dt) {
+  switch (dt) {
+    case MPI_BYTE: return 1;
+    case MPI_INT: return 4;
+    case MPI_DOUBLE: return 8;
+    case MPI_FLOAT: return 4;
+    case MPIX_BFLOAT16: return 2;
+    default: return 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Hex codec (info.cpp:37-59 semantics: lowercase, high nibble first).
+// ---------------------------------------------------------------------------
+std::string hex_encode(const void* bytes, size_t len) {
+  static const char d[] = "0123456789abcdef";
+  const uint8_t* p = static_cast<const uint8_t*>(bytes);
+  std::string s;
+  s.reserve(len * 2);
+  for (size_t i = 0; i < len; ++i) {
+    s.push_back(d[p[i] >> 4]);
+    s.push_back(d[p[i] & 15]);
+  }
+  return s;
+}
+
+int nibble(char c) {
+  if (c >= '0' && c <= '9') return c - '0';
+  if (c >= 'a' && c <= 'f') return c - 'a' + 10;
+  return -1;
+}
+
+int hex_decode(const std::string& s, std::vector<uint8_t>& out) {
+  if (s.size() % 2) return MPIX_ERR_BAD_ENCODING;
+  out.clear();
+  out.reserve(s.size() / 2);
+  for (size_t i = 0; i < s.size(); i += 2) {
+    int hi = nibble(s[i]), lo = nibble(s[i + 1]);
+    if (hi < 0 || lo < 0) return MPIX_ERR_BAD_ENCODING;
+    out.push_back((uint8_t)((hi << 4) | lo));
+  }
+  return MPI_SUCCESS;
+}
+
+// ---------------------------------------------------------------------------
+// Rank setup
+// ---------------------------------------------------------------------------
+int rank_init(RankState& r, const Config& cfg) {
+  CK(cudaSetDevice(r.device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, r.device));
+  r.sms = prop.multiProcessorCount;
+  CK(cudaMalloc(&r.d_done, kReqSlots * sizeof(uint64_t)));
+  CK(cudaMemset(r.d_done, 0, kReqSlots * sizeof(uint64_t)));
+  CK(cudaMalloc(&r.d_rec, kOpRecords * sizeof(OpRecord)));
+  CK(cudaMemset(r.d_rec, 0, kOpRecords * sizeof(OpRecord)));
+  CK(cudaHostAlloc(&r.h_err, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(r.h_err, 0, 64);
+  CK(cudaHostGetDevicePointer(&r.d_err, r.h_err, 0));
+  CK(cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&r.reclaim, cudaStreamNonBlocking));
+  r.reqs.resize(kReqSlots);
+  int occ_p2p = p2p_occupancy();
+  int occ_ar = allreduce_occupancy();
+  int per = std::max(1, r.per_device);
+  r.p2p_cap = std::max(1, r.sms * occ_p2p / per);
+  r.ar_cap = std::max(1, r.sms * occ_ar / per);
+  if (cfg.max_ctas > 0) {
+    r.p2p_cap = std::min(r.p2p_cap, cfg.max_ctas);
+    r.ar_cap = std::min(r.ar_cap, cfg.max_ctas);
+  }
+  CK(cudaDeviceSynchronize());
+  return MPI_SUCCESS;
+}
+
+int rank_pool(World& w, RankState& r) {
+  CK(cudaSetDevice(r.device));
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = r.device;
+  CK(cudaMemPoolCreate(&r.pool, &props));
+  uint64_t thr = UINT64_MAX;
+  CK(cudaMemPoolSetAttribute(r.pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  // Peers read staging buffers and regions over NVLink.
+  std::vector<int> seen;
+  for (auto& o : w.ranks) {
+    if (o->device == r.device) continue;
+    if (std::find(seen.begin(), seen.end(), o->device) != seen.end()) continue;
+    seen.push_back(o->device);
+    cudaMemAccessDesc ad = {};
+    ad.location.type = cudaMemLocationTypeDevice;
+    ad.location.id = o->device;
+    ad.flags = cudaMemAccessFlagsProtReadWrite;
+    CK(cudaMemPoolSetAccess(r.pool, &ad, 1));
+  }
+  return MPI_SUCCESS;
+}
+
+World* world() { return g_world; }
+
+RankState& rank_of(int r) { return *g_world->ranks[r]; }
+
+int pick_grid(uint64_t bytes, uint64_t per_cta, int cap) {
+  uint64_t g = (bytes + per_cta - 1) / per_cta;
+  if (g < 1) g = 1;
+  if (g > (uint64_t)cap) g = cap;
+  return (int)g;
+}
+
+// Build and publish the per-rank view of a communicator. Collective over the
+// parent's members (proc_comm.cpp:60-176): root allocates the context id,
+// everyone allocates its region, then region bases are exchanged.
+int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bool multiplex,
+                mpix_comm_s** out) {
+  World& w = *g_world;
+  const int me = par->rank;
+  const int P = par->sh->P;
+  RankState& rs = rank_of(me);
+
+  // Validate locally before the rendezvous (proc_comm.cpp:64-77).
+  for (auto* s : streams) {
+    if (s && s->kind == mpix_stream_s::cuda && s->device != rs.device)
+      return MPIX_ERR_INVALID_STREAM;
+  }
+
+  // Phase 1: context id from the root + stream counts.
+  CollMsg m1;
+  m1.i0 = (int64_t)streams.size();
+  if (me == 0) m1.u0 = w.alloc_ctx();
+  auto v1 = par->sh->rv.exchange(P, me, par->rv_seq++, m1);
+  uint32_t ctx = (uint32_t)v1[0].u0;
+
+  // Shared state is created by the root and handed out in phase 2.
+  std::shared_ptr<CommShared> sh;
+  if (me == 0) {
+    sh = std::make_shared<CommShared>();
+    sh->ctx = ctx;
+    sh->P = P;
+    sh->multiplex = multiplex;
+    sh->L = RegionLayout{P, w.cfg.ring_slots, w.cfg.eager_bytes};
+    sh->base.assign(P, nullptr);
+    sh->counts.resize(P);
+    for (int q = 0; q < P; ++q) sh->counts[q] = (int)v1[q].i0;
+  }
+
+  // My region on my GPU, zeroed (all rings FREE, all epochs 0).
+  RegionLayout L{P, w.cfg.ring_slots, w.cfg.eager_bytes};
+  uint8_t* region = nullptr;
+  {
+    CK(cudaSetDevice(rs.device));
+    CK(cudaMallocFromPoolAsync((void**)&region, L.total(), rs.pool, rs.aux));
+    CK(cudaMemsetAsync(region, 0, L.total(), rs.aux));
+    CK(cudaStreamSynchronize(rs.aux));
+  }
+
+  CollMsg m2;
+  m2.p0 = region;
+  if (me == 0) m2.sp = sh;
+  auto v2 = par->sh->rv.exchange(P, me, par->rv_seq++, m2);
+  sh = std::static_pointer_cast<CommShared>(v2[0].sp);
+  {
+    // every member writes the same values; guard with the rank mutex of root
+    std::lock_guard<std::mutex> lk(rank_of(0).mu);
+    for (int q = 0; q < P; ++q) sh->base[q] = static_cast<uint8_t*>(v2[q].p0);
+  }
+  // Phase 3: nobody uses the comm until every member has filled the table.
+  par->sh->rv.exchange(P, me, par->rv_seq++, CollMsg{});
+
+  auto* c = new mpix_comm_s();
+  c->sh = sh;
+  c->rank = me;
+  c->local_streams = streams;
+  for (auto* s : streams)
+    if (s) s->refcount.fetch_add(1);
+  // proc_enqueue.cpp:23-28: only a single-stream comm whose local stream is
+  // a GPU stream accepts enqueue operations.
+  c->enqueue_ok = !multiplex && streams.size() == 1 && streams[0] &&
+                  streams[0]->kind == mpix_stream_s::cuda;
+  c->cu = c->enqueue_ok ? streams[0]->cu : nullptr;
+  c->send_pseq.assign(P, 0);
+  c->recv_pseq.assign(P, 0);
+  {
+    std::lock_guard<std::mutex> lk(w.comms_mu);
+    w.all_comms.push_back(c);
+  }
+  *out = c;
+  return MPI_SUCCESS;
+}
+
+uint64_t tagseq_key(int peer, int tag) { return ((uint64_t)(uint32_t)peer << 32) | (uint32_t)tag; }
+
+// check_args of proc_enqueue.cpp:8-20 (enqueue precedence: rank, tag, count).
+int check_args(const mpix_comm_s* c, int count, int peer, int tag, bool recv_side) {
+  const int P = c->sh->P;
+  if (recv_side) {
+    if (peer != MPI_ANY_SOURCE && (peer < 0 || peer >= P)) return MPIX_ERR_INVALID_RANK;
+    if (tag != MPI_ANY_TAG && tag < 0) return MPIX_ERR_INVALID_TAG;
+  } else {
+    if (peer < 0 || peer >= P) return MPIX_ERR_INVALID_RANK;
+    if (tag < 0) return MPIX_ERR_INVALID_TAG;
+  }
+  if (count < 0) return MPIX_ERR_INVALID_COUNT;
+  return MPI_SUCCESS;
+}
+
+struct Ticket {
+  uint64_t handle;
+  uint64_t* flag;
+  uint64_t gen;
+};
+
+Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag) {
+  uint64_t n = rs.req_next.fetch_add(1);
+  uint64_t slot = n % kReqSlots;
+  uint64_t gen = n / kReqSlots + 1;
+  auto& ri = rs.reqs[slot];
+  ri.gen = gen;
+  ri.stream = s;
+  ri.source = source;
+  ri.tag = tag;
+  Ticket t;
+  t.handle = ((uint64_t)(rs.rank + 1) << 48) | (n + 1);
+  t.flag = rs.d_done + slot;
+  t.gen = gen;
+  return t;
+}
+
+bool decode_ticket(uint64_t h, int* rank, uint64_t* n) {
+  if (h == 0) return false;
+  int r = (int)(h >> 48) - 1;
+  if (r < 0 || !g_world || r >= g_world->n) return false;
+  uint64_t v = h & ((1ull << 48) - 1);
+  if (v == 0) return false;
+  *rank = r;
+  *n = v - 1;
+  return true;
+}
+
+// Point-to-point enqueue (send side and receive side).
+int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
+                bool is_recv, bool blocking, MPI_Request* req) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!c) return MPIX_ERR_INVALID_COMM;
+  if (!c->enqueue_ok) return MPIX_ERR_NOT_ENQUEUE_COMM;  // proc_enqueue.cpp:33-34
+  int rc = check_args(c, count, peer, tag, is_recv);
+  if (rc) return rc;
+  int esz = type_size(dt);
+  if (!esz) return MPIX_ERR_TYPE;
+  if (is_recv && (peer == MPI_ANY_SOURCE || tag == MPI_ANY_TAG)) return MPIX_ERR_UNSUPPORTED;
+  if (!blocking && !req) return MPIX_ERR_INVALID_ARG;
+
+  World& w = *g_world;
+  CommShared& sh = *c->sh;
+  const RegionLayout& L = sh.L;
+  const int me = c->rank;
+  RankState& rs = rank_of(me);
+  const uint64_t bytes = (uint64_t)count * (uint64_t)esz;
+
+  P2PArgs a = {};
+  a.is_recv = is_recv;
+  a.blocking = blocking;
+  a.R = L.R;
+  a.E = L.E;
+  a.buf = static_cast<uint8_t*>(buf);
+  a.bytes = bytes;
+  a.err_word = rs.d_err;
+  a.spin_limit_ns = w.cfg.spin_limit_ns;
+  uint32_t tseq;
+  if (!is_recv) {
+    const int d = peer;
+    tseq = c->send_tagseq[tagseq_key(d, tag)]++;
+    a.pseq = c->send_pseq[d]++;
+    a.post_ring = reinterpret_cast<SlotDesc*>(sh.base[d] + L.sr(me));
+    a.post_mirror = reinterpret_cast<uint64_t*>(sh.base[me] + L.sr_free(d));
+    a.scan_ring = reinterpret_cast<SlotDesc*>(sh.base[me] + L.rr(d));
+    a.scan_mirror = reinterpret_cast<uint64_t*>(sh.base[d] + L.rr_free(me));
+    a.eager_ring = sh.base[d] + L.eager(me);
+    a.mode = !blocking ? MODE_ISEND : (bytes <= L.E ? MODE_EAGER : MODE_STAGED);
+  } else {
+    const int s = peer;
+    tseq = c->recv_tagseq[tagseq_key(s, tag)]++;
+    a.pseq = c->recv_pseq[s]++;
+    a.post_ring = reinterpret_cast<SlotDesc*>(sh.base[s] + L.rr(me));
+    a.post_mirror = reinterpret_cast<uint64_t*>(sh.base[me] + L.rr_free(s));
+    a.scan_ring = reinterpret_cast<SlotDesc*>(sh.base[me] + L.sr(s));
+    a.scan_mirror = reinterpret_cast<uint64_t*>(sh.base[s] + L.sr_free(me));
+    a.mode = 0;
+  }
+  a.key = ((uint64_t)(uint32_t)tag << 32) | tseq;
+
+  CK(cudaSetDevice(rs.device));
+  cudaStream_t s = c->cu;
+  Ticket t{};
+  if (!blocking || is_recv) {
+    t = new_ticket(rs, s, is_recv ? peer : me, tag);
+    a.my_done = t.flag;
+    a.my_gen = t.gen;
+  }
+  Ticket st{};
+  uint8_t* staging = nullptr;
+  if (a.mode == MODE_STAGED && !is_recv) {
+    CK(cudaMallocFromPoolAsync((void**)&staging, bytes ? bytes : 16, rs.pool, s));
+    st = new_ticket(rs, rs.reclaim, me, tag);
+    a.staging = staging;
+    a.stage_done = st.flag;
+    a.stage_gen = st.gen;
+  }
+  int grid = (is_recv || a.mode != MODE_EAGER) ? pick_grid(bytes, w.cfg.bytes_per_cta, rs.p2p_cap)
+                                               : 1;
+  if (grid > 1) {
+    uint64_t op = rs.op_next.fetch_add(1);
+    a.rec = rs.d_rec + (op % kOpRecords);
+    a.opid = op;
+  }
+  CK(launch_p2p(a, grid, s));
+  g_launches.fetch_add(1);
+  if (staging) {
+    // Release the staging copy once its consumer signals (stream-ordered
+    // after this kernel so the allocator sees the dependency).
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, s));
+    CK(cudaStreamWaitEvent(rs.reclaim, ev, 0));
+    CK(cudaEventDestroy(ev));
+    WaitArgs* wa = new WaitArgs;
+    wa->n = 1;
+    wa->err_word = rs.d_err;
+    wa->spin_limit_ns = 0;
+    wa->e[0].flag = st.flag;
+    wa->e[0].gen = st.gen;
+    cudaError_t e = launch_wait(*wa, rs.reclaim);
+    delete wa;
+    if (e != cudaSuccess) return MPIX_ERR_CUDA;
+    g_launches.fetch_add(1);
+    CK(cudaFreeAsync(staging, rs.reclaim));
+  }
+  if (req) *req = (!blocking) ? t.handle : MPI_REQUEST_NULL;
+  return MPI_SUCCESS;
+}
+
+int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (n < 0) return MPIX_ERR_INVALID_ARG;
+  if (n == 0) return MPI_SUCCESS;  // proc_enqueue.cpp:121
+  if (!reqs) return MPIX_ERR_INVALID_REQUEST;
+  struct Item {
+    int rank;
+    uint64_t n;
+  };
+  std::vector<Item> items(n);
+  for (int i = 0; i < n; ++i) {  // proc_enqueue.cpp:122-123
+    if (!decode_ticket(reqs[i], &items[i].rank, &items[i].n)) return MPIX_ERR_INVALID_REQUEST;
+  }
+  cudaStream_t s0 = nullptr;
+  int dev0 = -1;
+  for (int i = 0; i < n; ++i) {  // proc_enqueue.cpp:124-126
+    RankState& rs = rank_of(items[i].rank);
+    auto& ri = rs.reqs[items[i].n % kReqSlots];
+    cudaStream_t s = ri.gen == items[i].n / kReqSlots + 1 ? ri.stream : nullptr;
+    if (i == 0) {
+      s0 = s;
+      dev0 = rs.device;
+    }
+    if (s != s0 || rs.device != dev0) return MPIX_ERR_STREAM_MISMATCH;
+  }
+  if (statuses) {
+    for (int i = 0; i < n; ++i) {
+      RankState& rs = rank_of(items[i].rank);
+      auto& ri = rs.reqs[items[i].n % kReqSlots];
+      statuses[i].MPI_SOURCE = ri.source;
+      statuses[i].MPI_TAG = ri.tag;
+      statuses[i].MPI_ERROR = MPI_SUCCESS;
+      statuses[i].source_index = -2;
+      statuses[i].count_bytes = UINT64_MAX;
+      statuses[i].truncated = 0;
+    }
+  }
+  CK(cudaSetDevice(dev0));
+  std::unique_ptr<WaitArgs> wa(new WaitArgs);
+  for (int i0 = 0; i0 < n; i0 += kWaitBatch) {
+    int m = std::min(kWaitBatch, n - i0);
+    wa->n = m;
+    wa->err_word = rank_of(items[i0].rank).d_err;
+    wa->spin_limit_ns = g_world->cfg.spin_limit_ns;
+    for (int k = 0; k < m; ++k) {
+      RankState& rs = rank_of(items[i0 + k].rank);
+      uint64_t nn = items[i0 + k].n;
+      wa->e[k].flag = rs.d_done + (nn % kReqSlots);
+      wa->e[k].gen = nn / kReqSlots + 1;
+    }
+    CK(launch_wait(*wa, s0));
+    g_launches.fetch_add(1);
+  }
+  return MPI_SUCCESS;
+}
+
+int allreduce_enqueue(const void* sbuf, void* rbuf, int count, MPI_Datatype dt, MPI_Op op,
+                      mpix_comm_s* c) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!c) return MPIX_ERR_INVALID_COMM;
+  if (!c->enqueue_ok) return MPIX_ERR_NOT_ENQUEUE_COMM;
+  if (count < 0) return MPIX_ERR_INVALID_COUNT;
+  int dtype;
+  switch (dt) {
+    case MPI_INT: dtype = AR_I32; break;
+    case MPI_FLOAT: dtype = AR_F32; break;
+    case MPIX_BFLOAT16: dtype = AR_BF16; break;
+    case MPI_DOUBLE: dtype = AR_F64; break;
+    default: return MPIX_ERR_TYPE;
+  }
+  int aop;
+  switch (op) {
+    case MPI_SUM: aop = AR_SUM; break;
+    case MPI_MAX: aop = AR_MAX; break;
+    case MPI_MIN: aop = AR_MIN; break;
+    default: return MPIX_ERR_OP;
+  }
+  CommShared& sh = *c->sh;
+  const int P = sh.P;
+  if (P > kMaxCollRanks) return MPIX_ERR_UNSUPPORTED;
+  if (!rbuf) return MPIX_ERR_INVALID_ARG;
+  if (sbuf == MPI_IN_PLACE) sbuf = rbuf;
+  const int me = c->rank;
+  RankState& rs = rank_of(me);
+  const int esz = type_size(dt);
+  const uint64_t bytes = (uint64_t)count * esz;
+
+  ARArgs a = {};
+  a.sbuf = static_cast<const uint8_t*>(sbuf);
+  a.rbuf = static_cast<uint8_t*>(rbuf);
+  a.count = (uint64_t)count;
+  a.esize = esz;
+  a.dtype = dtype;
+  a.op = aop;
+  a.P = P;
+  a.me = me;
+  a.epoch = ++c->coll_epoch;
+  a.algo = (bytes <= g_world->cfg.oneshot_max || P <= 2) ? AR_ONESHOT : AR_TWOSHOT;
+  const RegionLayout& L = sh.L;
+  for (int q = 0; q < P; ++q) {
+    a.peer_in[q] = reinterpret_cast<CollSlot*>(sh.base[q] + L.coll_in(me));
+    a.peer_exit[q] = reinterpret_cast<uint64_t*>(sh.base[q] + L.coll_exit(me));
+  }
+  a.my_in = reinterpret_cast<CollSlot*>(sh.base[me] + L.coll_in(0));
+  a.my_exit = reinterpret_cast<uint64_t*>(sh.base[me] + L.coll_exit(0));
+  a.err_word = rs.d_err;
+  a.spin_limit_ns = g_world->cfg.spin_limit_ns;
+  uint64_t work = a.algo == AR_TWOSHOT ? (bytes + P - 1) / P : bytes;
+  int grid = pick_grid(work, g_world->cfg.bytes_per_cta, rs.ar_cap);
+  if (grid > 1) {
+    uint64_t opid = rs.op_next.fetch_add(1);
+    a.rec = rs.d_rec + (opid % kOpRecords);
+    a.opid = opid;
+  }
+  CK(cudaSetDevice(rs.device));
+  CK(launch_allreduce(a, grid, c->cu));
+  g_launches.fetch_add(1);
+  return MPI_SUCCESS;
+}
+
+}  // namespace mpix
+
+using namespace mpix;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* MPIX_Error_string(int code) {
+  switch (code) {  // result.cpp:5-32
+    case MPI_SUCCESS: return "OK";
+    case MPIX_ERR_POOL_EXHAUSTED: return "POOL_EXHAUSTED";
+    case MPIX_ERR_NO_EXPLICIT_POOL: return "NO_EXPLICIT_POOL";
+    case MPIX_ERR_PENDING_OPS: return "PENDING_OPS";
+    case MPIX_ERR_IN_USE: return "IN_USE";
+    case MPIX_ERR_BAD_HINT: return "BAD_HINT";
+    case MPIX_ERR_INVALID_STREAM: return "INVALID_STREAM";
+    case MPIX_ERR_INVALID_COMM: return "INVALID_COMM";
+    case MPIX_ERR_INVALID_RANK: return "INVALID_RANK";
+    case MPIX_ERR_INVALID_COUNT: return "INVALID_COUNT";
+    case MPIX_ERR_INVALID_TAG: return "INVALID_TAG";
+    case MPIX_ERR_INVALID_REQUEST: return "INVALID_REQUEST";
+    case MPIX_ERR_INVALID_INDEX: return "INVALID_INDEX";
+    case MPIX_ERR_MULTIPLEX_COMM: return "MULTIPLEX_COMM";
+    case MPIX_ERR_NOT_MULTIPLEX: return "NOT_MULTIPLEX";
+    case MPIX_ERR_WILDCARD_DST: return "WILDCARD_DST";
+    case MPIX_ERR_EMPTY_LIST: return "EMPTY_LIST";
+    case MPIX_ERR_NOT_ENQUEUE_COMM: return "NOT_ENQUEUE_COMM";
+    case MPIX_ERR_STREAM_MISMATCH: return "STREAM_MISMATCH";
+    case MPIX_ERR_QUEUE_BUSY: return "QUEUE_BUSY";
+    case MPIX_ERR_CONFIG_INVALID: return "CONFIG_INVALID";
+    case MPIX_ERR_NOT_FOUND: return "NOT_FOUND";
+    case MPIX_ERR_BAD_ENCODING: return "BAD_ENCODING";
+    case MPIX_ERR_CUDA: return "CUDA_ERROR";
+    case MPIX_ERR_NOT_INITIALIZED: return "NOT_INITIALIZED";
+    case MPIX_ERR_UNSUPPORTED: return "UNSUPPORTED";
+    case MPIX_ERR_INVALID_ARG: return "INVALID_ARG";
+    case MPIX_ERR_TYPE: return "INVALID_TYPE";
+    case MPIX_ERR_OP: return "INVALID_OP";
+    case MPIX_ERR_NO_MEM: return "NO_MEM";
+    default: return "UNKNOWN";
+  }
+}
+
+// --------------------------------------------------------------------------
+// World
+// --------------------------------------------------------------------------
+int MPIX_World_init(int nranks, const int* devices) {
+  std::lock_guard<std::mutex> lk(g_world_mu);
+  if (g_world) return MPIX_ERR_IN_USE;
+  if (nranks < 1) return MPIX_ERR_INVALID_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return MPIX_ERR_CUDA;
+  std::unique_ptr<World> w(new World());
+  w->cfg = Config::from_env();
+  w->n = nranks;
+  for (int r = 0; r < nranks; ++r) {
+    auto rs = std::make_unique<RankState>();
+    rs->rank = r;
+    rs->device = devices ? devices[r] : r % ndev;
+    if (rs->device < 0 || rs->device >= ndev) return MPIX_ERR_INVALID_ARG;
+    w->ranks.push_back(std::move(rs));
+  }
+  for (auto& rs : w->ranks) {
+    int per = 0;
+    for (auto& o : w->ranks) per += o->device == rs->device;
+    rs->per_device = per;
+  }
+  // Peer access between every pair of distinct devices (NVLink / NVSwitch).
+  std::vector<int> devs;
+  for (auto& rs : w->ranks)
+    if (std::find(devs.begin(), devs.end(), rs->device) == devs.end()) devs.push_back(rs->device);
+  for (int i : devs) {
+    for (int j : devs) {
+      if (i == j) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, i, j);
+      if (!can) return MPIX_ERR_UNSUPPORTED;
+      cudaSetDevice(i);
+      cudaError_t e = cudaDeviceEnablePeerAccess(j, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else if (e != cudaSuccess)
+        return MPIX_ERR_CUDA;
+    }
+  }
+  for (auto& rs : w->ranks) {
+    int rc = rank_init(*rs, w->cfg);
+    if (rc) return rc;
+  }
+  for (auto& rs : w->ranks) {
+    int rc = rank_pool(*w, *rs);
+    if (rc) return rc;
+  }
+  // Bootstrap world communicator, ctx 0 (world.cpp:61-76). It carries no
+  // stream, so enqueue on it is NOT_ENQUEUE_COMM; it has no region.
+  auto sh = std::make_shared<CommShared>();
+  sh->ctx = 0;
+  sh->P = nranks;
+  sh->is_world = true;
+  sh->counts.assign(nranks, 1);
+  sh->L = RegionLayout{nranks, w->cfg.ring_slots, w->cfg.eager_bytes};
+  sh->base.assign(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    auto* c = new mpix_comm_s();
+    c->sh = sh;
+    c->rank = r;
+    c->send_pseq.assign(nranks, 0);
+    c->recv_pseq.assign(nranks, 0);
+    w->world_comms.push_back(c);
+  }
+  g_world = w.release();
+  return MPI_SUCCESS;
+}
+
+int MPIX_World_finalize(void) {
+  std::lock_guard<std::mutex> lk(g_world_mu);
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  World* w = g_world;
+  for (auto& rs : w->ranks) {
+    cudaSetDevice(rs->device);
+    cudaDeviceSynchronize();
+  }
+  for (auto* c : w->all_comms) {
+    RankState& rs = *w->ranks[c->rank];
+    cudaSetDevice(rs.device);
+    if (c->sh && c->sh->base[c->rank]) {
+      cudaFreeAsync(c->sh->base[c->rank], rs.aux);
+      c->sh->base[c->rank] = nullptr;
+    }
+    delete c;
+  }
+  for (auto* c : w->world_comms) delete c;
+  for (auto& rs : w->ranks) {
+    cudaSetDevice(rs->device);
+    cudaStreamSynchronize(rs->aux);
+    cudaStreamSynchronize(rs->reclaim);
+    cudaFree(rs->d_done);
+    cudaFree(rs->d_rec);
+    cudaFreeHost(rs->h_err);
+    cudaStreamDestroy(rs->aux);
+    cudaStreamDestroy(rs->reclaim);
+    if (rs->pool) cudaMemPoolDestroy(rs->pool);
+  }
+  delete w;
+  g_world = nullptr;
+  return MPI_SUCCESS;
+}
+
+int MPIX_World_size(int* n) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  *n = g_world->n;
+  return MPI_SUCCESS;
+}
+
+int MPIX_World_comm(int rank, MPI_Comm* comm) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (rank < 0 || rank >= g_world->n) return MPIX_ERR_INVALID_RANK;
+  *comm = g_world->world_comms[rank];
+  return MPI_SUCCESS;
+}
+
+int MPIX_Rank_bind(int rank) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (rank < 0 || rank >= g_world->n) return MPIX_ERR_INVALID_RANK;
+  t_bound_rank = rank;
+  return MPI_SUCCESS;
+}
+
+int MPIX_Comm_world_self(MPI_Comm* comm) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (t_bound_rank < 0) return MPIX_ERR_INVALID_RANK;
+  *comm = g_world->world_comms[t_bound_rank];
+  return MPI_SUCCESS;
+}
+
+int MPI_Comm_rank(MPI_Comm comm, int* rank) {
+  if (!comm) return MPIX_ERR_INVALID_COMM;
+  *rank = comm->rank;
+  return MPI_SUCCESS;
+}
+
+int MPI_Comm_size(MPI_Comm comm, int* size) {
+  if (!comm) return MPIX_ERR_INVALID_COMM;
+  *size = comm->sh->P;
+  return MPI_SUCCESS;
+}
+
+int MPI_Barrier(MPI_Comm comm) {  // proc_comm.cpp:31-46 (host-side)
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!comm) return MPIX_ERR_INVALID_COMM;
+  comm->sh->rv.exchange(comm->sh->P, comm->rank, comm->rv_seq++, CollMsg{});
+  return MPI_SUCCESS;
+}
+
+int MPI_Comm_free(MPI_Comm* comm) {  // proc_comm.cpp:178-194
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!comm || !*comm) return MPIX_ERR_INVALID_COMM;
+  mpix_comm_s* c = *comm;
+  if (c->sh->is_world) return MPIX_ERR_INVALID_COMM;
+  World& w = *g_world;
+  RankState& rs = rank_of(c->rank);
+  const int P = c->sh->P;
+  // Every member's outstanding work on this comm must retire before any
+  // region is released: exchange one event per member and make each aux
+  // stream wait on all of them.
+  cudaEvent_t ev = nullptr;
+  CK(cudaSetDevice(rs.device));
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, c->cu ? c->cu : rs.aux));
+  CollMsg m;
+  m.p0 = ev;
+  auto v = c->sh->rv.exchange(P, c->rank, c->rv_seq++, m);
+  for (int q = 0; q < P; ++q) CK(cudaStreamWaitEvent(rs.aux, (cudaEvent_t)v[q].p0, 0));
+  // Nobody destroys an event before all members have enqueued their waits.
+  c->sh->rv.exchange(P, c->rank, c->rv_seq++, CollMsg{});
+  CK(cudaEventDestroy(ev));
+  uint8_t* region = c->sh->base[c->rank];
+  if (region) CK(cudaFreeAsync(region, rs.aux));
+  c->sh->base[c->rank] = nullptr;
+  for (auto* s : c->local_streams)
+    if (s) s->refcount.fetch_sub(1);
+  if (c->rank == 0) w.retire_ctx(c->sh->ctx);
+  {
+    std::lock_guard<std::mutex> lk(w.comms_mu);
+    w.all_comms.erase(std::remove(w.all_comms.begin(), w.all_comms.end(), c), w.all_comms.end());
+  }
+  delete c;
+  *comm = MPI_COMM_NULL;
+  return MPI_SUCCESS;
+}
+
+// --------------------------------------------------------------------------
+// Info
+// --------------------------------------------------------------------------
+int MPI_Info_create(MPI_Info* info) {
+  if (!info) return MPIX_ERR_INVALID_ARG;
+  *info = new mpix_info_s();
+  return MPI_SUCCESS;
+}
+
+int MPI_Info_free(MPI_Info* info) {
+  if (!info || !*info) return MPIX_ERR_INVALID_ARG;
+  delete *info;
+  *info = MPI_INFO_NULL;
+  return MPI_SUCCESS;
+}
+
+int MPI_Info_set(MPI_Info info, const char* key, const char* value) {
+  if (!info || !key || !value) return MPIX_ERR_INVALID_ARG;
+  info->entries[key] = value;
+  return MPI_SUCCESS;
+}
+
+int MPI_Info_get(MPI_Info info, const char* key, int valuelen, char* value, int* flag) {
+  if (!info || !key || !flag) return MPIX_ERR_INVALID_ARG;
+  auto it = info->entries.find(key);
+  if (it == info->entries.end()) {
+    *flag = 0;
+    return MPI_SUCCESS;
+  }
+  *flag = 1;
+  if (value && valuelen > 0) {
+    size_t n = std::min((size_t)valuelen - 1, it->second.size());
+    memcpy(value, it->second.data(), n);
+    value[n] = 0;
+  }
+  return MPI_SUCCESS;
+}
+
+int MPIX_Info_set_hex(MPI_Info info, const char* key, const void* value, int vallen) {
+  if (!info || !key || vallen < 0 || (vallen > 0 && !value)) return MPIX_ERR_INVALID_ARG;
+  info->entries[key] = hex_encode(value, (size_t)vallen);
+  return MPI_SUCCESS;
+}
+
+int MPIX_Info_get_hex(MPI_Info info, const char* key, void* value, int maxlen, int* outlen) {
+  if (!info || !key) return MPIX_ERR_INVALID_ARG;
+  auto it = info->entries.find(key);
+  if (it == info->entries.end()) return MPIX_ERR_NOT_FOUND;
+  std::vector<uint8_t> out;
+  int rc = hex_decode(it->second, out);
+  if (rc) return rc;
+  if (outlen) *outlen = (int)out.size();
+  if (value && maxlen > 0) memcpy(value, out.data(), std::min((size_t)maxlen, out.size()));
+  return MPI_SUCCESS;
+}
+
+// --------------------------------------------------------------------------
+// Streams
+// --------------------------------------------------------------------------
+int MPIX_Stream_create(MPI_Info info, MPIX_Stream* stream) {
+  if (!stream) return MPIX_ERR_INVALID_ARG;
+  auto s = std::make_unique<mpix_stream_s>();
+  s->kind = mpix_stream_s::serial;
+  s->exclusive = true;
+  if (info) {
+    auto it = info->entries.find("type");
+    if (it != info->entries.end()) {  // proc_stream.cpp:11-17
+      if (it->second != "cudaStream_t") return MPIX_ERR_BAD_HINT;
+      auto v = info->entries.find("value");
+      if (v == info->entries.end()) return MPIX_ERR_BAD_HINT;
+      std::vector<uint8_t> bytes;
+      if (hex_decode(v->second, bytes) != MPI_SUCCESS) return MPIX_ERR_BAD_HINT;
+      if (bytes.size() != sizeof(cudaStream_t)) return MPIX_ERR_BAD_HINT;
+      cudaStream_t cs;
+      memcpy(&cs, bytes.data(), sizeof(cs));
+      int dev = -1;
+      if (cudaStreamGetDevice(cs, &dev) != cudaSuccess) {
+        cudaGetLastError();
+        return MPIX_ERR_BAD_HINT;  // not a live stream
+      }
+      s->kind = mpix_stream_s::cuda;
+      s->cu = cs;
+      s->device = dev;
+      s->exclusive = false;  // proc_stream.cpp:23-24
+    }
+    auto p = info->entries.find("endpoint_policy");  // proc_stream.cpp:27-33
+    if (p != info->entries.end()) {
+      if (p->second == "shared")
+        s->exclusive = false;
+      else if (p->second == "exclusive")
+        s->exclusive = true;
+      else
+        return MPIX_ERR_BAD_HINT;
+    }
+  }
+  *stream = s.release();
+  return MPI_SUCCESS;
+}
+
+int MPIX_Stream_free(MPIX_Stream* stream) {  // proc_stream.cpp:49-60
+  if (!stream || !*stream) return MPIX_ERR_INVALID_STREAM;
+  if ((*stream)->refcount.load() > 0) return MPIX_ERR_IN_USE;
+  delete *stream;
+  *stream = MPIX_STREAM_NULL;
+  return MPI_SUCCESS;
+}
+
+int MPIX_Stream_get_cuda(MPIX_Stream stream, void** cuda_stream) {
+  if (!stream || !cuda_stream) return MPIX_ERR_INVALID_STREAM;
+  *cuda_stream = stream->kind == mpix_stream_s::cuda ? (void*)stream->cu : nullptr;
+  return MPI_SUCCESS;
+}
+
+// --------------------------------------------------------------------------
+// Communicators
+// --------------------------------------------------------------------------
+int MPIX_Stream_comm_create(MPI_Comm parent, MPIX_Stream stream, MPI_Comm* newcomm) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!parent) return MPIX_ERR_INVALID_COMM;
+  if (!newcomm) return MPIX_ERR_INVALID_ARG;
+  return create_comm(parent, {stream}, false, newcomm);
+}
+
+int MPIX_Stream_comm_create_multiplex(MPI_Comm parent, int count, MPIX_Stream streams[],
+                                      MPI_Comm* newcomm) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!parent) return MPIX_ERR_INVALID_COMM;
+  if (!newcomm) return MPIX_ERR_INVALID_ARG;
+  if (count <= 0 || !streams) return MPIX_ERR_EMPTY_LIST;  // proc_comm.cpp:55
+  std::vector<mpix_stream_s*> v(streams, streams + count);
+  return create_comm(parent, v, true, newcomm);
+}
+
+int MPIX_Stream_comm_create_multiple(MPI_Comm parent, int count, MPIX_Stream streams[],
+                                     MPI_Comm* newcomm) {
+  return MPIX_Stream_comm_create_multiplex(parent, count, streams, newcomm);
+}
+
+// --------------------------------------------------------------------------
+// Enqueue
+// --------------------------------------------------------------------------
+int MPIX_Send_enqueue(const void* buf, int count, MPI_Datatype datatype, int dest, int tag,
+                      MPI_Comm comm) {
+  return p2p_enqueue(comm, const_cast<void*>(buf), count, datatype, dest, tag, false, true,
+                     nullptr);
+}
+
+int MPIX_Recv_enqueue(void* buf, int count, MPI_Datatype datatype, int source, int tag,
+                      MPI_Comm comm, MPI_Status* status) {
+  int rc = p2p_enqueue(comm, buf, count, datatype, source, tag, true, true, nullptr);
+  if (rc == MPI_SUCCESS && status) {
+    status->MPI_SOURCE = source;
+    status->MPI_TAG = tag;
+    status->MPI_ERROR = MPI_SUCCESS;
+    status->source_index = -2;
+    status->count_bytes = UINT64_MAX;
+    status->truncated = 0;
+  }
+  return rc;
+}
+
+int MPIX_Isend_enqueue(const void* buf, int count, MPI_Datatype datatype, int dest, int tag,
+                       MPI_Comm comm, MPI_Request* request) {
+  return p2p_enqueue(comm, const_cast<void*>(buf), count, datatype, dest, tag, false, false,
+                     request);
+}
+
+int MPIX_Irecv_enqueue(void* buf, int count, MPI_Datatype datatype, int source, int tag,
+                       MPI_Comm comm, MPI_Request* request) {
+  return p2p_enqueue(comm, buf, count, datatype, source, tag, true, false, request);
+}
+
+int MPIX_Wait_enqueue(MPI_Request* request, MPI_Status* status) {
+  if (!request) return MPIX_ERR_INVALID_REQUEST;
+  return waitall_enqueue(1, request, status);
+}
+
+int MPIX_Waitall_enqueue(int count, MPI_Request requests[], MPI_Status statuses[]) {
+  return waitall_enqueue(count, requests, statuses);
+}
+
+int MPIX_Request_free(MPI_Request* request) {
+  if (!request) return MPIX_ERR_INVALID_REQUEST;
+  *request = MPI_REQUEST_NULL;
+  return MPI_SUCCESS;
+}
+
+int MPIX_Allreduce_enqueue(const void* sendbuf, void* recvbuf, int count, MPI_Datatype datatype,
+                           MPI_Op op, MPI_Comm comm) {
+  return allreduce_enqueue(sendbuf, recvbuf, count, datatype, op, comm);
+}
+
+// --------------------------------------------------------------------------
+// Introspection
+// --------------------------------------------------------------------------
+uint64_t MPIX_Launch_count(void) { return g_launches.load(); }
+
+int MPIX_Config_get(uint64_t* eager_bytes, int* ring_slots, int* max_ctas,
+                    uint64_t* oneshot_max_bytes) {
+  Config c = g_world ? g_world->cfg : Config::from_env();
+  if (eager_bytes) *eager_bytes = c.eager_bytes;
+  if (ring_slots) *ring_slots = c.ring_slots;
+  if (max_ctas) *max_ctas = g_world ? g_world->ranks[0]->p2p_cap : c.max_ctas;
+  if (oneshot_max_bytes) *oneshot_max_bytes = c.oneshot_max;
+  return MPI_SUCCESS;
+}
+
+int MPIX_Comm_get_ctx(MPI_Comm comm, uint32_t* ctx) {
+  if (!comm) return MPIX_ERR_INVALID_COMM;
+  *ctx = comm->sh->ctx;
+  return MPI_SUCCESS;
+}
+
+int MPIX_Comm_is_enqueue(MPI_Comm comm, int* flag) {
+  if (!comm) return MPIX_ERR_INVALID_COMM;
+  *flag = comm->enqueue_ok ? 1 : 0;
+  return MPI_SUCCESS;
+}
+
+int MPIX_Type_size(MPI_Datatype datatype) { return type_size(datatype); }
+
+const char* MPIX_Version(void) { return "mpix-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

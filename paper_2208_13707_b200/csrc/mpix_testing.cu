@@ -1,0 +1,236 @@
+// mpix_testing.cu — producer/consumer helper kernels for tests and bench
+// (include/mpix_testing.h). Their host-side restatements live in
+// oracle/streamix_oracle.c (orc_pattern_u32, orc_checksum64, orc_stencil7).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "mpix_testing.h"
+
+namespace {
+
+std::atomic<uint64_t> g_test_launches{0};
+
+__host__ __device__ __forceinline__ uint32_t pattern_u32(uint32_t seed, uint32_t iter, uint64_t i) {
+  // lowbias32 over (seed, iter, i); identical to orc_pattern_u32.
+  uint32_t x = seed ^ (iter * 0x9E3779B9u) ^ (uint32_t)i ^ (uint32_t)(i >> 32) * 0x85EBCA6Bu;
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_fill_pattern(uint32_t* w, uint64_t nwords, uint8_t* tail, uint64_t ntail,
+                               uint32_t seed, uint32_t iter) {
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = t; i < nwords; i += nt) w[i] = pattern_u32(seed, iter, i);
+  if (t < ntail) {
+    uint32_t v = pattern_u32(seed, iter, nwords);
+    tail[t] = (uint8_t)(v >> (8 * t));
+  }
+}
+
+// checksum = sum_i mix64(word64_i ^ (i * golden)) mod 2^64, zero-padded tail.
+__global__ void k_checksum(const uint8_t* buf, uint64_t nbytes, unsigned long long* out) {
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t nw = nbytes / 8;
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(buf);
+  uint64_t acc = 0;
+  bool aligned = ((uint64_t)buf & 7) == 0;
+  for (uint64_t i = t; i < nw; i += nt) {
+    uint64_t v;
+    if (aligned) {
+      v = w[i];
+    } else {
+      v = 0;
+      for (int k = 0; k < 8; ++k) v |= (uint64_t)buf[i * 8 + k] << (8 * k);
+    }
+    acc += mix64(v ^ (i * 0x9E3779B97F4A7C15ull));
+  }
+  if (t == 0 && (nbytes & 7)) {
+    uint64_t v = 0;
+    for (uint64_t k = nw * 8; k < nbytes; ++k) v |= (uint64_t)buf[k] << (8 * (k - nw * 8));
+    acc += mix64(v ^ (nw * 0x9E3779B97F4A7C15ull));
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
+__global__ void k_saxpy(int n, float a, const float* x, float* y) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = a * x[i] + y[i];
+}
+
+__global__ void k_delay(uint64_t ns) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 >= ns) break;
+    __nanosleep(1000);
+  }
+}
+
+__global__ void k_empty() {}
+
+__global__ void k_fill_f32(float* x, uint64_t n, float v) {
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = t; i < n; i += nt) x[i] = v;
+}
+
+// Halo geometry: storage index of (x, y, z) in [0, n+2).
+__host__ __device__ __forceinline__ uint64_t hidx(int x, int y, int z, int nx, int ny) {
+  return ((uint64_t)z * (ny + 2) + y) * (uint64_t)(nx + 2) + x;
+}
+
+// Face plane: (a, b) spans the two tangential axes, interior range [1, n].
+__device__ __forceinline__ void face_coord(int face, int a, int b, int layer, int nx, int ny,
+                                           int nz, int& x, int& y, int& z) {
+  int axis = face >> 1;
+  int hi = face & 1;
+  if (axis == 0) {
+    x = hi ? nx + 1 - layer : layer;
+    y = a + 1;
+    z = b + 1;
+  } else if (axis == 1) {
+    x = a + 1;
+    y = hi ? ny + 1 - layer : layer;
+    z = b + 1;
+  } else {
+    x = a + 1;
+    y = b + 1;
+    z = hi ? nz + 1 - layer : layer;
+  }
+}
+
+__device__ __forceinline__ void face_dims(int face, int nx, int ny, int nz, int& na, int& nb) {
+  int axis = face >> 1;
+  if (axis == 0) { na = ny; nb = nz; }
+  else if (axis == 1) { na = nx; nb = nz; }
+  else { na = nx; nb = ny; }
+}
+
+// pack: interior boundary layer (layer 1); unpack: halo layer (layer 0).
+__global__ void k_halo(float* u, int nx, int ny, int nz, int face, float* buf, int pack) {
+  int na, nb;
+  face_dims(face, nx, ny, nz, na, nb);
+  uint64_t n = (uint64_t)na * nb;
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = t; i < n; i += nt) {
+    int a = (int)(i % na), b = (int)(i / na);
+    int x, y, z;
+    face_coord(face, a, b, pack ? 1 : 0, nx, ny, nz, x, y, z);
+    uint64_t c = hidx(x, y, z, nx, ny);
+    if (pack)
+      buf[i] = u[c];
+    else
+      u[c] = buf[i];
+  }
+}
+
+__global__ void k_stencil7(const float* __restrict__ u, float* __restrict__ out, int nx, int ny,
+                           int nz, float w0, float w1) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  int y = blockIdx.y + 1;
+  int z = blockIdx.z + 1;
+  if (x > nx) return;
+  const uint64_t sx = 1, sy = nx + 2, sz = (uint64_t)(nx + 2) * (ny + 2);
+  uint64_t c = hidx(x, y, z, nx, ny);
+  float s = u[c - sx] + u[c + sx];
+  s += u[c - sy] + u[c + sy];
+  s += u[c - sz] + u[c + sz];
+  out[c] = w0 * u[c] + w1 * s;
+}
+
+int grid_for(uint64_t n, int threads) {
+  uint64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int done(cudaError_t e) {
+  g_test_launches.fetch_add(1);
+  return e == cudaSuccess ? 0 : 100;
+}
+
+}  // namespace
+
+extern "C" {
+
+int MPIXT_Fill_pattern(void* buf, uint64_t nbytes, uint32_t seed, uint32_t iter, void* stream) {
+  uint64_t nw = nbytes / 4;
+  k_fill_pattern<<<grid_for(nw, 256), 256, 0, (cudaStream_t)stream>>>(
+      (uint32_t*)buf, nw, (uint8_t*)buf + nw * 4, nbytes - nw * 4, seed, iter);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Checksum(const void* buf, uint64_t nbytes, uint64_t* out_dev, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(out_dev, 0, 8, s) != cudaSuccess) return 100;
+  k_checksum<<<grid_for(nbytes / 8 + 1, 256), 256, 0, s>>>((const uint8_t*)buf, nbytes,
+                                                           (unsigned long long*)out_dev);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Saxpy(int n, float a, const float* x, float* y, void* stream) {
+  k_saxpy<<<(n + 255) / 256 > 0 ? (n + 255) / 256 : 1, 256, 0, (cudaStream_t)stream>>>(n, a, x, y);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Delay(uint64_t ns, void* stream) {
+  k_delay<<<1, 1, 0, (cudaStream_t)stream>>>(ns);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Empty(void* stream) {
+  k_empty<<<1, 32, 0, (cudaStream_t)stream>>>();
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Fill_f32(float* x, uint64_t n, float value, void* stream) {
+  k_fill_f32<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, n, value);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Halo_pack(const float* u, int nx, int ny, int nz, int face, float* buf, void* stream) {
+  uint64_t n = (uint64_t)nx * ny * nz;  // upper bound of face size
+  k_halo<<<grid_for(n / (uint64_t)(nx < ny ? nx : ny) + 1, 256), 256, 0, (cudaStream_t)stream>>>(
+      const_cast<float*>(u), nx, ny, nz, face, buf, 1);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Halo_unpack(float* u, int nx, int ny, int nz, int face, const float* buf,
+                      void* stream) {
+  uint64_t n = (uint64_t)nx * ny * nz;
+  k_halo<<<grid_for(n / (uint64_t)(nx < ny ? nx : ny) + 1, 256), 256, 0, (cudaStream_t)stream>>>(
+      u, nx, ny, nz, face, const_cast<float*>(buf), 0);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Stencil7(const float* u, float* out, int nx, int ny, int nz, float w0, float w1,
+                   void* stream) {
+  dim3 block(128);
+  dim3 grid((nx + 127) / 128, ny, nz);
+  k_stencil7<<<grid, block, 0, (cudaStream_t)stream>>>(u, out, nx, ny, nz, w0, w1);
+  return done(cudaGetLastError());
+}
+
+uint64_t MPIXT_Launch_count(void) { return g_test_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,433 @@
+"""ctypes binding of include/mpix.h — the Python face of the drop-in boundary.
+
+This mirrors the reference's `streamix::Proc` surface
+(proj/include/streamix/world.hpp:35-92) the way a maintainer would bind the
+C ABI: one `World` of N ranks (world.hpp:132-159), `run_ranks` to drive
+collective calls from one thread per rank (proj/src/world.cpp:78-84),
+`Info` hints (info.hpp:16-31), streams, stream communicators and the
+enqueue family. Errors raise `MPIXError` whose `.name` is the reference's
+`to_string(Err)` name (proj/src/result.cpp:5-32).
+
+The library is the in-tree `libmpix.so`; there is no fallback path: if the
+library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from typing import Callable, List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpix.so")
+
+# --- constants (include/mpix.h) ---------------------------------------------
+MPI_SUCCESS = 0
+MPI_BYTE, MPI_INT, MPI_DOUBLE, MPI_FLOAT, MPIX_BFLOAT16 = 1, 2, 3, 4, 5
+MPI_SUM, MPI_MAX, MPI_MIN = 1, 2, 3
+MPI_ANY_SOURCE = -1
+MPI_ANY_TAG = -1
+MPI_REQUEST_NULL = 0
+
+ERR_NAMES = [
+    "OK", "POOL_EXHAUSTED", "NO_EXPLICIT_POOL", "PENDING_OPS", "IN_USE", "BAD_HINT",
+    "INVALID_STREAM", "INVALID_COMM", "INVALID_RANK", "INVALID_COUNT", "INVALID_TAG",
+    "INVALID_REQUEST", "INVALID_INDEX", "MULTIPLEX_COMM", "NOT_MULTIPLEX", "WILDCARD_DST",
+    "EMPTY_LIST", "NOT_ENQUEUE_COMM", "STREAM_MISMATCH", "QUEUE_BUSY", "CONFIG_INVALID",
+    "NOT_FOUND", "BAD_ENCODING",
+]
+ERR = {n: i for i, n in enumerate(ERR_NAMES)}
+ERR.update({"CUDA_ERROR": 100, "NOT_INITIALIZED": 101, "UNSUPPORTED": 102,
+            "INVALID_ARG": 103, "INVALID_TYPE": 104, "INVALID_OP": 105, "NO_MEM": 106})
+
+_TORCH_DT = {}
+
+
+class MPIXError(RuntimeError):
+    def __init__(self, code: int, where: str = ""):
+        self.code = code
+        self.name = error_string(code)
+        super().__init__(f"{where}: {self.name} ({code})" if where else f"{self.name} ({code})")
+
+
+class MPIStatus(C.Structure):
+    _fields_ = [("MPI_SOURCE", C.c_int), ("MPI_TAG", C.c_int), ("MPI_ERROR", C.c_int),
+                ("source_index", C.c_int), ("count_bytes", C.c_uint64), ("truncated", C.c_int)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib() -> C.CDLL:
+    """Load libmpix.so (raises if it was not built: no CPU fallback exists)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+            L = C.CDLL(LIB_PATH)
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def _declare(L: C.CDLL) -> None:
+    P, I, U64, U32 = C.c_void_p, C.c_int, C.c_uint64, C.c_uint32
+    sig = {
+        "MPIX_Error_string": (C.c_char_p, [I]),
+        "MPIX_World_init": (I, [I, P]),
+        "MPIX_World_finalize": (I, []),
+        "MPIX_World_size": (I, [C.POINTER(I)]),
+        "MPIX_World_comm": (I, [I, C.POINTER(P)]),
+        "MPIX_Rank_bind": (I, [I]),
+        "MPIX_Comm_world_self": (I, [C.POINTER(P)]),
+        "MPI_Comm_rank": (I, [P, C.POINTER(I)]),
+        "MPI_Comm_size": (I, [P, C.POINTER(I)]),
+        "MPI_Barrier": (I, [P]),
+        "MPI_Comm_free": (I, [C.POINTER(P)]),
+        "MPI_Info_create": (I, [C.POINTER(P)]),
+        "MPI_Info_free": (I, [C.POINTER(P)]),
+        "MPI_Info_set": (I, [P, C.c_char_p, C.c_char_p]),
+        "MPI_Info_get": (I, [P, C.c_char_p, I, C.c_char_p, C.POINTER(I)]),
+        "MPIX_Info_set_hex": (I, [P, C.c_char_p, P, I]),
+        "MPIX_Info_get_hex": (I, [P, C.c_char_p, P, I, C.POINTER(I)]),
+        "MPIX_Stream_create": (I, [P, C.POINTER(P)]),
+        "MPIX_Stream_free": (I, [C.POINTER(P)]),
+        "MPIX_Stream_get_cuda": (I, [P, C.POINTER(P)]),
+        "MPIX_Stream_comm_create": (I, [P, P, C.POINTER(P)]),
+        "MPIX_Stream_comm_create_multiplex": (I, [P, I, C.POINTER(P), C.POINTER(P)]),
+        "MPIX_Stream_comm_create_multiple": (I, [P, I, C.POINTER(P), C.POINTER(P)]),
+        "MPIX_Send_enqueue": (I, [P, I, I, I, I, P]),
+        "MPIX_Recv_enqueue": (I, [P, I, I, I, I, P, P]),
+        "MPIX_Isend_enqueue": (I, [P, I, I, I, I, P, C.POINTER(U64)]),
+        "MPIX_Irecv_enqueue": (I, [P, I, I, I, I, P, C.POINTER(U64)]),
+        "MPIX_Wait_enqueue": (I, [C.POINTER(U64), P]),
+        "MPIX_Waitall_enqueue": (I, [I, C.POINTER(U64), P]),
+        "MPIX_Request_free": (I, [C.POINTER(U64)]),
+        "MPIX_Allreduce_enqueue": (I, [P, P, I, I, I, P]),
+        "MPIX_Launch_count": (U64, []),
+        "MPIX_Config_get": (I, [C.POINTER(U64), C.POINTER(I), C.POINTER(I), C.POINTER(U64)]),
+        "MPIX_Comm_get_ctx": (I, [P, C.POINTER(U32)]),
+        "MPIX_Comm_is_enqueue": (I, [P, C.POINTER(I)]),
+        "MPIX_Type_size": (I, [I]),
+        "MPIX_Version": (C.c_char_p, []),
+        "MPIXT_Fill_pattern": (I, [P, U64, U32, U32, P]),
+        "MPIXT_Checksum": (I, [P, U64, P, P]),
+        "MPIXT_Saxpy": (I, [I, C.c_float, P, P, P]),
+        "MPIXT_Delay": (I, [U64, P]),
+        "MPIXT_Empty": (I, [P]),
+        "MPIXT_Fill_f32": (I, [P, U64, C.c_float, P]),
+        "MPIXT_Halo_pack": (I, [P, I, I, I, I, P, P]),
+        "MPIXT_Halo_unpack": (I, [P, I, I, I, I, P, P]),
+        "MPIXT_Stencil7": (I, [P, P, I, I, I, C.c_float, C.c_float, P]),
+        "MPIXT_Launch_count": (U64, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+
+
+# Symbols declared by include/mpix.h and include/mpix_testing.h (checked by
+# tests/test_abi.py against the headers).
+def exported_symbols() -> List[str]:
+    import re
+    out = []
+    root = os.path.dirname(_HERE)
+    for h in ("mpix.h", "mpix_testing.h"):
+        txt = open(os.path.join(root, "include", h)).read()
+        out += re.findall(r"^\s*(?:const\s+char\s*\*|int|uint64_t)\s+\**(MPIX?T?_\w+)\s*\(", txt, re.M)
+    return out
+
+
+def error_string(code: int) -> str:
+    return lib().MPIX_Error_string(code).decode()
+
+
+def check(rc: int, where: str = "") -> None:
+    if rc != MPI_SUCCESS:
+        raise MPIXError(rc, where)
+
+
+def type_size(dt: int) -> int:
+    return lib().MPIX_Type_size(dt)
+
+
+def launch_count() -> int:
+    return lib().MPIX_Launch_count() + lib().MPIXT_Launch_count()
+
+
+def config() -> dict:
+    e, o = C.c_uint64(), C.c_uint64()
+    r, m = C.c_int(), C.c_int()
+    check(lib().MPIX_Config_get(C.byref(e), C.byref(r), C.byref(m), C.byref(o)))
+    return {"eager_bytes": e.value, "ring_slots": r.value, "max_ctas": m.value,
+            "oneshot_max_bytes": o.value}
+
+
+def _ptr(buf) -> int:
+    """Device address of a torch tensor, or an int address."""
+    if buf is None:
+        return 0
+    if isinstance(buf, int):
+        return buf
+    return buf.data_ptr()
+
+
+def _stream_handle(s) -> int:
+    if s is None:
+        return 0
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream  # torch.cuda.Stream
+
+
+# --- Info ---------------------------------------------------------------------
+class Info:
+    """MPI_Info with MPIX_Info_set_hex (info.cpp:37-59)."""
+
+    def __init__(self, **kv):
+        h = C.c_void_p()
+        check(lib().MPI_Info_create(C.byref(h)), "MPI_Info_create")
+        self.h = h
+        for k, v in kv.items():
+            self.set(k, v)
+
+    def set(self, key: str, value: str) -> None:
+        check(lib().MPI_Info_set(self.h, key.encode(), value.encode()), "MPI_Info_set")
+
+    def set_hex(self, key: str, value: bytes) -> None:
+        b = C.create_string_buffer(bytes(value), max(1, len(value)))
+        check(lib().MPIX_Info_set_hex(self.h, key.encode(), b, len(value)), "MPIX_Info_set_hex")
+
+    def get(self, key: str) -> Optional[str]:
+        buf = C.create_string_buffer(4096)
+        flag = C.c_int()
+        check(lib().MPI_Info_get(self.h, key.encode(), 4096, buf, C.byref(flag)))
+        return buf.value.decode() if flag.value else None
+
+    def get_hex(self, key: str) -> bytes:
+        n = C.c_int()
+        check(lib().MPIX_Info_get_hex(self.h, key.encode(), None, 0, C.byref(n)), "get_hex")
+        buf = C.create_string_buffer(max(1, n.value))
+        check(lib().MPIX_Info_get_hex(self.h, key.encode(), buf, n.value, C.byref(n)), "get_hex")
+        return buf.raw[: n.value]
+
+    def free(self) -> None:
+        if self.h:
+            check(lib().MPI_Info_free(C.byref(self.h)))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def cuda_stream_info(stream) -> Info:
+    """info{type="cudaStream_t", value=hex(stream)} — PAPER.md:839-840."""
+    info = Info(type="cudaStream_t")
+    info.set_hex("value", _stream_handle(stream).to_bytes(C.sizeof(C.c_void_p), "little"))
+    return info
+
+
+# --- Streams ---------------------------------------------------------------------
+class Stream:
+    """MPIX_Stream (proc_stream.cpp:7-60)."""
+
+    def __init__(self, info: Optional[Info] = None, _keep=None):
+        h = C.c_void_p()
+        check(lib().MPIX_Stream_create(info.h if info else None, C.byref(h)), "MPIX_Stream_create")
+        self.h = h
+        self._keep = _keep  # the torch stream object, kept alive
+
+    @classmethod
+    def from_cuda(cls, torch_stream) -> "Stream":
+        return cls(cuda_stream_info(torch_stream), _keep=torch_stream)
+
+    def free(self) -> None:
+        check(lib().MPIX_Stream_free(C.byref(self.h)), "MPIX_Stream_free")
+
+
+NULL_STREAM = None
+
+
+# --- Communicators -----------------------------------------------------------------
+class Request:
+    __slots__ = ("h",)
+
+    def __init__(self, h: int):
+        self.h = h
+
+
+class Comm:
+    """One rank's view of a communicator (CommH, comm.hpp:38-41)."""
+
+    def __init__(self, h: C.c_void_p):
+        self.h = h
+
+    @property
+    def rank(self) -> int:
+        r = C.c_int()
+        check(lib().MPI_Comm_rank(self.h, C.byref(r)))
+        return r.value
+
+    @property
+    def size(self) -> int:
+        r = C.c_int()
+        check(lib().MPI_Comm_size(self.h, C.byref(r)))
+        return r.value
+
+    @property
+    def ctx(self) -> int:
+        r = C.c_uint32()
+        check(lib().MPIX_Comm_get_ctx(self.h, C.byref(r)))
+        return r.value
+
+    @property
+    def is_enqueue(self) -> bool:
+        r = C.c_int()
+        check(lib().MPIX_Comm_is_enqueue(self.h, C.byref(r)))
+        return bool(r.value)
+
+    # collective ------------------------------------------------------------------
+    def stream_comm_create(self, stream: Optional[Stream]) -> "Comm":
+        out = C.c_void_p()
+        check(lib().MPIX_Stream_comm_create(self.h, stream.h if stream else None, C.byref(out)),
+              "MPIX_Stream_comm_create")
+        return Comm(out)
+
+    def stream_comm_create_multiplex(self, streams: Sequence[Optional[Stream]]) -> "Comm":
+        arr = (C.c_void_p * max(1, len(streams)))(*[s.h.value if s else None for s in streams])
+        out = C.c_void_p()
+        check(lib().MPIX_Stream_comm_create_multiplex(self.h, len(streams), arr, C.byref(out)),
+              "MPIX_Stream_comm_create_multiplex")
+        return Comm(out)
+
+    def barrier(self) -> None:
+        check(lib().MPI_Barrier(self.h), "MPI_Barrier")
+
+    def free(self) -> None:
+        check(lib().MPI_Comm_free(C.byref(self.h)), "MPI_Comm_free")
+
+    # enqueue ---------------------------------------------------------------------
+    def send_enqueue(self, buf, count: int, dt: int, dest: int, tag: int) -> None:
+        check(lib().MPIX_Send_enqueue(_ptr(buf), count, dt, dest, tag, self.h), "MPIX_Send_enqueue")
+
+    def recv_enqueue(self, buf, count: int, dt: int, source: int, tag: int) -> None:
+        check(lib().MPIX_Recv_enqueue(_ptr(buf), count, dt, source, tag, self.h, None),
+              "MPIX_Recv_enqueue")
+
+    def isend_enqueue(self, buf, count: int, dt: int, dest: int, tag: int) -> Request:
+        r = C.c_uint64()
+        check(lib().MPIX_Isend_enqueue(_ptr(buf), count, dt, dest, tag, self.h, C.byref(r)),
+              "MPIX_Isend_enqueue")
+        return Request(r.value)
+
+    def irecv_enqueue(self, buf, count: int, dt: int, source: int, tag: int) -> Request:
+        r = C.c_uint64()
+        check(lib().MPIX_Irecv_enqueue(_ptr(buf), count, dt, source, tag, self.h, C.byref(r)),
+              "MPIX_Irecv_enqueue")
+        return Request(r.value)
+
+    def allreduce_enqueue(self, sendbuf, recvbuf, count: int, dt: int, op: int = MPI_SUM) -> None:
+        sb = 1 if sendbuf == "in_place" else _ptr(sendbuf)
+        check(lib().MPIX_Allreduce_enqueue(sb, _ptr(recvbuf), count, dt, op, self.h),
+              "MPIX_Allreduce_enqueue")
+
+
+def wait_enqueue(req: Request) -> None:
+    h = C.c_uint64(req.h if req else 0)
+    check(lib().MPIX_Wait_enqueue(C.byref(h), None), "MPIX_Wait_enqueue")
+
+
+def waitall_enqueue(reqs: Sequence[Optional[Request]]) -> None:
+    arr = (C.c_uint64 * max(1, len(reqs)))(*[(r.h if r else 0) for r in reqs])
+    check(lib().MPIX_Waitall_enqueue(len(reqs), arr, None), "MPIX_Waitall_enqueue")
+
+
+# --- World ------------------------------------------------------------------------
+class World:
+    """N ranks in this process, rank r on GPU devices[r] (world.hpp:132-159)."""
+
+    def __init__(self, nranks: int, devices: Optional[Sequence[int]] = None):
+        arr = (C.c_int * nranks)(*devices) if devices is not None else None
+        check(lib().MPIX_World_init(nranks, arr), "MPIX_World_init")
+        self.n = nranks
+        self.devices = list(devices) if devices is not None else None
+
+    def comm(self, rank: int) -> Comm:
+        h = C.c_void_p()
+        check(lib().MPIX_World_comm(rank, C.byref(h)), "MPIX_World_comm")
+        return Comm(h)
+
+    def run_ranks(self, fn: Callable[[int], object]) -> list:
+        """fn(rank) once per rank on its own thread; re-raises the first error
+        (proj/src/world.cpp:78-84)."""
+        out = [None] * self.n
+        errs = []
+
+        def body(r):
+            try:
+                out[r] = fn(r)
+            except BaseException as e:  # noqa: BLE001
+                errs.append(e)
+
+        ts = [threading.Thread(target=body, args=(r,)) for r in range(self.n)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if errs:
+            raise errs[0]
+        return out
+
+    def finalize(self) -> None:
+        check(lib().MPIX_World_finalize(), "MPIX_World_finalize")
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.finalize()
+
+
+# --- test/bench helper kernels (include/mpix_testing.h) ---------------------------
+class testing:
+    @staticmethod
+    def fill_pattern(buf, nbytes: int, seed: int, it: int, stream) -> None:
+        check(lib().MPIXT_Fill_pattern(_ptr(buf), nbytes, seed, it, _stream_handle(stream)))
+
+    @staticmethod
+    def checksum(buf, nbytes: int, out_dev, stream) -> None:
+        check(lib().MPIXT_Checksum(_ptr(buf), nbytes, _ptr(out_dev), _stream_handle(stream)))
+
+    @staticmethod
+    def saxpy(n: int, a: float, x, y, stream) -> None:
+        check(lib().MPIXT_Saxpy(n, a, _ptr(x), _ptr(y), _stream_handle(stream)))
+
+    @staticmethod
+    def delay(ns: int, stream) -> None:
+        check(lib().MPIXT_Delay(ns, _stream_handle(stream)))
+
+    @staticmethod
+    def empty(stream) -> None:
+        check(lib().MPIXT_Empty(_stream_handle(stream)))
+
+    @staticmethod
+    def fill_f32(x, n: int, v: float, stream) -> None:
+        check(lib().MPIXT_Fill_f32(_ptr(x), n, v, _stream_handle(stream)))
+
+    @staticmethod
+    def halo_pack(u, nx, ny, nz, face, buf, stream) -> None:
+        check(lib().MPIXT_Halo_pack(_ptr(u), nx, ny, nz, face, _ptr(buf), _stream_handle(stream)))
+
+    @staticmethod
+    def halo_unpack(u, nx, ny, nz, face, buf, stream) -> None:
+        check(lib().MPIXT_Halo_unpack(_ptr(u), nx, ny, nz, face, _ptr(buf), _stream_handle(stream)))
+
+    @staticmethod
+    def stencil7(u, out, nx, ny, nz, w0, w1, stream) -> None:
+        check(lib().MPIXT_Stencil7(_ptr(u), _ptr(out), nx, ny, nz, w0, w1, _stream_handle(stream)))
