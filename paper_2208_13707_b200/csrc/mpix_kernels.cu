@@ -284,7 +284,6 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   __shared__ int s_phase;  // 0 = decided, 1 = need eager copy
-  __shared__ Snap s_snap;
   if (warp == 0) {
     Snap sn;
     int j = warp_scan(a.scan_ring, a.R, a.key, &sn);
@@ -372,7 +371,6 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
       __syncwarp();
     }
   }
-  (void)s_snap;
   __syncthreads();
 }
 
