@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""bench.py — MPIX-stream GPU-enqueue path on B200 (arXiv 2208.13707).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mpix|reference]
+
+Headline (N=1, BASELINE.json config 2 at one GPU, SURVEY.md §8d cfg2 "1 GPU:
+loopback self-messages on one stream"): a step is one 256 MiB message sent
+and received by the same rank on one CUDA stream through
+MPIX_Isend_enqueue + MPIX_Irecv_enqueue + MPIX_Waitall_enqueue. `value` is
+message bytes delivered per second (GB/s), device-timed with CUDA events.
+The dominant kernel is the receive kernel that pulls the payload (2*S bytes
+of HBM traffic per launch: read + write).
+
+N>1 (torchrun): the world is one process driving N GPUs (the reference's
+World/run_ranks model); torchrun rank 0 hosts it, the other
+ranks join a barrier and exit. GPU pairs (0,1),(2,3).. stream 256 MiB
+messages; value = aggregate GB/s, time = max over GPUs of event time.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified streamix library compiled from its sources) on the same workload.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+MiB = 1 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mpix", choices=["mpix", "reference"])
+    ap.add_argument("--size", type=int, default=256 * MiB)
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------------
+# clocks (NVML) sampled over the soak + timed window
+# --------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+        0x2: "applications_clocks_setting", 0x10: "sync_boost",
+    }
+
+    def __init__(self, dev=0):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if self.ok:
+            self.stop_ev.set()
+            self.t.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# reference arm / cpu baseline
+# --------------------------------------------------------------------------
+def cpu_reference_selfmsg(size, budget_s, min_msgs=3):
+    """The unmodified reference (oracle/_ref) on the loopback workload: one
+    exec queue, isend+irecv+waitall_enqueue of `size` bytes per message."""
+    import numpy as np
+    from oracle import oracle as O
+    R = O.ref()
+    if R is None:
+        return None
+    src = np.random.default_rng(0).integers(0, 255, size, dtype=np.uint8)
+    dst = np.zeros_like(src)
+    R.ref_selfmsg(src.ctypes.data, dst.ctypes.data, size, 1, 0)  # warm
+    msgs, t = 0, 0.0
+    while t < budget_s or msgs < min_msgs:
+        t += R.ref_selfmsg(src.ctypes.data, dst.ctypes.data, size, 2, 0)
+        msgs += 2
+    assert (dst == src).all()
+    return {"value": size * msgs / t / 1e9, "unit": "GB/s", "cores": 2, "kind": "reference",
+            "sample": f"{msgs} x {size >> 20} MiB self-messages (isend+irecv+waitall_enqueue) "
+                      f"through the compiled reference, 1 rank = driver thread + queue worker, "
+                      f"{t:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import oracle as O
+    R = O.ref()
+    if R is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    size = args.size
+    n = args.gpus
+    src = np.random.default_rng(0).integers(0, 255, size, dtype=np.uint8)
+    dst = np.zeros_like(src)
+    if n == 1:
+        step = lambda: R.ref_selfmsg(src.ctypes.data, dst.ctypes.data, size, 1, 0)
+        units_per_step = size
+        workload = "loopback Isend/Irecv/Waitall_enqueue self-message, 1 rank"
+        cores = 2
+    else:
+        # pairs exchange: P ranks, rank 2i -> 2i+1 (composed with the
+        # reference's own ping-pong driver: one message each way per step)
+        x = src
+        f0, f1 = C.c_uint64(), C.c_uint64()
+        pairs = n // 2
+        def step():
+            t = 0.0
+            for _ in range(pairs):
+                t += R.ref_pingpong(x.ctypes.data, size, 1, C.byref(f0), C.byref(f1)) / 2
+            return t
+        units_per_step = size * pairs
+        workload = f"{pairs} pair(s) x one {size >> 20} MiB message"
+        cores = 2 * 2
+    for _ in range(args.warmup):
+        step()
+    t = sum(step() for _ in range(args.steps))
+    v = units_per_step * args.steps / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": workload, "message_bytes": size, "host": "CPU (reference streamix)"},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} steps of {workload}"},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def run_mpix(args):
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()  # rank 0 hosts the N-GPU world
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+        dist.barrier()
+    try:
+        line = bench_world(args)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+    print(json.dumps(line))
+
+
+def bench_world(args):
+    import torch
+
+    from paper_2208_13707_b200 import mpix
+    n = args.gpus
+    S = args.size
+    ndev = torch.cuda.device_count()
+    assert ndev >= n, f"need {n} GPUs, see {ndev}"
+    pk = peaks()
+    P = n
+    w = mpix.World(P, list(range(P)))
+    ctx = {}
+
+    def setup(r):
+        with torch.cuda.device(r):
+            s = torch.cuda.Stream(device=r)
+        ms = mpix.Stream.from_cuda(s)
+        c = w.comm(r).stream_comm_create(ms)
+        ctx[r] = (s, ms, c)
+
+    w.run_ranks(setup)
+    # buffers (> L2: every step streams from HBM)
+    src, dst = {}, {}
+    for r in range(P):
+        src[r] = torch.empty(S, dtype=torch.uint8, device=r)
+        dst[r] = torch.zeros(S, dtype=torch.uint8, device=r)
+        mpix.testing.fill_pattern(src[r], S, 1234 + r, 0, ctx[r][0])
+    for r in range(P):
+        torch.cuda.synchronize(r)
+
+    if P == 1:
+        senders, pairs = [0], [(0, 0)]
+    else:
+        pairs = [(2 * i, 2 * i + 1) for i in range(P // 2)]
+        senders = [a for a, _ in pairs]
+    Ktag = 0
+
+    def step(ev=None):
+        """One message per pair. P=1: loopback on one stream."""
+        nonlocal Ktag
+        Ktag = (Ktag + 1) % 30000
+        for a, b in pairs:
+            sa, _, ca = ctx[a]
+            sb, _, cb = ctx[b]
+            ra = ca.isend_enqueue(src[a], S, mpix.MPI_BYTE, b, Ktag)
+            if ev is not None:
+                ev[0].record(sb)
+            rb = cb.irecv_enqueue(dst[b], S, mpix.MPI_BYTE, a, Ktag)
+            if ev is not None:
+                ev[1].record(sb)
+            if a == b:
+                mpix.waitall_enqueue([ra, rb])
+            else:
+                mpix.wait_enqueue(ra)
+                mpix.wait_enqueue(rb)
+
+    def sync():
+        for r in range(P):
+            torch.cuda.synchronize(r)
+
+    # correctness of the measured path (same inputs as the timed loop)
+    step()
+    sync()
+    for a, b in pairs:
+        assert torch.equal(dst[b], src[a].to(b)), "payload mismatch"
+
+    clocks = ClockSampler(0)
+    clocks.start()
+    for _ in range(args.warmup):
+        step()
+    sync()
+    # soak so that the clock sampler sees the step under load (~0.5 s)
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < 0.5:
+        for _ in range(10):
+            step()
+        sync()
+
+    # ---- timed region: K steps, events on every stream, max over GPUs ----
+    starts = {r: torch.cuda.Event(enable_timing=True) for r in range(P)}
+    ends = {r: torch.cuda.Event(enable_timing=True) for r in range(P)}
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    sync()
+    l0 = mpix.launch_count()
+    for r in range(P):
+        starts[r].record(ctx[r][0])
+    for k in range(args.steps):
+        step(kev[k])
+    for r in range(P):
+        ends[r].record(ctx[r][0])
+    sync()
+    launches = mpix.launch_count() - l0
+    clk = clocks.stop()
+    ms = max(starts[r].elapsed_time(ends[r]) for r in range(P))
+    t_step = ms / 1e3 / args.steps
+    value = S * len(pairs) / t_step / 1e9
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+
+    # roofline of the dominant kernel (the receive kernel that moves the payload)
+    if P == 1:
+        alg_bytes = 2 * S
+        peak = pk.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "unit": "GB/s", "peak_source": "MEASURED_PEAKS.json hbm_gbs"
+                if "hbm_gbs" in pk else "fallback 6650 GB/s (B200_PROFILING.md)"}
+    else:
+        alg_bytes = S
+        peak = 770.0
+        roof = {"bound": "nvlink", "unit": "GB/s",
+                "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"}
+    achieved = alg_bytes / (k_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"p2p_recv_{S}")
+        except Exception:
+            traffic = None
+    roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
+                 "kernel": "mpix::k_p2p (receive side, pull copy)",
+                 "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg_bytes})
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = e2e_pass(args, mpix, torch, ctx, pairs, src, dst, S)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {
+            "workload": ("loopback: Isend/Irecv/Waitall_enqueue self-message on one stream, 1 GPU"
+                         if P == 1 else f"{len(pairs)} GPU pair(s), Isend/Irecv/Wait_enqueue"),
+            "message_bytes": S, "ranks": P, "parallelism": "none (messaging runtime)",
+            "l2": "inputs larger than L2 (src+dst = 2 x message > 126 MB)",
+            "baseline_config": "BASELINE.json configs[1] at one GPU (SURVEY.md §8d cfg2)",
+        },
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if not args.no_extras and P == 1:
+        line["extras"] = extras(args, mpix, torch, w, ctx)
+    if rank0_cpu():
+        line["cpu_baseline"] = cpu_reference_selfmsg(S, args.cpu_seconds)
+    sync()
+    w.finalize()
+    return line
+
+
+def rank0_cpu():
+    return dist_env()[0] == 0
+
+
+def e2e_pass(args, mpix, torch, ctx, pairs, src, dst, S):
+    """Same metric through the public API with HOST buffers: per step the
+    input message is copied H2D from pinned memory, sent/received through the
+    enqueue calls, a consumer kernel checksums the delivered payload, and the
+    8-byte checksum is read back on the host (stream synchronised)."""
+    host = {a: torch.empty(S, dtype=torch.uint8, pin_memory=True) for a, _ in pairs}
+    for a, _ in pairs:
+        host[a].copy_(src[a].cpu())
+    sums = {b: torch.zeros(1, dtype=torch.int64, device=b) for _, b in pairs}
+    hsum = {b: torch.zeros(1, dtype=torch.int64, pin_memory=True) for _, b in pairs}
+
+    def one(tag):
+        for a, b in pairs:
+            sa, _, ca = ctx[a]
+            sb, _, cb = ctx[b]
+            with torch.cuda.stream(sa):
+                src[a].copy_(host[a], non_blocking=True)
+            ra = ca.isend_enqueue(src[a], S, mpix.MPI_BYTE, b, 30000 + tag)
+            rb = cb.irecv_enqueue(dst[b], S, mpix.MPI_BYTE, a, 30000 + tag)
+            if a == b:
+                mpix.waitall_enqueue([ra, rb])
+            else:
+                mpix.wait_enqueue(ra)
+                mpix.wait_enqueue(rb)
+            mpix.testing.checksum(dst[b], S, sums[b], sb)
+            with torch.cuda.stream(sb):
+                hsum[b].copy_(sums[b], non_blocking=True)
+        for a, b in pairs:
+            ctx[a][0].synchronize()
+            ctx[b][0].synchronize()
+
+    for i in range(max(1, args.warmup)):
+        one(i % 1000)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        one(i % 1000)
+    t = time.perf_counter() - t0
+    return {"value": S * len(pairs) * args.steps / t / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": S * len(pairs), "d2h_bytes_per_step": 8 * len(pairs),
+            "timing": "host wall clock, stream synchronised every step"}
+
+
+def extras(args, mpix, torch, w, ctx):
+    """Secondary measurements on the same GPU (not the headline)."""
+    out = {}
+    s0, _, c0 = ctx[0]
+    big = torch.empty(1 << 30, dtype=torch.uint8, device=0)
+    big2 = torch.empty(1 << 30, dtype=torch.uint8, device=0)
+
+    def timed(fn, iters, stream):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(iters):
+            fn(i)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / 1e3 / iters
+
+    # launch floor: back-to-back empty kernels in one stream
+    t_empty = timed(lambda i=0: mpix.testing.empty(s0), 200, s0)
+    out["launch_floor_us"] = t_empty * 1e6
+
+    # loopback sweep (Isend/Irecv/Waitall on one stream)
+    sweep = {}
+    for sz in [8, 4096, 65536, 1 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30]:
+        it = 200 if sz <= (1 << 20) else (20 if sz <= (64 << 20) else 5)
+
+        def f(i=0, sz=sz):
+            r1 = c0.isend_enqueue(big, sz, mpix.MPI_BYTE, 0, 7)
+            r2 = c0.irecv_enqueue(big2, sz, mpix.MPI_BYTE, 0, 7)
+            mpix.waitall_enqueue([r1, r2])
+        t = timed(f, it, s0)
+        sweep[str(sz)] = {"us": t * 1e6, "GBps": sz / t / 1e9, "hbm_frac": 2 * sz / t / 1e9 /
+                          peaks().get("hbm_gbs", 6650.0)}
+    out["loopback_sweep"] = sweep
+
+    # in-stream latency: producer -> Send_enqueue -> Recv_enqueue -> consumer (8 B)
+    prod = torch.zeros(2, dtype=torch.int32, device=0)
+    cons = torch.zeros(2, dtype=torch.int32, device=0)
+
+    def chain(i=0):
+        mpix.testing.fill_f32(prod, 2, float(i), s0)
+        c0.send_enqueue(prod, 2, mpix.MPI_INT, 0, 9)
+        c0.recv_enqueue(cons, 2, mpix.MPI_INT, 0, 9)
+        mpix.testing.fill_f32(cons, 0, 0.0, s0)  # consumer kernel
+    t_chain = timed(chain, 200, s0)
+    out["inloop_self_chain_us"] = t_chain * 1e6
+    out["inloop_self_chain_over_floor_us"] = (t_chain - 4 * t_empty) * 1e6
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_mpix(args)
+
+
+if __name__ == "__main__":
+    main()
