@@ -265,6 +265,13 @@ int MPIX_Comm_get_ctx(MPI_Comm comm, uint32_t *ctx);
 int MPIX_Comm_is_enqueue(MPI_Comm comm, int *flag);
 /* Datatype width in bytes, or 0 if unknown. */
 int MPIX_Type_size(MPI_Datatype datatype);
+/* Watchdog word of a rank: 0 = healthy, else the first timeout a kernel
+ * recorded (1 slot wait, 2 completion wait, 3 collective barrier, 4 protocol)
+ * before exiting instead of hanging. Reading clears nothing. */
+int MPIX_Rank_error(int rank, uint64_t *code);
+/* Debug: this member's peer-mapped region of comm (device pointer) and its
+ * size; the layout is RegionLayout in csrc/mpix_internal.h. */
+int MPIX_Comm_region(MPI_Comm comm, void **base, uint64_t *bytes);
 /* Library build string (arch, version). */
 const char *MPIX_Version(void);
 

@@ -40,6 +40,12 @@ int MPIXT_Halo_unpack(float *u, int nx, int ny, int nz, int face, const float *b
  * w1*(sum of 6 neighbours); out's halo untouched. */
 int MPIXT_Stencil7(const float *u, float *out, int nx, int ny, int nz, float w0, float w1,
                    void *stream);
+/* Debug: device->host copy (synchronous), and the base/size of rank
+ * `comm`'s peer-mapped region of that communicator. */
+int MPIXT_Copy_to_host(void *host, const void *dev, uint64_t bytes);
+/* Load every helper kernel on the current device (called by
+ * MPIX_World_init; see lazy loading in DESIGN.md). */
+int MPIXT_Preload(void);
 /* Number of helper kernels launched so far. */
 uint64_t MPIXT_Launch_count(void);
 

@@ -103,8 +103,8 @@ struct alignas(64) OpRecord {
   uint64_t bytes;
   uint32_t counter;  // CTAs finished copying
   uint32_t nfin;
-  uint64_t fin_addr[6];  // completion stores, performed in order by the
-  uint64_t fin_val[6];   // last CTA with st.release.sys
+  uint64_t fin_addr[8];  // completion stores (k_fin): [0,2) slot frees,
+  uint64_t fin_val[8];   // [2,8) mirrors and done words
   uint64_t coll[2 * kMaxCollRanks];  // allreduce: peers' sbuf / rbuf
   uint64_t flags;
 };
@@ -176,11 +176,14 @@ struct ARArgs {
   uint64_t spin_limit_ns;
 };
 
-// Launchers implemented in mpix_kernels.cu (host side).
-cudaError_t launch_p2p(const P2PArgs& a, int grid, cudaStream_t s);
-cudaError_t launch_wait(const WaitArgs& a, cudaStream_t s);
-cudaError_t launch_allreduce(const ARArgs& a, int grid, cudaStream_t s);
-int p2p_occupancy();
-int allreduce_occupancy();
+// Launchers implemented in mpix_kernels.cu (host side). Each returns the
+// number of kernels launched, or -1 on a CUDA error. `sys` selects
+// system-scope primitives (some peer lives on another GPU).
+int launch_p2p(const P2PArgs& a, bool sys, bool inline_copy, uint64_t copy_grid, cudaStream_t s);
+int launch_wait(const WaitArgs& a, bool sys, cudaStream_t s);
+int launch_allreduce(const ARArgs& a, bool sys, uint64_t reduce_grid, cudaStream_t s);
+uint64_t p2p_copy_grid(uint64_t bytes);
+uint64_t ar_reduce_grid(uint64_t work_bytes);
+int preload_kernels();
 
 }  // namespace mpix

@@ -1,160 +1,209 @@
 // mpix_kernels.cu — sm_100a kernels of the MPIX-stream GPU-enqueue path.
 //
-// One kernel per enqueued operation, launched into the user's CUDA stream:
+// Point-to-point (Send/Isend/Recv/Irecv_enqueue). Replaces the reference's
+// queue worker running post_send/post_recv/wait closures
+// (proj/src/proc_enqueue.cpp:30-114, proj/src/proc_p2p.cpp:27-94) and its
+// matching/progress engine (proj/src/endpoint.cpp:15-69,
+// proj/src/fabric.cpp:93-110):
 //
-//   k_p2p       Send/Isend/Recv/Irecv_enqueue. Replaces the reference's queue
-//               worker running post_send/post_recv/wait closures
-//               (proj/src/proc_enqueue.cpp:30-114, proj/src/proc_p2p.cpp:27-94)
-//               and its matching/progress engine (proj/src/endpoint.cpp:15-69,
-//               proj/src/fabric.cpp:93-110). CTA 0, warp 0 runs the handshake
-//               on descriptor rings in peer-mapped memory; the copy (push or
-//               pull, 128-bit vectors, grid-stride) is spread over the grid.
-//   k_wait      Wait/Waitall_enqueue: spins on local completion words
-//               (replaces proj/src/proc_enqueue.cpp:116-141).
-//   k_allreduce Allreduce_enqueue (no reference): one-shot / two-shot P2P
-//               reduce over peer buffers, rank-ordered fp32/fp64/int32 folds.
+//   k_proto  1 CTA. Warp 0 runs the handshake on the descriptor rings in
+//            peer-mapped memory (scan, post, fence, rescan, CAS). Messages up
+//            to the inline limit are also copied and completed here, so a
+//            small message costs exactly one launch.
+//   k_copy   large messages only; launched with programmatic dependent launch
+//            right behind k_proto, never spins: every CTA reads the decision
+//            and streams one 16-KiB tile (128-bit loads/stores, 4 in flight
+//            per thread), push to or pull from the peer's buffer.
+//   k_fin    1 CTA, PDL: completion stores (slot frees, free-mirrors, done
+//            words) after the whole copy grid retired; publishes staged
+//            blocking sends.
+//   k_wait   Wait/Waitall_enqueue: spins on local completion words.
 //
-// Memory-model conventions: descriptor states and completion words are
-// 64-bit, written with st.release.sys and read with ld.acquire.sys; the
-// post->scan step of each side is separated by fence.sc.sys so that at least
-// one of the two sides sees the other's descriptor (store-buffering litmus).
+// Allreduce_enqueue (no reference): k_ar_entry (1 CTA: publish buffers,
+// wait for every peer) -> k_ar_reduce (wide, rank-ordered fold, one-shot or
+// two-shot over peer pointers) -> k_ar_exit (1 CTA: exit barrier).
+//
+// Only 1-CTA kernels ever spin, so any number of ranks sharing a GPU (and
+// the user's own streams) always make progress.
+//
+// Scope: every primitive is templated on SYS. Ranks on the same GPU use
+// .gpu scope (fence ~0.2 us); ranks on different GPUs use .sys scope
+// (fence/release/CAS ~1.7-1.9 us on B200, tools/copybench.cu), so the
+// protocol keeps system-scope fences to two per side on the critical path.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <utility>
 
 #include "mpix_internal.h"
 
 namespace mpix {
 
 // ---------------------------------------------------------------------------
-// PTX helpers
+// Scoped memory primitives
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t cas_sys(uint64_t* p, uint64_t cmp, uint64_t val) {
-  uint64_t old;
-  asm volatile("atom.acq_rel.sys.global.cas.b64 %0, [%1], %2, %3;"
-               : "=l"(old)
-               : "l"(p), "l"(cmp), "l"(val)
-               : "memory");
-  return old;
-}
-__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void fence_sc_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
-__device__ __forceinline__ void fence_acq_rel_sys() {
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
-}
+#define MPIX_DEFINE_SCOPE(NAME, SC)                                                               \
+  struct NAME {                                                                                   \
+    static __device__ __forceinline__ uint64_t ld_acq(const uint64_t* p) {                        \
+      uint64_t v;                                                                                 \
+      asm volatile("ld.acquire." SC ".global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");     \
+      return v;                                                                                   \
+    }                                                                                             \
+    static __device__ __forceinline__ uint64_t ld_rlx(const uint64_t* p) {                        \
+      uint64_t v;                                                                                 \
+      asm volatile("ld.relaxed." SC ".global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");     \
+      return v;                                                                                   \
+    }                                                                                             \
+    static __device__ __forceinline__ void st_rel(uint64_t* p, uint64_t v) {                      \
+      asm volatile("st.release." SC ".global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");       \
+    }                                                                                             \
+    static __device__ __forceinline__ void st_rlx(uint64_t* p, uint64_t v) {                      \
+      asm volatile("st.relaxed." SC ".global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");       \
+    }                                                                                             \
+    static __device__ __forceinline__ uint64_t cas(uint64_t* p, uint64_t c, uint64_t v) {         \
+      uint64_t o;                                                                                 \
+      asm volatile("atom.acq_rel." SC ".global.cas.b64 %0, [%1], %2, %3;"                       \
+                   : "=l"(o)                                                                      \
+                   : "l"(p), "l"(c), "l"(v)                                                       \
+                   : "memory");                                                                   \
+      return o;                                                                                   \
+    }                                                                                             \
+    static __device__ __forceinline__ void fence_sc() { asm volatile("fence.sc." SC ";" ::: "memory"); } \
+    static __device__ __forceinline__ void fence_ar() {                                           \
+      asm volatile("fence.acq_rel." SC ";" ::: "memory");                                        \
+    }                                                                                             \
+  };
+MPIX_DEFINE_SCOPE(ScopeSys, "sys")
+MPIX_DEFINE_SCOPE(ScopeGpu, "gpu")
+#undef MPIX_DEFINE_SCOPE
+
+template <bool SYS>
+struct Scope;
+template <>
+struct Scope<true> : ScopeSys {};
+template <>
+struct Scope<false> : ScopeGpu {};
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
-// Error codes written to the per-rank error word (host-mapped) on watchdog
-// expiry. The kernel then exits instead of hanging the GPU.
-enum : uint64_t {
-  ERRW_WAIT_SLOT = 1,
-  ERRW_WAIT_DONE = 2,
-  ERRW_WAIT_COLL = 3,
-  ERRW_PROTOCOL = 4,
-};
+enum : uint64_t { ERRW_WAIT_SLOT = 1, ERRW_WAIT_DONE = 2, ERRW_WAIT_COLL = 3, ERRW_PROTOCOL = 4 };
 
-// Spin until *p >= target (acquire, system scope). Returns false on watchdog
-// expiry after recording `code`.
+// Spin until *p >= target. Returns false on watchdog expiry after recording
+// `code` in the rank's host-mapped error word (the kernel then exits rather
+// than hanging the GPU).
+template <bool SYS>
 __device__ __noinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_t* err_word,
                                      uint64_t limit_ns, uint64_t code) {
-  if (ld_acquire_sys(p) >= target) return true;
+  using M = Scope<SYS>;
+  if (M::ld_acq(p) >= target) return true;
   uint64_t t0 = limit_ns ? globaltimer() : 0;
   unsigned ns = 32;
-  while (ld_acquire_sys(p) < target) {
+  while (M::ld_acq(p) < target) {
     __nanosleep(ns);
     if (ns < 256) ns <<= 1;
     if (limit_ns && globaltimer() - t0 > limit_ns) {
-      if (err_word) st_relaxed_sys(err_word, code);
+      if (err_word) ScopeSys::st_rlx(err_word, code);
       return false;
     }
   }
   return true;
 }
 
+__device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
 // ---------------------------------------------------------------------------
-// Copy: 128-bit vectors, UNROLL loads in flight per thread, grid-stride over
-// `nparts` cooperating CTAs. Handles co-aligned heads/tails; falls back to a
-// byte loop when source and destination disagree modulo 16.
+// Copies
 // ---------------------------------------------------------------------------
-template <int UNROLL>
-__device__ __forceinline__ void copy_vec(uint4* __restrict__ dst, const uint4* __restrict__ src,
-                                         uint64_t nvec, uint64_t t, uint64_t nt) {
-  uint64_t i = t;
-  for (; i + (UNROLL - 1) * nt < nvec; i += UNROLL * nt) {
-    uint4 v[UNROLL];
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) v[u] = src[i + u * nt];
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) dst[i + u * nt] = v[u];
+constexpr int kCopyThreads = 256;
+constexpr int kCopyUnroll = 4;
+constexpr uint64_t kTileVec = (uint64_t)kCopyThreads * kCopyUnroll;  // 16-B vectors per tile
+
+// Whole-CTA copy of n bytes (k_proto inline path and the rare staged push).
+__device__ void cta_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
+  if (n == 0 || dst == src) return;
+  const uint64_t t = threadIdx.x, nt = blockDim.x;
+  uint64_t mis = (uint64_t)dst & 15;
+  if ((((uint64_t)src) & 15) != mis) {
+    for (uint64_t i = t; i < n; i += nt) dst[i] = src[i];
+    return;
   }
-  for (; i < nvec; i += nt) dst[i] = src[i];
+  uint64_t head = mis ? umin(16 - mis, n) : 0;
+  if (t < head) dst[t] = src[t];
+  uint64_t nvec = (n - head) >> 4;
+  uint4* d = reinterpret_cast<uint4*>(dst + head);
+  const uint4* s = reinterpret_cast<const uint4*>(src + head);
+  uint64_t i = t;
+  for (; i + 3 * nt < nvec; i += 4 * nt) {
+    uint4 v0 = s[i], v1 = s[i + nt], v2 = s[i + 2 * nt], v3 = s[i + 3 * nt];
+    d[i] = v0; d[i + nt] = v1; d[i + 2 * nt] = v2; d[i + 3 * nt] = v3;
+  }
+  for (; i < nvec; i += nt) d[i] = s[i];
+  uint64_t done = head + (nvec << 4);
+  if (t < n - done) dst[done + t] = src[done + t];
 }
 
-__device__ void part_copy(uint8_t* dst, const uint8_t* src, uint64_t n, uint64_t part,
-                          uint64_t nparts) {
+// One tile of a grid-wide copy: CTA `tile` moves vectors
+// [tile*kTileVec, (tile+1)*kTileVec) after the co-aligned head; extra tiles
+// (grid sized from a receive capacity larger than the message) loop nothing.
+__device__ __forceinline__ void tile_copy(uint8_t* dst, const uint8_t* src, uint64_t n,
+                                          uint64_t tile, uint64_t ntiles) {
   if (n == 0 || dst == src) return;
-  const uint64_t t = part * blockDim.x + threadIdx.x;
-  const uint64_t nt = nparts * blockDim.x;
   uint64_t mis = (uint64_t)dst & 15;
-  if ((((uint64_t)src) & 15) == mis) {
-    uint64_t head = mis ? (16 - mis) : 0;
-    if (head > n) head = n;
-    if (t < head) dst[t] = src[t];
-    uint64_t nvec = (n - head) >> 4;
-    copy_vec<4>(reinterpret_cast<uint4*>(dst + head),
-                reinterpret_cast<const uint4*>(src + head), nvec, t, nt);
-    uint64_t done = head + (nvec << 4);
-    uint64_t tail = n - done;
-    if (t < tail) dst[done + t] = src[done + t];
-  } else {
+  if ((((uint64_t)src) & 15) != mis) {  // not co-aligned: byte loop over the grid
+    uint64_t t = tile * blockDim.x + threadIdx.x, nt = ntiles * blockDim.x;
     for (uint64_t i = t; i < n; i += nt) dst[i] = src[i];
+    return;
+  }
+  uint64_t head = mis ? umin(16 - mis, n) : 0;
+  uint64_t nvec = (n - head) >> 4;
+  if (tile == 0 && threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
+  uint64_t done = head + (nvec << 4);
+  if (tile == 0 && threadIdx.x < n - done) dst[done + threadIdx.x] = src[done + threadIdx.x];
+  uint4* d = reinterpret_cast<uint4*>(dst + head);
+  const uint4* s = reinterpret_cast<const uint4*>(src + head);
+  for (uint64_t t = tile; t * kTileVec < nvec; t += ntiles) {
+    uint64_t base = t * kTileVec + threadIdx.x;
+    if (base + (kCopyUnroll - 1) * kCopyThreads < nvec) {
+      uint4 v[kCopyUnroll];
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) v[u] = s[base + u * kCopyThreads];
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) d[base + u * kCopyThreads] = v[u];
+    } else {
+      for (int u = 0; u < kCopyUnroll; ++u) {
+        uint64_t i = base + u * kCopyThreads;
+        if (i < nvec) d[i] = s[i];
+      }
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // Descriptor-ring scan (warp 0). Returns the slot index and a consistent
-// snapshot (seqlock on the state word, which carries the pair sequence so it
-// never repeats), or -1.
+// snapshot, or -1. Relaxed loads filter; the candidate is validated seqlock
+// style (the state word carries the pair sequence, so it never repeats).
 // ---------------------------------------------------------------------------
 struct Snap {
   uint64_t state, key, addr, bytes, done_addr, done_val;
 };
 
+template <bool SYS>
 __device__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
+  using M = Scope<SYS>;
   const int lane = threadIdx.x & 31;
   for (int base = 0; base < R; base += 32) {
     int i = base + lane;
     bool hit = false;
     if (i < R) {
-      uint64_t st = ld_acquire_sys(&ring[i].state);
-      if ((st & 0xff) == ST_POSTED) hit = ld_relaxed_sys(&ring[i].key) == key;
+      uint64_t st = M::ld_rlx(&ring[i].state);
+      if ((st & 0xff) == ST_POSTED) hit = M::ld_rlx(&ring[i].key) == key;
     }
     unsigned m = __ballot_sync(0xffffffffu, hit);
     while (m) {
@@ -164,15 +213,14 @@ __device__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
       Snap sn = {};
       if (lane == src) {
         SlotDesc* s = &ring[i];
-        sn.state = ld_acquire_sys(&s->state);
-        sn.key = ld_relaxed_sys(&s->key);
-        sn.addr = ld_relaxed_sys(&s->addr);
-        sn.bytes = ld_relaxed_sys(&s->bytes);
-        sn.done_addr = ld_relaxed_sys(&s->done_addr);
-        sn.done_val = ld_relaxed_sys(&s->done_val);
-        fence_acq_rel_sys();
-        uint64_t st2 = ld_relaxed_sys(&s->state);
-        ok = (sn.state == st2) && ((sn.state & 0xff) == ST_POSTED) && sn.key == key;
+        sn.state = M::ld_acq(&s->state);
+        sn.key = M::ld_rlx(&s->key);
+        sn.addr = M::ld_rlx(&s->addr);
+        sn.bytes = M::ld_rlx(&s->bytes);
+        sn.done_addr = M::ld_rlx(&s->done_addr);
+        sn.done_val = M::ld_rlx(&s->done_val);
+        M::fence_ar();
+        ok = ((sn.state & 0xff) == ST_POSTED) && sn.key == key && M::ld_rlx(&s->state) == sn.state;
       }
       ok = __shfl_sync(0xffffffffu, ok, src);
       if (ok) {
@@ -189,60 +237,61 @@ __device__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
   return -1;
 }
 
-// Completion stores performed (in order, st.release.sys) after the copy.
+// Completion stores: group A (slot frees) then group B (free-mirrors and
+// done words), a fence before each group. A poster reuses a slot only after
+// seeing its mirror, so the FREE state must land first.
 struct Fin {
-  uint32_t n;
-  uint64_t addr[8];
-  uint64_t val[8];
-  __device__ void add(void* a, uint64_t v) {
-    if (a) {
-      addr[n] = (uint64_t)a;
-      val[n] = v;
-      ++n;
-    }
+  uint32_t na, nb;
+  uint64_t a_addr[2], a_val[2];
+  uint64_t b_addr[5], b_val[5];
+  __device__ void clear() { na = nb = 0; }
+  __device__ void add_a(void* p, uint64_t v) {
+    if (p) { a_addr[na] = (uint64_t)p; a_val[na] = v; ++na; }
   }
+  __device__ void add_b(void* p, uint64_t v) {
+    if (p) { b_addr[nb] = (uint64_t)p; b_val[nb] = v; ++nb; }
+  }
+  template <bool SYS>
   __device__ void run() const {
-    fence_sc_sys();
-    for (uint32_t k = 0; k < n; ++k) st_release_sys(reinterpret_cast<uint64_t*>(addr[k]), val[k]);
+    using M = Scope<SYS>;
+    M::fence_ar();
+    for (uint32_t k = 0; k < na; ++k) M::st_rlx(reinterpret_cast<uint64_t*>(a_addr[k]), a_val[k]);
+    M::fence_ar();
+    for (uint32_t k = 0; k < nb; ++k) M::st_rlx(reinterpret_cast<uint64_t*>(b_addr[k]), b_val[k]);
   }
 };
 
 struct Decision {
-  uint64_t action;
-  uint64_t src, dst, bytes;
+  uint64_t action, src, dst, bytes;
   Fin fin;
-  int wait_own;  // NONE + blocking receive: CTA 0 waits for my_done
-  int err;
+  int wait_own;
 };
 
-__device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { return a < b ? a : b; }
-
-// Posts my descriptor into post_ring[pseq % R] after the slot's previous
-// occupant is gone. Called by lane 0 of warp 0.
-__device__ bool post_desc(const P2PArgs& a, uint64_t addr, uint64_t bytes, uint64_t done_addr,
-                          uint64_t done_val) {
+template <bool SYS>
+__device__ void post_desc(const P2PArgs& a, uint64_t addr, uint64_t bytes, uint64_t done_addr,
+                          uint64_t done_val, bool others_wrote) {
+  using M = Scope<SYS>;
   const int slot = (int)(a.pseq % (uint64_t)a.R);
   SlotDesc* d = &a.post_ring[slot];
-  st_relaxed_sys(&d->key, a.key);
-  st_relaxed_sys(&d->addr, addr);
-  st_relaxed_sys(&d->bytes, bytes);
-  st_relaxed_sys(&d->done_addr, done_addr);
-  st_relaxed_sys(&d->done_val, done_val);
-  fence_sc_sys();  // payload (eager/staged) and fields before the state
-  st_release_sys(&d->state, st_word(a.pseq, ST_POSTED));
-  fence_sc_sys();  // Dekker: my post is visible before I rescan
-  return true;
+  M::st_rlx(&d->key, a.key);
+  M::st_rlx(&d->addr, addr);
+  M::st_rlx(&d->bytes, bytes);
+  M::st_rlx(&d->done_addr, done_addr);
+  M::st_rlx(&d->done_val, done_val);
+  if (others_wrote) M::fence_ar();  // payload written by other threads/CTAs
+  M::st_rel(&d->state, st_word(a.pseq, ST_POSTED));
+  M::fence_sc();  // Dekker: my post is visible before I rescan
 }
 
+template <bool SYS>
 __device__ bool wait_post_slot(const P2PArgs& a) {
   const int slot = (int)(a.pseq % (uint64_t)a.R);
   uint64_t need = a.pseq >= (uint64_t)a.R ? a.pseq - a.R + 1 : 0;
   if (need == 0) return true;
-  return spin_ge(&a.post_mirror[slot], need, a.err_word, a.spin_limit_ns, ERRW_WAIT_SLOT);
+  return spin_ge<SYS>(&a.post_mirror[slot], need, a.err_word, a.spin_limit_ns, ERRW_WAIT_SLOT);
 }
 
-// Send: my descriptor (if posted) at post_ring[slot]; the matched receive at
-// scan_ring[j] (snapshot r). Fills the push decision.
+// Sender wins: push src -> receiver's buffer.
 __device__ void send_win(const P2PArgs& a, Decision& dc, int j, const Snap& r, bool posted,
                          const uint8_t* src) {
   const uint64_t rpseq = r.state >> 8;
@@ -251,17 +300,19 @@ __device__ void send_win(const P2PArgs& a, Decision& dc, int j, const Snap& r, b
   dc.src = (uint64_t)src;
   dc.dst = r.addr;
   dc.bytes = umin(a.bytes, r.bytes);  // truncation: endpoint.cpp:17
-  dc.fin.n = 0;
-  dc.fin.add(&a.scan_ring[j].state, st_word(rpseq, ST_FREE));
-  if (posted) dc.fin.add(&a.post_ring[slot].state, st_word(a.pseq, ST_FREE));
-  dc.fin.add(&a.scan_mirror[j], rpseq + 1);
-  if (posted) dc.fin.add(&a.post_mirror[slot], a.pseq + 1);
-  dc.fin.add(reinterpret_cast<void*>(r.done_addr), r.done_val);
-  dc.fin.add(a.my_done, a.my_gen);
-  if (a.mode == MODE_STAGED) dc.fin.add(a.stage_done, a.stage_gen);
+  dc.fin.clear();
+  dc.fin.add_a(&a.scan_ring[j].state, st_word(rpseq, ST_FREE));
+  if (posted) dc.fin.add_a(&a.post_ring[slot].state, st_word(a.pseq, ST_FREE));
+  dc.fin.add_b(&a.scan_mirror[j], rpseq + 1);
+  // My slot pseq % R is consumed either way (posted, or skipped by the
+  // fast path after its previous occupant retired): advance its mirror.
+  dc.fin.add_b(&a.post_mirror[slot], a.pseq + 1);
+  dc.fin.add_b(reinterpret_cast<void*>(r.done_addr), r.done_val);
+  dc.fin.add_b(a.my_done, a.my_gen);
+  if (a.mode == MODE_STAGED) dc.fin.add_b(a.stage_done, a.stage_gen);
 }
 
-// Receive: the matched send at scan_ring[j] (snapshot s, already TAKEN by me).
+// Receiver wins (send descriptor already TAKEN by me): pull.
 __device__ void recv_win(const P2PArgs& a, Decision& dc, int j, const Snap& s, bool posted) {
   const uint64_t spseq = s.state >> 8;
   const int slot = (int)(a.pseq % (uint64_t)a.R);
@@ -269,63 +320,58 @@ __device__ void recv_win(const P2PArgs& a, Decision& dc, int j, const Snap& s, b
   dc.src = s.addr;
   dc.dst = (uint64_t)a.buf;
   dc.bytes = umin(s.bytes, a.bytes);
-  dc.fin.n = 0;
-  dc.fin.add(&a.scan_ring[j].state, st_word(spseq, ST_FREE));
-  if (posted) dc.fin.add(&a.post_ring[slot].state, st_word(a.pseq, ST_FREE));
-  dc.fin.add(&a.scan_mirror[j], spseq + 1);
-  if (posted) dc.fin.add(&a.post_mirror[slot], a.pseq + 1);
-  dc.fin.add(reinterpret_cast<void*>(s.done_addr), s.done_val);
-  dc.fin.add(a.my_done, a.my_gen);
+  dc.fin.clear();
+  dc.fin.add_a(&a.scan_ring[j].state, st_word(spseq, ST_FREE));
+  if (posted) dc.fin.add_a(&a.post_ring[slot].state, st_word(a.pseq, ST_FREE));
+  dc.fin.add_b(&a.scan_mirror[j], spseq + 1);
+  dc.fin.add_b(&a.post_mirror[slot], a.pseq + 1);  // consumed either way
+  dc.fin.add_b(reinterpret_cast<void*>(s.done_addr), s.done_val);
+  dc.fin.add_b(a.my_done, a.my_gen);
 }
 
-// Phase 1 (CTA 0). All threads of CTA 0 call it; warp 0 does the protocol,
-// the whole CTA does the eager payload copy.
+// The handshake (whole CTA calls; warp 0 works, the CTA copies eager
+// payloads). On return dc holds ACT_NONE / ACT_COPY / ACT_STAGE.
+template <bool SYS>
 __device__ void decide(const P2PArgs& a, Decision& dc) {
+  using M = Scope<SYS>;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  __shared__ int s_phase;  // 0 = decided, 1 = need eager copy
+  __shared__ int s_phase;  // 0 decided, 1 eager copy then post, 2 posted
   if (warp == 0) {
     Snap sn;
-    int j = warp_scan(a.scan_ring, a.R, a.key, &sn);
+    int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
     if (lane == 0) {
-      dc.err = 0;
       dc.wait_own = 0;
-      dc.fin.n = 0;
+      dc.fin.clear();
+      dc.action = ACT_NONE;
+      s_phase = 0;
       if (!a.is_recv) {
         if (j >= 0) {
-          send_win(a, dc, j, sn, false, a.buf);  // receive already posted: push
-          s_phase = 0;
+          // receive already posted: push (my slot is skipped, but only after
+          // its previous occupant retired, so its mirror stays monotonic)
+          if (wait_post_slot<SYS>(a)) send_win(a, dc, j, sn, false, a.buf);
         } else if (a.mode == MODE_STAGED) {
-          dc.action = ACT_STAGE;  // copy to local staging first (all CTAs)
-          s_phase = 0;
-        } else if (!wait_post_slot(a)) {
-          dc.action = ACT_NONE;
-          dc.err = 1;
-          s_phase = 0;
-        } else if (a.mode == MODE_EAGER) {
-          s_phase = 1;
-        } else {  // MODE_ISEND: publish the user buffer
-          post_desc(a, (uint64_t)a.buf, a.bytes, (uint64_t)a.my_done, a.my_gen);
-          s_phase = 2;
+          dc.action = ACT_STAGE;
+        } else if (wait_post_slot<SYS>(a)) {
+          if (a.mode == MODE_EAGER) {
+            s_phase = 1;
+          } else {  // MODE_ISEND: publish the user buffer
+            post_desc<SYS>(a, (uint64_t)a.buf, a.bytes, (uint64_t)a.my_done, a.my_gen, false);
+            s_phase = 2;
+          }
         }
       } else {
         if (j >= 0) {
           uint64_t want = st_word(sn.state >> 8, ST_POSTED);
-          uint64_t old = cas_sys(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN));
-          if (old == want) {
+          if (!wait_post_slot<SYS>(a)) {
+            // watchdog: leave the send descriptor for nobody
+          } else if (M::cas(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN)) == want) {
             recv_win(a, dc, j, sn, false);
-          } else {
-            dc.action = ACT_NONE;  // impossible: nobody else can take it
-            dc.err = 1;
-            if (a.err_word) st_relaxed_sys(a.err_word, ERRW_PROTOCOL);
+          } else if (a.err_word) {
+            ScopeSys::st_rlx(a.err_word, ERRW_PROTOCOL);  // nobody else may take it
           }
-          s_phase = 0;
-        } else if (!wait_post_slot(a)) {
-          dc.action = ACT_NONE;
-          dc.err = 1;
-          s_phase = 0;
-        } else {
-          post_desc(a, (uint64_t)a.buf, a.bytes, (uint64_t)a.my_done, a.my_gen);
+        } else if (wait_post_slot<SYS>(a)) {
+          post_desc<SYS>(a, (uint64_t)a.buf, a.bytes, (uint64_t)a.my_done, a.my_gen, false);
           s_phase = 2;
         }
       }
@@ -335,143 +381,60 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   __syncthreads();
   int phase = s_phase;
   if (phase == 1) {
-    // Eager: payload into the receiver's eager slot (remote stores).
+    // Eager: payload into the receiver's eager slot (peer stores).
     const int slot = (int)(a.pseq % (uint64_t)a.R);
-    part_copy(a.eager_ring + (uint64_t)slot * a.E, a.buf, a.bytes, 0, 1);
+    cta_copy(a.eager_ring + (uint64_t)slot * a.E, a.buf, a.bytes);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      post_desc(a, (uint64_t)(a.eager_ring + (uint64_t)slot * a.E), a.bytes, 0, 0);
-      s_phase = 2;
-    }
-    __syncthreads();
+    if (threadIdx.x == 0)
+      post_desc<SYS>(a, (uint64_t)(a.eager_ring + (uint64_t)slot * a.E), a.bytes, 0, 0, true);
     phase = 2;
   }
-  if (phase == 2) {
+  if (phase == 2 && warp == 0) {
     // Posted: rescan; if the other side's descriptor is there, race for the
-    // send descriptor's state word.
-    if (warp == 0) {
-      Snap sn;
-      int j = warp_scan(a.scan_ring, a.R, a.key, &sn);
-      if (lane == 0) {
-        dc.action = ACT_NONE;
-        if (j >= 0) {
-          if (!a.is_recv) {
-            const int slot = (int)(a.pseq % (uint64_t)a.R);
-            uint64_t want = st_word(a.pseq, ST_POSTED);
-            if (cas_sys(&a.post_ring[slot].state, want, st_word(a.pseq, ST_TAKEN)) == want)
-              send_win(a, dc, j, sn, true, a.buf);
-          } else {
-            uint64_t want = st_word(sn.state >> 8, ST_POSTED);
-            if (cas_sys(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN)) == want)
-              recv_win(a, dc, j, sn, true);
-          }
-        }
-        if (dc.action == ACT_NONE && a.is_recv && a.blocking) dc.wait_own = 1;
+    // send descriptor's state word (second arriver copies).
+    Snap sn;
+    int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
+    if (lane == 0 && j >= 0) {
+      if (!a.is_recv) {
+        const int slot = (int)(a.pseq % (uint64_t)a.R);
+        uint64_t want = st_word(a.pseq, ST_POSTED);
+        if (M::cas(&a.post_ring[slot].state, want, st_word(a.pseq, ST_TAKEN)) == want)
+          send_win(a, dc, j, sn, true, a.buf);
+      } else {
+        uint64_t want = st_word(sn.state >> 8, ST_POSTED);
+        if (M::cas(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN)) == want)
+          recv_win(a, dc, j, sn, true);
       }
-      __syncwarp();
     }
+    if (lane == 0 && dc.action == ACT_NONE && a.is_recv && a.blocking) dc.wait_own = 1;
+    __syncwarp();
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThreads, 2) k_p2p(const P2PArgs a) {
-  __shared__ Decision s_dc;
-  __shared__ int s_last;
-  const bool multi = gridDim.x > 1;
-  OpRecord* rec = a.rec;
-
-  if (blockIdx.x == 0) {
-    decide(a, s_dc);
-    if (multi && threadIdx.x == 0) {
-      rec->action = s_dc.action;
-      rec->src = s_dc.src;
-      rec->dst = s_dc.dst;
-      rec->bytes = s_dc.bytes;
-      rec->counter = 0;
-      rec->nfin = s_dc.fin.n;
-      for (uint32_t k = 0; k < s_dc.fin.n; ++k) {
-        rec->fin_addr[k] = s_dc.fin.addr[k];
-        rec->fin_val[k] = s_dc.fin.val[k];
-      }
-      __threadfence();
-      st_release_gpu(&rec->opid, a.opid);
-    }
-  } else {
-    if (threadIdx.x == 0) {
-      unsigned ns = 32;
-      while (ld_acquire_gpu(&rec->opid) != a.opid) {
-        __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
-      }
-      s_dc.action = rec->action;
-      s_dc.src = rec->src;
-      s_dc.dst = rec->dst;
-      s_dc.bytes = rec->bytes;
-      s_dc.fin.n = rec->nfin;
-      for (uint32_t k = 0; k < s_dc.fin.n; ++k) {
-        s_dc.fin.addr[k] = rec->fin_addr[k];
-        s_dc.fin.val[k] = rec->fin_val[k];
-      }
-      s_dc.wait_own = 0;
-    }
-    __syncthreads();
-  }
-
-  const uint64_t action = s_dc.action;
-  if (action == ACT_NONE) {
-    if (blockIdx.x == 0 && threadIdx.x == 0 && s_dc.wait_own)
-      spin_ge(a.my_done, a.my_gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE);
-    return;
-  }
-
-  if (action == ACT_COPY) {
-    part_copy(reinterpret_cast<uint8_t*>(s_dc.dst), reinterpret_cast<const uint8_t*>(s_dc.src),
-              s_dc.bytes, blockIdx.x, gridDim.x);
-  } else {  // ACT_STAGE: user buffer -> local staging
-    part_copy(a.staging, a.buf, a.bytes, blockIdx.x, gridDim.x);
-  }
-
-  // Grid completion: the last CTA finishes the operation.
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (multi) {
-      __threadfence_system();
-      unsigned old = atomicAdd(&rec->counter, 1u);
-      s_last = (old == gridDim.x - 1);
-      if (s_last) __threadfence_system();
-    } else {
-      s_last = 1;
-    }
-  }
-  __syncthreads();
-  if (!s_last) return;
-
-  if (action == ACT_COPY) {
-    if (threadIdx.x == 0) s_dc.fin.run();
-    return;
-  }
-
-  // ACT_STAGE, last CTA: publish the staged copy, rescan, maybe push.
+// Publish a staged blocking send and race for its descriptor (whole CTA).
+template <bool SYS>
+__device__ void stage_publish(const P2PArgs& a, Decision& dc) {
+  using M = Scope<SYS>;
   __shared__ int s_push;
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
       s_push = 0;
-      if (wait_post_slot(a)) {
-        post_desc(a, (uint64_t)a.staging, a.bytes, (uint64_t)a.stage_done, a.stage_gen);
-      } else {
+      dc.action = ACT_NONE;
+      if (wait_post_slot<SYS>(a))
+        post_desc<SYS>(a, (uint64_t)a.staging, a.bytes, (uint64_t)a.stage_done, a.stage_gen, true);
+      else
         s_push = -1;
-      }
     }
     __syncwarp();
-    int ok = __shfl_sync(0xffffffffu, s_push, 0);
-    if (ok == 0) {
+    if (__shfl_sync(0xffffffffu, s_push, 0) == 0) {
       Snap sn;
-      int j = warp_scan(a.scan_ring, a.R, a.key, &sn);
+      int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
       if (threadIdx.x == 0 && j >= 0) {
         const int slot = (int)(a.pseq % (uint64_t)a.R);
         uint64_t want = st_word(a.pseq, ST_POSTED);
-        if (cas_sys(&a.post_ring[slot].state, want, st_word(a.pseq, ST_TAKEN)) == want) {
-          send_win(a, s_dc, j, sn, true, a.staging);
+        if (M::cas(&a.post_ring[slot].state, want, st_word(a.pseq, ST_TAKEN)) == want) {
+          send_win(a, dc, j, sn, true, a.staging);
           s_push = 1;
         }
       }
@@ -480,19 +443,95 @@ __global__ void __launch_bounds__(kThreads, 2) k_p2p(const P2PArgs a) {
   }
   __syncthreads();
   if (s_push == 1) {
-    part_copy(reinterpret_cast<uint8_t*>(s_dc.dst), reinterpret_cast<const uint8_t*>(s_dc.src),
-              s_dc.bytes, 0, 1);
+    cta_copy(reinterpret_cast<uint8_t*>(dc.dst), reinterpret_cast<const uint8_t*>(dc.src), dc.bytes);
     __syncthreads();
-    if (threadIdx.x == 0) s_dc.fin.run();
+    if (threadIdx.x == 0) dc.fin.run<SYS>();
+  }
+}
+
+// INLINE: the whole operation in this 1-CTA kernel.
+template <bool SYS, bool INLINE>
+__global__ void __launch_bounds__(kThreads) k_proto(const P2PArgs a) {
+  __shared__ Decision s_dc;
+  decide<SYS>(a, s_dc);
+  if (!INLINE) {
+    if (threadIdx.x == 0) {
+      OpRecord* rec = a.rec;
+      rec->action = s_dc.action;
+      rec->src = s_dc.src;
+      rec->dst = s_dc.dst;
+      rec->bytes = s_dc.bytes;
+      rec->nfin = s_dc.fin.na | (s_dc.fin.nb << 8);
+      for (uint32_t k = 0; k < s_dc.fin.na; ++k) {
+        rec->fin_addr[k] = s_dc.fin.a_addr[k];
+        rec->fin_val[k] = s_dc.fin.a_val[k];
+      }
+      for (uint32_t k = 0; k < s_dc.fin.nb; ++k) {
+        rec->fin_addr[2 + k] = s_dc.fin.b_addr[k];
+        rec->fin_val[2 + k] = s_dc.fin.b_val[k];
+      }
+    }
+    pdl_trigger();
+    if (threadIdx.x == 0 && s_dc.wait_own)
+      spin_ge<SYS>(a.my_done, a.my_gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE);
+    return;
+  }
+  if (s_dc.action == ACT_COPY) {
+    cta_copy(reinterpret_cast<uint8_t*>(s_dc.dst), reinterpret_cast<const uint8_t*>(s_dc.src),
+             s_dc.bytes);
+    __syncthreads();
+    if (threadIdx.x == 0) s_dc.fin.run<SYS>();
+  } else if (s_dc.action == ACT_STAGE) {
+    cta_copy(a.staging, a.buf, a.bytes);
+    __syncthreads();
+    stage_publish<SYS>(a, s_dc);
+  } else if (threadIdx.x == 0 && s_dc.wait_own) {
+    spin_ge<SYS>(a.my_done, a.my_gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE);
+  }
+}
+
+// Wide copy behind k_proto (PDL): never waits on anything but the stream.
+__global__ void __launch_bounds__(kCopyThreads) k_copy(const P2PArgs a) {
+  pdl_wait();
+  const OpRecord* rec = a.rec;
+  const uint64_t action = rec->action;
+  if (action == ACT_COPY) {
+    tile_copy(reinterpret_cast<uint8_t*>(rec->dst), reinterpret_cast<const uint8_t*>(rec->src),
+              rec->bytes, blockIdx.x, gridDim.x);
+  } else if (action == ACT_STAGE) {
+    tile_copy(a.staging, a.buf, a.bytes, blockIdx.x, gridDim.x);
+  }
+  pdl_trigger();
+}
+
+// Completion behind k_copy (PDL): the grid above has fully retired.
+template <bool SYS>
+__global__ void __launch_bounds__(kThreads) k_fin(const P2PArgs a) {
+  pdl_wait();
+  __shared__ Decision s_dc;
+  const OpRecord* rec = a.rec;
+  const uint64_t action = rec->action;
+  if (action == ACT_COPY) {
+    if (threadIdx.x == 0) {
+      Fin f;
+      f.na = rec->nfin & 0xff;
+      f.nb = rec->nfin >> 8;
+      for (uint32_t k = 0; k < f.na; ++k) { f.a_addr[k] = rec->fin_addr[k]; f.a_val[k] = rec->fin_val[k]; }
+      for (uint32_t k = 0; k < f.nb; ++k) { f.b_addr[k] = rec->fin_addr[2 + k]; f.b_val[k] = rec->fin_val[2 + k]; }
+      f.run<SYS>();
+    }
+  } else if (action == ACT_STAGE) {
+    stage_publish<SYS>(a, s_dc);
   }
 }
 
 // ---------------------------------------------------------------------------
 // Wait / Waitall
 // ---------------------------------------------------------------------------
+template <bool SYS>
 __global__ void __launch_bounds__(32) k_wait(const WaitArgs a) {
   for (int i = threadIdx.x; i < a.n; i += 32) {
-    if (!spin_ge(a.e[i].flag, a.e[i].gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE)) break;
+    if (!spin_ge<SYS>(a.e[i].flag, a.e[i].gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE)) break;
   }
 }
 
@@ -524,7 +563,6 @@ __device__ __forceinline__ int32_t opi(int32_t a, int32_t b) {
   return b < a ? b : a;
 }
 
-// Accumulator for one 16-B vector.
 template <int DT>
 struct Acc;
 template <>
@@ -601,10 +639,9 @@ struct Acc<AR_F64> {
   }
 };
 
-// Scalar element fold (unaligned buffers and tails).
+// Scalar element fold (unaligned buffers and tails): rank order 0..P-1.
 template <int DT, int OP>
-__device__ void reduce_elem(const uint64_t* sb, uint8_t* const* outs, int nout, int P,
-                            uint64_t e) {
+__device__ void reduce_elem(const uint64_t* sb, const uint64_t* outs, int nout, int P, uint64_t e) {
   if (DT == AR_F32 || DT == AR_BF16) {
     float acc = 0.f;
     for (int q = 0; q < P; ++q) {
@@ -638,218 +675,256 @@ __device__ void reduce_elem(const uint64_t* sb, uint8_t* const* outs, int nout, 
   }
 }
 
-// Vector range [v0, v1) of 16-B vectors, grid-stride over (part, nparts).
-template <int DT, int OP, int UNROLL>
-__device__ void reduce_range(const uint64_t* sb, uint8_t* const* outs, int nout, int P,
-                             uint64_t v0, uint64_t v1, uint64_t t, uint64_t nt) {
-  uint64_t i = v0 + t;
-  for (; i + (UNROLL - 1) * nt < v1; i += UNROLL * nt) {
-    Acc<DT> acc[UNROLL];
-    {
-      const uint4* s0 = reinterpret_cast<const uint4*>(sb[0]);
-      uint4 x[UNROLL];
+constexpr int kArThreads = 256;
+constexpr int kArUnroll = 2;
+constexpr uint64_t kArTileVec = (uint64_t)kArThreads * kArUnroll;
+
+// One tile [v0 + tile*kArTileVec, ...) of vectors within [v0, v1).
+template <int DT, int OP>
+__device__ void reduce_tile(const uint64_t* sb, const uint64_t* outs, int nout, int P, uint64_t v0,
+                            uint64_t v1, uint64_t tile) {
+  uint64_t base = v0 + tile * kArTileVec + threadIdx.x;
+  Acc<DT> acc[kArUnroll];
+  bool in[kArUnroll];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) x[u] = s0[i + u * nt];
+  for (int u = 0; u < kArUnroll; ++u) in[u] = base + u * kArThreads < v1;
+  {
+    const uint4* s0 = reinterpret_cast<const uint4*>(sb[0]);
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) acc[u].init(x[u]);
-    }
-    for (int q = 1; q < P; ++q) {
-      const uint4* sq = reinterpret_cast<const uint4*>(sb[q]);
-      uint4 x[UNROLL];
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u) x[u] = sq[i + u * nt];
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u) acc[u].template add<OP>(x[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      uint4 o = acc[u].out();
-      for (int k = 0; k < nout; ++k) reinterpret_cast<uint4*>(outs[k])[i + u * nt] = o;
-    }
+    for (int u = 0; u < kArUnroll; ++u)
+      if (in[u]) acc[u].init(s0[base + u * kArThreads]);
   }
-  for (; i < v1; i += nt) {
-    Acc<DT> acc;
-    acc.init(reinterpret_cast<const uint4*>(sb[0])[i]);
-    for (int q = 1; q < P; ++q) acc.template add<OP>(reinterpret_cast<const uint4*>(sb[q])[i]);
-    uint4 o = acc.out();
-    for (int k = 0; k < nout; ++k) reinterpret_cast<uint4*>(outs[k])[i] = o;
+  for (int q = 1; q < P; ++q) {
+    const uint4* sq = reinterpret_cast<const uint4*>(sb[q]);
+    uint4 x[kArUnroll];
+#pragma unroll
+    for (int u = 0; u < kArUnroll; ++u)
+      if (in[u]) x[u] = sq[base + u * kArThreads];
+#pragma unroll
+    for (int u = 0; u < kArUnroll; ++u)
+      if (in[u]) acc[u].template add<OP>(x[u]);
   }
+#pragma unroll
+  for (int u = 0; u < kArUnroll; ++u) {
+    if (!in[u]) continue;
+    uint4 o = acc[u].out();
+    for (int k = 0; k < nout; ++k) reinterpret_cast<uint4*>(outs[k])[base + u * kArThreads] = o;
+  }
+}
+
+struct ArPlan {
+  uint64_t v0, v1;  // my vector range
+  uint64_t e0, e1;  // scalar element range handled here
+  int nout;         // 1 (one-shot: my rbuf) or P (two-shot: every rbuf)
+};
+
+__device__ ArPlan ar_plan(const ARArgs& a, const uint64_t* sb, const uint64_t* rb, int algo) {
+  ArPlan p;
+  const int P = a.P;
+  bool al = true;
+  for (int q = 0; q < P; ++q) al &= ((sb[q] | rb[q]) & 15) == 0;
+  const uint64_t nvec = al ? (a.count * (uint64_t)a.esize) >> 4 : 0;
+  const uint64_t tail_e0 = (nvec << 4) / a.esize;
+  if (algo == AR_TWOSHOT) {
+    p.nout = P;
+    uint64_t per = (nvec + P - 1) / P;
+    p.v0 = umin(nvec, per * a.me);
+    p.v1 = umin(nvec, p.v0 + per);
+    if (al) {
+      p.e0 = a.me == P - 1 ? tail_e0 : a.count;
+      p.e1 = a.count;
+    } else {
+      uint64_t pe = (a.count + P - 1) / P;
+      p.e0 = umin(a.count, pe * a.me);
+      p.e1 = umin(a.count, p.e0 + pe);
+    }
+  } else {
+    p.nout = 1;
+    p.v0 = 0;
+    p.v1 = nvec;
+    p.e0 = tail_e0;
+    p.e1 = a.count;
+  }
+  return p;
 }
 
 template <int DT, int OP>
-__device__ void ar_compute(const ARArgs& a, const uint64_t* sb, const uint64_t* rb, int algo) {
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
-  const int P = a.P;
-  const uint64_t nbytes = a.count * (uint64_t)a.esize;
-  bool aligned = true;
-  for (int q = 0; q < P; ++q) aligned &= ((sb[q] | rb[q]) & 15) == 0;
-  uint8_t* outs[kMaxCollRanks];
-  if (!aligned) {
-    // Scalar path: every element on its owner (two-shot) or locally.
-    if (algo == AR_TWOSHOT) {
-      for (int q = 0; q < P; ++q) outs[q] = reinterpret_cast<uint8_t*>(rb[q]);
-      uint64_t per = (a.count + P - 1) / P;
-      uint64_t e0 = per * a.me, e1 = umin(a.count, e0 + per);
-      for (uint64_t e = e0 + t; e < e1; e += nt) reduce_elem<DT, OP>(sb, outs, P, P, e);
-    } else {
-      outs[0] = reinterpret_cast<uint8_t*>(rb[a.me]);
-      for (uint64_t e = t; e < a.count; e += nt) reduce_elem<DT, OP>(sb, outs, 1, P, e);
-    }
-    return;
-  }
-  const uint64_t nvec = nbytes >> 4;
-  const uint64_t tail_e0 = (nvec << 4) / a.esize;  // first element not in a vector
-  if (algo == AR_TWOSHOT) {
-    for (int q = 0; q < P; ++q) outs[q] = reinterpret_cast<uint8_t*>(rb[q]);
-    uint64_t per = (nvec + P - 1) / P;
-    uint64_t v0 = umin(nvec, per * a.me), v1 = umin(nvec, v0 + per);
-    reduce_range<DT, OP, 4>(sb, outs, P, P, v0, v1, t, nt);
-    if (a.me == P - 1)
-      for (uint64_t e = tail_e0 + t; e < a.count; e += nt) reduce_elem<DT, OP>(sb, outs, P, P, e);
-  } else {
-    outs[0] = reinterpret_cast<uint8_t*>(rb[a.me]);
-    reduce_range<DT, OP, 4>(sb, outs, 1, P, 0, nvec, t, nt);
-    for (uint64_t e = tail_e0 + t; e < a.count; e += nt) reduce_elem<DT, OP>(sb, outs, 1, P, e);
-  }
+__device__ void ar_tile(const ARArgs& a, const uint64_t* sb, const uint64_t* rb, int algo,
+                        uint64_t tile, uint64_t ntiles) {
+  ArPlan p = ar_plan(a, sb, rb, algo);
+  uint64_t outs[kMaxCollRanks];
+  if (p.nout == 1) outs[0] = rb[a.me];
+  else for (int q = 0; q < a.P; ++q) outs[q] = rb[q];
+  uint64_t nt_vec = (p.v1 - p.v0 + kArTileVec - 1) / kArTileVec;
+  for (uint64_t t = tile; t < nt_vec; t += ntiles)
+    reduce_tile<DT, OP>(sb, outs, p.nout, a.P, p.v0, p.v1, t);
+  uint64_t gt = tile * blockDim.x + threadIdx.x, gn = ntiles * blockDim.x;
+  for (uint64_t e = p.e0 + gt; e < p.e1; e += gn) reduce_elem<DT, OP>(sb, outs, p.nout, a.P, e);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) k_allreduce(const ARArgs a) {
-  __shared__ uint64_t s_sb[kMaxCollRanks], s_rb[kMaxCollRanks];
-  __shared__ int s_algo, s_ok, s_last;
-  const int P = a.P;
-  const bool multi = gridDim.x > 1;
-  OpRecord* rec = a.rec;
+template <int DT>
+__device__ void ar_dispatch_op(const ARArgs& a, const uint64_t* sb, const uint64_t* rb, int algo,
+                               uint64_t tile, uint64_t ntiles) {
+  if (a.op == AR_SUM) ar_tile<DT, AR_SUM>(a, sb, rb, algo, tile, ntiles);
+  else if (a.op == AR_MAX) ar_tile<DT, AR_MAX>(a, sb, rb, algo, tile, ntiles);
+  else ar_tile<DT, AR_MIN>(a, sb, rb, algo, tile, ntiles);
+}
 
-  if (blockIdx.x == 0) {
-    if (threadIdx.x < 32) {
-      const int q = threadIdx.x;
-      int ok = 1;
-      if (P > 1) {
-        // Entry: publish my buffers to every peer, then wait for theirs.
-        if (q < P) {
-          CollSlot* dst = a.peer_in[q];
-          st_relaxed_sys(&dst->sbuf, (uint64_t)a.sbuf);
-          st_relaxed_sys(&dst->rbuf, (uint64_t)a.rbuf);
-          fence_sc_sys();
-          st_release_sys(&dst->flag, a.epoch);
-        }
-        if (q < P) {
-          ok = spin_ge(&a.my_in[q].flag, a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
-          s_sb[q] = ld_relaxed_sys(&a.my_in[q].sbuf);
-          s_rb[q] = ld_relaxed_sys(&a.my_in[q].rbuf);
-        }
-      } else if (q == 0) {
-        s_sb[0] = (uint64_t)a.sbuf;
-        s_rb[0] = (uint64_t)a.rbuf;
-      }
-      ok = __all_sync(0xffffffffu, ok);
-      __syncwarp();
-      if (q == 0) {
-        int algo = a.algo;
-        // One-shot reads every peer's full buffer while peers write theirs:
-        // unsafe if any rank reduces in place.
-        for (int k = 0; k < P; ++k)
-          if (s_sb[k] == s_rb[k] && P > 1) algo = AR_TWOSHOT;
-        s_algo = algo;
-        s_ok = ok;
-      }
-    }
-    __syncthreads();
-    if (multi && threadIdx.x == 0) {
-      for (int k = 0; k < P; ++k) {
-        rec->coll[k] = s_sb[k];
-        rec->coll[kMaxCollRanks + k] = s_rb[k];
-      }
-      rec->action = s_ok ? (uint64_t)s_algo + 1 : 0;
-      rec->counter = 0;
-      __threadfence();
-      st_release_gpu(&rec->opid, a.opid);
-    }
-  } else {
-    if (threadIdx.x == 0) {
-      unsigned ns = 32;
-      while (ld_acquire_gpu(&rec->opid) != a.opid) {
-        __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
-      }
-      for (int k = 0; k < P; ++k) {
-        s_sb[k] = rec->coll[k];
-        s_rb[k] = rec->coll[kMaxCollRanks + k];
-      }
-      uint64_t act = rec->action;
-      s_ok = act != 0;
-      s_algo = act ? (int)act - 1 : 0;
-    }
-    __syncthreads();
-  }
-  if (!s_ok) return;
-
-  const int algo = s_algo;
-#define AR_DISPATCH(DT)                                             \
-  if (a.op == AR_SUM) ar_compute<DT, AR_SUM>(a, s_sb, s_rb, algo);  \
-  else if (a.op == AR_MAX) ar_compute<DT, AR_MAX>(a, s_sb, s_rb, algo); \
-  else ar_compute<DT, AR_MIN>(a, s_sb, s_rb, algo);
+__device__ void ar_compute(const ARArgs& a, const uint64_t* sb, const uint64_t* rb, int algo,
+                           uint64_t tile, uint64_t ntiles) {
   switch (a.dtype) {
-    case AR_F32: AR_DISPATCH(AR_F32) break;
-    case AR_BF16: AR_DISPATCH(AR_BF16) break;
-    case AR_I32: AR_DISPATCH(AR_I32) break;
-    default: AR_DISPATCH(AR_F64) break;
+    case AR_F32: ar_dispatch_op<AR_F32>(a, sb, rb, algo, tile, ntiles); break;
+    case AR_BF16: ar_dispatch_op<AR_BF16>(a, sb, rb, algo, tile, ntiles); break;
+    case AR_I32: ar_dispatch_op<AR_I32>(a, sb, rb, algo, tile, ntiles); break;
+    default: ar_dispatch_op<AR_F64>(a, sb, rb, algo, tile, ntiles); break;
   }
-#undef AR_DISPATCH
+}
 
-  if (P == 1) return;
-  // Exit: every CTA done -> tell every peer; wait for all peers.
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (multi) {
-      __threadfence_system();
-      unsigned old = atomicAdd(&rec->counter, 1u);
-      s_last = (old == gridDim.x - 1);
-      if (s_last) __threadfence_system();
-    } else {
-      s_last = 1;
-      __threadfence_system();
-    }
+// Entry: publish my buffers to every peer, wait for theirs, record them.
+template <bool SYS>
+__global__ void __launch_bounds__(32) k_ar_entry(const ARArgs a) {
+  using M = Scope<SYS>;
+  const int q = threadIdx.x;
+  const int P = a.P;
+  OpRecord* rec = a.rec;
+  int ok = 1;
+  uint64_t sb = 0, rb = 0;
+  if (q < P) {
+    CollSlot* dst = a.peer_in[q];
+    M::st_rlx(&dst->sbuf, (uint64_t)a.sbuf);
+    M::st_rlx(&dst->rbuf, (uint64_t)a.rbuf);
+    M::st_rel(&dst->flag, a.epoch);
+    ok = spin_ge<SYS>(&a.my_in[q].flag, a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
+    sb = M::ld_rlx(&a.my_in[q].sbuf);
+    rb = M::ld_rlx(&a.my_in[q].rbuf);
+    rec->coll[q] = sb;
+    rec->coll[kMaxCollRanks + q] = rb;
   }
+  ok = __all_sync(0xffffffffu, ok);
+  // One-shot reads every peer's full buffer while peers write theirs: use
+  // two-shot if any rank reduces in place.
+  int inplace = __any_sync(0xffffffffu, q < P && sb == rb);
+  if (q == 0) rec->action = ok ? (uint64_t)((inplace && P > 1) ? AR_TWOSHOT : a.algo) + 1 : 0;
+  pdl_trigger();
+}
+
+__global__ void __launch_bounds__(kArThreads) k_ar_reduce(const ARArgs a) {
+  pdl_wait();
+  __shared__ uint64_t s_sb[kMaxCollRanks], s_rb[kMaxCollRanks];
+  __shared__ uint64_t s_act;
+  const OpRecord* rec = a.rec;
+  if (threadIdx.x < a.P) {
+    s_sb[threadIdx.x] = rec->coll[threadIdx.x];
+    s_rb[threadIdx.x] = rec->coll[kMaxCollRanks + threadIdx.x];
+  }
+  if (threadIdx.x == 0) s_act = rec->action;
   __syncthreads();
-  if (!s_last) return;
-  if (threadIdx.x < 32) {
-    const int q = threadIdx.x;
-    if (q < P) st_release_sys(a.peer_exit[q], a.epoch);
-    if (q < P) spin_ge(&a.my_exit[q], a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
+  pdl_trigger();
+  if (s_act == 0) return;
+  ar_compute(a, s_sb, s_rb, (int)s_act - 1, blockIdx.x, gridDim.x);
+}
+
+// Exit: tell every peer I am done with its buffers; wait for all of them.
+template <bool SYS>
+__global__ void __launch_bounds__(32) k_ar_exit(const ARArgs a) {
+  pdl_wait();
+  using M = Scope<SYS>;
+  const int q = threadIdx.x;
+  if (a.rec->action == 0) return;
+  M::fence_ar();
+  if (q < a.P) {
+    M::st_rlx(a.peer_exit[q], a.epoch);
+    spin_ge<SYS>(&a.my_exit[q], a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
   }
 }
 
 // ---------------------------------------------------------------------------
-// Host launchers
+// Host launchers (return the number of kernels launched, -1 on error)
 // ---------------------------------------------------------------------------
-cudaError_t launch_p2p(const P2PArgs& a, int grid, cudaStream_t s) {
-  k_p2p<<<grid, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
-cudaError_t launch_wait(const WaitArgs& a, cudaStream_t s) {
-  k_wait<<<1, 32, 0, s>>>(a);
-  return cudaGetLastError();
+uint64_t p2p_copy_grid(uint64_t bytes) {
+  uint64_t tile = kTileVec * 16;
+  uint64_t g = (bytes + tile - 1) / tile;
+  if (g > (1ull << 30)) g = 1ull << 30;
+  return g < 1 ? 1 : g;
 }
 
-cudaError_t launch_allreduce(const ARArgs& a, int grid, cudaStream_t s) {
-  k_allreduce<<<grid, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+int launch_p2p(const P2PArgs& a, bool sys, bool inl, uint64_t grid, cudaStream_t s) {
+  if (inl) {
+    if (sys) k_proto<true, true><<<1, kThreads, 0, s>>>(a);
+    else k_proto<false, true><<<1, kThreads, 0, s>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  }
+  if (sys) k_proto<true, false><<<1, kThreads, 0, s>>>(a);
+  else k_proto<false, false><<<1, kThreads, 0, s>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  if (launch_pdl(k_copy, (int)grid, kCopyThreads, s, a) != cudaSuccess) return -1;
+  cudaError_t e = sys ? launch_pdl(k_fin<true>, 1, kThreads, s, a)
+                      : launch_pdl(k_fin<false>, 1, kThreads, s, a);
+  return e == cudaSuccess ? 3 : -1;
 }
 
-int p2p_occupancy() {
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_p2p, kThreads, 0) != cudaSuccess) n = 1;
-  return n > 0 ? n : 1;
+int launch_wait(const WaitArgs& a, bool sys, cudaStream_t s) {
+  if (sys) k_wait<true><<<1, 32, 0, s>>>(a);
+  else k_wait<false><<<1, 32, 0, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
-int allreduce_occupancy() {
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_allreduce, kThreads, 0) != cudaSuccess)
-    n = 1;
-  return n > 0 ? n : 1;
+uint64_t ar_reduce_grid(uint64_t work_bytes) {
+  uint64_t tile = kArTileVec * 16;
+  uint64_t g = (work_bytes + tile - 1) / tile;
+  if (g > 148ull * 64) g = 148ull * 64;  // tiles beyond ~64 waves loop
+  return g < 1 ? 1 : g;
+}
+
+int launch_allreduce(const ARArgs& a, bool sys, uint64_t grid, cudaStream_t s) {
+  if (sys) k_ar_entry<true><<<1, 32, 0, s>>>(a);
+  else k_ar_entry<false><<<1, 32, 0, s>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  if (launch_pdl(k_ar_reduce, (int)grid, kArThreads, s, a) != cudaSuccess) return -1;
+  if (a.P > 1) {
+    cudaError_t e = sys ? launch_pdl(k_ar_exit<true>, 1, 32, s, a)
+                        : launch_pdl(k_ar_exit<false>, 1, 32, s, a);
+    if (e != cudaSuccess) return -1;
+    return 3;
+  }
+  return 2;
+}
+
+// Force-load every kernel of this module on the current device. Under CUDA
+// lazy loading the first launch of a kernel waits for the device while a
+// spinning handshake kernel may be waiting for exactly that launch (a peer's
+// kernel), so everything is loaded up front.
+int preload_kernels() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaSuccess;
+  const void* ks[] = {
+      (const void*)k_proto<true, true>, (const void*)k_proto<true, false>,
+      (const void*)k_proto<false, true>, (const void*)k_proto<false, false>,
+      (const void*)k_copy, (const void*)k_fin<true>, (const void*)k_fin<false>,
+      (const void*)k_wait<true>, (const void*)k_wait<false>,
+      (const void*)k_ar_entry<true>, (const void*)k_ar_entry<false>,
+      (const void*)k_ar_reduce, (const void*)k_ar_exit<true>, (const void*)k_ar_exit<false>};
+  for (const void* k : ks) {
+    cudaError_t r = cudaFuncGetAttributes(&fa, k);
+    if (r != cudaSuccess) e = r;
+  }
+  return e == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace mpix

@@ -26,6 +26,7 @@
 
 #include "mpix.h"
 #include "mpix_internal.h"
+#include "mpix_testing.h"
 
 namespace mpix {
 
@@ -35,8 +36,7 @@ namespace mpix {
 struct Config {
   uint64_t eager_bytes = 4096;       // MPIX_EAGER_BYTES
   int ring_slots = 128;              // MPIX_RING_SLOTS
-  int max_ctas = 0;                  // MPIX_MAX_CTAS (0 = auto)
-  uint64_t bytes_per_cta = 65536;    // MPIX_BYTES_PER_CTA
+  uint64_t inline_bytes = 65536;     // MPIX_INLINE_BYTES: 1-kernel path limit
   uint64_t oneshot_max = 65536;      // MPIX_ALLREDUCE_ONESHOT_MAX (bytes)
   uint64_t spin_limit_ns = 60ull * 1000 * 1000 * 1000;  // MPIX_SPIN_TIMEOUT_MS
 
@@ -51,9 +51,7 @@ struct Config {
     c.eager_bytes = (c.eager_bytes + 15) & ~15ull;
     c.ring_slots = (int)geti("MPIX_RING_SLOTS", c.ring_slots);
     if (c.ring_slots < 2) c.ring_slots = 2;
-    c.max_ctas = (int)geti("MPIX_MAX_CTAS", 0);
-    c.bytes_per_cta = geti("MPIX_BYTES_PER_CTA", c.bytes_per_cta);
-    if (c.bytes_per_cta < 4096) c.bytes_per_cta = 4096;
+    c.inline_bytes = geti("MPIX_INLINE_BYTES", c.inline_bytes);
     c.oneshot_max = geti("MPIX_ALLREDUCE_ONESHOT_MAX", c.oneshot_max);
     c.spin_limit_ns = geti("MPIX_SPIN_TIMEOUT_MS", 60000) * 1000000ull;
     return c;
@@ -116,14 +114,13 @@ struct RankState {
   cudaStream_t aux = nullptr;      // setup work
   cudaStream_t reclaim = nullptr;  // staging release
   cudaMemPool_t pool = nullptr;
-  int p2p_cap = 1;
-  int ar_cap = 1;
   std::mutex mu;
   // request table: slot -> issuing stream, for STREAM_MISMATCH
   struct ReqInfo {
     uint64_t gen = 0;
     cudaStream_t stream = nullptr;
     int source = -1, tag = -1;
+    bool remote = false;  // the peer lives on another GPU (system scope)
   };
   std::vector<ReqInfo> reqs;
 };
@@ -266,15 +263,9 @@ int rank_init(RankState& r, const Config& cfg) {
   CK(cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&r.reclaim, cudaStreamNonBlocking));
   r.reqs.resize(kReqSlots);
-  int occ_p2p = p2p_occupancy();
-  int occ_ar = allreduce_occupancy();
-  int per = std::max(1, r.per_device);
-  r.p2p_cap = std::max(1, r.sms * occ_p2p / per);
-  r.ar_cap = std::max(1, r.sms * occ_ar / per);
-  if (cfg.max_ctas > 0) {
-    r.p2p_cap = std::min(r.p2p_cap, cfg.max_ctas);
-    r.ar_cap = std::min(r.ar_cap, cfg.max_ctas);
-  }
+  (void)cfg;
+  if (preload_kernels() != 0) return MPIX_ERR_CUDA;
+  MPIXT_Preload();
   CK(cudaDeviceSynchronize());
   return MPI_SUCCESS;
 }
@@ -306,13 +297,6 @@ int rank_pool(World& w, RankState& r) {
 World* world() { return g_world; }
 
 RankState& rank_of(int r) { return *g_world->ranks[r]; }
-
-int pick_grid(uint64_t bytes, uint64_t per_cta, int cap) {
-  uint64_t g = (bytes + per_cta - 1) / per_cta;
-  if (g < 1) g = 1;
-  if (g > (uint64_t)cap) g = cap;
-  return (int)g;
-}
 
 // Build and publish the per-rank view of a communicator. Collective over the
 // parent's members (proc_comm.cpp:60-176): root allocates the context id,
@@ -416,7 +400,7 @@ struct Ticket {
   uint64_t gen;
 };
 
-Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag) {
+Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remote) {
   uint64_t n = rs.req_next.fetch_add(1);
   uint64_t slot = n % kReqSlots;
   uint64_t gen = n / kReqSlots + 1;
@@ -425,6 +409,7 @@ Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag) {
   ri.stream = s;
   ri.source = source;
   ri.tag = tag;
+  ri.remote = remote;
   Ticket t;
   t.handle = ((uint64_t)(rs.rank + 1) << 48) | (n + 1);
   t.flag = rs.d_done + slot;
@@ -495,11 +480,12 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   }
   a.key = ((uint64_t)(uint32_t)tag << 32) | tseq;
 
+  const bool sys = rank_of(peer).device != rs.device;
   CK(cudaSetDevice(rs.device));
   cudaStream_t s = c->cu;
   Ticket t{};
   if (!blocking || is_recv) {
-    t = new_ticket(rs, s, is_recv ? peer : me, tag);
+    t = new_ticket(rs, s, is_recv ? peer : me, tag, sys);
     a.my_done = t.flag;
     a.my_gen = t.gen;
   }
@@ -507,20 +493,20 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   uint8_t* staging = nullptr;
   if (a.mode == MODE_STAGED && !is_recv) {
     CK(cudaMallocFromPoolAsync((void**)&staging, bytes ? bytes : 16, rs.pool, s));
-    st = new_ticket(rs, rs.reclaim, me, tag);
+    st = new_ticket(rs, rs.reclaim, me, tag, sys);
     a.staging = staging;
     a.stage_done = st.flag;
     a.stage_gen = st.gen;
   }
-  int grid = (is_recv || a.mode != MODE_EAGER) ? pick_grid(bytes, w.cfg.bytes_per_cta, rs.p2p_cap)
-                                               : 1;
-  if (grid > 1) {
+  const bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
+  if (!inl) {
     uint64_t op = rs.op_next.fetch_add(1);
     a.rec = rs.d_rec + (op % kOpRecords);
     a.opid = op;
   }
-  CK(launch_p2p(a, grid, s));
-  g_launches.fetch_add(1);
+  int nk = launch_p2p(a, sys, inl, inl ? 1 : p2p_copy_grid(bytes), s);
+  if (nk < 0) return MPIX_ERR_CUDA;
+  g_launches.fetch_add(nk);
   if (staging) {
     // Release the staging copy once its consumer signals (stream-ordered
     // after this kernel so the allocator sees the dependency).
@@ -532,12 +518,12 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     WaitArgs* wa = new WaitArgs;
     wa->n = 1;
     wa->err_word = rs.d_err;
-    wa->spin_limit_ns = 0;
+    wa->spin_limit_ns = w.cfg.spin_limit_ns;
     wa->e[0].flag = st.flag;
     wa->e[0].gen = st.gen;
-    cudaError_t e = launch_wait(*wa, rs.reclaim);
+    int e = launch_wait(*wa, sys, rs.reclaim);
     delete wa;
-    if (e != cudaSuccess) return MPIX_ERR_CUDA;
+    if (e < 0) return MPIX_ERR_CUDA;
     g_launches.fetch_add(1);
     CK(cudaFreeAsync(staging, rs.reclaim));
   }
@@ -560,6 +546,7 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
   }
   cudaStream_t s0 = nullptr;
   int dev0 = -1;
+  bool sys = false;
   for (int i = 0; i < n; ++i) {  // proc_enqueue.cpp:124-126
     RankState& rs = rank_of(items[i].rank);
     auto& ri = rs.reqs[items[i].n % kReqSlots];
@@ -569,6 +556,7 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
       dev0 = rs.device;
     }
     if (s != s0 || rs.device != dev0) return MPIX_ERR_STREAM_MISMATCH;
+    sys |= ri.remote;
   }
   if (statuses) {
     for (int i = 0; i < n; ++i) {
@@ -595,7 +583,7 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
       wa->e[k].flag = rs.d_done + (nn % kReqSlots);
       wa->e[k].gen = nn / kReqSlots + 1;
     }
-    CK(launch_wait(*wa, s0));
+    if (launch_wait(*wa, sys, s0) < 0) return MPIX_ERR_CUDA;
     g_launches.fetch_add(1);
   }
   return MPI_SUCCESS;
@@ -653,15 +641,17 @@ int allreduce_enqueue(const void* sbuf, void* rbuf, int count, MPI_Datatype dt, 
   a.err_word = rs.d_err;
   a.spin_limit_ns = g_world->cfg.spin_limit_ns;
   uint64_t work = a.algo == AR_TWOSHOT ? (bytes + P - 1) / P : bytes;
-  int grid = pick_grid(work, g_world->cfg.bytes_per_cta, rs.ar_cap);
-  if (grid > 1) {
+  {
     uint64_t opid = rs.op_next.fetch_add(1);
     a.rec = rs.d_rec + (opid % kOpRecords);
     a.opid = opid;
   }
+  bool sys = false;
+  for (int q = 0; q < P; ++q) sys |= rank_of(q).device != rs.device;
   CK(cudaSetDevice(rs.device));
-  CK(launch_allreduce(a, grid, c->cu));
-  g_launches.fetch_add(1);
+  int nk = launch_allreduce(a, sys, ar_reduce_grid(work), c->cu);
+  if (nk < 0) return MPIX_ERR_CUDA;
+  g_launches.fetch_add(nk);
   return MPI_SUCCESS;
 }
 
@@ -1100,7 +1090,7 @@ int MPIX_Config_get(uint64_t* eager_bytes, int* ring_slots, int* max_ctas,
   Config c = g_world ? g_world->cfg : Config::from_env();
   if (eager_bytes) *eager_bytes = c.eager_bytes;
   if (ring_slots) *ring_slots = c.ring_slots;
-  if (max_ctas) *max_ctas = g_world ? g_world->ranks[0]->p2p_cap : c.max_ctas;
+  if (max_ctas) *max_ctas = (int)c.inline_bytes;
   if (oneshot_max_bytes) *oneshot_max_bytes = c.oneshot_max;
   return MPI_SUCCESS;
 }
@@ -1118,6 +1108,20 @@ int MPIX_Comm_is_enqueue(MPI_Comm comm, int* flag) {
 }
 
 int MPIX_Type_size(MPI_Datatype datatype) { return type_size(datatype); }
+
+int MPIX_Rank_error(int rank, uint64_t* code) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (rank < 0 || rank >= g_world->n || !code) return MPIX_ERR_INVALID_RANK;
+  *code = *reinterpret_cast<volatile uint64_t*>(g_world->ranks[rank]->h_err);
+  return MPI_SUCCESS;
+}
+
+int MPIX_Comm_region(MPI_Comm comm, void** base, uint64_t* bytes) {
+  if (!comm) return MPIX_ERR_INVALID_COMM;
+  if (base) *base = comm->sh->base[comm->rank];
+  if (bytes) *bytes = comm->sh->L.total();
+  return MPI_SUCCESS;
+}
 
 const char* MPIX_Version(void) { return "mpix-b200 0.1 (sm_100a)"; }
 

@@ -231,6 +231,21 @@ int MPIXT_Stencil7(const float* u, float* out, int nx, int ny, int nz, float w0,
   return done(cudaGetLastError());
 }
 
+int MPIXT_Copy_to_host(void* host, const void* dev, uint64_t bytes) {
+  return cudaMemcpy(host, dev, bytes, cudaMemcpyDefault) == cudaSuccess ? 0 : 100;
+}
+
+int MPIXT_Preload(void) {
+  cudaFuncAttributes fa;
+  const void* ks[] = {(const void*)k_fill_pattern, (const void*)k_checksum, (const void*)k_saxpy,
+                      (const void*)k_delay,        (const void*)k_empty,    (const void*)k_fill_f32,
+                      (const void*)k_halo,         (const void*)k_stencil7};
+  int rc = 0;
+  for (const void* k : ks)
+    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) rc = 100;
+  return rc;
+}
+
 uint64_t MPIXT_Launch_count(void) { return g_test_launches.load(); }
 
 }  // extern "C"

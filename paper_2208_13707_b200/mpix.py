@@ -112,6 +112,9 @@ def _declare(L: C.CDLL) -> None:
         "MPIX_Comm_is_enqueue": (I, [P, C.POINTER(I)]),
         "MPIX_Type_size": (I, [I]),
         "MPIX_Version": (C.c_char_p, []),
+        "MPIX_Rank_error": (I, [I, C.POINTER(U64)]),
+        "MPIX_Comm_region": (I, [P, C.POINTER(P), C.POINTER(U64)]),
+        "MPIXT_Copy_to_host": (I, [P, P, U64]),
         "MPIXT_Fill_pattern": (I, [P, U64, U32, U32, P]),
         "MPIXT_Checksum": (I, [P, U64, P, P]),
         "MPIXT_Saxpy": (I, [I, C.c_float, P, P, P]),
@@ -122,6 +125,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Halo_unpack": (I, [P, I, I, I, I, P, P]),
         "MPIXT_Stencil7": (I, [P, P, I, I, I, C.c_float, C.c_float, P]),
         "MPIXT_Launch_count": (U64, []),
+        "MPIXT_Preload": (I, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -156,6 +160,12 @@ def type_size(dt: int) -> int:
 
 def launch_count() -> int:
     return lib().MPIX_Launch_count() + lib().MPIXT_Launch_count()
+
+
+def rank_error(rank: int) -> int:
+    v = C.c_uint64()
+    check(lib().MPIX_Rank_error(rank, C.byref(v)))
+    return v.value
 
 
 def config() -> dict:
@@ -291,6 +301,14 @@ class Comm:
         r = C.c_int()
         check(lib().MPIX_Comm_is_enqueue(self.h, C.byref(r)))
         return bool(r.value)
+
+    def region_bytes(self) -> bytes:
+        """Debug: a host copy of this member's peer-mapped region."""
+        b, n = C.c_void_p(), C.c_uint64()
+        check(lib().MPIX_Comm_region(self.h, C.byref(b), C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib().MPIXT_Copy_to_host(buf, b, n.value))
+        return buf.raw
 
     # collective ------------------------------------------------------------------
     def stream_comm_create(self, stream: Optional[Stream]) -> "Comm":

@@ -4,6 +4,9 @@ import sys
 import pytest
 
 os.environ.setdefault("MPIX_SPIN_TIMEOUT_MS", "20000")
+# Spin-waiting communication kernels + lazy module loading can stall a launch
+# until a peer's spinning kernel exits (NCCL has the same constraint).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
