@@ -269,6 +269,12 @@ int MPIX_Type_size(MPI_Datatype datatype);
  * recorded (1 slot wait, 2 completion wait, 3 collective barrier, 4 protocol)
  * before exiting instead of hanging. Reading clears nothing. */
 int MPIX_Rank_error(int rank, uint64_t *code);
+/* Tracing (MPIX_TRACE=1 at MPIX_World_init): copies up to max_records
+ * 128-byte per-operation records (struct TraceRec in csrc/mpix_internal.h:
+ * op sequence, kind/mode/decision, bytes, key, clock64 stamps of the
+ * handshake phases, globaltimer start/end) of `rank`. Synchronises the
+ * rank's device. */
+int MPIX_Trace_read(int rank, void *out, int max_records, int *n_records);
 /* Debug: this member's peer-mapped region of comm (device pointer) and its
  * size; the layout is RegionLayout in csrc/mpix_internal.h. */
 int MPIX_Comm_region(MPI_Comm comm, void **base, uint64_t *bytes);

@@ -24,7 +24,7 @@ namespace mpix {
 
 constexpr int kThreads = 512;          // threads per CTA for every op kernel
 constexpr int kMaxCollRanks = 16;      // max communicator size for Allreduce
-constexpr int kWaitBatch = 1024;       // requests per wait kernel launch
+constexpr int kWaitBatch = 32;         // requests per wait kernel launch (small params)
 constexpr uint64_t kOpRecords = 16384; // op-record ring entries per rank
 
 enum : uint64_t { ST_FREE = 0, ST_POSTED = 1, ST_TAKEN = 2 };
@@ -111,6 +111,22 @@ struct alignas(64) OpRecord {
 
 enum : uint64_t { ACT_NONE = 0, ACT_COPY = 1, ACT_STAGE = 2 };
 
+// Per-op trace record (MPIX_TRACE=1), written by the op's kernels.
+// t[]: clock64 stamps of k_proto phases: 0 start, 1 first scan done,
+// 2 posted (or decided without posting), 3 final decision, 4 copy done,
+// 5 completion stores done. g0/g1: globaltimer at k_proto start/end.
+struct TraceRec {
+  uint64_t seq;     // host op sequence (0 = unused)
+  uint64_t info;    // is_recv | mode << 4 | inline << 8 | action << 12
+  uint64_t bytes;
+  uint64_t key;
+  uint64_t t[6];
+  uint64_t g0, g1;
+  uint64_t pad[4];
+};
+static_assert(sizeof(TraceRec) == 128, "trace record is 128 B");
+constexpr uint64_t kTraceRecs = 4096;
+
 enum SendMode : int { MODE_ISEND = 0, MODE_EAGER = 1, MODE_STAGED = 2 };
 
 struct P2PArgs {
@@ -137,6 +153,7 @@ struct P2PArgs {
   uint64_t opid;
   uint64_t* err_word;     // per-rank error word (watchdog)
   uint64_t spin_limit_ns; // 0 = wait forever
+  TraceRec* trace;        // MPIX_TRACE: this op's trace record, else null
 };
 
 struct WaitEntry {

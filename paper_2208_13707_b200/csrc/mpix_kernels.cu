@@ -118,11 +118,15 @@ __device__ __noinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_
 
 __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+__device__ __forceinline__ void trace_t(TraceRec* tr, int k) {
+  if (tr) tr->t[k] = clock64();
+}
+
 // ---------------------------------------------------------------------------
 // Copies
 // ---------------------------------------------------------------------------
-constexpr int kCopyThreads = 256;
-constexpr int kCopyUnroll = 4;
+constexpr int kCopyThreads = 1024;
+constexpr int kCopyUnroll = 2;
 constexpr uint64_t kTileVec = (uint64_t)kCopyThreads * kCopyUnroll;  // 16-B vectors per tile
 
 // Whole-CTA copy of n bytes (k_proto inline path and the rare staged push).
@@ -195,16 +199,33 @@ struct Snap {
 };
 
 template <bool SYS>
+__device__ __forceinline__ void ld_pair(const SlotDesc* s, uint64_t& st, uint64_t& key) {
+  if (SYS)
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(st), "=l"(key) : "l"(s) : "memory");
+  else
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(st), "=l"(key) : "l"(s) : "memory");
+}
+
+constexpr int kMaxScanPerLane = 8;  // R <= 256
+
+template <bool SYS>
 __device__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
   using M = Scope<SYS>;
   const int lane = threadIdx.x & 31;
-  for (int base = 0; base < R; base += 32) {
-    int i = base + lane;
-    bool hit = false;
-    if (i < R) {
-      uint64_t st = M::ld_rlx(&ring[i].state);
-      if ((st & 0xff) == ST_POSTED) hit = M::ld_rlx(&ring[i].key) == key;
-    }
+  // Issue every (state, key) load of this lane before looking at any.
+  uint64_t st[kMaxScanPerLane], ky[kMaxScanPerLane];
+#pragma unroll
+  for (int k = 0; k < kMaxScanPerLane; ++k) {
+    int i = k * 32 + lane;
+    st[k] = 0;
+    ky[k] = 0;
+    if (i < R) ld_pair<SYS>(&ring[i], st[k], ky[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxScanPerLane; ++k) {
+    if (k * 32 >= R) break;
+    int i = k * 32 + lane;
+    bool hit = i < R && (st[k] & 0xff) == ST_POSTED && ky[k] == key;
     unsigned m = __ballot_sync(0xffffffffu, hit);
     while (m) {
       int src = __ffs(m) - 1;
@@ -230,7 +251,7 @@ __device__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
         out->bytes = __shfl_sync(0xffffffffu, sn.bytes, src);
         out->done_addr = __shfl_sync(0xffffffffu, sn.done_addr, src);
         out->done_val = __shfl_sync(0xffffffffu, sn.done_val, src);
-        return base + src;
+        return k * 32 + src;
       }
     }
   }
@@ -341,6 +362,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     Snap sn;
     int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
     if (lane == 0) {
+      trace_t(a.trace, 1);
       dc.wait_own = 0;
       dc.fin.clear();
       dc.action = ACT_NONE;
@@ -379,6 +401,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     __syncwarp();
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_t(a.trace, 2);
   int phase = s_phase;
   if (phase == 1) {
     // Eager: payload into the receiver's eager slot (peer stores).
@@ -410,6 +433,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     __syncwarp();
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_t(a.trace, 3);
 }
 
 // Publish a staged blocking send and race for its descriptor (whole CTA).
@@ -453,7 +477,14 @@ __device__ void stage_publish(const P2PArgs& a, Decision& dc) {
 template <bool SYS, bool INLINE>
 __global__ void __launch_bounds__(kThreads) k_proto(const P2PArgs a) {
   __shared__ Decision s_dc;
+  if (a.trace && threadIdx.x == 0) {
+    a.trace->g0 = globaltimer();
+    a.trace->t[0] = clock64();
+  }
   decide<SYS>(a, s_dc);
+  if (a.trace && threadIdx.x == 0)
+    a.trace->info = (uint64_t)a.is_recv | ((uint64_t)a.mode << 4) | ((uint64_t)INLINE << 8) |
+                    (s_dc.action << 12);
   if (!INLINE) {
     if (threadIdx.x == 0) {
       OpRecord* rec = a.rec;
@@ -480,18 +511,24 @@ __global__ void __launch_bounds__(kThreads) k_proto(const P2PArgs a) {
     cta_copy(reinterpret_cast<uint8_t*>(s_dc.dst), reinterpret_cast<const uint8_t*>(s_dc.src),
              s_dc.bytes);
     __syncthreads();
-    if (threadIdx.x == 0) s_dc.fin.run<SYS>();
+    if (threadIdx.x == 0) {
+      trace_t(a.trace, 4);
+      s_dc.fin.run<SYS>();
+      trace_t(a.trace, 5);
+      if (a.trace) a.trace->g1 = globaltimer();
+    }
   } else if (s_dc.action == ACT_STAGE) {
     cta_copy(a.staging, a.buf, a.bytes);
     __syncthreads();
     stage_publish<SYS>(a, s_dc);
-  } else if (threadIdx.x == 0 && s_dc.wait_own) {
-    spin_ge<SYS>(a.my_done, a.my_gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE);
+  } else if (threadIdx.x == 0) {
+    if (s_dc.wait_own) spin_ge<SYS>(a.my_done, a.my_gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE);
+    if (a.trace) a.trace->g1 = globaltimer();
   }
 }
 
 // Wide copy behind k_proto (PDL): never waits on anything but the stream.
-__global__ void __launch_bounds__(kCopyThreads) k_copy(const P2PArgs a) {
+__global__ void __launch_bounds__(kCopyThreads, 2) k_copy(const P2PArgs a) {
   pdl_wait();
   const OpRecord* rec = a.rec;
   const uint64_t action = rec->action;

@@ -39,6 +39,7 @@ struct Config {
   uint64_t inline_bytes = 65536;     // MPIX_INLINE_BYTES: 1-kernel path limit
   uint64_t oneshot_max = 65536;      // MPIX_ALLREDUCE_ONESHOT_MAX (bytes)
   uint64_t spin_limit_ns = 60ull * 1000 * 1000 * 1000;  // MPIX_SPIN_TIMEOUT_MS
+  bool trace = false;                // MPIX_TRACE=1: per-op device trace ring
 
   static Config from_env() {
     Config c;
@@ -51,14 +52,17 @@ struct Config {
     c.eager_bytes = (c.eager_bytes + 15) & ~15ull;
     c.ring_slots = (int)geti("MPIX_RING_SLOTS", c.ring_slots);
     if (c.ring_slots < 2) c.ring_slots = 2;
+    if (c.ring_slots > 256) c.ring_slots = 256;  // warp_scan holds 8 slots per lane
     c.inline_bytes = geti("MPIX_INLINE_BYTES", c.inline_bytes);
     c.oneshot_max = geti("MPIX_ALLREDUCE_ONESHOT_MAX", c.oneshot_max);
     c.spin_limit_ns = geti("MPIX_SPIN_TIMEOUT_MS", 60000) * 1000000ull;
+    c.trace = geti("MPIX_TRACE", 0) != 0;
     return c;
   }
 };
 
 constexpr uint64_t kReqSlots = 1ull << 20;  // completion words per rank
+constexpr uint64_t kStageSlots = 4096;      // staging buffers per rank
 
 std::atomic<uint64_t> g_launches{0};
 
@@ -109,12 +113,26 @@ struct RankState {
   std::atomic<uint64_t> req_next{0};
   OpRecord* d_rec = nullptr;
   std::atomic<uint64_t> op_next{1};
+  TraceRec* d_trace = nullptr;  // MPIX_TRACE ring
+  std::atomic<uint64_t> trace_next{0};
   uint64_t* h_err = nullptr;  // host-mapped error word
   uint64_t* d_err = nullptr;
   cudaStream_t aux = nullptr;      // setup work
-  cudaStream_t reclaim = nullptr;  // staging release
   cudaMemPool_t pool = nullptr;
   std::mutex mu;
+  // Staging buffers for large blocking sends whose receive is not posted yet
+  // (the eager contract, proj/src/proc_p2p.cpp:60-62). Buffer b is released
+  // when the consumer of the staged copy writes h_stage[b] >= its gen; the
+  // flags live in host-mapped memory so the host reclaims without syncing.
+  struct StageBuf {
+    uint8_t* p = nullptr;
+    uint64_t size = 0;
+    uint64_t gen = 0;  // last use; free when h_stage[b] >= gen
+  };
+  uint64_t* h_stage = nullptr;
+  uint64_t* d_stage = nullptr;
+  std::vector<StageBuf> stage;
+  std::mutex stage_mu;
   // request table: slot -> issuing stream, for STREAM_MISMATCH
   struct ReqInfo {
     uint64_t gen = 0;
@@ -257,13 +275,18 @@ int rank_init(RankState& r, const Config& cfg) {
   CK(cudaMemset(r.d_done, 0, kReqSlots * sizeof(uint64_t)));
   CK(cudaMalloc(&r.d_rec, kOpRecords * sizeof(OpRecord)));
   CK(cudaMemset(r.d_rec, 0, kOpRecords * sizeof(OpRecord)));
+  if (cfg.trace) {
+    CK(cudaMalloc(&r.d_trace, kTraceRecs * sizeof(TraceRec)));
+    CK(cudaMemset(r.d_trace, 0, kTraceRecs * sizeof(TraceRec)));
+  }
   CK(cudaHostAlloc(&r.h_err, 64, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(r.h_err, 0, 64);
   CK(cudaHostGetDevicePointer(&r.d_err, r.h_err, 0));
   CK(cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&r.reclaim, cudaStreamNonBlocking));
+  CK(cudaHostAlloc(&r.h_stage, kStageSlots * sizeof(uint64_t), cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(r.h_stage, 0, kStageSlots * sizeof(uint64_t));
+  CK(cudaHostGetDevicePointer(&r.d_stage, r.h_stage, 0));
   r.reqs.resize(kReqSlots);
-  (void)cfg;
   if (preload_kernels() != 0) return MPIX_ERR_CUDA;
   MPIXT_Preload();
   CK(cudaDeviceSynchronize());
@@ -428,6 +451,35 @@ bool decode_ticket(uint64_t h, int* rank, uint64_t* n) {
   return true;
 }
 
+// A staging buffer of >= bytes for a staged blocking send (stream-ordered
+// allocation on first use, cached afterwards).
+int acquire_staging(RankState& rs, uint64_t bytes, cudaStream_t s, uint8_t** p, uint64_t** flag,
+                    uint64_t* gen) {
+  std::lock_guard<std::mutex> lk(rs.stage_mu);
+  int best = -1;
+  for (size_t b = 0; b < rs.stage.size(); ++b) {
+    auto& sb = rs.stage[b];
+    bool free = *reinterpret_cast<volatile uint64_t*>(&rs.h_stage[b]) >= sb.gen;
+    if (free && sb.size >= bytes && (best < 0 || sb.size < rs.stage[best].size)) best = (int)b;
+  }
+  if (best < 0) {
+    if (rs.stage.size() >= kStageSlots) return MPIX_ERR_NO_MEM;
+    uint64_t size = 1ull << 20;
+    while (size < bytes) size <<= 1;
+    RankState::StageBuf sb;
+    if (cudaMallocFromPoolAsync((void**)&sb.p, size, rs.pool, s) != cudaSuccess) return MPIX_ERR_NO_MEM;
+    sb.size = size;
+    rs.stage.push_back(sb);
+    best = (int)rs.stage.size() - 1;
+  }
+  auto& sb = rs.stage[best];
+  sb.gen += 1;
+  *p = sb.p;
+  *flag = rs.d_stage + best;
+  *gen = sb.gen;
+  return MPI_SUCCESS;
+}
+
 // Point-to-point enqueue (send side and receive side).
 int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
                 bool is_recv, bool blocking, MPI_Request* req) {
@@ -489,14 +541,18 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     a.my_done = t.flag;
     a.my_gen = t.gen;
   }
-  Ticket st{};
-  uint8_t* staging = nullptr;
   if (a.mode == MODE_STAGED && !is_recv) {
-    CK(cudaMallocFromPoolAsync((void**)&staging, bytes ? bytes : 16, rs.pool, s));
-    st = new_ticket(rs, rs.reclaim, me, tag, sys);
-    a.staging = staging;
-    a.stage_done = st.flag;
-    a.stage_gen = st.gen;
+    int rc2 = acquire_staging(rs, bytes, s, &a.staging, &a.stage_done, &a.stage_gen);
+    if (rc2) return rc2;
+  }
+  if (rs.d_trace) {
+    uint64_t n = rs.trace_next.fetch_add(1);
+    a.trace = rs.d_trace + (n % kTraceRecs);
+    TraceRec head = {};
+    head.seq = n + 1;
+    head.bytes = bytes;
+    head.key = a.key;
+    CK(cudaMemcpyAsync(a.trace, &head, 32, cudaMemcpyHostToDevice, s));
   }
   const bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
   if (!inl) {
@@ -507,26 +563,6 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   int nk = launch_p2p(a, sys, inl, inl ? 1 : p2p_copy_grid(bytes), s);
   if (nk < 0) return MPIX_ERR_CUDA;
   g_launches.fetch_add(nk);
-  if (staging) {
-    // Release the staging copy once its consumer signals (stream-ordered
-    // after this kernel so the allocator sees the dependency).
-    cudaEvent_t ev;
-    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    CK(cudaEventRecord(ev, s));
-    CK(cudaStreamWaitEvent(rs.reclaim, ev, 0));
-    CK(cudaEventDestroy(ev));
-    WaitArgs* wa = new WaitArgs;
-    wa->n = 1;
-    wa->err_word = rs.d_err;
-    wa->spin_limit_ns = w.cfg.spin_limit_ns;
-    wa->e[0].flag = st.flag;
-    wa->e[0].gen = st.gen;
-    int e = launch_wait(*wa, sys, rs.reclaim);
-    delete wa;
-    if (e < 0) return MPIX_ERR_CUDA;
-    g_launches.fetch_add(1);
-    CK(cudaFreeAsync(staging, rs.reclaim));
-  }
   if (req) *req = (!blocking) ? t.handle : MPI_REQUEST_NULL;
   return MPI_SUCCESS;
 }
@@ -791,13 +827,14 @@ int MPIX_World_finalize(void) {
   for (auto* c : w->world_comms) delete c;
   for (auto& rs : w->ranks) {
     cudaSetDevice(rs->device);
+    for (auto& sb : rs->stage) cudaFreeAsync(sb.p, rs->aux);
     cudaStreamSynchronize(rs->aux);
-    cudaStreamSynchronize(rs->reclaim);
     cudaFree(rs->d_done);
     cudaFree(rs->d_rec);
+    if (rs->d_trace) cudaFree(rs->d_trace);
     cudaFreeHost(rs->h_err);
     cudaStreamDestroy(rs->aux);
-    cudaStreamDestroy(rs->reclaim);
+    cudaFreeHost(rs->h_stage);
     if (rs->pool) cudaMemPoolDestroy(rs->pool);
   }
   delete w;
@@ -1113,6 +1150,22 @@ int MPIX_Rank_error(int rank, uint64_t* code) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
   if (rank < 0 || rank >= g_world->n || !code) return MPIX_ERR_INVALID_RANK;
   *code = *reinterpret_cast<volatile uint64_t*>(g_world->ranks[rank]->h_err);
+  return MPI_SUCCESS;
+}
+
+int MPIX_Trace_read(int rank, void* out, int max_records, int* n_records) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (rank < 0 || rank >= g_world->n) return MPIX_ERR_INVALID_RANK;
+  RankState& rs = *g_world->ranks[rank];
+  if (!rs.d_trace) {
+    if (n_records) *n_records = 0;
+    return MPI_SUCCESS;
+  }
+  int n = (int)std::min<uint64_t>({(uint64_t)max_records, rs.trace_next.load(), kTraceRecs});
+  CK(cudaSetDevice(rs.device));
+  CK(cudaDeviceSynchronize());
+  if (n > 0) CK(cudaMemcpy(out, rs.d_trace, (size_t)n * sizeof(TraceRec), cudaMemcpyDeviceToHost));
+  if (n_records) *n_records = n;
   return MPI_SUCCESS;
 }
 

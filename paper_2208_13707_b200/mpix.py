@@ -114,6 +114,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIX_Version": (C.c_char_p, []),
         "MPIX_Rank_error": (I, [I, C.POINTER(U64)]),
         "MPIX_Comm_region": (I, [P, C.POINTER(P), C.POINTER(U64)]),
+        "MPIX_Trace_read": (I, [I, P, I, C.POINTER(I)]),
         "MPIXT_Copy_to_host": (I, [P, P, U64]),
         "MPIXT_Fill_pattern": (I, [P, U64, U32, U32, P]),
         "MPIXT_Checksum": (I, [P, U64, P, P]),
@@ -166,6 +167,21 @@ def rank_error(rank: int) -> int:
     v = C.c_uint64()
     check(lib().MPIX_Rank_error(rank, C.byref(v)))
     return v.value
+
+
+def trace_read(rank: int, max_records: int = 4096):
+    """Per-op trace records of `rank` (MPIX_TRACE=1) as dicts."""
+    import struct
+    buf = C.create_string_buffer(128 * max_records)
+    n = C.c_int()
+    check(lib().MPIX_Trace_read(rank, buf, max_records, C.byref(n)))
+    out = []
+    for i in range(n.value):
+        f = struct.unpack_from("<16Q", buf.raw, 128 * i)
+        out.append({"seq": f[0], "is_recv": f[1] & 15, "mode": (f[1] >> 4) & 15,
+                    "inline": (f[1] >> 8) & 15, "action": (f[1] >> 12) & 15, "bytes": f[2],
+                    "key": f[3], "t": list(f[4:10]), "g0": f[10], "g1": f[11]})
+    return out
 
 
 def config() -> dict:

@@ -170,6 +170,18 @@ __global__ void k_prims(uint64_t* buf, uint64_t* out, int iters) {
 
 __global__ void k_empty() {}
 
+// non-persistent tiles: CTA b copies TILE_VEC vectors (UNROLL per thread)
+template <int THREADS, int UNROLL>
+__global__ void __launch_bounds__(THREADS) k_tile(uint4* __restrict__ dst, const uint4* __restrict__ src, uint64_t nvec) {
+  uint64_t base = (uint64_t)blockIdx.x * THREADS * UNROLL + threadIdx.x;
+  uint4 v[UNROLL];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) if (base + u * THREADS < nvec) v[u] = src[base + u * THREADS];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) if (base + u * THREADS < nvec) dst[base + u * THREADS] = v[u];
+}
+__global__ void k_exit_if(const uint64_t* flag) { if (*flag == 0) return; }
+
 template <typename F>
 float time_it(F f, int iters) {
   cudaEvent_t a, b;
@@ -215,6 +227,20 @@ int main() {
   }
   // torch-like: one vector per thread, huge grid
   rep("gs<1> thr=128 grid=nvec/128", time_it([&] { k_copy_gs<1><<<(unsigned)(nvec / 128), 128>>>((uint4*)b, (uint4*)a, nvec); }, 20));
+  rep("tile<128,1>", time_it([&] { k_tile<128, 1><<<(unsigned)(nvec / 128), 128>>>((uint4*)b, (uint4*)a, nvec); }, 20));
+  rep("tile<256,1>", time_it([&] { k_tile<256, 1><<<(unsigned)(nvec / 256), 256>>>((uint4*)b, (uint4*)a, nvec); }, 20));
+  rep("tile<256,2>", time_it([&] { k_tile<256, 2><<<(unsigned)(nvec / 512), 256>>>((uint4*)b, (uint4*)a, nvec); }, 20));
+  rep("tile<256,4>", time_it([&] { k_tile<256, 4><<<(unsigned)(nvec / 1024), 256>>>((uint4*)b, (uint4*)a, nvec); }, 20));
+  rep("tile<256,8>", time_it([&] { k_tile<256, 8><<<(unsigned)(nvec / 2048), 256>>>((uint4*)b, (uint4*)a, nvec); }, 20));
+  rep("tile<512,4>", time_it([&] { k_tile<512, 4><<<(unsigned)(nvec / 2048), 512>>>((uint4*)b, (uint4*)a, nvec); }, 20));
+  rep("tile<1024,2>", time_it([&] { k_tile<1024, 2><<<(unsigned)(nvec / 2048), 1024>>>((uint4*)b, (uint4*)a, nvec); }, 20));
+  {
+    uint64_t* z;
+    cudaMalloc(&z, 8);
+    cudaMemset(z, 0, 8);
+    for (unsigned g : {148u, 1184u, 4096u, 16384u, 131072u})
+      printf("empty-exit grid %6u x256: %.2f us\n", g, time_it([&] { k_exit_if<<<g, 256>>>(z); }, 50) * 1e3);
+  }
   rep("cudaMemcpyAsync D2D", time_it([&] { cudaMemcpyAsync(b, a, n, cudaMemcpyDeviceToDevice); }, 20));
   {
     constexpr int CH = 32768, ST = 4;
