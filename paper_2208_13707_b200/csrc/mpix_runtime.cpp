@@ -40,6 +40,7 @@ struct Config {
   uint64_t oneshot_max = 65536;      // MPIX_ALLREDUCE_ONESHOT_MAX (bytes)
   uint64_t spin_limit_ns = 60ull * 1000 * 1000 * 1000;  // MPIX_SPIN_TIMEOUT_MS
   bool trace = false;                // MPIX_TRACE=1: per-op device trace ring
+  bool force_sys = false;            // MPIX_FORCE_SYS=1: system scope even on one GPU
 
   static Config from_env() {
     Config c;
@@ -57,6 +58,7 @@ struct Config {
     c.oneshot_max = geti("MPIX_ALLREDUCE_ONESHOT_MAX", c.oneshot_max);
     c.spin_limit_ns = geti("MPIX_SPIN_TIMEOUT_MS", 60000) * 1000000ull;
     c.trace = geti("MPIX_TRACE", 0) != 0;
+    c.force_sys = geti("MPIX_FORCE_SYS", 0) != 0;
     return c;
   }
 };
@@ -532,7 +534,7 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   }
   a.key = ((uint64_t)(uint32_t)tag << 32) | tseq;
 
-  const bool sys = rank_of(peer).device != rs.device;
+  const bool sys = w.cfg.force_sys || rank_of(peer).device != rs.device;
   CK(cudaSetDevice(rs.device));
   cudaStream_t s = c->cu;
   Ticket t{};
@@ -682,7 +684,7 @@ int allreduce_enqueue(const void* sbuf, void* rbuf, int count, MPI_Datatype dt, 
     a.rec = rs.d_rec + (opid % kOpRecords);
     a.opid = opid;
   }
-  bool sys = false;
+  bool sys = g_world->cfg.force_sys;
   for (int q = 0; q < P; ++q) sys |= rank_of(q).device != rs.device;
   CK(cudaSetDevice(rs.device));
   int nk = launch_allreduce(a, sys, ar_reduce_grid(work), c->cu);

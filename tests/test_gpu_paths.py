@@ -17,6 +17,9 @@ VARIANTS = {
     "tiny_eager": {"MPIX_EAGER_BYTES": "16"},
     "tiny_ring": {"MPIX_RING_SLOTS": "2"},
     "ring3_split": {"MPIX_RING_SLOTS": "3", "MPIX_INLINE_BYTES": "0", "MPIX_EAGER_BYTES": "0"},
+    # the cross-GPU (system-scope) kernel instantiations, on one GPU
+    "sys_scope": {"MPIX_FORCE_SYS": "1"},
+    "sys_scope_split": {"MPIX_FORCE_SYS": "1", "MPIX_INLINE_BYTES": "0", "MPIX_RING_SLOTS": "4"},
 }
 
 
