@@ -355,6 +355,8 @@ def bench_world(args):
         line["cpu_baseline"] = cpu_reference_selfmsg(S, args.cpu_seconds)
     sync()
     w.finalize()
+    if not args.no_extras and P == 1:
+        line["extras"].update(extras_multirank(args, mpix, torch))
     return line
 
 
@@ -452,6 +454,116 @@ def extras(args, mpix, torch, w, ctx):
     t_chain = timed(chain, 200, s0)
     out["inloop_self_chain_us"] = t_chain * 1e6
     out["inloop_self_chain_over_floor_us"] = (t_chain - 4 * t_empty) * 1e6
+    return out
+
+
+def extras_multirank(args, mpix, torch):
+    """cfg3 / cfg4 / cfg5 on the visible GPU(s); ranks share GPUs when fewer
+    than 8 are visible (numbers are then HBM-bound, not NVLink-bound)."""
+    from paper_2208_13707_b200.workloads import HaloStencil, msgrate
+    out = {}
+    ndev = torch.cuda.device_count()
+
+    def world(P):
+        devs = [r % ndev for r in range(P)]
+        w = mpix.World(P, devs)
+        ctx = {}
+
+        def setup(r):
+            with torch.cuda.device(devs[r]):
+                s = torch.cuda.Stream(device=devs[r])
+            ctx[r] = (s, w.comm(r).stream_comm_create(mpix.Stream.from_cuda(s)), devs[r])
+        w.run_ranks(setup)
+        return w, ctx
+
+    def sync_all(ctx):
+        for s, _, _ in ctx.values():
+            s.synchronize()
+
+    # cfg3: Allreduce_enqueue 256 MiB fp32 and bf16 at P = 1, 2, 4, 8
+    ar = {}
+    for P in (1, 2, 4, 8):
+        w, ctx = world(P)
+        for dt, tdt, mdt in (("f32", torch.float32, mpix.MPI_FLOAT), ("bf16", torch.bfloat16, mpix.MPIX_BFLOAT16)):
+            nbytes = 256 << 20
+            cnt = nbytes // torch.tensor([], dtype=tdt).element_size()
+            sb = {r: torch.ones(cnt, dtype=tdt, device=ctx[r][2]) for r in range(P)}
+            rb = {r: torch.empty(cnt, dtype=tdt, device=ctx[r][2]) for r in range(P)}
+            def one():
+                w.run_ranks(lambda r: ctx[r][1].allreduce_enqueue(sb[r], rb[r], cnt, mdt))
+            one()
+            sync_all(ctx)
+            ev = {r: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for r in range(P)}
+            iters = 5
+            for r in range(P):
+                ev[r][0].record(ctx[r][0])
+            for _ in range(iters):
+                one()
+            for r in range(P):
+                ev[r][1].record(ctx[r][0])
+            sync_all(ctx)
+            t = max(a.elapsed_time(b) for a, b in ev.values()) / 1e3 / iters
+            algbw = nbytes / t / 1e9
+            ar[f"{dt}_P{P}"] = {"ms": t * 1e3, "algbw_GBps": algbw,
+                                "busbw_GBps": algbw * 2 * (P - 1) / P,
+                                "ranks_per_gpu": -(-P // ndev),
+                                "check": float(rb[0][0]) == float(P)}
+            del sb, rb
+        w.finalize()
+    out["allreduce_256MiB"] = ar
+
+    # cfg5: 3-D halo stencil, 2x2x2 periodic, 512^3 fp32 per rank
+    n = 512 if ndev >= 8 else 256
+    w, ctx = world(8)
+    blocks = {r: HaloStencil(r, n, ctx[r][0], ctx[r][1], device=ctx[r][2]) for r in range(8)}
+    w.run_ranks(lambda r: blocks[r].step())
+    sync_all(ctx)
+    steps = 5
+    e = {r: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for r in range(8)}
+    for r in range(8):
+        e[r][0].record(ctx[r][0])
+    w.run_ranks(lambda r: [blocks[r].step() for _ in range(steps)])
+    for r in range(8):
+        e[r][1].record(ctx[r][0])
+    sync_all(ctx)
+    t_step = max(a.elapsed_time(b) for a, b in e.values()) / 1e3 / steps
+    for r in range(8):
+        e[r][0].record(ctx[r][0])
+    for r in range(8):
+        for _ in range(steps):
+            mpix.testing.stencil7(blocks[r].u, blocks[r].v, n, n, n, 0.5, 0.1, ctx[r][0])
+    for r in range(8):
+        e[r][1].record(ctx[r][0])
+    sync_all(ctx)
+    t_comp = max(a.elapsed_time(b) for a, b in e.values()) / 1e3 / steps
+    out["halo3d"] = {"block": f"{n}^3 fp32 per rank, 8 ranks 2x2x2 periodic",
+                     "ranks_per_gpu": -(-8 // ndev), "step_ms": t_step * 1e3,
+                     "stencil_only_ms": t_comp * 1e3, "comm_overhead_ms": (t_step - t_comp) * 1e3,
+                     "face_bytes": n * n * 4}
+    del blocks
+    w.finalize()
+
+    # cfg4: 8 ranks x 4 stream comms, ring, 8-byte messages, window 64
+    P, S, W, B = 8, 4, 64, 10
+    devs = [r % ndev for r in range(P)]
+    w = mpix.World(P, devs)
+    ctxs = [[] for _ in range(P)]
+
+    def setup(r):
+        for k in range(S):
+            with torch.cuda.device(devs[r]):
+                s = torch.cuda.Stream(device=devs[r])
+            ctxs[r].append((s, w.comm(r).stream_comm_create(mpix.Stream.from_cuda(s))))
+    w.run_ranks(setup)
+    bufs = [[(torch.zeros(2, dtype=torch.int32, device=devs[r]),
+              torch.zeros((W, 2), dtype=torch.int32, device=devs[r])) for _ in range(S)] for r in range(P)]
+    msgrate(w, ctxs, S, W, 1, bufs)
+    res = msgrate(w, ctxs, S, W, B, bufs)
+    for d in range(ndev):
+        torch.cuda.synchronize(d)
+    out["msgrate_8B"] = {"ranks": P, "streams_per_rank": S, "window": W, **res,
+                         "bound": "host enqueue (one kernel launch per operation)"}
+    w.finalize()
     return out
 
 

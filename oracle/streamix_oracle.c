@@ -347,10 +347,14 @@ void orc_stencil7(const float *u, float *out, int nx, int ny, int nz, float w0, 
     for (int y = 1; y <= ny; ++y)
       for (int x = 1; x <= nx; ++x) {
         uint64_t c = hidx(x, y, z, nx, ny);
-        float s = u[c - sx] + u[c + sx];
-        s += u[c - sy] + u[c + sy];
-        s += u[c - sz] + u[c + sz];
-        out[c] = w0 * u[c] + w1 * s;
+        volatile float a = u[c - sx] + u[c + sx];
+        volatile float b = u[c - sy] + u[c + sy];
+        volatile float d = u[c - sz] + u[c + sz];
+        volatile float s = a + b;
+        s = s + d;
+        volatile float p0 = w0 * u[c];
+        volatile float p1 = w1 * s;
+        out[c] = p0 + p1;
       }
 }
 

@@ -151,10 +151,11 @@ __global__ void k_stencil7(const float* __restrict__ u, float* __restrict__ out,
   if (x > nx) return;
   const uint64_t sx = 1, sy = nx + 2, sz = (uint64_t)(nx + 2) * (ny + 2);
   uint64_t c = hidx(x, y, z, nx, ny);
-  float s = u[c - sx] + u[c + sx];
-  s += u[c - sy] + u[c + sy];
-  s += u[c - sz] + u[c + sz];
-  out[c] = w0 * u[c] + w1 * s;
+  // explicit roundings (no FMA contraction): bit-identical to orc_stencil7
+  float s = __fadd_rn(u[c - sx], u[c + sx]);
+  s = __fadd_rn(s, __fadd_rn(u[c - sy], u[c + sy]));
+  s = __fadd_rn(s, __fadd_rn(u[c - sz], u[c + sz]));
+  out[c] = __fadd_rn(__fmul_rn(w0, u[c]), __fmul_rn(w1, s));
 }
 
 int grid_for(uint64_t n, int threads) {

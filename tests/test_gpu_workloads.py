@@ -1,0 +1,106 @@
+"""GPU: BASELINE.json configs 4 and 5 end to end, checked against the oracle.
+
+cfg5 (halo stencil): 8 ranks in a 2x2x2 periodic decomposition (all on the
+visible GPUs). After every exchange each halo must equal the neighbour's
+boundary layer bit for bit; the stencil is bit-exact with orc_stencil7 (no
+FMA contraction on either side), so after k steps the whole distributed field
+equals the oracle's global periodic stencil.
+cfg4 (message rate): 8 ranks x 4 stream comms, ring neighbours, window 64;
+every 8-byte payload must arrive.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2208_13707_b200 import mpix
+from paper_2208_13707_b200.workloads import HaloStencil, coords, msgrate
+from tests.gpu_util import gpu_world, sync_all
+
+pytestmark = pytest.mark.gpu
+
+
+def global_step(g, w0, w1):
+    """Oracle: one periodic 7-point step of the global field g (N^3),
+    through orc_stencil7 on a padded copy."""
+    N = g.shape[0]
+    p = np.pad(g, 1, mode="wrap").astype(np.float32)
+    out = O.stencil7(p.reshape(-1), N, N, N, w0, w1).reshape(N + 2, N + 2, N + 2)
+    return out[1:-1, 1:-1, 1:-1].copy()
+
+
+@pytest.mark.parametrize("n", [6, 17])
+def test_halo_stencil_matches_global_oracle(n):
+    P = 8
+    N = 2 * n
+    rng = np.random.default_rng(n)
+    g = rng.uniform(-1, 1, (N, N, N)).astype(np.float32)  # [z][y][x]
+    with gpu_world(P) as (w, ctx):
+        blocks = []
+        for r in range(P):
+            b = HaloStencil(r, n, ctx[r].stream, ctx[r].comm)
+            cx, cy, cz = coords(r)
+            pad = np.zeros((n + 2, n + 2, n + 2), dtype=np.float32)
+            pad[1:-1, 1:-1, 1:-1] = g[cz * n:(cz + 1) * n, cy * n:(cy + 1) * n, cx * n:(cx + 1) * n]
+            b.u.copy_(torch.from_numpy(pad.reshape(-1)).to(0))
+            blocks.append(b)
+        torch.cuda.synchronize()
+        steps = 3
+        w.run_ranks(lambda r: [blocks[r].step() for _ in range(steps)])
+        sync_all(ctx)
+        exp = g
+        for _ in range(steps):
+            exp = global_step(exp, HaloStencil.W0, HaloStencil.W1)
+        got = np.zeros_like(g)
+        for r in range(P):
+            cx, cy, cz = coords(r)
+            blk = blocks[r].u.cpu().numpy().reshape(n + 2, n + 2, n + 2)[1:-1, 1:-1, 1:-1]
+            got[cz * n:(cz + 1) * n, cy * n:(cy + 1) * n, cx * n:(cx + 1) * n] = blk
+        assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+
+
+def test_halo_faces_bit_exact_after_exchange():
+    P, n = 8, 9
+    with gpu_world(P) as (w, ctx):
+        blocks = [HaloStencil(r, n, ctx[r].stream, ctx[r].comm) for r in range(P)]
+        for r, b in enumerate(blocks):
+            b.u.copy_(torch.arange(b.u.numel(), dtype=torch.float32, device=0) + 1000 * r)
+        torch.cuda.synchronize()
+        w.run_ranks(lambda r: blocks[r].exchange())
+        sync_all(ctx)
+        from paper_2208_13707_b200.workloads import OPP, neighbour
+        for r in range(P):
+            for d in range(6):
+                q = neighbour(r, d)
+                # my halo d == neighbour's packed face OPP(d) (its interior layer)
+                assert torch.equal(blocks[r].rbuf[d].cpu(), blocks[q].sbuf[OPP[d]].cpu()), (r, d)
+
+
+def test_msgrate_ring_all_messages_arrive():
+    P, S, W, B = 8, 4, 64, 3
+    with gpu_world(P) as (w, ctx0):
+        ctxs = [[] for _ in range(P)]
+        bufs = [[] for _ in range(P)]
+
+        def setup(r):
+            for k in range(S):
+                s = torch.cuda.Stream(device=0)
+                c = w.comm(r).stream_comm_create(mpix.Stream.from_cuda(s))
+                ctxs[r].append((s, c))
+
+        # comm creation is collective per stream index: all ranks create comm k together
+        w.run_ranks(setup)
+        for r in range(P):
+            for k in range(S):
+                sb = torch.tensor([r, k], dtype=torch.int32, device=0)
+                rb = torch.full((W, 2), -1, dtype=torch.int32, device=0)
+                bufs[r].append((sb, rb))
+        torch.cuda.synchronize()
+        res = msgrate(w, ctxs, S, W, B, bufs)
+        torch.cuda.synchronize()
+        assert res["messages"] == P * S * W * B
+        for r in range(P):
+            left = (r + P - 1) % P
+            for k in range(S):
+                rb = bufs[r][k][1].cpu()
+                assert bool((rb[:, 0] == left).all()) and bool((rb[:, 1] == k).all()), (r, k)
