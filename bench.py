@@ -30,6 +30,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # see paper_2208_13707_b200/mpix.py
 sys.path.insert(0, ROOT)
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
@@ -223,7 +224,7 @@ def bench_world(args):
 
     def setup(r):
         with torch.cuda.device(r):
-            s = torch.cuda.Stream(device=r)
+            s = mpix.testing.new_stream(r)
         ms = mpix.Stream.from_cuda(s)
         c = w.comm(r).stream_comm_create(ms)
         ctx[r] = (s, ms, c)
@@ -424,9 +425,12 @@ def extras(args, mpix, torch, w, ctx):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / 1e3 / iters
 
-    # launch floor: back-to-back empty kernels in one stream
-    t_empty = timed(lambda i=0: mpix.testing.empty(s0), 200, s0)
+    # launch floor: back-to-back empty kernels in one stream (native loop)
+    mpix.testing.empty_loop(50, s0)
+    dev, host = mpix.testing.empty_loop(2000, s0)
+    t_empty = dev / 2000
     out["launch_floor_us"] = t_empty * 1e6
+    out["launch_floor_host_us"] = host / 2000 * 1e6
 
     # loopback sweep (Isend/Irecv/Waitall on one stream)
     sweep = {}
@@ -442,18 +446,15 @@ def extras(args, mpix, torch, w, ctx):
                           peaks().get("hbm_gbs", 6650.0)}
     out["loopback_sweep"] = sweep
 
-    # in-stream latency: producer -> Send_enqueue -> Recv_enqueue -> consumer (8 B)
-    prod = torch.zeros(2, dtype=torch.int32, device=0)
-    cons = torch.zeros(2, dtype=torch.int32, device=0)
-
-    def chain(i=0):
-        mpix.testing.fill_f32(prod, 2, float(i), s0)
-        c0.send_enqueue(prod, 2, mpix.MPI_INT, 0, 9)
-        c0.recv_enqueue(cons, 2, mpix.MPI_INT, 0, 9)
-        mpix.testing.fill_f32(cons, 0, 0.0, s0)  # consumer kernel
-    t_chain = timed(chain, 200, s0)
-    out["inloop_self_chain_us"] = t_chain * 1e6
-    out["inloop_self_chain_over_floor_us"] = (t_chain - 4 * t_empty) * 1e6
+    # in-stream latency: producer -> Send_enqueue -> Recv_enqueue -> consumer
+    # (8 B self message, one stream, native driver so the host runs ahead)
+    prod = torch.zeros(2, dtype=torch.float32, device=0)
+    cons = torch.zeros(2, dtype=torch.float32, device=0)
+    mpix.testing.selfchain(c0, prod, cons, 2, 50, s0)
+    dev, host = mpix.testing.selfchain(c0, prod, cons, 2, 1000, s0)
+    out["inloop_self_chain_us"] = dev / 1000 * 1e6
+    out["inloop_self_chain_host_us"] = host / 1000 * 1e6
+    out["inloop_self_chain_over_floor_us"] = (dev / 1000 - 4 * t_empty) * 1e6
     return out
 
 
@@ -471,7 +472,7 @@ def extras_multirank(args, mpix, torch):
 
         def setup(r):
             with torch.cuda.device(devs[r]):
-                s = torch.cuda.Stream(device=devs[r])
+                s = mpix.testing.new_stream(devs[r])
             ctx[r] = (s, w.comm(r).stream_comm_create(mpix.Stream.from_cuda(s)), devs[r])
         w.run_ranks(setup)
         return w, ctx
@@ -479,6 +480,24 @@ def extras_multirank(args, mpix, torch):
     def sync_all(ctx):
         for s, _, _ in ctx.values():
             s.synchronize()
+
+    # cfg2 latency: blocking Send/Recv_enqueue ping-pong between 2 ranks
+    # (both on GPU 0 unless 2 GPUs are visible), half round trip
+    w, ctx = world(2)
+    pp = {}
+    for nb in (8, 4096, 65536, 1 << 20):
+        b0 = torch.zeros(max(nb, 16), dtype=torch.uint8, device=ctx[0][2])
+        b1 = torch.zeros(max(nb, 16), dtype=torch.uint8, device=ctx[1][2])
+        mpix.testing.pingpong(ctx[0][1], ctx[1][1], b0, b1, nb, 20, ctx[0][0], ctx[1][0],
+                              ctx[0][2], ctx[1][2])
+        iters = 500 if nb <= 65536 else 100
+        dev, host = mpix.testing.pingpong(ctx[0][1], ctx[1][1], b0, b1, nb, iters, ctx[0][0],
+                                          ctx[1][0], ctx[0][2], ctx[1][2])
+        pp[str(nb)] = {"half_rtt_us": dev / (2 * iters) * 1e6,
+                       "host_us_per_half_rtt": host / (2 * iters) * 1e6}
+    sync_all(ctx)
+    w.finalize()
+    out["pingpong_2ranks"] = {"gpus": len({ctx[0][2], ctx[1][2]}), **pp}
 
     # cfg3: Allreduce_enqueue 256 MiB fp32 and bf16 at P = 1, 2, 4, 8
     ar = {}
@@ -544,7 +563,7 @@ def extras_multirank(args, mpix, torch):
     w.finalize()
 
     # cfg4: 8 ranks x 4 stream comms, ring, 8-byte messages, window 64
-    P, S, W, B = 8, 4, 64, 10
+    P, S, W, B = 8, 4, 64, 50
     devs = [r % ndev for r in range(P)]
     w = mpix.World(P, devs)
     ctxs = [[] for _ in range(P)]
@@ -552,7 +571,7 @@ def extras_multirank(args, mpix, torch):
     def setup(r):
         for k in range(S):
             with torch.cuda.device(devs[r]):
-                s = torch.cuda.Stream(device=devs[r])
+                s = mpix.testing.new_stream(devs[r])
             ctxs[r].append((s, w.comm(r).stream_comm_create(mpix.Stream.from_cuda(s))))
     w.run_ranks(setup)
     bufs = [[(torch.zeros(2, dtype=torch.int32, device=devs[r]),
@@ -562,7 +581,8 @@ def extras_multirank(args, mpix, torch):
     for d in range(ndev):
         torch.cuda.synchronize(d)
     out["msgrate_8B"] = {"ranks": P, "streams_per_rank": S, "window": W, **res,
-                         "bound": "host enqueue (one kernel launch per operation)"}
+                         "driver": "native C++ threads over the C ABI (MPIXT_Msgrate)",
+                         "launches_per_window": "1 coalesced k_batch + ceil(2W/64)-1 flushes"}
     w.finalize()
     return out
 

@@ -12,6 +12,8 @@
 
 #include <stdint.h>
 
+#include "mpix.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -25,6 +27,10 @@ int MPIXT_Checksum(const void *buf, uint64_t nbytes, uint64_t *out_dev, void *st
 int MPIXT_Saxpy(int n, float a, const float *x, float *y, void *stream);
 /* Busy-wait `ns` nanoseconds inside the stream (peer-delay tests). */
 int MPIXT_Delay(uint64_t ns, void *stream);
+/* A fresh non-blocking CUDA stream on `device` (not from torch's 32-stream
+ * pool, which aliases streams beyond 32), and its destruction. */
+int MPIXT_Stream_create(int device, void **stream);
+int MPIXT_Stream_destroy(void *stream);
 /* One empty kernel (launch-floor measurement). */
 int MPIXT_Empty(void *stream);
 /* fill float buffer: x[i] = value */
@@ -46,6 +52,25 @@ int MPIXT_Copy_to_host(void *host, const void *dev, uint64_t bytes);
 /* Load every helper kernel on the current device (called by
  * MPIX_World_init; see lazy loading in DESIGN.md). */
 int MPIXT_Preload(void);
+/* Native benchmark drivers (csrc/mpix_drivers.cpp): one host thread per
+ * rank, every call through the C ABI, device time from CUDA events.
+ * Msgrate (cfg4): P ranks x S single-stream comms (index r*S+k); per batch
+ * and stream, W x {Irecv_enqueue(left, tag i) + Isend_enqueue(right, tag i)}
+ * of 8 bytes, then Waitall_enqueue. rbufs hold W*8 bytes. host_s[0] = enqueue
+ * time, host_s[1] = until the last stream drained; *dev_s = max over streams
+ * of event time. */
+int MPIXT_Msgrate(int P, int S, int W, int batches, MPI_Comm *comms, void **streams, void **sbufs,
+                  void **rbufs, int *devices, double *host_s, double *dev_s);
+/* Blocking ping-pong of `bytes` between ranks 0 (c0, s0) and 1 (c1, s1):
+ * Send+Recv / Recv+Send, `iters` round trips; *dev_s = event time on s0. */
+int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void *b0, void *b1, uint64_t bytes, int iters,
+                   void *s0, void *s1, int dev0, int dev1, double *dev_s, double *host_s);
+/* producer kernel -> Send_enqueue -> Recv_enqueue -> consumer kernel (self
+ * messages of n floats on one stream), `iters` times. */
+int MPIXT_Selfchain(MPI_Comm c, float *prod, float *cons, int n, int iters, void *stream,
+                    double *dev_s, double *host_s);
+/* `iters` back-to-back empty kernels launched from C++ (launch floor). */
+int MPIXT_Empty_loop(int iters, void *stream, double *dev_s, double *host_s);
 /* Number of helper kernels launched so far. */
 uint64_t MPIXT_Launch_count(void);
 

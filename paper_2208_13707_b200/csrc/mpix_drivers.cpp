@@ -1,0 +1,193 @@
+// mpix_drivers.cpp — native benchmark drivers over the public C ABI
+// (include/mpix_testing.h, MPIXT_Msgrate / MPIXT_Pingpong / MPIXT_Selfchain).
+//
+// The reference's own benchmark drivers are C++ threads calling Proc methods
+// (proj/src/bench.cpp:118-235, oracle/ref_driver.cpp mirrors them for the
+// enqueue path). These do the same against include/mpix.h: one host thread
+// per rank, every call through the C ABI, device time from CUDA events on
+// the ranks' streams. Python (ctypes) would otherwise bound the host side of
+// the message-rate and latency measurements.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <thread>
+#include <vector>
+
+#include "mpix.h"
+#include "mpix_testing.h"
+
+namespace {
+
+struct Spin {  // host-thread barrier (all ranks start enqueueing together)
+  std::atomic<int> n{0};
+  int total;
+  explicit Spin(int t) : total(t) {}
+  void arrive_and_wait() {
+    n.fetch_add(1);
+    while (n.load() < total) std::this_thread::yield();
+  }
+};
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+int MPIXT_Msgrate(int P, int S, int W, int batches, MPI_Comm* comms, void** streams, void** sbufs,
+                  void** rbufs, int* devices, double* host_s, double* dev_s) {
+  if (P < 1 || S < 1 || W < 1 || W > 4096 || batches < 1) return MPIX_ERR_INVALID_ARG;
+  std::vector<cudaEvent_t> e0(P * S), e1(P * S);
+  for (int i = 0; i < P * S; ++i) {
+    cudaSetDevice(devices[i / S]);
+    if (cudaEventCreate(&e0[i]) != cudaSuccess || cudaEventCreate(&e1[i]) != cudaSuccess)
+      return MPIX_ERR_CUDA;
+  }
+  std::atomic<int> err{0};
+  Spin go(P);
+  double t0 = 0, t1 = 0;
+  auto rank = [&](int r) {
+    cudaSetDevice(devices[r]);
+    MPIX_Rank_bind(r);
+    const int right = (r + 1) % P, left = (r + P - 1) % P;
+    std::vector<MPI_Request> reqs(2 * W);
+    for (int k = 0; k < S; ++k) cudaEventRecord(e0[r * S + k], (cudaStream_t)streams[r * S + k]);
+    go.arrive_and_wait();
+    if (r == 0) t0 = now_s();
+    for (int b = 0; b < batches && !err.load(); ++b) {
+      for (int k = 0; k < S; ++k) {
+        MPI_Comm c = comms[r * S + k];
+        uint8_t* rb = static_cast<uint8_t*>(rbufs[r * S + k]);
+        for (int i = 0; i < W; ++i) {
+          int rc = MPIX_Irecv_enqueue(rb + 8 * i, 2, MPI_INT, left, i, c, &reqs[2 * i]);
+          rc |= MPIX_Isend_enqueue(sbufs[r * S + k], 2, MPI_INT, right, i, c, &reqs[2 * i + 1]);
+          if (rc) err.store(rc);
+        }
+        int rc = MPIX_Waitall_enqueue(2 * W, reqs.data(), MPI_STATUSES_IGNORE);
+        if (rc) err.store(rc);
+      }
+    }
+    for (int k = 0; k < S; ++k) cudaEventRecord(e1[r * S + k], (cudaStream_t)streams[r * S + k]);
+  };
+  std::vector<std::thread> th;
+  for (int r = 0; r < P; ++r) th.emplace_back(rank, r);
+  for (auto& t : th) t.join();
+  t1 = now_s();
+  for (int i = 0; i < P * S; ++i) cudaEventSynchronize(e1[i]);
+  double tend = now_s();
+  float mx = 0;
+  for (int i = 0; i < P * S; ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0[i], e1[i]);
+    mx = std::max(mx, ms);
+    cudaEventDestroy(e0[i]);
+    cudaEventDestroy(e1[i]);
+  }
+  if (host_s) host_s[0] = t1 - t0, host_s[1] = tend - t0;
+  if (dev_s) *dev_s = mx / 1e3;
+  return err.load();
+}
+
+int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void* b0, void* b1, uint64_t bytes, int iters,
+                   void* s0, void* s1, int dev0, int dev1, double* dev_s, double* host_s) {
+  if (iters < 1) return MPIX_ERR_INVALID_ARG;
+  cudaEvent_t a, b;
+  cudaSetDevice(dev0);
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return MPIX_ERR_CUDA;
+  std::atomic<int> err{0};
+  Spin go(2);
+  double t0 = 0, t1 = 0;
+  const int count = (int)bytes;
+  auto side = [&](int r) {
+    cudaSetDevice(r ? dev1 : dev0);
+    MPIX_Rank_bind(r);
+    if (r == 0) cudaEventRecord(a, (cudaStream_t)s0);
+    go.arrive_and_wait();
+    if (r == 0) t0 = now_s();
+    for (int i = 0; i < iters && !err.load(); ++i) {
+      int rc;
+      if (r == 0) {
+        rc = MPIX_Send_enqueue(b0, count, MPI_BYTE, 1, 1, c0);
+        rc |= MPIX_Recv_enqueue(b0, count, MPI_BYTE, 1, 2, c0, MPI_STATUS_IGNORE);
+      } else {
+        rc = MPIX_Recv_enqueue(b1, count, MPI_BYTE, 0, 1, c1, MPI_STATUS_IGNORE);
+        rc |= MPIX_Send_enqueue(b1, count, MPI_BYTE, 0, 2, c1);
+      }
+      if (rc) err.store(rc);
+    }
+    if (r == 0) {
+      cudaEventRecord(b, (cudaStream_t)s0);
+      t1 = now_s();
+    }
+  };
+  std::thread t(side, 1);
+  side(0);
+  t.join();
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (dev_s) *dev_s = ms / 1e3;
+  if (host_s) *host_s = t1 - t0;
+  return err.load();
+}
+
+// producer kernel -> Send_enqueue -> Recv_enqueue -> consumer kernel, all on
+// one stream (self messages), `iters` times.
+int MPIXT_Selfchain(MPI_Comm c, float* prod, float* cons, int n, int iters, void* stream,
+                    double* dev_s, double* host_s) {
+  if (iters < 1) return MPIX_ERR_INVALID_ARG;
+  int me = 0;
+  MPI_Comm_rank(c, &me);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t a, b;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return MPIX_ERR_CUDA;
+  int err = 0;
+  cudaEventRecord(a, s);
+  double t0 = now_s();
+  for (int i = 0; i < iters && !err; ++i) {
+    err |= MPIXT_Fill_f32(prod, n, (float)i, s);
+    err |= MPIX_Send_enqueue(prod, n, MPI_FLOAT, me, 3, c);
+    err |= MPIX_Recv_enqueue(cons, n, MPI_FLOAT, me, 3, c, MPI_STATUS_IGNORE);
+    err |= MPIXT_Fill_f32(cons, 0, 0.f, s);  // consumer kernel
+  }
+  cudaEventRecord(b, s);
+  double t1 = now_s();
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (dev_s) *dev_s = ms / 1e3;
+  if (host_s) *host_s = t1 - t0;
+  return err;
+}
+
+// Back-to-back empty kernels from C++ (the in-stream launch floor).
+int MPIXT_Empty_loop(int iters, void* stream, double* dev_s, double* host_s) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t a, b;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return MPIX_ERR_CUDA;
+  cudaEventRecord(a, s);
+  double t0 = now_s();
+  int err = 0;
+  for (int i = 0; i < iters && !err; ++i) err |= MPIXT_Empty(s);
+  cudaEventRecord(b, s);
+  double t1 = now_s();
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (dev_s) *dev_s = ms / 1e3;
+  if (host_s) *host_s = t1 - t0;
+  return err;
+}
+
+}  // extern "C"

@@ -24,7 +24,6 @@ namespace mpix {
 
 constexpr int kThreads = 512;          // threads per CTA for every op kernel
 constexpr int kMaxCollRanks = 16;      // max communicator size for Allreduce
-constexpr int kWaitBatch = 32;         // requests per wait kernel launch (small params)
 constexpr uint64_t kOpRecords = 16384; // op-record ring entries per rank
 
 enum : uint64_t { ST_FREE = 0, ST_POSTED = 1, ST_TAKEN = 2 };
@@ -161,11 +160,38 @@ struct WaitEntry {
   uint64_t gen;
 };
 
-struct WaitArgs {
-  int n;
+// One operation of a coalesced batch (k_batch): the P2PArgs fields of an
+// inline operation, packed (112 B) because the batch travels as kernel
+// parameters.
+struct BatchOp {
+  SlotDesc* post_ring;
+  uint64_t* post_mirror;
+  SlotDesc* scan_ring;
+  uint64_t* scan_mirror;
+  uint8_t* eager_ring;
+  uint8_t* buf;
+  uint64_t bytes;
+  uint64_t key;
+  uint64_t pseq;
+  uint64_t* my_done;
+  uint64_t my_gen;
   uint64_t* err_word;
+  uint32_t E;
+  uint16_t R;
+  uint8_t is_recv, mode, blocking, pad_[3];
+};
+static_assert(sizeof(BatchOp) == 112, "BatchOp packing");
+
+constexpr int kBatchOps = 64;     // operations per coalesced launch
+constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch
+
+template <int NOPS, int NWAIT>
+struct BatchArgs {
+  int n, nwait;
   uint64_t spin_limit_ns;
-  WaitEntry e[kWaitBatch];
+  uint64_t* err_word;
+  WaitEntry w[NWAIT];
+  BatchOp ops[NOPS];
 };
 
 enum ARDtype : int { AR_I32 = 0, AR_F32 = 1, AR_BF16 = 2, AR_F64 = 3 };
@@ -197,7 +223,8 @@ struct ARArgs {
 // number of kernels launched, or -1 on a CUDA error. `sys` selects
 // system-scope primitives (some peer lives on another GPU).
 int launch_p2p(const P2PArgs& a, bool sys, bool inline_copy, uint64_t copy_grid, cudaStream_t s);
-int launch_wait(const WaitArgs& a, bool sys, cudaStream_t s);
+int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint64_t* err_word,
+                 uint64_t spin_limit_ns, bool sys, cudaStream_t s);
 int launch_allreduce(const ARArgs& a, bool sys, uint64_t reduce_grid, cudaStream_t s);
 uint64_t p2p_copy_grid(uint64_t bytes);
 uint64_t ar_reduce_grid(uint64_t work_bytes);

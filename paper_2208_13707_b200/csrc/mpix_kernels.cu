@@ -12,12 +12,14 @@
 //            small message costs exactly one launch.
 //   k_copy   large messages only; launched with programmatic dependent launch
 //            right behind k_proto, never spins: every CTA reads the decision
-//            and streams one 16-KiB tile (128-bit loads/stores, 4 in flight
+//            and streams one 64-KiB tile (128-bit loads/stores, 4 in flight
 //            per thread), push to or pull from the peer's buffer.
 //   k_fin    1 CTA, PDL: completion stores (slot frees, free-mirrors, done
 //            words) after the whole copy grid retired; publishes staged
 //            blocking sends.
-//   k_wait   Wait/Waitall_enqueue: spins on local completion words.
+//   k_batch  coalesced launch: the inline operations enqueued on a stream
+//            since its last launch (one CTA each) plus the Wait/Waitall or
+//            blocking operation that closed the batch.
 //
 // Allreduce_enqueue (no reference): k_ar_entry (1 CTA: publish buffers,
 // wait for every peer) -> k_ar_reduce (wide, rank-ordered fold, one-shot or
@@ -126,7 +128,7 @@ __device__ __forceinline__ void trace_t(TraceRec* tr, int k) {
 // Copies
 // ---------------------------------------------------------------------------
 constexpr int kCopyThreads = 1024;
-constexpr int kCopyUnroll = 2;
+constexpr int kCopyUnroll = 4;  // 64-KiB tiles (tools/copyshape.cu)
 constexpr uint64_t kTileVec = (uint64_t)kCopyThreads * kCopyUnroll;  // 16-B vectors per tile
 
 // Whole-CTA copy of n bytes (k_proto inline path and the rare staged push).
@@ -473,10 +475,11 @@ __device__ void stage_publish(const P2PArgs& a, Decision& dc) {
   }
 }
 
-// INLINE: the whole operation in this 1-CTA kernel.
+// The whole handshake of one operation (one CTA). INLINE: the copy and the
+// completion stores happen here too; otherwise the decision goes to the op
+// record for k_copy / k_fin.
 template <bool SYS, bool INLINE>
-__global__ void __launch_bounds__(kThreads) k_proto(const P2PArgs a) {
-  __shared__ Decision s_dc;
+__device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
   if (a.trace && threadIdx.x == 0) {
     a.trace->g0 = globaltimer();
     a.trace->t[0] = clock64();
@@ -527,6 +530,57 @@ __global__ void __launch_bounds__(kThreads) k_proto(const P2PArgs a) {
   }
 }
 
+template <bool SYS, bool INLINE>
+__global__ void __launch_bounds__(kThreads) k_proto(const P2PArgs a) {
+  __shared__ Decision s_dc;
+  proto_body<SYS, INLINE>(a, s_dc);
+}
+
+// A coalesced batch (host-side op batching): CTA b < n runs
+// the whole inline operation ops[b]; CTA n (if any waits) is the
+// Wait/Waitall that closed the batch. Operations of one batch are mutually
+// unordered (all non-blocking, at most one trailing blocking op), so they
+// run concurrently; the kernel retires when all of them and the wait have.
+template <bool SYS, int NOPS, int NWAIT>
+__global__ void __launch_bounds__(kThreads) k_batch(const BatchArgs<NOPS, NWAIT> b) {
+  __shared__ Decision s_dc;
+  if ((int)blockIdx.x < b.n) {
+    __shared__ P2PArgs a;
+    if (threadIdx.x == 0) {
+      const BatchOp& o = b.ops[blockIdx.x];
+      a.is_recv = o.is_recv;
+      a.mode = o.mode;
+      a.blocking = o.blocking;
+      a.R = o.R;
+      a.key = o.key;
+      a.pseq = o.pseq;
+      a.post_ring = o.post_ring;
+      a.post_mirror = o.post_mirror;
+      a.scan_ring = o.scan_ring;
+      a.scan_mirror = o.scan_mirror;
+      a.eager_ring = o.eager_ring;
+      a.E = o.E;
+      a.buf = o.buf;
+      a.bytes = o.bytes;
+      a.staging = nullptr;
+      a.my_done = o.my_done;
+      a.my_gen = o.my_gen;
+      a.stage_done = nullptr;
+      a.stage_gen = 0;
+      a.rec = nullptr;
+      a.opid = 0;
+      a.err_word = o.err_word;
+      a.spin_limit_ns = b.spin_limit_ns;
+      a.trace = nullptr;
+    }
+    __syncthreads();
+    proto_body<SYS, true>(a, s_dc);
+  } else {
+    for (int i = threadIdx.x; i < b.nwait; i += blockDim.x)
+      if (!spin_ge<SYS>(b.w[i].flag, b.w[i].gen, b.err_word, b.spin_limit_ns, ERRW_WAIT_DONE)) break;
+  }
+}
+
 // Wide copy behind k_proto (PDL): never waits on anything but the stream.
 __global__ void __launch_bounds__(kCopyThreads, 2) k_copy(const P2PArgs a) {
   pdl_wait();
@@ -559,16 +613,6 @@ __global__ void __launch_bounds__(kThreads) k_fin(const P2PArgs a) {
     }
   } else if (action == ACT_STAGE) {
     stage_publish<SYS>(a, s_dc);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Wait / Waitall
-// ---------------------------------------------------------------------------
-template <bool SYS>
-__global__ void __launch_bounds__(32) k_wait(const WaitArgs a) {
-  for (int i = threadIdx.x; i < a.n; i += 32) {
-    if (!spin_ge<SYS>(a.e[i].flag, a.e[i].gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE)) break;
   }
 }
 
@@ -916,10 +960,34 @@ int launch_p2p(const P2PArgs& a, bool sys, bool inl, uint64_t grid, cudaStream_t
   return e == cudaSuccess ? 3 : -1;
 }
 
-int launch_wait(const WaitArgs& a, bool sys, cudaStream_t s) {
-  if (sys) k_wait<true><<<1, 32, 0, s>>>(a);
-  else k_wait<false><<<1, 32, 0, s>>>(a);
+template <int NOPS, int NWAIT>
+static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwait,
+                          uint64_t* err_word, uint64_t spin_limit_ns, bool sys, cudaStream_t s) {
+  BatchArgs<NOPS, NWAIT> b;
+  b.n = n;
+  b.nwait = nwait;
+  b.spin_limit_ns = spin_limit_ns;
+  b.err_word = err_word;
+  for (int i = 0; i < n; ++i) b.ops[i] = ops[i];
+  for (int i = 0; i < nwait; ++i) b.w[i] = w[i];
+  const int grid = n + (nwait > 0 ? 1 : 0);
+  if (sys) k_batch<true, NOPS, NWAIT><<<grid, kThreads, 0, s>>>(b);
+  else k_batch<false, NOPS, NWAIT><<<grid, kThreads, 0, s>>>(b);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+// Parameter-size classes: the whole struct is copied into the launch, so
+// small batches use the small instantiations.
+int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint64_t* err_word,
+                 uint64_t spin_limit_ns, bool sys, cudaStream_t s) {
+  if (n <= 0 && nwait <= 0) return 0;
+  if (n <= 4 && nwait <= 8)
+    return launch_batch_t<4, 8>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s);
+  if (n <= 16 && nwait <= 32)
+    return launch_batch_t<16, 32>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s);
+  if (n <= kBatchOps && nwait <= kBatchWaits)
+    return launch_batch_t<kBatchOps, kBatchWaits>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s);
+  return -1;
 }
 
 uint64_t ar_reduce_grid(uint64_t work_bytes) {
@@ -954,9 +1022,12 @@ int preload_kernels() {
       (const void*)k_proto<true, true>, (const void*)k_proto<true, false>,
       (const void*)k_proto<false, true>, (const void*)k_proto<false, false>,
       (const void*)k_copy, (const void*)k_fin<true>, (const void*)k_fin<false>,
-      (const void*)k_wait<true>, (const void*)k_wait<false>,
       (const void*)k_ar_entry<true>, (const void*)k_ar_entry<false>,
-      (const void*)k_ar_reduce, (const void*)k_ar_exit<true>, (const void*)k_ar_exit<false>};
+      (const void*)k_ar_reduce, (const void*)k_ar_exit<true>, (const void*)k_ar_exit<false>,
+      (const void*)k_batch<true, 4, 8>, (const void*)k_batch<false, 4, 8>,
+      (const void*)k_batch<true, 16, 32>, (const void*)k_batch<false, 16, 32>,
+      (const void*)k_batch<true, kBatchOps, kBatchWaits>,
+      (const void*)k_batch<false, kBatchOps, kBatchWaits>};
   for (const void* k : ks) {
     cudaError_t r = cudaFuncGetAttributes(&fa, k);
     if (r != cudaSuccess) e = r;

@@ -41,6 +41,7 @@ struct Config {
   uint64_t spin_limit_ns = 60ull * 1000 * 1000 * 1000;  // MPIX_SPIN_TIMEOUT_MS
   bool trace = false;                // MPIX_TRACE=1: per-op device trace ring
   bool force_sys = false;            // MPIX_FORCE_SYS=1: system scope even on one GPU
+  bool batch = true;                 // MPIX_BATCH=0: one launch per operation
 
   static Config from_env() {
     Config c;
@@ -59,6 +60,7 @@ struct Config {
     c.spin_limit_ns = geti("MPIX_SPIN_TIMEOUT_MS", 60000) * 1000000ull;
     c.trace = geti("MPIX_TRACE", 0) != 0;
     c.force_sys = geti("MPIX_FORCE_SYS", 0) != 0;
+    c.batch = geti("MPIX_BATCH", 1) != 0;
     return c;
   }
 };
@@ -185,8 +187,26 @@ struct mpix_comm_s {
 
 namespace mpix {
 
+// Host-side op batching (DESIGN.md §3 "Coalesced launches"): inline-sized
+// non-blocking operations enqueued on a CUDA stream are held here and
+// launched together, as one k_batch, by the next call that orders that
+// stream — a blocking operation (which joins the batch as its last member),
+// a Wait/Waitall (whose wait joins it), a large operation, an allreduce,
+// MPI_Comm_free, or the batch filling up. Non-blocking operations only have
+// to start before the stream's next ordering point, so results are
+// unchanged; the launch count drops from one per operation to one per window.
+struct StreamBatch {
+  std::mutex mu;
+  int device = 0;
+  bool sys = false;
+  uint64_t* err_word = nullptr;
+  std::vector<BatchOp> ops;
+};
+
 struct World {
   Config cfg;
+  std::mutex batch_mu;
+  std::unordered_map<cudaStream_t, std::unique_ptr<StreamBatch>> batches;
   int n = 0;
   std::vector<std::unique_ptr<RankState>> ranks;
   std::vector<mpix_comm_s*> world_comms;
@@ -320,6 +340,78 @@ int rank_pool(World& w, RankState& r) {
 }
 
 World* world() { return g_world; }
+
+StreamBatch& batch_of(cudaStream_t s, int device) {
+  World& w = *g_world;
+  std::lock_guard<std::mutex> lk(w.batch_mu);
+  auto& b = w.batches[s];
+  if (!b) {
+    b.reset(new StreamBatch());
+    b->device = device;
+  }
+  return *b;
+}
+
+// Launch the held operations of `b` plus `nwait` wait entries (caller holds
+// b.mu and has selected b's device). Returns the number of launches or -1.
+int flush_locked(StreamBatch& b, cudaStream_t s, const WaitEntry* w, int nwait, bool wsys,
+                 uint64_t* w_err) {
+  const Config& cfg = g_world->cfg;
+  int launches = 0;
+  int n = (int)b.ops.size();
+  int wi = 0;
+  uint64_t* err = b.err_word ? b.err_word : w_err;
+  do {
+    int m = std::min(nwait - wi, kBatchWaits);
+    int rc = launch_batch(b.ops.data(), n, w + wi, m, err, cfg.spin_limit_ns, b.sys || wsys, s);
+    if (rc < 0) return -1;
+    launches += rc;
+    n = 0;
+    b.ops.clear();
+    wi += m;
+  } while (wi < nwait);
+  b.sys = false;
+  b.err_word = nullptr;
+  g_launches.fetch_add(launches);
+  return launches;
+}
+
+int flush_stream(cudaStream_t s) {
+  World& w = *g_world;
+  StreamBatch* b = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(w.batch_mu);
+    auto it = w.batches.find(s);
+    if (it == w.batches.end()) return 0;
+    b = it->second.get();
+  }
+  std::lock_guard<std::mutex> lk(b->mu);
+  if (b->ops.empty()) return 0;
+  if (cudaSetDevice(b->device) != cudaSuccess) return -1;
+  return flush_locked(*b, s, nullptr, 0, false, nullptr);
+}
+
+BatchOp pack_op(const P2PArgs& a) {
+  BatchOp o = {};
+  o.post_ring = a.post_ring;
+  o.post_mirror = a.post_mirror;
+  o.scan_ring = a.scan_ring;
+  o.scan_mirror = a.scan_mirror;
+  o.eager_ring = a.eager_ring;
+  o.buf = a.buf;
+  o.bytes = a.bytes;
+  o.key = a.key;
+  o.pseq = a.pseq;
+  o.my_done = a.my_done;
+  o.my_gen = a.my_gen;
+  o.err_word = a.err_word;
+  o.E = (uint32_t)a.E;
+  o.R = (uint16_t)a.R;
+  o.is_recv = (uint8_t)a.is_recv;
+  o.mode = (uint8_t)a.mode;
+  o.blocking = (uint8_t)a.blocking;
+  return o;
+}
 
 RankState& rank_of(int r) { return *g_world->ranks[r]; }
 
@@ -562,9 +654,23 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     a.rec = rs.d_rec + (op % kOpRecords);
     a.opid = op;
   }
-  int nk = launch_p2p(a, sys, inl, inl ? 1 : p2p_copy_grid(bytes), s);
-  if (nk < 0) return MPIX_ERR_CUDA;
-  g_launches.fetch_add(nk);
+  StreamBatch& b = batch_of(s, rs.device);
+  std::lock_guard<std::mutex> lk(b.mu);
+  if (w.cfg.batch && !a.trace && inl && a.mode != MODE_STAGED) {
+    // Join the stream's batch; a blocking operation closes it (it must have
+    // completed before anything behind it in the stream runs).
+    if ((int)b.ops.size() >= kBatchOps && flush_locked(b, s, nullptr, 0, false, nullptr) < 0)
+      return MPIX_ERR_CUDA;
+    if (b.ops.empty()) b.err_word = rs.d_err;
+    b.ops.push_back(pack_op(a));
+    b.sys |= sys;
+    if (blocking && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
+  } else {
+    if (!b.ops.empty() && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
+    int nk = launch_p2p(a, sys, inl, inl ? 1 : p2p_copy_grid(bytes), s);
+    if (nk < 0) return MPIX_ERR_CUDA;
+    g_launches.fetch_add(nk);
+  }
   if (req) *req = (!blocking) ? t.handle : MPI_REQUEST_NULL;
   return MPI_SUCCESS;
 }
@@ -609,21 +715,17 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
     }
   }
   CK(cudaSetDevice(dev0));
-  std::unique_ptr<WaitArgs> wa(new WaitArgs);
-  for (int i0 = 0; i0 < n; i0 += kWaitBatch) {
-    int m = std::min(kWaitBatch, n - i0);
-    wa->n = m;
-    wa->err_word = rank_of(items[i0].rank).d_err;
-    wa->spin_limit_ns = g_world->cfg.spin_limit_ns;
-    for (int k = 0; k < m; ++k) {
-      RankState& rs = rank_of(items[i0 + k].rank);
-      uint64_t nn = items[i0 + k].n;
-      wa->e[k].flag = rs.d_done + (nn % kReqSlots);
-      wa->e[k].gen = nn / kReqSlots + 1;
-    }
-    if (launch_wait(*wa, sys, s0) < 0) return MPIX_ERR_CUDA;
-    g_launches.fetch_add(1);
+  std::vector<WaitEntry> we(n);
+  for (int k = 0; k < n; ++k) {
+    RankState& rs = rank_of(items[k].rank);
+    uint64_t nn = items[k].n;
+    we[k].flag = rs.d_done + (nn % kReqSlots);
+    we[k].gen = nn / kReqSlots + 1;
   }
+  // The wait closes the stream's batch: one launch for the window.
+  StreamBatch& b = batch_of(s0, dev0);
+  std::lock_guard<std::mutex> lk(b.mu);
+  if (flush_locked(b, s0, we.data(), n, sys, rank_of(items[0].rank).d_err) < 0) return MPIX_ERR_CUDA;
   return MPI_SUCCESS;
 }
 
@@ -687,6 +789,9 @@ int allreduce_enqueue(const void* sbuf, void* rbuf, int count, MPI_Datatype dt, 
   bool sys = g_world->cfg.force_sys;
   for (int q = 0; q < P; ++q) sys |= rank_of(q).device != rs.device;
   CK(cudaSetDevice(rs.device));
+  StreamBatch& b = batch_of(c->cu, rs.device);
+  std::lock_guard<std::mutex> lk(b.mu);
+  if (!b.ops.empty() && flush_locked(b, c->cu, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
   int nk = launch_allreduce(a, sys, ar_reduce_grid(work), c->cu);
   if (nk < 0) return MPIX_ERR_CUDA;
   g_launches.fetch_add(nk);
@@ -813,6 +918,9 @@ int MPIX_World_finalize(void) {
   std::lock_guard<std::mutex> lk(g_world_mu);
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
   World* w = g_world;
+  std::vector<cudaStream_t> held;
+  for (auto& kv : w->batches) held.push_back(kv.first);
+  for (cudaStream_t s : held) flush_stream(s);
   for (auto& rs : w->ranks) {
     cudaSetDevice(rs->device);
     cudaDeviceSynchronize();
@@ -902,6 +1010,7 @@ int MPI_Comm_free(MPI_Comm* comm) {  // proc_comm.cpp:178-194
   // region is released: exchange one event per member and make each aux
   // stream wait on all of them.
   cudaEvent_t ev = nullptr;
+  if (c->cu && flush_stream(c->cu) < 0) return MPIX_ERR_CUDA;
   CK(cudaSetDevice(rs.device));
   CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   CK(cudaEventRecord(ev, c->cu ? c->cu : rs.aux));

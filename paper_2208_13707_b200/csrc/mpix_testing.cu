@@ -199,6 +199,27 @@ int MPIXT_Delay(uint64_t ns, void* stream) {
   return done(cudaGetLastError());
 }
 
+// A fresh (non-pooled) non-blocking CUDA stream on `device`. torch's
+// torch.cuda.Stream() hands out one of 32 pooled streams per device, so
+// creating more than 32 aliases them; aliased streams serialise ranks that
+// must run concurrently (a Waitall of one rank would block the operations of
+// another queued behind it).
+int MPIXT_Stream_create(int device, void** stream) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) return 1;
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return 1;
+  *stream = (void*)s;
+  return 0;
+}
+
+int MPIXT_Stream_destroy(void* stream) {
+  return cudaStreamDestroy((cudaStream_t)stream) == cudaSuccess ? 0 : 1;
+}
+
 int MPIXT_Empty(void* stream) {
   k_empty<<<1, 32, 0, (cudaStream_t)stream>>>();
   return done(cudaGetLastError());

@@ -57,6 +57,15 @@ class MPIStatus(C.Structure):
 
 _lib = None
 _lib_lock = threading.Lock()
+_owned_streams: list = []  # streams made by testing.new_stream (live for the process)
+
+# Every spinning wait runs inside a stream-ordered kernel. CUDA multiplexes
+# streams onto CUDA_DEVICE_MAX_CONNECTIONS hardware queues (default 8); a
+# stream blocked behind its own spinning Waitall would also hold back other
+# streams sharing its queue, including the peers it waits for. Use the
+# maximum (32) unless the user chose otherwise; it must be set before the
+# CUDA context exists (DESIGN.md §6 "Hardware queues").
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 
 def lib() -> C.CDLL:
@@ -127,6 +136,12 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Stencil7": (I, [P, P, I, I, I, C.c_float, C.c_float, P]),
         "MPIXT_Launch_count": (U64, []),
         "MPIXT_Preload": (I, []),
+        "MPIXT_Msgrate": (I, [I, I, I, I, P, P, P, P, P, P, P]),
+        "MPIXT_Pingpong": (I, [P, P, P, P, U64, I, P, P, I, I, P, P]),
+        "MPIXT_Selfchain": (I, [P, P, P, I, I, P, P, P]),
+        "MPIXT_Empty_loop": (I, [I, P, P, P]),
+        "MPIXT_Stream_create": (I, [I, C.POINTER(P)]),
+        "MPIXT_Stream_destroy": (I, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -431,6 +446,18 @@ class World:
 # --- test/bench helper kernels (include/mpix_testing.h) ---------------------------
 class testing:
     @staticmethod
+    def new_stream(device: int = 0):
+        """A fresh CUDA stream as a torch ExternalStream (torch.cuda.Stream()
+        draws from a 32-entry pool per device and aliases beyond that; ranks
+        on aliased streams would be serialised)."""
+        import torch
+        h = C.c_void_p()
+        check(lib().MPIXT_Stream_create(device, C.byref(h)), "MPIXT_Stream_create")
+        s = torch.cuda.ExternalStream(h.value, device=torch.device("cuda", device))
+        _owned_streams.append(h.value)
+        return s
+
+    @staticmethod
     def fill_pattern(buf, nbytes: int, seed: int, it: int, stream) -> None:
         check(lib().MPIXT_Fill_pattern(_ptr(buf), nbytes, seed, it, _stream_handle(stream)))
 
@@ -465,3 +492,40 @@ class testing:
     @staticmethod
     def stencil7(u, out, nx, ny, nz, w0, w1, stream) -> None:
         check(lib().MPIXT_Stencil7(_ptr(u), _ptr(out), nx, ny, nz, w0, w1, _stream_handle(stream)))
+
+    # native drivers (csrc/mpix_drivers.cpp) -------------------------------
+    @staticmethod
+    def msgrate(comms, streams, sbufs, rbufs, devices, P: int, S: int, W: int, batches: int) -> dict:
+        n = P * S
+        CA = (C.c_void_p * n)(*[c.h for c in comms])
+        SA = (C.c_void_p * n)(*[_stream_handle(s) for s in streams])
+        SB = (C.c_void_p * n)(*[_ptr(b) for b in sbufs])
+        RB = (C.c_void_p * n)(*[_ptr(b) for b in rbufs])
+        DV = (C.c_int * P)(*devices)
+        hs = (C.c_double * 2)()
+        ds = C.c_double()
+        check(lib().MPIXT_Msgrate(P, S, W, batches, CA, SA, SB, RB, DV, hs, C.byref(ds)), "Msgrate")
+        msgs = P * S * W * batches
+        return {"messages": msgs, "enqueue_s": hs[0], "host_s": hs[1], "device_s": ds.value,
+                "msgs_per_s": msgs / max(ds.value, hs[1])}
+
+    @staticmethod
+    def pingpong(c0, c1, b0, b1, nbytes: int, iters: int, s0, s1, dev0: int = 0, dev1: int = 0):
+        ds, hs = C.c_double(), C.c_double()
+        check(lib().MPIXT_Pingpong(c0.h, c1.h, _ptr(b0), _ptr(b1), nbytes, iters,
+                                   _stream_handle(s0), _stream_handle(s1), dev0, dev1,
+                                   C.byref(ds), C.byref(hs)), "Pingpong")
+        return ds.value, hs.value
+
+    @staticmethod
+    def selfchain(c, prod, cons, n: int, iters: int, stream):
+        ds, hs = C.c_double(), C.c_double()
+        check(lib().MPIXT_Selfchain(c.h, _ptr(prod), _ptr(cons), n, iters, _stream_handle(stream),
+                                    C.byref(ds), C.byref(hs)), "Selfchain")
+        return ds.value, hs.value
+
+    @staticmethod
+    def empty_loop(iters: int, stream):
+        ds, hs = C.c_double(), C.c_double()
+        check(lib().MPIXT_Empty_loop(iters, _stream_handle(stream), C.byref(ds), C.byref(hs)))
+        return ds.value, hs.value

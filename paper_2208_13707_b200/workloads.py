@@ -14,9 +14,6 @@ workloads (oracle/ref_driver.cpp) and of PAPER.md Listing 2.
 """
 from __future__ import annotations
 
-import threading
-import time
-
 from . import mpix
 
 # face d: 0=-x 1=+x 2=-y 3=+y 4=-z 5=+z
@@ -72,39 +69,19 @@ class HaloStencil:
 
 
 def msgrate(world, ctxs, S: int, W: int, batches: int, bufs) -> dict:
-    """ctxs[r][k] = (torch stream, comm) for stream k of rank r. Each host
-    thread drives one rank. Returns messages and device-timed seconds."""
-    import torch
+    """ctxs[r][k] = (torch stream, comm) for stream k of rank r; bufs[r][k] =
+    (8-byte send buffer, W x 8-byte receive buffer). One native host thread
+    per rank drives the C ABI (csrc/mpix_drivers.cpp, the analogue of the
+    reference's C++ bench driver). Returns messages, host and device-timed
+    seconds, and msgs/s over the larger of the two."""
     P = len(ctxs)
-    ev = {}
-
-    def rank(r):
-        right, left = (r + 1) % P, (r + P - 1) % P
+    comms, streams, sb, rb, devs = [], [], [], [], []
+    for r in range(P):
+        devs.append(ctxs[r][0][0].device.index or 0)
         for k in range(S):
-            s = ctxs[r][k][0]
-            e0 = torch.cuda.Event(enable_timing=True)
-            e0.record(s)
-            ev[(r, k)] = [e0, None]
-        for b in range(batches):
-            for k in range(S):
-                c = ctxs[r][k][1]
-                sb, rb = bufs[r][k]
-                reqs = []
-                for i in range(W):
-                    reqs.append(c.irecv_enqueue(rb[i], 2, mpix.MPI_INT, left, i))
-                    reqs.append(c.isend_enqueue(sb, 2, mpix.MPI_INT, right, i))
-                mpix.waitall_enqueue(reqs)
-        for k in range(S):
-            e1 = torch.cuda.Event(enable_timing=True)
-            e1.record(ctxs[r][k][0])
-            ev[(r, k)][1] = e1
-
-    t0 = time.perf_counter()
-    world.run_ranks(rank)
-    for d in {0}:
-        torch.cuda.synchronize(d)
-    host_s = time.perf_counter() - t0
-    dev_s = max(a.elapsed_time(b) for a, b in ev.values()) / 1e3
-    msgs = P * S * W * batches
-    return {"messages": msgs, "device_s": dev_s, "host_s": host_s,
-            "msgs_per_s": msgs / max(dev_s, host_s)}
+            s, c = ctxs[r][k][0], ctxs[r][k][1]
+            comms.append(c)
+            streams.append(s)
+            sb.append(bufs[r][k][0])
+            rb.append(bufs[r][k][1])
+    return mpix.testing.msgrate(comms, streams, sb, rb, devs, P, S, W, batches)

@@ -7,6 +7,7 @@ os.environ.setdefault("MPIX_SPIN_TIMEOUT_MS", "20000")
 # Spin-waiting communication kernels + lazy module loading can stall a launch
 # until a peer's spinning kernel exits (NCCL has the same constraint).
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:

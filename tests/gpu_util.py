@@ -30,7 +30,7 @@ def gpu_world(P, devices=None, spread=False):
         def setup(r):
             dev = devices[r]
             with torch.cuda.device(dev):
-                s = torch.cuda.Stream(device=dev)
+                s = mpix.testing.new_stream(dev)
             ms = mpix.Stream.from_cuda(s)
             wc = w.comm(r)
             c = wc.stream_comm_create(ms)

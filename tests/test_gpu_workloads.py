@@ -84,7 +84,7 @@ def test_msgrate_ring_all_messages_arrive():
 
         def setup(r):
             for k in range(S):
-                s = torch.cuda.Stream(device=0)
+                s = mpix.testing.new_stream(0)
                 c = w.comm(r).stream_comm_create(mpix.Stream.from_cuda(s))
                 ctxs[r].append((s, c))
 
