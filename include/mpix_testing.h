@@ -71,6 +71,18 @@ int MPIXT_Selfchain(MPI_Comm c, float *prod, float *cons, int n, int iters, void
                     double *dev_s, double *host_s);
 /* `iters` back-to-back empty kernels launched from C++ (launch floor). */
 int MPIXT_Empty_loop(int iters, void *stream, double *dev_s, double *host_s);
+/* The Allreduce_enqueue reduce stage alone (no entry/exit barrier): rank
+ * `me`'s share of a P-rank allreduce over P send/recv buffers on the current
+ * GPU (one-shot: all of rank me's output; two-shot: chunk me into every
+ * output). For ncu, which serialises kernels and so cannot run the spinning
+ * barriers of several ranks sharing one GPU. Not thread-safe. */
+int MPIXT_Reduce_only(int P, int me, void **sendbufs, void **recvbufs, int count,
+                      MPI_Datatype datatype, MPI_Op op, int twoshot, void *stream);
+/* Timing probe for the benchmark's roofline: while enabled, the runtime
+ * records CUDA events around every receive-side copy grid (k_copy) it
+ * launches; read returns their summed duration and count. Enabling clears. */
+int MPIXT_Copy_timing(int enable);
+int MPIXT_Copy_timing_read(double *total_ms, int *n);
 /* Number of helper kernels launched so far. */
 uint64_t MPIXT_Launch_count(void);
 

@@ -106,6 +106,7 @@ struct alignas(64) OpRecord {
   uint64_t fin_val[8];   // [2,8) mirrors and done words
   uint64_t coll[2 * kMaxCollRanks];  // allreduce: peers' sbuf / rbuf
   uint64_t flags;
+  uint64_t stage_ptr, stage_done, stage_gen;  // staged send: buffer + release
 };
 
 enum : uint64_t { ACT_NONE = 0, ACT_COPY = 1, ACT_STAGE = 2 };
@@ -148,6 +149,12 @@ struct P2PArgs {
   uint64_t my_gen;
   uint64_t* stage_done;   // MODE_STAGED: released by the consumer of staging
   uint64_t stage_gen;
+  // MODE_STAGED with staging == null: claim a slot of the rank's device
+  // staging arena in the kernel, only if the receive is not posted yet
+  uint8_t* arena;
+  uint64_t* arena_state;  // arena_slots words: even = free
+  uint32_t arena_slots;
+  uint64_t arena_chunk;
   OpRecord* rec;
   uint64_t opid;
   uint64_t* err_word;     // per-rank error word (watchdog)
@@ -222,12 +229,15 @@ struct ARArgs {
 // Launchers implemented in mpix_kernels.cu (host side). Each returns the
 // number of kernels launched, or -1 on a CUDA error. `sys` selects
 // system-scope primitives (some peer lives on another GPU).
-int launch_p2p(const P2PArgs& a, bool sys, bool inline_copy, uint64_t copy_grid, cudaStream_t s);
+int launch_p2p(const P2PArgs& a, bool sys, bool inline_copy, uint64_t copy_grid, cudaStream_t s,
+               cudaEvent_t copy_ev0 = nullptr, cudaEvent_t copy_ev1 = nullptr);
 int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint64_t* err_word,
                  uint64_t spin_limit_ns, bool sys, cudaStream_t s);
 int launch_allreduce(const ARArgs& a, bool sys, uint64_t reduce_grid, cudaStream_t s);
 uint64_t p2p_copy_grid(uint64_t bytes);
 uint64_t ar_reduce_grid(uint64_t work_bytes);
 int preload_kernels();
+int launch_reduce_only(const uint64_t* sb, const uint64_t* rb, int P, int me, uint64_t count,
+                       int esize, int dtype, int op, int algo, OpRecord* rec, cudaStream_t s);
 
 }  // namespace mpix

@@ -288,6 +288,11 @@ struct Decision {
   uint64_t action, src, dst, bytes;
   Fin fin;
   int wait_own;
+  // staged blocking send: the staging buffer and its release word/value
+  // (host-provided, or claimed from the rank's device arena)
+  uint8_t* stage_ptr;
+  uint64_t* stage_done;
+  uint64_t stage_gen;
 };
 
 template <bool SYS>
@@ -332,7 +337,7 @@ __device__ void send_win(const P2PArgs& a, Decision& dc, int j, const Snap& r, b
   dc.fin.add_b(&a.post_mirror[slot], a.pseq + 1);
   dc.fin.add_b(reinterpret_cast<void*>(r.done_addr), r.done_val);
   dc.fin.add_b(a.my_done, a.my_gen);
-  if (a.mode == MODE_STAGED) dc.fin.add_b(a.stage_done, a.stage_gen);
+  if (a.mode == MODE_STAGED && dc.stage_done) dc.fin.add_b(dc.stage_done, dc.stage_gen);
 }
 
 // Receiver wins (send descriptor already TAKEN by me): pull.
@@ -352,6 +357,48 @@ __device__ void recv_win(const P2PArgs& a, Decision& dc, int j, const Snap& s, b
   dc.fin.add_b(a.my_done, a.my_gen);
 }
 
+// Claim a slot of the rank's device staging arena (warp 0, all lanes). A
+// slot's state word is even when free; the claimer moves v -> v+1 and the
+// consumer of the staged copy releases it by storing v+2 (the descriptor's
+// done word/value). Returns false on watchdog expiry.
+template <bool SYS>
+__device__ bool claim_stage_slot(const P2PArgs& a, Decision& dc) {
+  using M = Scope<SYS>;
+  const int lane = threadIdx.x & 31;
+  const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
+  unsigned ns = 32;
+  for (;;) {
+    for (int base = 0; base < (int)a.arena_slots; base += 32) {
+      const int i = base + lane;
+      uint64_t v = i < (int)a.arena_slots ? M::ld_rlx(&a.arena_state[i]) : 1;
+      unsigned m = __ballot_sync(0xffffffffu, (v & 1) == 0);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        int won = 0;
+        if (lane == src) won = M::cas(&a.arena_state[i], v, v + 1) == v;
+        if (__shfl_sync(0xffffffffu, won, src)) {
+          const uint64_t vv = __shfl_sync(0xffffffffu, v, src);
+          const int slot = base + src;
+          if (lane == 0) {
+            dc.stage_ptr = a.arena + (uint64_t)slot * a.arena_chunk;
+            dc.stage_done = &a.arena_state[slot];
+            dc.stage_gen = vv + 2;
+          }
+          __syncwarp();
+          return true;
+        }
+      }
+    }
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+    if (a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
+      if (lane == 0 && a.err_word) ScopeSys::st_rlx(a.err_word, ERRW_WAIT_SLOT);
+      return false;
+    }
+  }
+}
+
 // The handshake (whole CTA calls; warp 0 works, the CTA copies eager
 // payloads). On return dc holds ACT_NONE / ACT_COPY / ACT_STAGE.
 template <bool SYS>
@@ -359,7 +406,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   using M = Scope<SYS>;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  __shared__ int s_phase;  // 0 decided, 1 eager copy then post, 2 posted
+  __shared__ int s_phase;  // 0 decided, 1 eager copy then post, 2 posted, 3 claim staging
   if (warp == 0) {
     Snap sn;
     int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
@@ -368,6 +415,9 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
       dc.wait_own = 0;
       dc.fin.clear();
       dc.action = ACT_NONE;
+      dc.stage_ptr = a.staging;  // null: claim from the device arena if needed
+      dc.stage_done = a.stage_done;
+      dc.stage_gen = a.stage_gen;
       s_phase = 0;
       if (!a.is_recv) {
         if (j >= 0) {
@@ -376,6 +426,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
           if (wait_post_slot<SYS>(a)) send_win(a, dc, j, sn, false, a.buf);
         } else if (a.mode == MODE_STAGED) {
           dc.action = ACT_STAGE;
+          if (!dc.stage_ptr) s_phase = 3;
         } else if (wait_post_slot<SYS>(a)) {
           if (a.mode == MODE_EAGER) {
             s_phase = 1;
@@ -401,6 +452,9 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
       }
     }
     __syncwarp();
+    if (s_phase == 3 && !claim_stage_slot<SYS>(a, dc) && lane == 0) dc.action = ACT_NONE;
+    __syncwarp();
+    if (lane == 0 && s_phase == 3) s_phase = 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) trace_t(a.trace, 2);
@@ -448,7 +502,7 @@ __device__ void stage_publish(const P2PArgs& a, Decision& dc) {
       s_push = 0;
       dc.action = ACT_NONE;
       if (wait_post_slot<SYS>(a))
-        post_desc<SYS>(a, (uint64_t)a.staging, a.bytes, (uint64_t)a.stage_done, a.stage_gen, true);
+        post_desc<SYS>(a, (uint64_t)dc.stage_ptr, a.bytes, (uint64_t)dc.stage_done, dc.stage_gen, true);
       else
         s_push = -1;
     }
@@ -460,7 +514,7 @@ __device__ void stage_publish(const P2PArgs& a, Decision& dc) {
         const int slot = (int)(a.pseq % (uint64_t)a.R);
         uint64_t want = st_word(a.pseq, ST_POSTED);
         if (M::cas(&a.post_ring[slot].state, want, st_word(a.pseq, ST_TAKEN)) == want) {
-          send_win(a, dc, j, sn, true, a.staging);
+          send_win(a, dc, j, sn, true, dc.stage_ptr);
           s_push = 1;
         }
       }
@@ -496,6 +550,9 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
       rec->dst = s_dc.dst;
       rec->bytes = s_dc.bytes;
       rec->nfin = s_dc.fin.na | (s_dc.fin.nb << 8);
+      rec->stage_ptr = (uint64_t)s_dc.stage_ptr;
+      rec->stage_done = (uint64_t)s_dc.stage_done;
+      rec->stage_gen = s_dc.stage_gen;
       for (uint32_t k = 0; k < s_dc.fin.na; ++k) {
         rec->fin_addr[k] = s_dc.fin.a_addr[k];
         rec->fin_val[k] = s_dc.fin.a_val[k];
@@ -521,7 +578,7 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
       if (a.trace) a.trace->g1 = globaltimer();
     }
   } else if (s_dc.action == ACT_STAGE) {
-    cta_copy(a.staging, a.buf, a.bytes);
+    cta_copy(s_dc.stage_ptr, a.buf, a.bytes);
     __syncthreads();
     stage_publish<SYS>(a, s_dc);
   } else if (threadIdx.x == 0) {
@@ -567,6 +624,10 @@ __global__ void __launch_bounds__(kThreads) k_batch(const BatchArgs<NOPS, NWAIT>
       a.my_gen = o.my_gen;
       a.stage_done = nullptr;
       a.stage_gen = 0;
+      a.arena = nullptr;
+      a.arena_state = nullptr;
+      a.arena_slots = 0;
+      a.arena_chunk = 0;
       a.rec = nullptr;
       a.opid = 0;
       a.err_word = o.err_word;
@@ -590,7 +651,7 @@ __global__ void __launch_bounds__(kCopyThreads, 2) k_copy(const P2PArgs a) {
     tile_copy(reinterpret_cast<uint8_t*>(rec->dst), reinterpret_cast<const uint8_t*>(rec->src),
               rec->bytes, blockIdx.x, gridDim.x);
   } else if (action == ACT_STAGE) {
-    tile_copy(a.staging, a.buf, a.bytes, blockIdx.x, gridDim.x);
+    tile_copy(reinterpret_cast<uint8_t*>(rec->stage_ptr), a.buf, a.bytes, blockIdx.x, gridDim.x);
   }
   pdl_trigger();
 }
@@ -612,6 +673,12 @@ __global__ void __launch_bounds__(kThreads) k_fin(const P2PArgs a) {
       f.run<SYS>();
     }
   } else if (action == ACT_STAGE) {
+    if (threadIdx.x == 0) {
+      s_dc.stage_ptr = reinterpret_cast<uint8_t*>(rec->stage_ptr);
+      s_dc.stage_done = reinterpret_cast<uint64_t*>(rec->stage_done);
+      s_dc.stage_gen = rec->stage_gen;
+    }
+    __syncthreads();
     stage_publish<SYS>(a, s_dc);
   }
 }
@@ -757,33 +824,44 @@ __device__ void reduce_elem(const uint64_t* sb, const uint64_t* outs, int nout, 
 }
 
 constexpr int kArThreads = 256;
-constexpr int kArUnroll = 2;
+constexpr int kArUnroll = 2;  // 8 KiB of every input per tile; kArGroup x 2 x 16 B in flight per thread
 constexpr uint64_t kArTileVec = (uint64_t)kArThreads * kArUnroll;
 
-// One tile [v0 + tile*kArTileVec, ...) of vectors within [v0, v1).
+// One tile [v0 + tile*kArTileVec, ...) of vectors within [v0, v1). Inputs
+// are loaded kArGroup ranks at a time (all loads of a group in flight before
+// any is folded) and folded strictly in rank order 0..P-1.
+constexpr int kArGroup = 4;
+
 template <int DT, int OP>
 __device__ void reduce_tile(const uint64_t* sb, const uint64_t* outs, int nout, int P, uint64_t v0,
                             uint64_t v1, uint64_t tile) {
-  uint64_t base = v0 + tile * kArTileVec + threadIdx.x;
+  const uint64_t base = v0 + tile * kArTileVec + threadIdx.x;
   Acc<DT> acc[kArUnroll];
   bool in[kArUnroll];
 #pragma unroll
   for (int u = 0; u < kArUnroll; ++u) in[u] = base + u * kArThreads < v1;
-  {
-    const uint4* s0 = reinterpret_cast<const uint4*>(sb[0]);
+  for (int q0 = 0; q0 < P; q0 += kArGroup) {
+    uint4 x[kArGroup][kArUnroll];
 #pragma unroll
-    for (int u = 0; u < kArUnroll; ++u)
-      if (in[u]) acc[u].init(s0[base + u * kArThreads]);
-  }
-  for (int q = 1; q < P; ++q) {
-    const uint4* sq = reinterpret_cast<const uint4*>(sb[q]);
-    uint4 x[kArUnroll];
+    for (int g = 0; g < kArGroup; ++g) {
+      if (q0 + g < P) {
+        const uint4* sq = reinterpret_cast<const uint4*>(sb[q0 + g]);
 #pragma unroll
-    for (int u = 0; u < kArUnroll; ++u)
-      if (in[u]) x[u] = sq[base + u * kArThreads];
+        for (int u = 0; u < kArUnroll; ++u)
+          if (in[u]) x[g][u] = sq[base + u * kArThreads];
+      }
+    }
 #pragma unroll
-    for (int u = 0; u < kArUnroll; ++u)
-      if (in[u]) acc[u].template add<OP>(x[u]);
+    for (int g = 0; g < kArGroup; ++g) {
+      if (q0 + g < P) {
+#pragma unroll
+        for (int u = 0; u < kArUnroll; ++u) {
+          if (!in[u]) continue;
+          if (q0 + g == 0) acc[u].init(x[g][u]);
+          else acc[u].template add<OP>(x[g][u]);
+        }
+      }
+    }
   }
 #pragma unroll
   for (int u = 0; u < kArUnroll; ++u) {
@@ -833,32 +911,12 @@ template <int DT, int OP>
 __device__ void ar_tile(const ARArgs& a, const uint64_t* sb, const uint64_t* rb, int algo,
                         uint64_t tile, uint64_t ntiles) {
   ArPlan p = ar_plan(a, sb, rb, algo);
-  uint64_t outs[kMaxCollRanks];
-  if (p.nout == 1) outs[0] = rb[a.me];
-  else for (int q = 0; q < a.P; ++q) outs[q] = rb[q];
+  const uint64_t* outs = p.nout == 1 ? rb + a.me : rb;  // shared-memory pointer table
   uint64_t nt_vec = (p.v1 - p.v0 + kArTileVec - 1) / kArTileVec;
   for (uint64_t t = tile; t < nt_vec; t += ntiles)
     reduce_tile<DT, OP>(sb, outs, p.nout, a.P, p.v0, p.v1, t);
   uint64_t gt = tile * blockDim.x + threadIdx.x, gn = ntiles * blockDim.x;
   for (uint64_t e = p.e0 + gt; e < p.e1; e += gn) reduce_elem<DT, OP>(sb, outs, p.nout, a.P, e);
-}
-
-template <int DT>
-__device__ void ar_dispatch_op(const ARArgs& a, const uint64_t* sb, const uint64_t* rb, int algo,
-                               uint64_t tile, uint64_t ntiles) {
-  if (a.op == AR_SUM) ar_tile<DT, AR_SUM>(a, sb, rb, algo, tile, ntiles);
-  else if (a.op == AR_MAX) ar_tile<DT, AR_MAX>(a, sb, rb, algo, tile, ntiles);
-  else ar_tile<DT, AR_MIN>(a, sb, rb, algo, tile, ntiles);
-}
-
-__device__ void ar_compute(const ARArgs& a, const uint64_t* sb, const uint64_t* rb, int algo,
-                           uint64_t tile, uint64_t ntiles) {
-  switch (a.dtype) {
-    case AR_F32: ar_dispatch_op<AR_F32>(a, sb, rb, algo, tile, ntiles); break;
-    case AR_BF16: ar_dispatch_op<AR_BF16>(a, sb, rb, algo, tile, ntiles); break;
-    case AR_I32: ar_dispatch_op<AR_I32>(a, sb, rb, algo, tile, ntiles); break;
-    default: ar_dispatch_op<AR_F64>(a, sb, rb, algo, tile, ntiles); break;
-  }
 }
 
 // Entry: publish my buffers to every peer, wait for theirs, record them.
@@ -889,7 +947,9 @@ __global__ void __launch_bounds__(32) k_ar_entry(const ARArgs a) {
   pdl_trigger();
 }
 
-__global__ void __launch_bounds__(kArThreads) k_ar_reduce(const ARArgs a) {
+// One instantiation per (dtype, op) so each gets its own register budget.
+template <int DT, int OP>
+__global__ void __launch_bounds__(kArThreads, (DT == AR_BF16 || DT == AR_F64) ? 3 : 4) k_ar_reduce(const ARArgs a) {
   pdl_wait();
   __shared__ uint64_t s_sb[kMaxCollRanks], s_rb[kMaxCollRanks];
   __shared__ uint64_t s_act;
@@ -902,7 +962,25 @@ __global__ void __launch_bounds__(kArThreads) k_ar_reduce(const ARArgs a) {
   __syncthreads();
   pdl_trigger();
   if (s_act == 0) return;
-  ar_compute(a, s_sb, s_rb, (int)s_act - 1, blockIdx.x, gridDim.x);
+  ar_tile<DT, OP>(a, s_sb, s_rb, (int)s_act - 1, blockIdx.x, gridDim.x);
+}
+
+using ReduceKernel = void (*)(const ARArgs);
+
+template <int DT>
+static ReduceKernel reduce_kernel_op(int op) {
+  if (op == AR_SUM) return k_ar_reduce<DT, AR_SUM>;
+  if (op == AR_MAX) return k_ar_reduce<DT, AR_MAX>;
+  return k_ar_reduce<DT, AR_MIN>;
+}
+
+static ReduceKernel reduce_kernel(int dtype, int op) {
+  switch (dtype) {
+    case AR_F32: return reduce_kernel_op<AR_F32>(op);
+    case AR_BF16: return reduce_kernel_op<AR_BF16>(op);
+    case AR_I32: return reduce_kernel_op<AR_I32>(op);
+    default: return reduce_kernel_op<AR_F64>(op);
+  }
 }
 
 // Exit: tell every peer I am done with its buffers; wait for all of them.
@@ -945,7 +1023,8 @@ uint64_t p2p_copy_grid(uint64_t bytes) {
   return g < 1 ? 1 : g;
 }
 
-int launch_p2p(const P2PArgs& a, bool sys, bool inl, uint64_t grid, cudaStream_t s) {
+int launch_p2p(const P2PArgs& a, bool sys, bool inl, uint64_t grid, cudaStream_t s,
+               cudaEvent_t copy_ev0, cudaEvent_t copy_ev1) {
   if (inl) {
     if (sys) k_proto<true, true><<<1, kThreads, 0, s>>>(a);
     else k_proto<false, true><<<1, kThreads, 0, s>>>(a);
@@ -954,7 +1033,9 @@ int launch_p2p(const P2PArgs& a, bool sys, bool inl, uint64_t grid, cudaStream_t
   if (sys) k_proto<true, false><<<1, kThreads, 0, s>>>(a);
   else k_proto<false, false><<<1, kThreads, 0, s>>>(a);
   if (cudaGetLastError() != cudaSuccess) return -1;
+  if (copy_ev0) cudaEventRecord(copy_ev0, s);  // timing probe (bench roofline) only
   if (launch_pdl(k_copy, (int)grid, kCopyThreads, s, a) != cudaSuccess) return -1;
+  if (copy_ev1) cudaEventRecord(copy_ev1, s);
   cudaError_t e = sys ? launch_pdl(k_fin<true>, 1, kThreads, s, a)
                       : launch_pdl(k_fin<false>, 1, kThreads, s, a);
   return e == cudaSuccess ? 3 : -1;
@@ -993,7 +1074,7 @@ int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint6
 uint64_t ar_reduce_grid(uint64_t work_bytes) {
   uint64_t tile = kArTileVec * 16;
   uint64_t g = (work_bytes + tile - 1) / tile;
-  if (g > 148ull * 64) g = 148ull * 64;  // tiles beyond ~64 waves loop
+  if (g > (1ull << 20)) g = 1ull << 20;
   return g < 1 ? 1 : g;
 }
 
@@ -1001,7 +1082,7 @@ int launch_allreduce(const ARArgs& a, bool sys, uint64_t grid, cudaStream_t s) {
   if (sys) k_ar_entry<true><<<1, 32, 0, s>>>(a);
   else k_ar_entry<false><<<1, 32, 0, s>>>(a);
   if (cudaGetLastError() != cudaSuccess) return -1;
-  if (launch_pdl(k_ar_reduce, (int)grid, kArThreads, s, a) != cudaSuccess) return -1;
+  if (launch_pdl(reduce_kernel(a.dtype, a.op), (int)grid, kArThreads, s, a) != cudaSuccess) return -1;
   if (a.P > 1) {
     cudaError_t e = sys ? launch_pdl(k_ar_exit<true>, 1, 32, s, a)
                         : launch_pdl(k_ar_exit<false>, 1, 32, s, a);
@@ -1009,6 +1090,34 @@ int launch_allreduce(const ARArgs& a, bool sys, uint64_t grid, cudaStream_t s) {
     return 3;
   }
   return 2;
+}
+
+// The reduce stage alone (profiling / roofline probe): P input buffers and
+// P output buffers on this GPU, as rank `me` of a P-rank allreduce would see
+// them after the entry barrier. `rec` is a device OpRecord the caller owns.
+int launch_reduce_only(const uint64_t* sb, const uint64_t* rb, int P, int me, uint64_t count,
+                       int esize, int dtype, int op, int algo, OpRecord* rec, cudaStream_t s) {
+  if (P < 1 || P > kMaxCollRanks) return -1;
+  OpRecord h = {};
+  for (int q = 0; q < P; ++q) {
+    h.coll[q] = sb[q];
+    h.coll[kMaxCollRanks + q] = rb[q];
+  }
+  h.action = (uint64_t)algo + 1;
+  if (cudaMemcpyAsync(rec, &h, sizeof(h), cudaMemcpyHostToDevice, s) != cudaSuccess) return -1;
+  ARArgs a = {};
+  a.count = count;
+  a.esize = esize;
+  a.dtype = dtype;
+  a.op = op;
+  a.algo = algo;
+  a.P = P;
+  a.me = me;
+  a.rec = rec;
+  uint64_t bytes = count * (uint64_t)esize;
+  uint64_t work = algo == AR_TWOSHOT ? (bytes + P - 1) / P : bytes;
+  reduce_kernel(dtype, op)<<<(unsigned)ar_reduce_grid(work), kArThreads, 0, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 // Force-load every kernel of this module on the current device. Under CUDA
@@ -1023,7 +1132,7 @@ int preload_kernels() {
       (const void*)k_proto<false, true>, (const void*)k_proto<false, false>,
       (const void*)k_copy, (const void*)k_fin<true>, (const void*)k_fin<false>,
       (const void*)k_ar_entry<true>, (const void*)k_ar_entry<false>,
-      (const void*)k_ar_reduce, (const void*)k_ar_exit<true>, (const void*)k_ar_exit<false>,
+      (const void*)k_ar_exit<true>, (const void*)k_ar_exit<false>,
       (const void*)k_batch<true, 4, 8>, (const void*)k_batch<false, 4, 8>,
       (const void*)k_batch<true, 16, 32>, (const void*)k_batch<false, 16, 32>,
       (const void*)k_batch<true, kBatchOps, kBatchWaits>,
@@ -1032,6 +1141,11 @@ int preload_kernels() {
     cudaError_t r = cudaFuncGetAttributes(&fa, k);
     if (r != cudaSuccess) e = r;
   }
+  for (int dt : {AR_I32, AR_F32, AR_BF16, AR_F64})
+    for (int op : {AR_SUM, AR_MAX, AR_MIN}) {
+      cudaError_t r = cudaFuncGetAttributes(&fa, (const void*)reduce_kernel(dt, op));
+      if (r != cudaSuccess) e = r;
+    }
   return e == cudaSuccess ? 0 : -1;
 }
 

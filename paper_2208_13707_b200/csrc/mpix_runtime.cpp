@@ -42,6 +42,8 @@ struct Config {
   bool trace = false;                // MPIX_TRACE=1: per-op device trace ring
   bool force_sys = false;            // MPIX_FORCE_SYS=1: system scope even on one GPU
   bool batch = true;                 // MPIX_BATCH=0: one launch per operation
+  int stage_slots = 64;              // MPIX_STAGE_SLOTS: device staging arena slots per rank
+  uint64_t stage_chunk = 4ull << 20; // MPIX_STAGE_CHUNK: bytes per arena slot
 
   static Config from_env() {
     Config c;
@@ -61,6 +63,9 @@ struct Config {
     c.trace = geti("MPIX_TRACE", 0) != 0;
     c.force_sys = geti("MPIX_FORCE_SYS", 0) != 0;
     c.batch = geti("MPIX_BATCH", 1) != 0;
+    c.stage_slots = (int)geti("MPIX_STAGE_SLOTS", c.stage_slots);
+    if (c.stage_slots > 1024) c.stage_slots = 1024;
+    c.stage_chunk = (geti("MPIX_STAGE_CHUNK", c.stage_chunk) + 255) & ~255ull;
     return c;
   }
 };
@@ -69,6 +74,14 @@ constexpr uint64_t kReqSlots = 1ull << 20;  // completion words per rank
 constexpr uint64_t kStageSlots = 4096;      // staging buffers per rank
 
 std::atomic<uint64_t> g_launches{0};
+
+// Timing probe for the bench's roofline (MPIXT_Copy_timing): CUDA events
+// around every receive-side copy grid while enabled.
+struct CopyTiming {
+  std::mutex mu;
+  std::atomic<bool> on{false};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+} g_copy_timing;
 
 // ---------------------------------------------------------------------------
 // Host rendezvous for collective calls (replaces ctrl_send/ctrl_recv over the
@@ -135,6 +148,11 @@ struct RankState {
   };
   uint64_t* h_stage = nullptr;
   uint64_t* d_stage = nullptr;
+  // Device staging arena: staged sends up to cfg.stage_chunk bytes claim a
+  // slot inside their own kernel, only when the receive is not posted yet
+  // (no host allocation on the enqueue path).
+  uint8_t* d_arena = nullptr;
+  uint64_t* d_arena_state = nullptr;
   std::vector<StageBuf> stage;
   std::mutex stage_mu;
   // request table: slot -> issuing stream, for STREAM_MISMATCH
@@ -335,6 +353,14 @@ int rank_pool(World& w, RankState& r) {
     ad.location.id = o->device;
     ad.flags = cudaMemAccessFlagsProtReadWrite;
     CK(cudaMemPoolSetAccess(r.pool, &ad, 1));
+  }
+  if (w.cfg.stage_slots > 0 && w.cfg.stage_chunk > 0) {
+    CK(cudaMallocFromPoolAsync((void**)&r.d_arena, (uint64_t)w.cfg.stage_slots * w.cfg.stage_chunk,
+                               r.pool, r.aux));
+    CK(cudaMallocFromPoolAsync((void**)&r.d_arena_state, (uint64_t)w.cfg.stage_slots * 8, r.pool,
+                               r.aux));
+    CK(cudaMemsetAsync(r.d_arena_state, 0, (uint64_t)w.cfg.stage_slots * 8, r.aux));
+    CK(cudaStreamSynchronize(r.aux));
   }
   return MPI_SUCCESS;
 }
@@ -636,8 +662,15 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     a.my_gen = t.gen;
   }
   if (a.mode == MODE_STAGED && !is_recv) {
-    int rc2 = acquire_staging(rs, bytes, s, &a.staging, &a.stage_done, &a.stage_gen);
-    if (rc2) return rc2;
+    if (rs.d_arena && bytes <= w.cfg.stage_chunk) {
+      a.arena = rs.d_arena;
+      a.arena_state = rs.d_arena_state;
+      a.arena_slots = (uint32_t)w.cfg.stage_slots;
+      a.arena_chunk = w.cfg.stage_chunk;
+    } else {
+      int rc2 = acquire_staging(rs, bytes, s, &a.staging, &a.stage_done, &a.stage_gen);
+      if (rc2) return rc2;
+    }
   }
   if (rs.d_trace) {
     uint64_t n = rs.trace_next.fetch_add(1);
@@ -648,7 +681,16 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     head.key = a.key;
     CK(cudaMemcpyAsync(a.trace, &head, 32, cudaMemcpyHostToDevice, s));
   }
-  const bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
+  bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
+  if (!inl && !blocking && peer == me) {
+    // Self-message whose counterpart has not been enqueued yet: it can only
+    // be enqueued later on this same stream (an enqueue comm has one stream),
+    // so it runs after this operation, which therefore only posts and never
+    // copies: one small launch instead of proto + copy grid + fin.
+    const auto& other = is_recv ? c->send_tagseq : c->recv_tagseq;
+    auto it = other.find(tagseq_key(me, tag));
+    if (it == other.end() || it->second <= tseq) inl = true;
+  }
   if (!inl) {
     uint64_t op = rs.op_next.fetch_add(1);
     a.rec = rs.d_rec + (op % kOpRecords);
@@ -667,7 +709,14 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     if (blocking && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
   } else {
     if (!b.ops.empty() && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
-    int nk = launch_p2p(a, sys, inl, inl ? 1 : p2p_copy_grid(bytes), s);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (!inl && is_recv && g_copy_timing.on.load()) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      std::lock_guard<std::mutex> tl(g_copy_timing.mu);
+      g_copy_timing.ev.emplace_back(e0, e1);
+    }
+    int nk = launch_p2p(a, sys, inl, inl ? 1 : p2p_copy_grid(bytes), s, e0, e1);
     if (nk < 0) return MPIX_ERR_CUDA;
     g_launches.fetch_add(nk);
   }
@@ -938,6 +987,8 @@ int MPIX_World_finalize(void) {
   for (auto& rs : w->ranks) {
     cudaSetDevice(rs->device);
     for (auto& sb : rs->stage) cudaFreeAsync(sb.p, rs->aux);
+    if (rs->d_arena) cudaFreeAsync(rs->d_arena, rs->aux);
+    if (rs->d_arena_state) cudaFreeAsync(rs->d_arena_state, rs->aux);
     cudaStreamSynchronize(rs->aux);
     cudaFree(rs->d_done);
     cudaFree(rs->d_rec);
@@ -1284,6 +1335,61 @@ int MPIX_Comm_region(MPI_Comm comm, void** base, uint64_t* bytes) {
   if (!comm) return MPIX_ERR_INVALID_COMM;
   if (base) *base = comm->sh->base[comm->rank];
   if (bytes) *bytes = comm->sh->L.total();
+  return MPI_SUCCESS;
+}
+
+int MPIXT_Reduce_only(int P, int me, void** sendbufs, void** recvbufs, int count,
+                      MPI_Datatype datatype, MPI_Op op, int twoshot, void* stream) {
+  int dtype, aop;
+  switch (datatype) {
+    case MPI_INT: dtype = AR_I32; break;
+    case MPI_FLOAT: dtype = AR_F32; break;
+    case MPIX_BFLOAT16: dtype = AR_BF16; break;
+    case MPI_DOUBLE: dtype = AR_F64; break;
+    default: return MPIX_ERR_TYPE;
+  }
+  switch (op) {
+    case MPI_SUM: aop = AR_SUM; break;
+    case MPI_MAX: aop = AR_MAX; break;
+    case MPI_MIN: aop = AR_MIN; break;
+    default: return MPIX_ERR_OP;
+  }
+  if (P < 1 || P > kMaxCollRanks || me < 0 || me >= P || count < 0) return MPIX_ERR_INVALID_ARG;
+  static OpRecord* rec = nullptr;
+  if (!rec && cudaMalloc(&rec, sizeof(OpRecord)) != cudaSuccess) return MPIX_ERR_CUDA;
+  std::vector<uint64_t> sb(P), rb(P);
+  for (int q = 0; q < P; ++q) {
+    sb[q] = (uint64_t)sendbufs[q];
+    rb[q] = (uint64_t)recvbufs[q];
+  }
+  int rc = launch_reduce_only(sb.data(), rb.data(), P, me, (uint64_t)count, type_size(datatype),
+                              dtype, aop, twoshot ? AR_TWOSHOT : AR_ONESHOT, rec,
+                              (cudaStream_t)stream);
+  return rc < 0 ? MPIX_ERR_CUDA : MPI_SUCCESS;
+}
+
+int MPIXT_Copy_timing(int enable) {
+  std::lock_guard<std::mutex> tl(g_copy_timing.mu);
+  for (auto& p : g_copy_timing.ev) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  g_copy_timing.ev.clear();
+  g_copy_timing.on.store(enable != 0);
+  return MPI_SUCCESS;
+}
+
+int MPIXT_Copy_timing_read(double* total_ms, int* n) {
+  std::lock_guard<std::mutex> tl(g_copy_timing.mu);
+  double tot = 0;
+  for (auto& p : g_copy_timing.ev) {
+    if (cudaEventSynchronize(p.second) != cudaSuccess) return MPIX_ERR_CUDA;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.first, p.second);
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (n) *n = (int)g_copy_timing.ev.size();
   return MPI_SUCCESS;
 }
 

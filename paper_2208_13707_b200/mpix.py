@@ -142,6 +142,9 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Empty_loop": (I, [I, P, P, P]),
         "MPIXT_Stream_create": (I, [I, C.POINTER(P)]),
         "MPIXT_Stream_destroy": (I, [P]),
+        "MPIXT_Reduce_only": (I, [I, I, P, P, I, I, I, I, P]),
+        "MPIXT_Copy_timing": (I, [I]),
+        "MPIXT_Copy_timing_read": (I, [C.POINTER(C.c_double), C.POINTER(I)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -523,6 +526,23 @@ class testing:
         check(lib().MPIXT_Selfchain(c.h, _ptr(prod), _ptr(cons), n, iters, _stream_handle(stream),
                                     C.byref(ds), C.byref(hs)), "Selfchain")
         return ds.value, hs.value
+
+    @staticmethod
+    def reduce_only(P: int, me: int, sbufs, rbufs, count: int, dt: int, op: int, twoshot: bool, stream):
+        SB = (C.c_void_p * P)(*[_ptr(b) for b in sbufs])
+        RB = (C.c_void_p * P)(*[_ptr(b) for b in rbufs])
+        check(lib().MPIXT_Reduce_only(P, me, SB, RB, count, dt, op, int(twoshot),
+                                      _stream_handle(stream)), "Reduce_only")
+
+    @staticmethod
+    def copy_timing(enable: bool) -> None:
+        check(lib().MPIXT_Copy_timing(int(enable)))
+
+    @staticmethod
+    def copy_timing_read():
+        ms, n = C.c_double(), C.c_int()
+        check(lib().MPIXT_Copy_timing_read(C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     @staticmethod
     def empty_loop(iters: int, stream):

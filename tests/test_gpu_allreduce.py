@@ -129,3 +129,22 @@ def test_allreduce_unaligned_buffers():
         exp = oracle(ins, "f32", mpix.MPI_SUM)
         for r in range(P):
             assert torch.equal(rb[r][3:].cpu(), exp)
+
+
+@pytest.mark.parametrize("twoshot", [False, True])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_reduce_stage_alone_matches_oracle(dt, twoshot):
+    """MPIXT_Reduce_only (the profiling entry: reduce stage without the
+    barriers) computes the same bits as the full collective's oracle."""
+    P, count = 4, (1 << 18) + 37
+    ins = make_inputs(P, count, dt, 11)
+    exp = oracle(ins, dt, mpix.MPI_SUM)
+    sb = [x.to(0) for x in ins]
+    rb = [torch.zeros(count, dtype=DT[dt][0], device=0) for _ in range(P)]
+    s = mpix.testing.new_stream(0)
+    for me in range(P):
+        mpix.testing.reduce_only(P, me, sb, rb, count, DT[dt][1], mpix.MPI_SUM, twoshot, s)
+    s.synchronize()
+    for r in range(P):
+        assert torch.equal(rb[r].cpu().view(torch.int16 if dt == "bf16" else torch.int32),
+                           exp.view(torch.int16 if dt == "bf16" else torch.int32)), r

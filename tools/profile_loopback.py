@@ -15,18 +15,21 @@ ap.add_argument("--size", type=int, default=256 << 20)
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--ranks", type=int, default=1)
+ap.add_argument("--window", type=int, default=1)
 a = ap.parse_args()
 w = mpix.World(1, [0])
-s = torch.cuda.Stream()
+s = mpix.testing.new_stream(0)
 c = w.comm(0).stream_comm_create(mpix.Stream.from_cuda(s))
 src = torch.empty(a.size, dtype=torch.uint8, device=0)
 dst = torch.zeros(a.size, dtype=torch.uint8, device=0)
 mpix.testing.fill_pattern(src, a.size, 1, 0, s)
 torch.cuda.synchronize()
 for i in range(a.warmup + a.steps):
-    r1 = c.isend_enqueue(src, a.size, mpix.MPI_BYTE, 0, i)
-    r2 = c.irecv_enqueue(dst, a.size, mpix.MPI_BYTE, 0, i)
-    mpix.waitall_enqueue([r1, r2])
+    reqs = []
+    for k in range(a.window):  # window > 1: one coalesced k_batch per step
+        reqs.append(c.isend_enqueue(src, a.size, mpix.MPI_BYTE, 0, k))
+        reqs.append(c.irecv_enqueue(dst, a.size, mpix.MPI_BYTE, 0, k))
+    mpix.waitall_enqueue(reqs)
 torch.cuda.synchronize()
 assert torch.equal(src, dst)
 w.finalize()
