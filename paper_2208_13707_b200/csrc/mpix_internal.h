@@ -160,7 +160,14 @@ struct P2PArgs {
   uint64_t* err_word;     // per-rank error word (watchdog)
   uint64_t spin_limit_ns; // 0 = wait forever
   TraceRec* trace;        // MPIX_TRACE: this op's trace record, else null
+  int early_trigger;      // large blocking receive: let the copy grid launch before
+                          // waiting for the sender (only when the grid is small)
 };
+
+// Copy grids up to this many CTAs may be launched (and park at
+// griddepcontrol.wait) while a blocking receive waits for its sender; larger
+// ones launch after it, so a parked grid never fills the GPU.
+constexpr uint64_t kEarlyTriggerTiles = 64;
 
 struct WaitEntry {
   uint64_t* flag;
@@ -168,8 +175,9 @@ struct WaitEntry {
 };
 
 // One operation of a coalesced batch (k_batch): the P2PArgs fields of an
-// inline operation, packed (112 B) because the batch travels as kernel
-// parameters.
+// operation, packed (168 B) because the batch travels as kernel parameters.
+// Large operations (inl == 0) decide in k_batch, copy in one grouped grid
+// (k_gcopy) and complete in k_gfin.
 struct BatchOp {
   SlotDesc* post_ring;
   uint64_t* post_mirror;
@@ -183,11 +191,19 @@ struct BatchOp {
   uint64_t* my_done;
   uint64_t my_gen;
   uint64_t* err_word;
+  OpRecord* rec;          // large operations: decision record
+  uint8_t* staging;       // staged send: host staging buffer (or null)
+  uint64_t* stage_done;
+  uint64_t stage_gen;
+  uint8_t* arena;         // staged send: device arena (staging == null)
+  uint64_t* arena_state;
+  uint64_t arena_chunk;
+  uint32_t arena_slots;
   uint32_t E;
   uint16_t R;
-  uint8_t is_recv, mode, blocking, pad_[3];
+  uint8_t is_recv, mode, blocking, inl, early, pad_;
 };
-static_assert(sizeof(BatchOp) == 112, "BatchOp packing");
+static_assert(sizeof(BatchOp) == 168, "BatchOp packing");
 
 constexpr int kBatchOps = 64;     // operations per coalesced launch
 constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch
@@ -199,6 +215,14 @@ struct BatchArgs {
   uint64_t* err_word;
   WaitEntry w[NWAIT];
   BatchOp ops[NOPS];
+};
+
+// The grouped copy grid of a batch's large operations: tiles
+// [tile_start[j], tile_start[j+1]) belong to large operation j.
+struct GCopyArgs {
+  int m;
+  uint32_t tile_start[kBatchOps + 1];
+  OpRecord* rec[kBatchOps];
 };
 
 enum ARDtype : int { AR_I32 = 0, AR_F32 = 1, AR_BF16 = 2, AR_F64 = 3 };
@@ -232,7 +256,8 @@ struct ARArgs {
 int launch_p2p(const P2PArgs& a, bool sys, bool inline_copy, uint64_t copy_grid, cudaStream_t s,
                cudaEvent_t copy_ev0 = nullptr, cudaEvent_t copy_ev1 = nullptr);
 int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint64_t* err_word,
-                 uint64_t spin_limit_ns, bool sys, cudaStream_t s);
+                 uint64_t spin_limit_ns, bool sys, cudaStream_t s, cudaEvent_t copy_ev0 = nullptr,
+                 cudaEvent_t copy_ev1 = nullptr);
 int launch_allreduce(const ARArgs& a, bool sys, uint64_t reduce_grid, cudaStream_t s);
 uint64_t p2p_copy_grid(uint64_t bytes);
 uint64_t ar_reduce_grid(uint64_t work_bytes);

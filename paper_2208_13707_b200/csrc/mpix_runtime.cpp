@@ -219,6 +219,14 @@ struct StreamBatch {
   bool sys = false;
   uint64_t* err_word = nullptr;
   std::vector<BatchOp> ops;
+  // Intra-batch dependencies that force a flush before an operation joins:
+  // - a large operation frees its ring slot only in k_gfin, after the whole
+  //   k_batch grid: an operation needing that slot (same ring, pseq >= the
+  //   large operation's pseq + R) must go to a later launch;
+  std::unordered_map<const void*, uint64_t> first_large_pseq;  // ring (post mirror) -> pseq
+  // - a self-message operation launched post-only relies on its
+  //   counterpart running after it, not concurrently in the same grid.
+  std::vector<std::pair<const void*, uint64_t>> post_only;  // (comm, key)
 };
 
 struct World {
@@ -387,13 +395,28 @@ int flush_locked(StreamBatch& b, cudaStream_t s, const WaitEntry* w, int nwait, 
   int n = (int)b.ops.size();
   int wi = 0;
   uint64_t* err = b.err_word ? b.err_word : w_err;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (g_copy_timing.on.load()) {
+    bool large_recv = false;
+    for (auto& o : b.ops) large_recv |= !o.inl && o.is_recv;
+    if (large_recv) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      std::lock_guard<std::mutex> tl(g_copy_timing.mu);
+      g_copy_timing.ev.emplace_back(e0, e1);
+    }
+  }
   do {
     int m = std::min(nwait - wi, kBatchWaits);
-    int rc = launch_batch(b.ops.data(), n, w + wi, m, err, cfg.spin_limit_ns, b.sys || wsys, s);
+    int rc = launch_batch(b.ops.data(), n, w + wi, m, err, cfg.spin_limit_ns, b.sys || wsys, s,
+                          e0, e1);
+    e0 = e1 = nullptr;
     if (rc < 0) return -1;
     launches += rc;
     n = 0;
     b.ops.clear();
+    b.first_large_pseq.clear();
+    b.post_only.clear();
     wi += m;
   } while (wi < nwait);
   b.sys = false;
@@ -417,7 +440,7 @@ int flush_stream(cudaStream_t s) {
   return flush_locked(*b, s, nullptr, 0, false, nullptr);
 }
 
-BatchOp pack_op(const P2PArgs& a) {
+BatchOp pack_op(const P2PArgs& a, bool inl) {
   BatchOp o = {};
   o.post_ring = a.post_ring;
   o.post_mirror = a.post_mirror;
@@ -431,11 +454,20 @@ BatchOp pack_op(const P2PArgs& a) {
   o.my_done = a.my_done;
   o.my_gen = a.my_gen;
   o.err_word = a.err_word;
+  o.rec = a.rec;
+  o.staging = a.staging;
+  o.stage_done = a.stage_done;
+  o.stage_gen = a.stage_gen;
+  o.arena = a.arena;
+  o.arena_state = a.arena_state;
+  o.arena_chunk = a.arena_chunk;
+  o.arena_slots = a.arena_slots;
   o.E = (uint32_t)a.E;
   o.R = (uint16_t)a.R;
   o.is_recv = (uint8_t)a.is_recv;
   o.mode = (uint8_t)a.mode;
   o.blocking = (uint8_t)a.blocking;
+  o.inl = inl ? 1 : 0;
   return o;
 }
 
@@ -682,6 +714,7 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     CK(cudaMemcpyAsync(a.trace, &head, 32, cudaMemcpyHostToDevice, s));
   }
   bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
+  bool post_only = false;
   if (!inl && !blocking && peer == me) {
     // Self-message whose counterpart has not been enqueued yet: it can only
     // be enqueued later on this same stream (an enqueue comm has one stream),
@@ -689,7 +722,7 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     // copies: one small launch instead of proto + copy grid + fin.
     const auto& other = is_recv ? c->send_tagseq : c->recv_tagseq;
     auto it = other.find(tagseq_key(me, tag));
-    if (it == other.end() || it->second <= tseq) inl = true;
+    if (it == other.end() || it->second <= tseq) inl = post_only = true;
   }
   if (!inl) {
     uint64_t op = rs.op_next.fetch_add(1);
@@ -698,13 +731,19 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   }
   StreamBatch& b = batch_of(s, rs.device);
   std::lock_guard<std::mutex> lk(b.mu);
-  if (w.cfg.batch && !a.trace && inl && a.mode != MODE_STAGED) {
+  if (w.cfg.batch && !a.trace) {
     // Join the stream's batch; a blocking operation closes it (it must have
     // completed before anything behind it in the stream runs).
-    if ((int)b.ops.size() >= kBatchOps && flush_locked(b, s, nullptr, 0, false, nullptr) < 0)
-      return MPIX_ERR_CUDA;
+    bool flush_first = (int)b.ops.size() >= kBatchOps;
+    auto fl = b.first_large_pseq.find(a.post_mirror);
+    flush_first |= fl != b.first_large_pseq.end() && a.pseq >= fl->second + (uint64_t)a.R;
+    for (auto& po : b.post_only) flush_first |= po.first == c && po.second == a.key;
+    if (flush_first && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
     if (b.ops.empty()) b.err_word = rs.d_err;
-    b.ops.push_back(pack_op(a));
+    if (!inl) b.first_large_pseq.emplace(a.post_mirror, a.pseq);
+    if (post_only) b.post_only.emplace_back(c, a.key);
+    BatchOp o = pack_op(a, inl);
+    b.ops.push_back(o);
     b.sys |= sys;
     if (blocking && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
   } else {
@@ -716,6 +755,7 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
       std::lock_guard<std::mutex> tl(g_copy_timing.mu);
       g_copy_timing.ev.emplace_back(e0, e1);
     }
+    a.early_trigger = p2p_copy_grid(bytes) <= kEarlyTriggerTiles;
     int nk = launch_p2p(a, sys, inl, inl ? 1 : p2p_copy_grid(bytes), s, e0, e1);
     if (nk < 0) return MPIX_ERR_CUDA;
     g_launches.fetch_add(nk);

@@ -189,3 +189,49 @@ def test_two_comms_one_stream_share_a_batch(batch_env):
         sync_all(ctx)
         assert torch.equal(dst_b.cpu(), src_b.cpu())
         assert torch.equal(dst_a.cpu(), src_a.cpu())
+
+
+@pytest.mark.parametrize("sizes", [[1 << 20] * 6, [70_000, (3 << 20) + 5, 1, 4096, 65537, 8 << 20]])
+def test_large_window_grouped(sizes, batch_env):
+    """A halo-like window of large and small Isend/Irecv between two ranks:
+    with batching it is three launches per rank (decisions, one grouped copy
+    grid, completions + wait) and the bytes are exact."""
+    k = len(sizes)
+    with gpu_world(2) as (w, ctx):
+        src = [[rand_bytes(n, 300 + 10 * r + i) for i, n in enumerate(sizes)] for r in range(2)]
+        dst = [[torch.zeros(max(n, 1), dtype=torch.uint8, device=0) for n in sizes] for _ in range(2)]
+        torch.cuda.synchronize()
+        launches = {}
+
+        def body(r):
+            c = ctx[r].comm
+            reqs = [c.irecv_enqueue(dst[r][i], n, mpix.MPI_BYTE, 1 - r, i) for i, n in enumerate(sizes)]
+            reqs += [c.isend_enqueue(src[r][i], n, mpix.MPI_BYTE, 1 - r, i) for i, n in enumerate(sizes)]
+            mpix.waitall_enqueue(reqs)
+
+        l0 = mpix.launch_count()
+        w.run_ranks(body)
+        launches = mpix.launch_count() - l0
+        sync_all(ctx)
+        for r in range(2):
+            for i, n in enumerate(sizes):
+                assert torch.equal(dst[r][i][:n].cpu(), src[1 - r][i].cpu()), (r, i)
+        if batch_env:
+            assert launches == 2 * 3
+        assert mpix.rank_error(0) == 0 and mpix.rank_error(1) == 0
+
+
+def test_blocking_large_recv_before_send_on_same_gpu(batch_env):
+    """Rank 1 blocks in a 64 MiB Recv_enqueue before rank 0 (same GPU) sends:
+    the receiver's idle copy grid must not occupy the SMs the sender needs."""
+    n = 64 << 20
+    with gpu_world(2) as (w, ctx):
+        src = rand_bytes(n, 400)
+        dst = torch.zeros(n, dtype=torch.uint8, device=0)
+        torch.cuda.synchronize()
+        ctx[1].comm.recv_enqueue(dst, n, mpix.MPI_BYTE, 0, 8)
+        mpix.testing.delay(2_000_000, ctx[0].stream)  # 2 ms: the receive is posted first
+        ctx[0].comm.send_enqueue(src, n, mpix.MPI_BYTE, 1, 8)
+        sync_all(ctx)
+        assert torch.equal(dst.cpu(), src.cpu())
+        assert mpix.rank_error(0) == 0 and mpix.rank_error(1) == 0
