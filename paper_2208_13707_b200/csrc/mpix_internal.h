@@ -211,6 +211,7 @@ constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch
 template <int NOPS, int NWAIT>
 struct BatchArgs {
   int n, nwait;
+  int early;  // no grouped copy follows: trigger the next (head) kernel at start
   uint64_t spin_limit_ns;
   uint64_t* err_word;
   WaitEntry w[NWAIT];
@@ -260,7 +261,7 @@ int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint6
                  cudaEvent_t copy_ev1 = nullptr);
 int launch_allreduce(const ARArgs& a, bool sys, uint64_t reduce_grid, cudaStream_t s);
 uint64_t p2p_copy_grid(uint64_t bytes);
-uint64_t ar_reduce_grid(uint64_t work_bytes);
+uint64_t ar_reduce_grid(uint64_t work_bytes, int P);
 int preload_kernels();
 int launch_reduce_only(const uint64_t* sb, const uint64_t* rb, int P, int me, uint64_t count,
                        int esize, int dtype, int op, int algo, OpRecord* rec, cudaStream_t s);

@@ -596,6 +596,8 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
 template <bool SYS, bool INLINE>
 __global__ void __launch_bounds__(kThreads) k_proto(const P2PArgs a) {
   __shared__ Decision s_dc;
+  pdl_wait();                 // (launched early behind a previous operation)
+  if (INLINE) pdl_trigger();  // the next small head kernel may park behind me
   proto_body<SYS, INLINE>(a, s_dc);
 }
 
@@ -641,6 +643,7 @@ __device__ void fin_body(const P2PArgs& a, Decision& s_dc) {
 template <bool SYS>
 __global__ void __launch_bounds__(kThreads) k_fin(const P2PArgs a) {
   pdl_wait();
+  pdl_trigger();
   __shared__ Decision s_dc;
   fin_body<SYS>(a, s_dc);
 }
@@ -694,6 +697,8 @@ __device__ void wait_all(const WaitEntry* w, int nwait, uint64_t* err_word, uint
 template <bool SYS, int NOPS, int NWAIT>
 __global__ void __launch_bounds__(kThreads) k_batch(const BatchArgs<NOPS, NWAIT> b) {
   __shared__ Decision s_dc;
+  pdl_wait();
+  if (b.early) pdl_trigger();  // no grouped copy behind me: the next head kernel may park
   if ((int)blockIdx.x < b.n) {
     __shared__ P2PArgs a;
     const BatchOp& o = b.ops[blockIdx.x];
@@ -730,6 +735,7 @@ __global__ void __launch_bounds__(kCopyThreads, 2) k_gcopy(const GCopyArgs g) {
 template <bool SYS, int NOPS, int NWAIT>
 __global__ void __launch_bounds__(kThreads) k_gfin(const BatchArgs<NOPS, NWAIT> b) {
   pdl_wait();
+  pdl_trigger();
   __shared__ Decision s_dc;
   if ((int)blockIdx.x < b.n) {
     const BatchOp& o = b.ops[blockIdx.x];
@@ -982,6 +988,7 @@ __device__ void ar_tile(const ARArgs& a, const uint64_t* sb, const uint64_t* rb,
 // Entry: publish my buffers to every peer, wait for theirs, record them.
 template <bool SYS>
 __global__ void __launch_bounds__(32) k_ar_entry(const ARArgs a) {
+  pdl_wait();
   using M = Scope<SYS>;
   const int q = threadIdx.x;
   const int P = a.P;
@@ -1047,6 +1054,7 @@ static ReduceKernel reduce_kernel(int dtype, int op) {
 template <bool SYS>
 __global__ void __launch_bounds__(32) k_ar_exit(const ARArgs a) {
   pdl_wait();
+  pdl_trigger();
   using M = Scope<SYS>;
   const int q = threadIdx.x;
   if (a.rec->action == 0) return;
@@ -1076,6 +1084,21 @@ static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStre
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
+// Operation head kernels (k_proto, k_batch, k_ar_entry) start with
+// griddepcontrol.wait, so they may be launched programmatically behind the
+// previous kernel of the stream and park there until it completes. Only
+// small grids do so: parked CTAs hold SM slots, and at most kEarlyHeadCTAs
+// per stream may wait behind a kernel that spins on a peer.
+constexpr int kEarlyHeadCTAs = 4;
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_head(void (*k)(KArgs...), int grid, int block, cudaStream_t s,
+                               Args&&... args) {
+  if (grid <= kEarlyHeadCTAs) return launch_pdl(k, grid, block, s, std::forward<Args>(args)...);
+  k<<<grid, block, 0, s>>>(std::forward<Args>(args)...);
+  return cudaGetLastError();
+}
+
 uint64_t p2p_copy_grid(uint64_t bytes) {
   uint64_t tile = kTileVec * 16;
   uint64_t g = (bytes + tile - 1) / tile;
@@ -1086,13 +1109,15 @@ uint64_t p2p_copy_grid(uint64_t bytes) {
 int launch_p2p(const P2PArgs& a, bool sys, bool inl, uint64_t grid, cudaStream_t s,
                cudaEvent_t copy_ev0, cudaEvent_t copy_ev1) {
   if (inl) {
-    if (sys) k_proto<true, true><<<1, kThreads, 0, s>>>(a);
-    else k_proto<false, true><<<1, kThreads, 0, s>>>(a);
-    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+    cudaError_t e = sys ? launch_pdl(k_proto<true, true>, 1, kThreads, s, a)
+                        : launch_pdl(k_proto<false, true>, 1, kThreads, s, a);
+    return e == cudaSuccess ? 1 : -1;
   }
-  if (sys) k_proto<true, false><<<1, kThreads, 0, s>>>(a);
-  else k_proto<false, false><<<1, kThreads, 0, s>>>(a);
-  if (cudaGetLastError() != cudaSuccess) return -1;
+  {
+    cudaError_t e = sys ? launch_pdl(k_proto<true, false>, 1, kThreads, s, a)
+                        : launch_pdl(k_proto<false, false>, 1, kThreads, s, a);
+    if (e != cudaSuccess) return -1;
+  }
   if (copy_ev0) cudaEventRecord(copy_ev0, s);  // timing probe (bench roofline) only
   if (launch_pdl(k_copy, (int)grid, kCopyThreads, s, a) != cudaSuccess) return -1;
   if (copy_ev1) cudaEventRecord(copy_ev1, s);
@@ -1126,16 +1151,20 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   for (int i = 0; i < n; ++i) b.ops[i].early = tiles <= kEarlyTriggerTiles;
   if (g.m == 0) {  // inline operations only: one launch, the wait included
     const int grid = n + (nwait > 0 ? 1 : 0);
-    if (sys) k_batch<true, NOPS, NWAIT><<<grid, kThreads, 0, s>>>(b);
-    else k_batch<false, NOPS, NWAIT><<<grid, kThreads, 0, s>>>(b);
-    return cudaGetLastError() == cudaSuccess ? 1 : -1;
+    b.early = 1;
+    cudaError_t e = sys ? launch_head(k_batch<true, NOPS, NWAIT>, grid, kThreads, s, b)
+                        : launch_head(k_batch<false, NOPS, NWAIT>, grid, kThreads, s, b);
+    return e == cudaSuccess ? 1 : -1;
   }
   // decisions (the wait moves to k_gfin) -> grouped copy -> completions + wait
   const int nw = b.nwait;
   b.nwait = 0;
-  if (sys) k_batch<true, NOPS, NWAIT><<<n, kThreads, 0, s>>>(b);
-  else k_batch<false, NOPS, NWAIT><<<n, kThreads, 0, s>>>(b);
-  if (cudaGetLastError() != cudaSuccess) return -1;
+  b.early = 0;
+  {
+    cudaError_t e = sys ? launch_head(k_batch<true, NOPS, NWAIT>, n, kThreads, s, b)
+                        : launch_head(k_batch<false, NOPS, NWAIT>, n, kThreads, s, b);
+    if (e != cudaSuccess) return -1;
+  }
   b.nwait = nw;
   if (ev0) cudaEventRecord(ev0, s);  // timing probe (bench roofline) only
   if (launch_pdl(k_gcopy, (int)tiles, kCopyThreads, s, g) != cudaSuccess) return -1;
@@ -1161,17 +1190,24 @@ int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint6
   return -1;
 }
 
-uint64_t ar_reduce_grid(uint64_t work_bytes) {
-  uint64_t tile = kArTileVec * 16;
-  uint64_t g = (work_bytes + tile - 1) / tile;
+// One CTA per tile when it moves enough bytes (P inputs + outputs of
+// kArTileVec x 16 B each); with few ranks a CTA takes several tiles so CTA
+// launch does not dominate (P = 1: 4 tiles = 32 KiB in + 32 KiB out).
+uint64_t ar_reduce_grid(uint64_t work_bytes, int P) {
+  const uint64_t tile = kArTileVec * 16;
+  const uint64_t tiles = (work_bytes + tile - 1) / tile;
+  const uint64_t per = P >= 4 ? 1 : (4 + P - 1) / P;
+  uint64_t g = (tiles + per - 1) / per;
   if (g > (1ull << 20)) g = 1ull << 20;
   return g < 1 ? 1 : g;
 }
 
 int launch_allreduce(const ARArgs& a, bool sys, uint64_t grid, cudaStream_t s) {
-  if (sys) k_ar_entry<true><<<1, 32, 0, s>>>(a);
-  else k_ar_entry<false><<<1, 32, 0, s>>>(a);
-  if (cudaGetLastError() != cudaSuccess) return -1;
+  {
+    cudaError_t e = sys ? launch_pdl(k_ar_entry<true>, 1, 32, s, a)
+                        : launch_pdl(k_ar_entry<false>, 1, 32, s, a);
+    if (e != cudaSuccess) return -1;
+  }
   if (launch_pdl(reduce_kernel(a.dtype, a.op), (int)grid, kArThreads, s, a) != cudaSuccess) return -1;
   if (a.P > 1) {
     cudaError_t e = sys ? launch_pdl(k_ar_exit<true>, 1, 32, s, a)
@@ -1206,7 +1242,7 @@ int launch_reduce_only(const uint64_t* sb, const uint64_t* rb, int P, int me, ui
   a.rec = rec;
   uint64_t bytes = count * (uint64_t)esize;
   uint64_t work = algo == AR_TWOSHOT ? (bytes + P - 1) / P : bytes;
-  reduce_kernel(dtype, op)<<<(unsigned)ar_reduce_grid(work), kArThreads, 0, s>>>(a);
+  reduce_kernel(dtype, op)<<<(unsigned)ar_reduce_grid(work, P), kArThreads, 0, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -881,7 +881,7 @@ int allreduce_enqueue(const void* sbuf, void* rbuf, int count, MPI_Datatype dt, 
   StreamBatch& b = batch_of(c->cu, rs.device);
   std::lock_guard<std::mutex> lk(b.mu);
   if (!b.ops.empty() && flush_locked(b, c->cu, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
-  int nk = launch_allreduce(a, sys, ar_reduce_grid(work), c->cu);
+  int nk = launch_allreduce(a, sys, ar_reduce_grid(work, P), c->cu);
   if (nk < 0) return MPIX_ERR_CUDA;
   g_launches.fetch_add(nk);
   return MPI_SUCCESS;
