@@ -82,8 +82,19 @@ struct RegionLayout {
   __host__ __device__ uint64_t coll_exit(int q) const {
     return coll_in(P) + (uint64_t)q * 8;
   }
+  // Dynamic matching (MPIX_MATCHING=dynamic, wildcard receives): the
+  // region bases of every member, then my matching domain (lock, receive
+  // ticket, arrival counter, per-source send tickets) and my posted-receive
+  // queue of R entries.
+  __host__ __device__ uint64_t bases() const { return (coll_exit(P) + 63) & ~63ull; }
+  __host__ __device__ uint64_t dom() const { return (bases() + 8ull * P + 63) & ~63ull; }
+  __host__ __device__ uint64_t dom_lock() const { return dom(); }
+  __host__ __device__ uint64_t dom_next_rpost() const { return dom() + 8; }
+  __host__ __device__ uint64_t dom_arrival() const { return dom() + 16; }
+  __host__ __device__ uint64_t dom_next_spost(int q) const { return dom() + 64 + 8ull * q; }
+  __host__ __device__ uint64_t pq() const { return (dom_next_spost(P) + 63) & ~63ull; }
   __host__ __device__ uint64_t eager_base() const {
-    return (coll_exit(P) + 255) & ~255ull;
+    return (pq() + ring_bytes() + 255) & ~255ull;
   }
   // eager payload ring of messages q -> me
   __host__ __device__ uint64_t eager(int q) const {
@@ -162,6 +173,10 @@ struct P2PArgs {
   TraceRec* trace;        // MPIX_TRACE: this op's trace record, else null
   int early_trigger;      // large blocking receive: let the copy grid launch before
                           // waiting for the sender (only when the grid is small)
+  // dynamic matching (dyn = 1): pseq is the receive ticket on the receive
+  // side; peer / tag may be -1 (ANY_SOURCE / ANY_TAG) on receives
+  int dyn, P, me, peer, tag;
+  uint64_t* bases;        // region bases of the comm's members (in my region)
 };
 
 // Copy grids up to this many CTAs may be launched (and park at
@@ -175,7 +190,7 @@ struct WaitEntry {
 };
 
 // One operation of a coalesced batch (k_batch): the P2PArgs fields of an
-// operation, packed (168 B) because the batch travels as kernel parameters.
+// operation, packed (192 B) because the batch travels as kernel parameters.
 // Large operations (inl == 0) decide in k_batch, copy in one grouped grid
 // (k_gcopy) and complete in k_gfin.
 struct BatchOp {
@@ -198,12 +213,14 @@ struct BatchOp {
   uint8_t* arena;         // staged send: device arena (staging == null)
   uint64_t* arena_state;
   uint64_t arena_chunk;
+  uint64_t* bases;        // dynamic matching
   uint32_t arena_slots;
   uint32_t E;
-  uint16_t R;
-  uint8_t is_recv, mode, blocking, inl, early, pad_;
+  int32_t peer, tag;      // dynamic matching (-1 = ANY on receives)
+  uint16_t R, P, me;
+  uint8_t is_recv, mode, blocking, inl, early, dyn;
 };
-static_assert(sizeof(BatchOp) == 168, "BatchOp packing");
+static_assert(sizeof(BatchOp) == 192, "BatchOp packing");
 
 constexpr int kBatchOps = 64;     // operations per coalesced launch
 constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch

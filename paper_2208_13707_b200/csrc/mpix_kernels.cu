@@ -288,6 +288,7 @@ struct Decision {
   uint64_t action, src, dst, bytes;
   Fin fin;
   int wait_own;
+  int now;  // copy + complete in the deciding CTA even on the split path
   // staged blocking send: the staging buffer and its release word/value
   // (host-provided, or claimed from the rank's device arena)
   uint8_t* stage_ptr;
@@ -399,6 +400,345 @@ __device__ bool claim_stage_slot(const P2PArgs& a, Decision& dc) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dynamic matching (MPIX_MATCHING=dynamic): the reference's single-queue
+// matcher (proj/src/endpoint.cpp:29-69) per (comm, receiver d), serialised by
+// a lock in d's region. Unexpected messages are the send descriptors in d's
+// SR rings, stamped with an arrival sequence; posted receives live in d's
+// posted-receive queue (PQ), possibly with ANY_SOURCE / ANY_TAG.
+//   receive (ticket = d's receive sequence, so a batch matches in post
+//     order): take the earliest-arrived acceptable send descriptor, else
+//     append to PQ;
+//   send (ticket = pseq per source, so sends of a source stay ordered): take
+//     the earliest-posted acceptable receive, else post a descriptor.
+// The winner copies and completes exactly as in the static protocol.
+// ---------------------------------------------------------------------------
+struct Dom {
+  uint64_t* lock;
+  uint64_t* next_rpost;
+  uint64_t* arrival;
+  uint64_t* next_spost;  // [P]
+  SlotDesc* pq;          // [R]
+};
+
+__device__ __forceinline__ Dom dom_at(uint8_t* base, const RegionLayout& L) {
+  Dom d;
+  d.lock = reinterpret_cast<uint64_t*>(base + L.dom_lock());
+  d.next_rpost = reinterpret_cast<uint64_t*>(base + L.dom_next_rpost());
+  d.arrival = reinterpret_cast<uint64_t*>(base + L.dom_arrival());
+  d.next_spost = reinterpret_cast<uint64_t*>(base + L.dom_next_spost(0));
+  d.pq = reinterpret_cast<SlotDesc*>(base + L.pq());
+  return d;
+}
+
+template <bool SYS>
+__device__ bool dom_lock(uint64_t* lock, const P2PArgs& a) {
+  using M = Scope<SYS>;
+  const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
+  unsigned ns = 32;
+  while (M::cas(lock, 0, 1) != 0) {
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+    if (a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
+      if (a.err_word) ScopeSys::st_rlx(a.err_word, ERRW_WAIT_SLOT);
+      return false;
+    }
+  }
+  return true;
+}
+
+template <bool SYS>
+__device__ __forceinline__ void dom_unlock(uint64_t* lock) {
+  Scope<SYS>::st_rel(lock, 0);
+}
+
+// Warp-wide argmin of (v, idx); lanes without a candidate pass v = ~0.
+__device__ __forceinline__ void warp_argmin(uint64_t& v, int& idx) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov < v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+}
+
+__device__ __forceinline__ bool tag_ok(int32_t want, int32_t have) { return want < 0 || want == have; }
+
+// Receive side (warp 0, lock held): the earliest-arrived POSTED send
+// descriptor from an acceptable source with an acceptable tag. Returns the
+// source (or -1) and the slot; every lane gets the result.
+template <bool SYS>
+__device__ int dyn_scan_sends(const P2PArgs& a, uint8_t* my_base, const RegionLayout& L, int* slot_out) {
+  const int lane = threadIdx.x & 31;
+  uint64_t best = ~0ull;
+  int best_idx = 0x7fffffff;
+  const int q0 = a.peer >= 0 ? a.peer : 0, q1 = a.peer >= 0 ? a.peer + 1 : a.P;
+  for (int q = q0; q < q1; ++q) {
+    SlotDesc* ring = reinterpret_cast<SlotDesc*>(my_base + L.sr(q));
+    for (int i = lane; i < a.R; i += 32) {
+      uint64_t st, key;
+      ld_pair<SYS>(&ring[i], st, key);
+      if ((st & 0xff) == ST_POSTED && tag_ok(a.tag, (int32_t)(key >> 32))) {
+        uint64_t arr = Scope<SYS>::ld_rlx(&ring[i].pad[0]);
+        if (arr < best) {
+          best = arr;
+          best_idx = q * a.R + i;
+        }
+      }
+    }
+  }
+  warp_argmin(best, best_idx);
+  if (best == ~0ull) return -1;
+  *slot_out = best_idx % a.R;
+  return best_idx / a.R;
+}
+
+// Send side (warp 0, lock held): the earliest-posted POSTED receive in the
+// receiver's PQ accepting (me, tag). Returns the PQ index or -1.
+template <bool SYS>
+__device__ int dyn_scan_recvs(const P2PArgs& a, SlotDesc* pq) {
+  const int lane = threadIdx.x & 31;
+  uint64_t best = ~0ull;
+  int best_idx = 0x7fffffff;
+  for (int i = lane; i < a.R; i += 32) {
+    uint64_t st, key;
+    ld_pair<SYS>(&pq[i], st, key);
+    const int32_t src = (int32_t)(key >> 32), tg = (int32_t)(uint32_t)key;
+    if ((st & 0xff) == ST_POSTED && (src < 0 || src == a.me) && tag_ok(tg, a.tag)) {
+      const uint64_t rseq = st >> 8;
+      if (rseq < best) {
+        best = rseq;
+        best_idx = i;
+      }
+    }
+  }
+  warp_argmin(best, best_idx);
+  return best == ~0ull ? -1 : best_idx;
+}
+
+// Sender takes posted receive pq[j] (lock held, lane 0): push src -> its buffer.
+template <bool SYS>
+__device__ void dyn_send_take(const P2PArgs& a, Decision& dc, SlotDesc* pq, int j, const Dom& D,
+                              const uint8_t* src) {
+  using M = Scope<SYS>;
+  SlotDesc* e = &pq[j];
+  const uint64_t st = M::ld_rlx(&e->state);
+  const uint64_t addr = M::ld_rlx(&e->addr), cap = M::ld_rlx(&e->bytes);
+  const uint64_t done_addr = M::ld_rlx(&e->done_addr), done_val = M::ld_rlx(&e->done_val);
+  M::st_rlx(&e->state, st_word(st >> 8, ST_TAKEN));
+  M::st_rlx(&D.next_spost[a.me], a.pseq + 1);
+  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  dc.action = ACT_COPY;
+  dc.src = (uint64_t)src;
+  dc.dst = addr;
+  dc.bytes = umin(a.bytes, cap);  // truncation: endpoint.cpp:17
+  dc.fin.clear();
+  // TAKEN is final for a PQ entry: the receiver reposts into the slot as soon
+  // as it is not POSTED, so no later FREE store may follow.
+  dc.fin.add_b(&a.post_mirror[slot], a.pseq + 1);  // my SR slot is skipped
+  dc.fin.add_b(reinterpret_cast<void*>(done_addr), done_val);
+  dc.fin.add_b(a.my_done, a.my_gen);
+  if (a.mode == MODE_STAGED && dc.stage_done) dc.fin.add_b(dc.stage_done, dc.stage_gen);
+}
+
+// Sender posts its descriptor (lock held, lane 0), stamped with the arrival.
+// key = tag << 32 | 1 if the payload sits in the eager ring slot.
+template <bool SYS>
+__device__ void dyn_send_post(const P2PArgs& a, const Dom& D, uint64_t addr, uint64_t done_addr,
+                              uint64_t done_val, bool eager) {
+  using M = Scope<SYS>;
+  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  SlotDesc* d = &a.post_ring[slot];
+  const uint64_t arr = M::ld_rlx(D.arrival);
+  M::st_rlx(D.arrival, arr + 1);
+  M::st_rlx(&d->key, ((uint64_t)(uint32_t)a.tag << 32) | (eager ? 1u : 0u));
+  M::st_rlx(&d->addr, addr);
+  M::st_rlx(&d->bytes, a.bytes);
+  M::st_rlx(&d->done_addr, done_addr);
+  M::st_rlx(&d->done_val, done_val);
+  M::st_rlx(&d->pad[0], arr);
+  M::st_rlx(&d->state, st_word(a.pseq, ST_POSTED));
+  M::st_rlx(&D.next_spost[a.me], a.pseq + 1);
+}
+
+template <bool SYS>
+__device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
+  using M = Scope<SYS>;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const RegionLayout L{a.P, a.R, a.E};
+  __shared__ int s_stage;  // 1: eager payload to copy first
+  uint8_t* my_base = reinterpret_cast<uint8_t*>(a.bases[a.me]);
+  if (threadIdx.x == 0) {
+    dc.wait_own = 0;
+    dc.now = 0;
+    dc.fin.clear();
+    dc.action = ACT_NONE;
+    dc.stage_ptr = a.staging;
+    dc.stage_done = a.stage_done;
+    dc.stage_gen = a.stage_gen;
+    s_stage = 0;
+  }
+  __syncthreads();
+  if (!a.is_recv) {
+    const Dom D = dom_at(reinterpret_cast<uint8_t*>(a.bases[a.peer]), L);
+    if (threadIdx.x == 0) {
+      bool ok = spin_ge<SYS>(&D.next_spost[a.me], a.pseq, a.err_word, a.spin_limit_ns, ERRW_WAIT_SLOT) &&
+                wait_post_slot<SYS>(a);
+      s_stage = ok ? (a.mode == MODE_EAGER ? 1 : 2) : 0;
+    }
+    __syncthreads();
+    if (s_stage == 1) {  // eager: payload into my slot of the receiver's eager ring first
+      const int slot = (int)(a.pseq % (uint64_t)a.R);
+      cta_copy(a.eager_ring + (uint64_t)slot * a.E, a.buf, a.bytes);
+      __syncthreads();
+      if (threadIdx.x == 0) M::fence_ar();
+    }
+    if (warp == 0 && s_stage != 0) {
+      int got = lane == 0 ? (int)dom_lock<SYS>(D.lock, a) : 0;
+      got = __shfl_sync(0xffffffffu, got, 0);
+      if (got) {
+        M::fence_ar();
+        const int j = dyn_scan_recvs<SYS>(a, D.pq);
+        if (lane == 0) {
+          if (j >= 0) {
+            dyn_send_take<SYS>(a, dc, D.pq, j, D, a.buf);
+          } else if (a.mode == MODE_STAGED) {
+            dc.action = ACT_STAGE;  // ticket kept until the staged copy is published
+          } else {
+            const int slot = (int)(a.pseq % (uint64_t)a.R);
+            const uint64_t addr = a.mode == MODE_EAGER ? (uint64_t)(a.eager_ring + (uint64_t)slot * a.E)
+                                                       : (uint64_t)a.buf;
+            if (a.mode == MODE_EAGER) dyn_send_post<SYS>(a, D, addr, 0, 0, true);
+            else dyn_send_post<SYS>(a, D, addr, (uint64_t)a.my_done, a.my_gen, false);
+          }
+          dom_unlock<SYS>(D.lock);
+        }
+        __syncwarp();
+        if (s_stage == 2 && a.mode == MODE_STAGED && !dc.stage_ptr) {
+          // claim staging only now that it is needed (lane 0 wrote dc first)
+          if (dc.action == ACT_STAGE && !claim_stage_slot<SYS>(a, dc) && lane == 0) dc.action = ACT_NONE;
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 0) {
+    const Dom D = dom_at(my_base, L);
+    const int qslot = (int)(a.pseq % (uint64_t)a.R);
+    int got = 0;
+    if (lane == 0) {
+      // my receive ticket, my PQ slot no longer POSTED, then the lock
+      got = spin_ge<SYS>(D.next_rpost, a.pseq, a.err_word, a.spin_limit_ns, ERRW_WAIT_SLOT);
+      if (got) {
+        const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
+        while ((M::ld_acq(&D.pq[qslot].state) & 0xff) == ST_POSTED) {
+          __nanosleep(128);
+          if (a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
+            if (a.err_word) ScopeSys::st_rlx(a.err_word, ERRW_WAIT_SLOT);
+            got = 0;
+            break;
+          }
+        }
+      }
+      if (got) got = dom_lock<SYS>(D.lock, a);
+    }
+    got = __shfl_sync(0xffffffffu, got, 0);
+    if (got) {
+      M::fence_ar();
+      int sslot = 0;
+      const int q = dyn_scan_sends<SYS>(a, my_base, L, &sslot);
+      if (lane == 0) {
+        if (q >= 0) {
+          SlotDesc* sd = reinterpret_cast<SlotDesc*>(my_base + L.sr(q)) + sslot;
+          const uint64_t st = M::ld_rlx(&sd->state);
+          const uint64_t key = M::ld_rlx(&sd->key);
+          const uint64_t addr = M::ld_rlx(&sd->addr), len = M::ld_rlx(&sd->bytes);
+          const uint64_t done_addr = M::ld_rlx(&sd->done_addr), done_val = M::ld_rlx(&sd->done_val);
+          const uint64_t spseq = st >> 8;
+          uint8_t* qbase = reinterpret_cast<uint8_t*>(a.bases[q]);
+          uint64_t* qmirror = reinterpret_cast<uint64_t*>(qbase + L.sr_free(a.me)) + sslot;
+          M::st_rlx(D.next_rpost, a.pseq + 1);
+          dc.action = ACT_COPY;
+          dc.src = addr;
+          dc.dst = (uint64_t)a.buf;
+          dc.bytes = umin(len, a.bytes);
+          dc.fin.clear();
+          if (key & 1) {
+            // payload in the eager ring slot: copy it now, then free the slot
+            M::st_rlx(&sd->state, st_word(spseq, ST_TAKEN));
+            dc.now = 1;
+            dc.fin.add_a(&sd->state, st_word(spseq, ST_FREE));
+            dc.fin.add_b(qmirror, spseq + 1);
+          } else {
+            // payload elsewhere (user buffer / staging): the slot is free as
+            // soon as it is taken, so a sender waiting for it never waits on
+            // this copy (or on the rest of this batch)
+            M::st_rlx(&sd->state, st_word(spseq, ST_FREE));
+            M::fence_ar();
+            M::st_rlx(qmirror, spseq + 1);
+          }
+          dc.fin.add_b(reinterpret_cast<void*>(done_addr), done_val);
+          dc.fin.add_b(a.my_done, a.my_gen);
+        } else {
+          SlotDesc* e = &D.pq[qslot];
+          M::st_rlx(&e->key, ((uint64_t)(uint32_t)a.peer << 32) | (uint32_t)a.tag);
+          M::st_rlx(&e->addr, (uint64_t)a.buf);
+          M::st_rlx(&e->bytes, a.bytes);
+          M::st_rlx(&e->done_addr, (uint64_t)a.my_done);
+          M::st_rlx(&e->done_val, a.my_gen);
+          M::st_rlx(&e->state, st_word(a.pseq, ST_POSTED));
+          M::st_rlx(D.next_rpost, a.pseq + 1);
+          if (a.blocking) dc.wait_own = 1;
+        }
+        dom_unlock<SYS>(D.lock);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// Publish a staged blocking send under dynamic matching (whole CTA): under
+// the lock, take a receive posted meanwhile (push from staging) or post the
+// staging buffer, then release the send ticket.
+template <bool SYS>
+__device__ void stage_publish_dyn(const P2PArgs& a, Decision& dc) {
+  using M = Scope<SYS>;
+  const RegionLayout L{a.P, a.R, a.E};
+  const Dom D = dom_at(reinterpret_cast<uint8_t*>(a.bases[a.peer]), L);
+  __shared__ int s_push;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int got = lane == 0 ? (int)dom_lock<SYS>(D.lock, a) : 0;
+    got = __shfl_sync(0xffffffffu, got, 0);
+    if (lane == 0) s_push = 0;
+    if (got) {
+      M::fence_ar();
+      const int j = dyn_scan_recvs<SYS>(a, D.pq);
+      if (lane == 0) {
+        if (j >= 0) {
+          dyn_send_take<SYS>(a, dc, D.pq, j, D, dc.stage_ptr);
+          s_push = 1;
+        } else {
+          dyn_send_post<SYS>(a, D, (uint64_t)dc.stage_ptr, (uint64_t)dc.stage_done, dc.stage_gen,
+                             false);
+        }
+        dom_unlock<SYS>(D.lock);
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (s_push == 1) {
+    cta_copy(reinterpret_cast<uint8_t*>(dc.dst), reinterpret_cast<const uint8_t*>(dc.src), dc.bytes);
+    __syncthreads();
+    if (threadIdx.x == 0) dc.fin.run<SYS>();
+  }
+}
+
 // The handshake (whole CTA calls; warp 0 works, the CTA copies eager
 // payloads). On return dc holds ACT_NONE / ACT_COPY / ACT_STAGE.
 template <bool SYS>
@@ -413,6 +753,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     if (lane == 0) {
       trace_t(a.trace, 1);
       dc.wait_own = 0;
+      dc.now = 0;
       dc.fin.clear();
       dc.action = ACT_NONE;
       dc.stage_ptr = a.staging;  // null: claim from the device arena if needed
@@ -538,10 +879,23 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
     a.trace->g0 = globaltimer();
     a.trace->t[0] = clock64();
   }
-  decide<SYS>(a, s_dc);
+  if (a.dyn) decide_dyn<SYS>(a, s_dc);
+  else decide<SYS>(a, s_dc);
   if (a.trace && threadIdx.x == 0)
     a.trace->info = (uint64_t)a.is_recv | ((uint64_t)a.mode << 4) | ((uint64_t)INLINE << 8) |
                     (s_dc.action << 12);
+  if (!INLINE && s_dc.now) {
+    cta_copy(reinterpret_cast<uint8_t*>(s_dc.dst), reinterpret_cast<const uint8_t*>(s_dc.src),
+             s_dc.bytes);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_dc.fin.run<SYS>();
+      a.rec->action = ACT_NONE;  // nothing left for the copy grid / k_fin
+    }
+    __syncthreads();
+    pdl_trigger();
+    return;
+  }
   if (!INLINE) {
     if (threadIdx.x == 0) {
       OpRecord* rec = a.rec;
@@ -586,7 +940,8 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
   } else if (s_dc.action == ACT_STAGE) {
     cta_copy(s_dc.stage_ptr, a.buf, a.bytes);
     __syncthreads();
-    stage_publish<SYS>(a, s_dc);
+    if (a.dyn) stage_publish_dyn<SYS>(a, s_dc);
+    else stage_publish<SYS>(a, s_dc);
   } else if (threadIdx.x == 0) {
     if (s_dc.wait_own) spin_ge<SYS>(a.my_done, a.my_gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE);
     if (a.trace) a.trace->g1 = globaltimer();
@@ -635,7 +990,8 @@ __device__ void fin_body(const P2PArgs& a, Decision& s_dc) {
       s_dc.stage_gen = rec->stage_gen;
     }
     __syncthreads();
-    stage_publish<SYS>(a, s_dc);
+    if (a.dyn) stage_publish_dyn<SYS>(a, s_dc);
+    else stage_publish<SYS>(a, s_dc);
   }
 }
 
@@ -686,6 +1042,12 @@ __device__ void load_op(const BatchOp& o, uint64_t spin_limit_ns, P2PArgs& a) {
   a.spin_limit_ns = spin_limit_ns;
   a.trace = nullptr;
   a.early_trigger = o.early;
+  a.dyn = o.dyn;
+  a.P = o.P;
+  a.me = o.me;
+  a.peer = o.peer;
+  a.tag = o.tag;
+  a.bases = o.bases;
 }
 
 template <bool SYS>

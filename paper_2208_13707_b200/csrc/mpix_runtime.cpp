@@ -42,6 +42,7 @@ struct Config {
   bool trace = false;                // MPIX_TRACE=1: per-op device trace ring
   bool force_sys = false;            // MPIX_FORCE_SYS=1: system scope even on one GPU
   bool batch = true;                 // MPIX_BATCH=0: one launch per operation
+  bool dyn_match = false;            // MPIX_MATCHING=dynamic: device matching engine, wildcards
   int stage_slots = 64;              // MPIX_STAGE_SLOTS: device staging arena slots per rank
   uint64_t stage_chunk = 4ull << 20; // MPIX_STAGE_CHUNK: bytes per arena slot
 
@@ -63,6 +64,8 @@ struct Config {
     c.trace = geti("MPIX_TRACE", 0) != 0;
     c.force_sys = geti("MPIX_FORCE_SYS", 0) != 0;
     c.batch = geti("MPIX_BATCH", 1) != 0;
+    const char* m = std::getenv("MPIX_MATCHING");
+    c.dyn_match = m && std::string(m) == "dynamic";
     c.stage_slots = (int)geti("MPIX_STAGE_SLOTS", c.stage_slots);
     if (c.stage_slots > 1024) c.stage_slots = 1024;
     c.stage_chunk = (geti("MPIX_STAGE_CHUNK", c.stage_chunk) + 255) & ~255ull;
@@ -198,6 +201,8 @@ struct mpix_comm_s {
   bool enqueue_ok = false;
   cudaStream_t cu = nullptr;
   std::vector<uint64_t> send_pseq, recv_pseq;
+  uint64_t recv_rseq = 0;  // dynamic matching: my receive ticket
+  bool any_remote = false; // some member lives on another GPU
   std::unordered_map<uint64_t, uint32_t> send_tagseq, recv_tagseq;
   uint64_t coll_epoch = 0;
   uint64_t rv_seq = 0;
@@ -464,6 +469,12 @@ BatchOp pack_op(const P2PArgs& a, bool inl) {
   o.arena_slots = a.arena_slots;
   o.E = (uint32_t)a.E;
   o.R = (uint16_t)a.R;
+  o.bases = a.bases;
+  o.peer = a.peer;
+  o.tag = a.tag;
+  o.P = (uint16_t)a.P;
+  o.me = (uint16_t)a.me;
+  o.dyn = (uint8_t)a.dyn;
   o.is_recv = (uint8_t)a.is_recv;
   o.mode = (uint8_t)a.mode;
   o.blocking = (uint8_t)a.blocking;
@@ -529,6 +540,15 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
     std::lock_guard<std::mutex> lk(rank_of(0).mu);
     for (int q = 0; q < P; ++q) sh->base[q] = static_cast<uint8_t*>(v2[q].p0);
   }
+  // The member bases also go into my region (dynamic matching resolves
+  // wildcard sources on the device).
+  {
+    std::vector<uint64_t> bases(P);
+    for (int q = 0; q < P; ++q) bases[q] = (uint64_t)v2[q].p0;
+    CK(cudaSetDevice(rs.device));
+    CK(cudaMemcpyAsync(region + L.bases(), bases.data(), 8ull * P, cudaMemcpyHostToDevice, rs.aux));
+    CK(cudaStreamSynchronize(rs.aux));
+  }
   // Phase 3: nobody uses the comm until every member has filled the table.
   par->sh->rv.exchange(P, me, par->rv_seq++, CollMsg{});
 
@@ -545,6 +565,7 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
   c->cu = c->enqueue_ok ? streams[0]->cu : nullptr;
   c->send_pseq.assign(P, 0);
   c->recv_pseq.assign(P, 0);
+  for (int q = 0; q < P; ++q) c->any_remote |= rank_of(q).device != rs.device;
   {
     std::lock_guard<std::mutex> lk(w.comms_mu);
     w.all_comms.push_back(c);
@@ -633,6 +654,8 @@ int acquire_staging(RankState& rs, uint64_t bytes, cudaStream_t s, uint8_t** p, 
 }
 
 // Point-to-point enqueue (send side and receive side).
+bool w_dyn() { return g_world && g_world->cfg.dyn_match; }
+
 int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
                 bool is_recv, bool blocking, MPI_Request* req) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
@@ -642,7 +665,9 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   if (rc) return rc;
   int esz = type_size(dt);
   if (!esz) return MPIX_ERR_TYPE;
-  if (is_recv && (peer == MPI_ANY_SOURCE || tag == MPI_ANY_TAG)) return MPIX_ERR_UNSUPPORTED;
+  const bool dyn = w_dyn();
+  // Wildcards need the device matching engine (MPIX_MATCHING=dynamic).
+  if (is_recv && !dyn && (peer == MPI_ANY_SOURCE || tag == MPI_ANY_TAG)) return MPIX_ERR_UNSUPPORTED;
   if (!blocking && !req) return MPIX_ERR_INVALID_ARG;
 
   World& w = *g_world;
@@ -672,6 +697,10 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     a.scan_mirror = reinterpret_cast<uint64_t*>(sh.base[d] + L.rr_free(me));
     a.eager_ring = sh.base[d] + L.eager(me);
     a.mode = !blocking ? MODE_ISEND : (bytes <= L.E ? MODE_EAGER : MODE_STAGED);
+  } else if (dyn) {
+    tseq = 0;
+    a.pseq = c->recv_rseq++;  // receive ticket (post order)
+    a.mode = 0;
   } else {
     const int s = peer;
     tseq = c->recv_tagseq[tagseq_key(s, tag)]++;
@@ -683,8 +712,17 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     a.mode = 0;
   }
   a.key = ((uint64_t)(uint32_t)tag << 32) | tseq;
+  if (dyn) {
+    a.dyn = 1;
+    a.P = sh.P;
+    a.me = me;
+    a.peer = peer;  // -1 = ANY_SOURCE (receives)
+    a.tag = tag;    // -1 = ANY_TAG (receives)
+    a.bases = reinterpret_cast<uint64_t*>(sh.base[me] + L.bases());
+  }
 
-  const bool sys = w.cfg.force_sys || rank_of(peer).device != rs.device;
+  const bool sys = w.cfg.force_sys ||
+                   (dyn ? c->any_remote : rank_of(peer).device != rs.device);
   CK(cudaSetDevice(rs.device));
   cudaStream_t s = c->cu;
   Ticket t{};
@@ -715,7 +753,7 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   }
   bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
   bool post_only = false;
-  if (!inl && !blocking && peer == me) {
+  if (!inl && !blocking && peer == me && !dyn) {
     // Self-message whose counterpart has not been enqueued yet: it can only
     // be enqueued later on this same stream (an enqueue comm has one stream),
     // so it runs after this operation, which therefore only posts and never
@@ -740,7 +778,7 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     for (auto& po : b.post_only) flush_first |= po.first == c && po.second == a.key;
     if (flush_first && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
     if (b.ops.empty()) b.err_word = rs.d_err;
-    if (!inl) b.first_large_pseq.emplace(a.post_mirror, a.pseq);
+    if (!inl && a.post_mirror) b.first_large_pseq.emplace(a.post_mirror, a.pseq);
     if (post_only) b.post_only.emplace_back(c, a.key);
     BatchOp o = pack_op(a, inl);
     b.ops.push_back(o);

@@ -20,6 +20,11 @@ VARIANTS = {
     # the cross-GPU (system-scope) kernel instantiations, on one GPU
     "sys_scope": {"MPIX_FORCE_SYS": "1"},
     "sys_scope_split": {"MPIX_FORCE_SYS": "1", "MPIX_INLINE_BYTES": "0", "MPIX_RING_SLOTS": "4"},
+    # the device matching engine (wildcard-capable) on concrete patterns
+    "dynamic": {"MPIX_MATCHING": "dynamic"},
+    "dynamic_split_sys": {"MPIX_MATCHING": "dynamic", "MPIX_INLINE_BYTES": "0",
+                          "MPIX_RING_SLOTS": "4", "MPIX_FORCE_SYS": "1"},
+    "dynamic_nobatch": {"MPIX_MATCHING": "dynamic", "MPIX_BATCH": "0", "MPIX_EAGER_BYTES": "16"},
 }
 
 
