@@ -557,6 +557,9 @@ def extras_multirank(args, mpix, torch):
         e[r][1].record(ctx[r][0])
     sync_all(ctx)
     t_step = max(a.elapsed_time(b) for a, b in e.values()) / 1e3 / steps
+    # the same steps from one native thread per rank (MPIXT_Halo_steps)
+    mpix.testing.halo_steps(list(blocks.values()), 2, [ctx[r][2] for r in range(8)])
+    nat_dev, nat_host = mpix.testing.halo_steps(list(blocks.values()), 20, [ctx[r][2] for r in range(8)])
     for r in range(8):
         e[r][0].record(ctx[r][0])
     for r in range(8):
@@ -569,6 +572,8 @@ def extras_multirank(args, mpix, torch):
     out["halo3d"] = {"block": f"{n}^3 fp32 per rank, 8 ranks 2x2x2 periodic",
                      "ranks_per_gpu": -(-8 // ndev), "step_ms": t_step * 1e3,
                      "stencil_only_ms": t_comp * 1e3, "comm_overhead_ms": (t_step - t_comp) * 1e3,
+                     "native_step_ms": nat_dev / 20 * 1e3, "native_host_ms": nat_host / 20 * 1e3,
+                     "native_comm_overhead_ms": (nat_dev / 20 - t_comp) * 1e3,
                      "face_bytes": n * n * 4}
     del blocks
     w.finalize()
@@ -595,6 +600,25 @@ def extras_multirank(args, mpix, torch):
                          "driver": "native C++ threads over the C ABI (MPIXT_Msgrate)",
                          "launches_per_window": "1 coalesced k_batch + ceil(2W/64)-1 flushes"}
     w.finalize()
+
+    # the same under the dynamic (wildcard-capable) matching engine
+    prev = os.environ.get("MPIX_MATCHING")
+    os.environ["MPIX_MATCHING"] = "dynamic"
+    try:
+        w = mpix.World(P, devs)
+        ctxs = [[] for _ in range(P)]
+        w.run_ranks(setup)
+        msgrate(w, ctxs, S, W, 1, bufs)
+        res = msgrate(w, ctxs, S, W, B, bufs)
+        for d in range(ndev):
+            torch.cuda.synchronize(d)
+        out["msgrate_8B_dynamic_matching"] = {"ranks": P, "streams_per_rank": S, "window": W, **res}
+        w.finalize()
+    finally:
+        if prev is None:
+            os.environ.pop("MPIX_MATCHING", None)
+        else:
+            os.environ["MPIX_MATCHING"] = prev
     return out
 
 

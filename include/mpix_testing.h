@@ -69,6 +69,13 @@ int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void *b0, void *b1, uint64_t bytes,
  * messages of n floats on one stream), `iters` times. */
 int MPIXT_Selfchain(MPI_Comm c, float *prod, float *cons, int n, int iters, void *stream,
                     double *dev_s, double *host_s);
+/* cfg5: `steps` halo steps of the 2x2x2 periodic 8-rank decomposition (pack
+ * 6 faces, 6 Irecv + 6 Isend_enqueue, Waitall_enqueue, unpack, stencil),
+ * one native thread per rank. Arrays are indexed by rank (u, v, comms,
+ * streams, devices) or rank*6+face (sbuf, rbuf). u and v swap every step. */
+int MPIXT_Halo_steps(int n, int steps, MPI_Comm *comms, void **streams, int *devices, float **u,
+                     float **v, float **sbuf, float **rbuf, float w0, float w1, double *dev_s,
+                     double *host_s);
 /* `iters` back-to-back empty kernels launched from C++ (launch floor). */
 int MPIXT_Empty_loop(int iters, void *stream, double *dev_s, double *host_s);
 /* The Allreduce_enqueue reduce stage alone (no entry/exit barrier): rank

@@ -169,6 +169,76 @@ int MPIXT_Selfchain(MPI_Comm c, float* prod, float* cons, int n, int iters, void
   return err;
 }
 
+// cfg5: `steps` halo-exchange steps of a 2x2x2 periodic decomposition, one
+// host thread per rank (8 ranks): pack 6 faces -> 6 Irecv + 6 Isend_enqueue ->
+// Waitall_enqueue -> unpack -> 7-point stencil, all in the rank's stream
+// (the structure of workloads.HaloStencil.step). u/v[r] are the rank's two
+// (n+2)^3 blocks (swapped each step), sbuf/rbuf[r*6+d] its n*n face buffers.
+int MPIXT_Halo_steps(int n, int steps, MPI_Comm* comms, void** streams, int* devices, float** u,
+                     float** v, float** sbuf, float** rbuf, float w0, float w1, double* dev_s,
+                     double* host_s) {
+  const int P = 8;
+  static const int opp[6] = {1, 0, 3, 2, 5, 4};
+  auto neighbour = [](int r, int d) {
+    int c[3] = {r & 1, (r >> 1) & 1, (r >> 2) & 1};
+    const int axis = d >> 1;
+    c[axis] = (c[axis] + ((d & 1) ? 1 : -1) + 2) % 2;
+    return c[0] | (c[1] << 1) | (c[2] << 2);
+  };
+  std::vector<cudaEvent_t> e0(P), e1(P);
+  for (int r = 0; r < P; ++r) {
+    cudaSetDevice(devices[r]);
+    if (cudaEventCreate(&e0[r]) != cudaSuccess || cudaEventCreate(&e1[r]) != cudaSuccess)
+      return MPIX_ERR_CUDA;
+  }
+  std::atomic<int> err{0};
+  Spin go(P);
+  double t0 = 0, t1 = 0;
+  auto rank = [&](int r) {
+    cudaSetDevice(devices[r]);
+    MPIX_Rank_bind(r);
+    void* s = streams[r];
+    float* a = u[r];
+    float* b = v[r];
+    cudaEventRecord(e0[r], (cudaStream_t)s);
+    go.arrive_and_wait();
+    if (r == 0) t0 = now_s();
+    MPI_Request reqs[12];
+    for (int it = 0; it < steps && !err.load(); ++it) {
+      int rc = 0;
+      for (int d = 0; d < 6; ++d) rc |= MPIXT_Halo_pack(a, n, n, n, d, sbuf[r * 6 + d], s);
+      for (int d = 0; d < 6; ++d)
+        rc |= MPIX_Irecv_enqueue(rbuf[r * 6 + d], n * n, MPI_FLOAT, neighbour(r, d), opp[d],
+                                 comms[r], &reqs[d]);
+      for (int d = 0; d < 6; ++d)
+        rc |= MPIX_Isend_enqueue(sbuf[r * 6 + d], n * n, MPI_FLOAT, neighbour(r, d), d, comms[r],
+                                 &reqs[6 + d]);
+      rc |= MPIX_Waitall_enqueue(12, reqs, MPI_STATUSES_IGNORE);
+      for (int d = 0; d < 6; ++d) rc |= MPIXT_Halo_unpack(a, n, n, n, d, rbuf[r * 6 + d], s);
+      rc |= MPIXT_Stencil7(a, b, n, n, n, w0, w1, s);
+      std::swap(a, b);
+      if (rc) err.store(rc);
+    }
+    cudaEventRecord(e1[r], (cudaStream_t)s);
+  };
+  std::vector<std::thread> th;
+  for (int r = 0; r < P; ++r) th.emplace_back(rank, r);
+  for (auto& t : th) t.join();
+  t1 = now_s();
+  float mx = 0;
+  for (int r = 0; r < P; ++r) {
+    cudaEventSynchronize(e1[r]);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0[r], e1[r]);
+    mx = std::max(mx, ms);
+    cudaEventDestroy(e0[r]);
+    cudaEventDestroy(e1[r]);
+  }
+  if (dev_s) *dev_s = mx / 1e3;
+  if (host_s) *host_s = t1 - t0;
+  return err.load();
+}
+
 // Back-to-back empty kernels from C++ (the in-stream launch floor).
 int MPIXT_Empty_loop(int iters, void* stream, double* dev_s, double* host_s) {
   cudaStream_t s = (cudaStream_t)stream;

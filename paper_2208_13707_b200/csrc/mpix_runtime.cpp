@@ -202,6 +202,7 @@ struct mpix_comm_s {
   cudaStream_t cu = nullptr;
   std::vector<uint64_t> send_pseq, recv_pseq;
   uint64_t recv_rseq = 0;  // dynamic matching: my receive ticket
+  void* batch = nullptr;   // the StreamBatch of cu (looked up once)
   bool any_remote = false; // some member lives on another GPU
   std::unordered_map<uint64_t, uint32_t> send_tagseq, recv_tagseq;
   uint64_t coll_epoch = 0;
@@ -767,7 +768,8 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     a.rec = rs.d_rec + (op % kOpRecords);
     a.opid = op;
   }
-  StreamBatch& b = batch_of(s, rs.device);
+  if (!c->batch) c->batch = &batch_of(s, rs.device);  // one agent per comm
+  StreamBatch& b = *static_cast<StreamBatch*>(c->batch);
   std::lock_guard<std::mutex> lk(b.mu);
   if (w.cfg.batch && !a.trace) {
     // Join the stream's batch; a blocking operation closes it (it must have
@@ -916,7 +918,8 @@ int allreduce_enqueue(const void* sbuf, void* rbuf, int count, MPI_Datatype dt, 
   bool sys = g_world->cfg.force_sys;
   for (int q = 0; q < P; ++q) sys |= rank_of(q).device != rs.device;
   CK(cudaSetDevice(rs.device));
-  StreamBatch& b = batch_of(c->cu, rs.device);
+  if (!c->batch) c->batch = &batch_of(c->cu, rs.device);
+  StreamBatch& b = *static_cast<StreamBatch*>(c->batch);
   std::lock_guard<std::mutex> lk(b.mu);
   if (!b.ops.empty() && flush_locked(b, c->cu, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
   int nk = launch_allreduce(a, sys, ar_reduce_grid(work, P), c->cu);

@@ -140,6 +140,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Pingpong": (I, [P, P, P, P, U64, I, P, P, I, I, P, P]),
         "MPIXT_Selfchain": (I, [P, P, P, I, I, P, P, P]),
         "MPIXT_Empty_loop": (I, [I, P, P, P]),
+        "MPIXT_Halo_steps": (I, [I, I, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P]),
         "MPIXT_Stream_create": (I, [I, C.POINTER(P)]),
         "MPIXT_Stream_destroy": (I, [P]),
         "MPIXT_Reduce_only": (I, [I, I, P, P, I, I, I, I, P]),
@@ -543,6 +544,28 @@ class testing:
         ms, n = C.c_double(), C.c_int()
         check(lib().MPIXT_Copy_timing_read(C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    @staticmethod
+    def halo_steps(blocks, steps: int, devices):
+        """Native cfg5 driver over 8 workloads.HaloStencil blocks (one per
+        rank); returns (device seconds, host seconds) for `steps` steps."""
+        assert len(blocks) == 8
+        VP = C.c_void_p
+        comms = (VP * 8)(*[b.comm.h for b in blocks])
+        streams = (VP * 8)(*[_stream_handle(b.stream) for b in blocks])
+        devs = (C.c_int * 8)(*devices)
+        u = (VP * 8)(*[_ptr(b.u) for b in blocks])
+        v = (VP * 8)(*[_ptr(b.v) for b in blocks])
+        sb = (VP * 48)(*[_ptr(b.sbuf[d]) for b in blocks for d in range(6)])
+        rb = (VP * 48)(*[_ptr(b.rbuf[d]) for b in blocks for d in range(6)])
+        ds, hs = C.c_double(), C.c_double()
+        b0 = blocks[0]
+        check(lib().MPIXT_Halo_steps(b0.n, steps, comms, streams, devs, u, v, sb, rb,
+                                     b0.W0, b0.W1, C.byref(ds), C.byref(hs)), "Halo_steps")
+        if steps % 2:
+            for b in blocks:
+                b.u, b.v = b.v, b.u
+        return ds.value, hs.value
 
     @staticmethod
     def empty_loop(iters: int, stream):

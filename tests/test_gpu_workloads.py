@@ -29,8 +29,10 @@ def global_step(g, w0, w1):
     return out[1:-1, 1:-1, 1:-1].copy()
 
 
+@pytest.mark.parametrize("native", [False, True], ids=["python", "native"])
 @pytest.mark.parametrize("n", [6, 17])
-def test_halo_stencil_matches_global_oracle(n):
+def test_halo_stencil_matches_global_oracle(n, native):
+    """native: the same steps through the C++ driver (MPIXT_Halo_steps)."""
     P = 8
     N = 2 * n
     rng = np.random.default_rng(n)
@@ -46,7 +48,10 @@ def test_halo_stencil_matches_global_oracle(n):
             blocks.append(b)
         torch.cuda.synchronize()
         steps = 3
-        w.run_ranks(lambda r: [blocks[r].step() for _ in range(steps)])
+        if native:
+            mpix.testing.halo_steps(blocks, steps, [0] * P)
+        else:
+            w.run_ranks(lambda r: [blocks[r].step() for _ in range(steps)])
         sync_all(ctx)
         exp = g
         for _ in range(steps):
