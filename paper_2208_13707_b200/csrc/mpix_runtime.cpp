@@ -170,6 +170,7 @@ struct RankState {
 
 struct CommShared {
   uint32_t ctx = 0;
+  bool dyn = false;  // dynamic (wildcard-capable) matching, agreed at creation
   int P = 0;
   bool multiplex = false;
   bool is_world = false;
@@ -191,6 +192,7 @@ struct mpix_stream_s {
   cudaStream_t cu = nullptr;
   int device = -1;
   bool exclusive = true;
+  int matching = -1;  // info "mpix_matching": 0 static, 1 dynamic, -1 default
   std::atomic<int> refcount{0};
 };
 
@@ -504,15 +506,24 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
   // Phase 1: context id from the root + stream counts.
   CollMsg m1;
   m1.i0 = (int64_t)streams.size();
+  // matching mode: the env default, or a member's "mpix_matching" stream hint
+  // (dynamic wins, so every member agrees)
+  int want = w.cfg.dyn_match ? 1 : 0;
+  for (auto* s : streams)
+    if (s && s->matching >= 0) want = s->matching;
+  m1.i1 = want;
   if (me == 0) m1.u0 = w.alloc_ctx();
   auto v1 = par->sh->rv.exchange(P, me, par->rv_seq++, m1);
   uint32_t ctx = (uint32_t)v1[0].u0;
+  bool dyn = false;
+  for (int q = 0; q < P; ++q) dyn |= v1[q].i1 != 0;
 
   // Shared state is created by the root and handed out in phase 2.
   std::shared_ptr<CommShared> sh;
   if (me == 0) {
     sh = std::make_shared<CommShared>();
     sh->ctx = ctx;
+    sh->dyn = dyn;
     sh->P = P;
     sh->multiplex = multiplex;
     sh->L = RegionLayout{P, w.cfg.ring_slots, w.cfg.eager_bytes};
@@ -655,8 +666,6 @@ int acquire_staging(RankState& rs, uint64_t bytes, cudaStream_t s, uint8_t** p, 
 }
 
 // Point-to-point enqueue (send side and receive side).
-bool w_dyn() { return g_world && g_world->cfg.dyn_match; }
-
 int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
                 bool is_recv, bool blocking, MPI_Request* req) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
@@ -666,7 +675,7 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   if (rc) return rc;
   int esz = type_size(dt);
   if (!esz) return MPIX_ERR_TYPE;
-  const bool dyn = w_dyn();
+  const bool dyn = c->sh->dyn;
   // Wildcards need the device matching engine (MPIX_MATCHING=dynamic).
   if (is_recv && !dyn && (peer == MPI_ANY_SOURCE || tag == MPI_ANY_TAG)) return MPIX_ERR_UNSUPPORTED;
   if (!blocking && !req) return MPIX_ERR_INVALID_ARG;
@@ -1252,6 +1261,15 @@ int MPIX_Stream_create(MPI_Info info, MPIX_Stream* stream) {
       s->cu = cs;
       s->device = dev;
       s->exclusive = false;  // proc_stream.cpp:23-24
+    }
+    auto mm = info->entries.find("mpix_matching");  // this library's hint
+    if (mm != info->entries.end()) {
+      if (mm->second == "dynamic")
+        s->matching = 1;
+      else if (mm->second == "static")
+        s->matching = 0;
+      else
+        return MPIX_ERR_BAD_HINT;
     }
     auto p = info->entries.find("endpoint_policy");  // proc_stream.cpp:27-33
     if (p != info->entries.end()) {

@@ -289,8 +289,13 @@ class Stream:
         self._keep = _keep  # the torch stream object, kept alive
 
     @classmethod
-    def from_cuda(cls, torch_stream) -> "Stream":
-        return cls(cuda_stream_info(torch_stream), _keep=torch_stream)
+    def from_cuda(cls, torch_stream, **hints) -> "Stream":
+        """hints: extra info keys, e.g. mpix_matching="dynamic" (a comm over
+        this stream then accepts ANY_SOURCE / ANY_TAG receives)."""
+        info = cuda_stream_info(torch_stream)
+        for k, v in hints.items():
+            info.set(k, v)
+        return cls(info, _keep=torch_stream)
 
     def free(self) -> None:
         check(lib().MPIX_Stream_free(C.byref(self.h)), "MPIX_Stream_free")

@@ -202,3 +202,45 @@ def test_static_mode_rejects_wildcards(monkeypatch):
         t = torch.zeros(8, dtype=torch.uint8, device=0)
         with pytest.raises(mpix.MPIXError):
             ctx[0].comm.irecv_enqueue(t, 8, mpix.MPI_BYTE, mpix.MPI_ANY_SOURCE, 0)
+
+
+def test_stream_hint_selects_dynamic_matching(monkeypatch):
+    """info "mpix_matching"="dynamic" on one member's stream makes the comm
+    wildcard-capable for every member (agreed at MPIX_Stream_comm_create)."""
+    monkeypatch.setenv("MPIX_MATCHING", "static")
+    w = mpix.World(2, [0, 0])
+    try:
+        comms = {}
+
+        def setup(r):
+            s = mpix.testing.new_stream(0)
+            hints = {"mpix_matching": "dynamic"} if r == 1 else {}
+            comms[r] = (s, w.comm(r).stream_comm_create(mpix.Stream.from_cuda(s, **hints)))
+
+        w.run_ranks(setup)
+        x = torch.full((4,), 7, dtype=torch.int64, device=0)
+        y = torch.zeros(4, dtype=torch.int64, device=0)
+        torch.cuda.synchronize()
+
+        def body(r):
+            s, c = comms[r]
+            if r == 0:
+                c.send_enqueue(x, 32, mpix.MPI_BYTE, 1, 3)
+            else:
+                c.recv_enqueue(y, 32, mpix.MPI_BYTE, mpix.MPI_ANY_SOURCE, mpix.MPI_ANY_TAG)
+
+        w.run_ranks(body)
+        for r in range(2):
+            comms[r][0].synchronize()
+        assert torch.equal(x.cpu(), y.cpu())
+    finally:
+        torch.cuda.synchronize()
+        w.finalize()
+
+
+def test_bad_matching_hint_is_bad_hint():
+    info = mpix.cuda_stream_info(mpix.testing.new_stream(0))
+    info.set("mpix_matching", "sometimes")
+    with pytest.raises(mpix.MPIXError) as e:
+        mpix.Stream(info)
+    assert e.value.name == "BAD_HINT"
