@@ -177,6 +177,15 @@ struct P2PArgs {
   // side; peer / tag may be -1 (ANY_SOURCE / ANY_TAG) on receives
   int dyn, P, me, peer, tag;
   uint64_t* bases;        // region bases of the comm's members (in my region)
+  // paired self-message (host-matched in a batch): this receive also carries
+  // its send; no descriptors, only both ring slots' retirement and the copy
+  int paired;
+  const uint8_t* pair_src;
+  uint64_t pair_bytes;
+  uint64_t* pair_done;
+  uint64_t pair_gen;
+  uint64_t* pair_mirror;
+  uint64_t pair_pseq;
 };
 
 // Copy grids up to this many CTAs may be launched (and park at
@@ -190,7 +199,7 @@ struct WaitEntry {
 };
 
 // One operation of a coalesced batch (k_batch): the P2PArgs fields of an
-// operation, packed (192 B) because the batch travels as kernel parameters.
+// operation, packed (200 B) because the batch travels as kernel parameters.
 // Large operations (inl == 0) decide in k_batch, copy in one grouped grid
 // (k_gcopy) and complete in k_gfin.
 struct BatchOp {
@@ -207,20 +216,32 @@ struct BatchOp {
   uint64_t my_gen;
   uint64_t* err_word;
   OpRecord* rec;          // large operations: decision record
-  uint8_t* staging;       // staged send: host staging buffer (or null)
-  uint64_t* stage_done;
-  uint64_t stage_gen;
-  uint8_t* arena;         // staged send: device arena (staging == null)
-  uint64_t* arena_state;
-  uint64_t arena_chunk;
+  union {
+    struct {                // staged send
+      uint8_t* staging;     // host staging buffer (or null: device arena)
+      uint64_t* stage_done;
+      uint64_t stage_gen;
+      uint8_t* arena;
+      uint64_t* arena_state;
+      uint64_t arena_chunk;
+    } st;
+    struct {                // paired self-message (a receive carrying its send)
+      uint8_t* src;
+      uint64_t bytes;
+      uint64_t* done;
+      uint64_t gen;
+      uint64_t* mirror;     // the send's SR-slot free-mirror
+      uint64_t pseq;
+    } pr;
+  };
   uint64_t* bases;        // dynamic matching
   uint32_t arena_slots;
   uint32_t E;
   int32_t peer, tag;      // dynamic matching (-1 = ANY on receives)
   uint16_t R, P, me;
-  uint8_t is_recv, mode, blocking, inl, early, dyn;
+  uint8_t is_recv, mode, blocking, inl, early, dyn, paired, pad_[7];
 };
-static_assert(sizeof(BatchOp) == 192, "BatchOp packing");
+static_assert(sizeof(BatchOp) == 200, "BatchOp packing");
 
 constexpr int kBatchOps = 64;     // operations per coalesced launch
 constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch

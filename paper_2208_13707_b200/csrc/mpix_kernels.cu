@@ -739,6 +739,41 @@ __device__ void stage_publish_dyn(const P2PArgs& a, Decision& dc) {
   }
 }
 
+// A self-message whose send and receive the host found in one batch (same
+// comm, same key): no descriptors and no scan. Both ring slots are consumed
+// only after their previous occupants retired, so the free-mirrors stay
+// monotonic; the receive then copies the send buffer and completes both.
+template <bool SYS>
+__device__ void decide_paired(const P2PArgs& a, Decision& dc) {
+  if (threadIdx.x == 0) {
+    dc.wait_own = 0;
+    dc.now = 0;
+    dc.fin.clear();
+    dc.action = ACT_NONE;
+    dc.stage_ptr = nullptr;
+    dc.stage_done = nullptr;
+    dc.stage_gen = 0;
+    const int rslot = (int)(a.pseq % (uint64_t)a.R);
+    const int sslot = (int)(a.pair_pseq % (uint64_t)a.R);
+    const uint64_t rneed = a.pseq >= (uint64_t)a.R ? a.pseq - a.R + 1 : 0;
+    const uint64_t sneed = a.pair_pseq >= (uint64_t)a.R ? a.pair_pseq - a.R + 1 : 0;
+    if ((rneed == 0 || spin_ge<SYS>(&a.post_mirror[rslot], rneed, a.err_word, a.spin_limit_ns,
+                                    ERRW_WAIT_SLOT)) &&
+        (sneed == 0 || spin_ge<SYS>(&a.pair_mirror[sslot], sneed, a.err_word, a.spin_limit_ns,
+                                    ERRW_WAIT_SLOT))) {
+      dc.action = ACT_COPY;
+      dc.src = (uint64_t)a.pair_src;
+      dc.dst = (uint64_t)a.buf;
+      dc.bytes = umin(a.pair_bytes, a.bytes);  // truncation: endpoint.cpp:17
+      dc.fin.add_b(&a.post_mirror[rslot], a.pseq + 1);
+      dc.fin.add_b(&a.pair_mirror[sslot], a.pair_pseq + 1);
+      dc.fin.add_b(a.pair_done, a.pair_gen);
+      dc.fin.add_b(a.my_done, a.my_gen);
+    }
+  }
+  __syncthreads();
+}
+
 // The handshake (whole CTA calls; warp 0 works, the CTA copies eager
 // payloads). On return dc holds ACT_NONE / ACT_COPY / ACT_STAGE.
 template <bool SYS>
@@ -879,7 +914,8 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
     a.trace->g0 = globaltimer();
     a.trace->t[0] = clock64();
   }
-  if (a.dyn) decide_dyn<SYS>(a, s_dc);
+  if (a.paired) decide_paired<SYS>(a, s_dc);
+  else if (a.dyn) decide_dyn<SYS>(a, s_dc);
   else decide<SYS>(a, s_dc);
   if (a.trace && threadIdx.x == 0)
     a.trace->info = (uint64_t)a.is_recv | ((uint64_t)a.mode << 4) | ((uint64_t)INLINE << 8) |
@@ -1027,15 +1063,31 @@ __device__ void load_op(const BatchOp& o, uint64_t spin_limit_ns, P2PArgs& a) {
   a.E = o.E;
   a.buf = o.buf;
   a.bytes = o.bytes;
-  a.staging = o.staging;
   a.my_done = o.my_done;
   a.my_gen = o.my_gen;
-  a.stage_done = o.stage_done;
-  a.stage_gen = o.stage_gen;
-  a.arena = o.arena;
-  a.arena_state = o.arena_state;
+  a.paired = o.paired;
+  if (o.paired) {
+    a.staging = nullptr;
+    a.stage_done = nullptr;
+    a.stage_gen = 0;
+    a.arena = nullptr;
+    a.arena_state = nullptr;
+    a.arena_chunk = 0;
+    a.pair_src = o.pr.src;
+    a.pair_bytes = o.pr.bytes;
+    a.pair_done = o.pr.done;
+    a.pair_gen = o.pr.gen;
+    a.pair_mirror = o.pr.mirror;
+    a.pair_pseq = o.pr.pseq;
+  } else {
+    a.staging = o.st.staging;
+    a.stage_done = o.st.stage_done;
+    a.stage_gen = o.st.stage_gen;
+    a.arena = o.st.arena;
+    a.arena_state = o.st.arena_state;
+    a.arena_chunk = o.st.arena_chunk;
+  }
   a.arena_slots = o.arena_slots;
-  a.arena_chunk = o.arena_chunk;
   a.rec = o.rec;
   a.opid = 0;
   a.err_word = o.err_word;

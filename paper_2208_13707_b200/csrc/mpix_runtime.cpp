@@ -233,8 +233,15 @@ struct StreamBatch {
   //   large operation's pseq + R) must go to a later launch;
   std::unordered_map<const void*, uint64_t> first_large_pseq;  // ring (post mirror) -> pseq
   // - a self-message operation launched post-only relies on its
-  //   counterpart running after it, not concurrently in the same grid.
-  std::vector<std::pair<const void*, uint64_t>> post_only;  // (comm, key)
+  //   counterpart running after it, not concurrently in the same grid; if
+  //   the counterpart joins the same batch the host pairs the two instead.
+  struct PostOnly {
+    const void* comm;
+    uint64_t key;
+    size_t idx;  // in ops
+    bool is_recv;
+  };
+  std::vector<PostOnly> post_only;
 };
 
 struct World {
@@ -463,12 +470,12 @@ BatchOp pack_op(const P2PArgs& a, bool inl) {
   o.my_gen = a.my_gen;
   o.err_word = a.err_word;
   o.rec = a.rec;
-  o.staging = a.staging;
-  o.stage_done = a.stage_done;
-  o.stage_gen = a.stage_gen;
-  o.arena = a.arena;
-  o.arena_state = a.arena_state;
-  o.arena_chunk = a.arena_chunk;
+  o.st.staging = a.staging;
+  o.st.stage_done = a.stage_done;
+  o.st.stage_gen = a.stage_gen;
+  o.st.arena = a.arena;
+  o.st.arena_state = a.arena_state;
+  o.st.arena_chunk = a.arena_chunk;
   o.arena_slots = a.arena_slots;
   o.E = (uint32_t)a.E;
   o.R = (uint16_t)a.R;
@@ -783,17 +790,54 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   if (w.cfg.batch && !a.trace) {
     // Join the stream's batch; a blocking operation closes it (it must have
     // completed before anything behind it in the stream runs).
-    bool flush_first = (int)b.ops.size() >= kBatchOps;
-    auto fl = b.first_large_pseq.find(a.post_mirror);
-    flush_first |= fl != b.first_large_pseq.end() && a.pseq >= fl->second + (uint64_t)a.R;
-    for (auto& po : b.post_only) flush_first |= po.first == c && po.second == a.key;
-    if (flush_first && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
-    if (b.ops.empty()) b.err_word = rs.d_err;
-    if (!inl && a.post_mirror) b.first_large_pseq.emplace(a.post_mirror, a.pseq);
-    if (post_only) b.post_only.emplace_back(c, a.key);
-    BatchOp o = pack_op(a, inl);
-    b.ops.push_back(o);
-    b.sys |= sys;
+    // A self-message whose counterpart is held post-only in this batch: the
+    // host has matched them (same comm, same key, static matching), so the
+    // two become one paired operation — no descriptors, one copy.
+    int pk = -1;
+    if (!dyn && peer == me && (!blocking || is_recv) && a.mode != MODE_STAGED) {
+      for (size_t k = 0; k < b.post_only.size(); ++k) {
+        const auto& po = b.post_only[k];
+        if (po.comm == c && po.key == a.key && po.is_recv != is_recv) pk = (int)k;
+      }
+      // my ring slot must not wait on a large operation of this batch
+      auto fl = b.first_large_pseq.find(a.post_mirror);
+      if (fl != b.first_large_pseq.end() && a.pseq >= fl->second + (uint64_t)a.R) pk = -1;
+    }
+    if (pk >= 0) {
+      const size_t j = b.post_only[pk].idx;
+      b.post_only.erase(b.post_only.begin() + pk);
+      const BatchOp held = b.ops[j];
+      BatchOp m = is_recv ? pack_op(a, true) : held;  // the receive carries the pair
+      const BatchOp snd = is_recv ? held : pack_op(a, true);
+      m.paired = 1;
+      m.pr.src = snd.buf;
+      m.pr.bytes = snd.bytes;
+      m.pr.done = snd.my_done;
+      m.pr.gen = snd.my_gen;
+      m.pr.mirror = snd.post_mirror;
+      m.pr.pseq = snd.pseq;
+      const uint64_t nb = std::min(snd.bytes, m.bytes);
+      m.inl = nb <= w.cfg.inline_bytes ? 1 : 0;
+      if (!m.inl) {
+        if (!m.rec) m.rec = rs.d_rec + (rs.op_next.fetch_add(1) % kOpRecords);
+        b.first_large_pseq.emplace(m.post_mirror, m.pseq);
+        b.first_large_pseq.emplace(m.pr.mirror, m.pr.pseq);
+      }
+      m.blocking = blocking ? 1 : held.blocking;
+      b.ops[j] = m;
+      b.sys |= sys;
+    } else {
+      bool flush_first = (int)b.ops.size() >= kBatchOps;
+      auto fl = b.first_large_pseq.find(a.post_mirror);
+      flush_first |= fl != b.first_large_pseq.end() && a.pseq >= fl->second + (uint64_t)a.R;
+      for (auto& po : b.post_only) flush_first |= po.comm == c && po.key == a.key;
+      if (flush_first && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
+      if (b.ops.empty()) b.err_word = rs.d_err;
+      if (!inl && a.post_mirror) b.first_large_pseq.emplace(a.post_mirror, a.pseq);
+      if (post_only) b.post_only.push_back({c, a.key, b.ops.size(), (bool)is_recv});
+      b.ops.push_back(pack_op(a, inl));
+      b.sys |= sys;
+    }
     if (blocking && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
   } else {
     if (!b.ops.empty() && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;

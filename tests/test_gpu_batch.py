@@ -235,3 +235,35 @@ def test_blocking_large_recv_before_send_on_same_gpu(batch_env):
         sync_all(ctx)
         assert torch.equal(dst.cpu(), src.cpu())
         assert mpix.rank_error(0) == 0 and mpix.rank_error(1) == 0
+
+
+@pytest.mark.parametrize("n", [(1 << 20) + 3, 5 << 20])
+@pytest.mark.parametrize("recv_first", [False, True])
+def test_paired_self_messages(n, recv_first, batch_env):
+    """Large self-messages whose send and receive meet in one batch are
+    paired by the host (no descriptors): exact bytes, truncation, tag order,
+    ring-slot reuse over many iterations, and blocking receives."""
+    with gpu_world(1) as (w, ctx):
+        c = ctx[0].comm
+        src = [rand_bytes(n, 500 + i) for i in range(3)]
+        dst = [torch.zeros(n, dtype=torch.uint8, device=0) for _ in range(3)]
+        small = torch.zeros(n // 2, dtype=torch.uint8, device=0)
+        torch.cuda.synchronize()
+        for it in range(70):  # > R/2 iterations: ring slots are reused
+            reqs = []
+            if recv_first:
+                reqs += [c.irecv_enqueue(dst[i], n, mpix.MPI_BYTE, 0, 4) for i in range(3)]
+                reqs += [c.isend_enqueue(src[i], n, mpix.MPI_BYTE, 0, 4) for i in range(3)]
+            else:
+                reqs += [c.isend_enqueue(src[i], n, mpix.MPI_BYTE, 0, 4) for i in range(3)]
+                reqs += [c.irecv_enqueue(dst[i], n, mpix.MPI_BYTE, 0, 4) for i in range(3)]
+            mpix.waitall_enqueue(reqs)
+        # truncation + a blocking receive closing the batch
+        r = c.isend_enqueue(src[0], n, mpix.MPI_BYTE, 0, 5)
+        c.recv_enqueue(small, n // 2, mpix.MPI_BYTE, 0, 5)
+        mpix.wait_enqueue(r)
+        sync_all(ctx)
+        for i in range(3):
+            assert torch.equal(dst[i].cpu(), src[i].cpu()), i
+        assert torch.equal(small.cpu(), src[0][: n // 2].cpu())
+        assert mpix.rank_error(0) == 0
