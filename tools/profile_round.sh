@@ -12,11 +12,12 @@ $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 # 2) launch list of 8-byte loopback windows (coalesced k_batch)
 $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/launches_window_8B.csv" \
   python tools/profile_loopback.py --size 8 --steps 5 --warmup 3 --window 32 > /dev/null 2>&1
-# 3) full capture of the receive-side pull copy (k_copy launch with the payload)
-$NCU --set full --import-source on -k regex:k_copy -s 7 -c 1 -o "$OUT/k_copy" \
+# 3) full capture of the payload copy of one loopback step (the grouped copy
+#    grid of the paired send/receive)
+$NCU --set full --import-source on -k regex:k_gcopy -s 3 -c 1 -o "$OUT/k_gcopy" \
   python tools/profile_loopback.py --steps 5 --warmup 3 > /dev/null 2>&1
-ncu -i "$OUT/k_copy.ncu-rep" --page raw --csv > "$OUT/k_copy_raw.csv" 2>/dev/null
-ncu -i "$OUT/k_copy.ncu-rep" --page details --csv > "$OUT/k_copy_details.csv" 2>/dev/null
+ncu -i "$OUT/k_gcopy.ncu-rep" --page raw --csv > "$OUT/k_gcopy_raw.csv" 2>/dev/null
+ncu -i "$OUT/k_gcopy.ncu-rep" --page details --csv > "$OUT/k_gcopy_details.csv" 2>/dev/null
 # 4) full capture of one coalesced window kernel (32 Isend + 32 Irecv + Waitall)
 $NCU --set full --import-source on -k regex:k_batch -s 3 -c 1 -o "$OUT/k_batch" \
   python tools/profile_loopback.py --size 8 --steps 5 --warmup 3 --window 32 > /dev/null 2>&1
