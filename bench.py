@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--size", type=int, default=256 * MiB)
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--share-gpus", action="store_true",
+                    help="validation only: map rank r to GPU r %% ndev (ranks share GPUs)")
     return ap.parse_args()
 
 
@@ -216,15 +218,16 @@ def bench_world(args):
     n = args.gpus
     S = args.size
     ndev = torch.cuda.device_count()
-    assert ndev >= n, f"need {n} GPUs, see {ndev}"
+    assert ndev >= n or args.share_gpus, f"need {n} GPUs, see {ndev}"
     pk = peaks()
     P = n
-    w = mpix.World(P, list(range(P)))
+    dev = [r % ndev for r in range(P)]
+    w = mpix.World(P, dev)
     ctx = {}
 
     def setup(r):
-        with torch.cuda.device(r):
-            s = mpix.testing.new_stream(r)
+        with torch.cuda.device(dev[r]):
+            s = mpix.testing.new_stream(dev[r])
         ms = mpix.Stream.from_cuda(s)
         c = w.comm(r).stream_comm_create(ms)
         ctx[r] = (s, ms, c)
@@ -233,11 +236,11 @@ def bench_world(args):
     # buffers (> L2: every step streams from HBM)
     src, dst = {}, {}
     for r in range(P):
-        src[r] = torch.empty(S, dtype=torch.uint8, device=r)
-        dst[r] = torch.zeros(S, dtype=torch.uint8, device=r)
+        src[r] = torch.empty(S, dtype=torch.uint8, device=dev[r])
+        dst[r] = torch.zeros(S, dtype=torch.uint8, device=dev[r])
         mpix.testing.fill_pattern(src[r], S, 1234 + r, 0, ctx[r][0])
-    for r in range(P):
-        torch.cuda.synchronize(r)
+    for d in set(dev):
+        torch.cuda.synchronize(d)
 
     if P == 1:
         senders, pairs = [0], [(0, 0)]
@@ -262,14 +265,14 @@ def bench_world(args):
                 mpix.wait_enqueue(rb)
 
     def sync():
-        for r in range(P):
-            torch.cuda.synchronize(r)
+        for d in set(dev):
+            torch.cuda.synchronize(d)
 
     # correctness of the measured path (same inputs as the timed loop)
     step()
     sync()
     for a, b in pairs:
-        assert torch.equal(dst[b], src[a].to(b)), "payload mismatch"
+        assert torch.equal(dst[b], src[a].to(dev[b])), "payload mismatch"
 
     clocks = ClockSampler(0)
     clocks.start()
@@ -326,7 +329,7 @@ def bench_world(args):
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf):
+    if P == 1 and os.path.exists(tf):  # captured on the loopback workload
         try:
             traffic = json.load(open(tf)).get(f"p2p_recv_{S}")
         except Exception:
@@ -352,6 +355,8 @@ def bench_world(args):
             "message_bytes": S, "ranks": P, "parallelism": "none (messaging runtime)",
             "l2": "inputs larger than L2 (src+dst = 2 x message > 126 MB)",
             "baseline_config": "BASELINE.json configs[1] at one GPU (SURVEY.md §8d cfg2)",
+            **({"devices": dev, "note": "--share-gpus validation run, not a measurement"}
+               if args.share_gpus else {}),
         },
         "roofline": roof,
         "e2e": e2e,
@@ -360,7 +365,7 @@ def bench_world(args):
     }
     if not args.no_extras and P == 1:
         line["extras"] = extras(args, mpix, torch, w, ctx)
-    if rank0_cpu():
+    if rank0_cpu() and P == 1:  # the CPU baseline: rank 0 at N=1 only
         line["cpu_baseline"] = cpu_reference_selfmsg(S, args.cpu_seconds)
     sync()
     w.finalize()
@@ -381,7 +386,7 @@ def e2e_pass(args, mpix, torch, ctx, pairs, src, dst, S):
     host = {a: torch.empty(S, dtype=torch.uint8, pin_memory=True) for a, _ in pairs}
     for a, _ in pairs:
         host[a].copy_(src[a].cpu())
-    sums = {b: torch.zeros(1, dtype=torch.int64, device=b) for _, b in pairs}
+    sums = {b: torch.zeros(1, dtype=torch.int64, device=dst[b].device) for _, b in pairs}
     hsum = {b: torch.zeros(1, dtype=torch.int64, pin_memory=True) for _, b in pairs}
 
     def one(tag):
