@@ -427,17 +427,6 @@ def extras(args, mpix, torch, w, ctx):
     big = torch.empty(1 << 30, dtype=torch.uint8, device=0)
     big2 = torch.empty(1 << 30, dtype=torch.uint8, device=0)
 
-    def timed(fn, iters, stream):
-        fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for i in range(iters):
-            fn(i)
-        b.record(stream)
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / 1e3 / iters
-
     # launch floor: back-to-back empty kernels in one stream (native loop)
     mpix.testing.empty_loop(50, s0)
     dev, host = mpix.testing.empty_loop(2000, s0)
@@ -445,18 +434,15 @@ def extras(args, mpix, torch, w, ctx):
     out["launch_floor_us"] = t_empty * 1e6
     out["launch_floor_host_us"] = host / 2000 * 1e6
 
-    # loopback sweep (Isend/Irecv/Waitall on one stream)
+    # loopback sweep (Isend/Irecv/Waitall on one stream, native loop)
     sweep = {}
     for sz in [8, 4096, 65536, 1 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30]:
-        it = 200 if sz <= (1 << 20) else (20 if sz <= (64 << 20) else 5)
-
-        def f(i=0, sz=sz):
-            r1 = c0.isend_enqueue(big, sz, mpix.MPI_BYTE, 0, 7)
-            r2 = c0.irecv_enqueue(big2, sz, mpix.MPI_BYTE, 0, 7)
-            mpix.waitall_enqueue([r1, r2])
-        t = timed(f, it, s0)
-        sweep[str(sz)] = {"us": t * 1e6, "GBps": sz / t / 1e9, "hbm_frac": 2 * sz / t / 1e9 /
-                          peaks().get("hbm_gbs", 6650.0)}
+        it = 500 if sz <= (1 << 20) else (50 if sz <= (64 << 20) else 10)
+        mpix.testing.loopback(c0, big, big2, sz, 5, s0)
+        dev, host = mpix.testing.loopback(c0, big, big2, sz, it, s0)
+        t = dev / it
+        sweep[str(sz)] = {"us": t * 1e6, "host_us": host / it * 1e6, "GBps": sz / t / 1e9,
+                          "hbm_frac": 2 * sz / t / 1e9 / peaks().get("hbm_gbs", 6650.0)}
     out["loopback_sweep"] = sweep
 
     # in-stream latency: producer -> Send_enqueue -> Recv_enqueue -> consumer
@@ -548,7 +534,7 @@ def extras_multirank(args, mpix, torch):
     out["allreduce_256MiB"] = ar
 
     # cfg5: 3-D halo stencil, 2x2x2 periodic, 512^3 fp32 per rank
-    n = 512 if ndev >= 8 else 256
+    n = 512  # BASELINE cfg5: 512^3 fp32 per rank (8 ranks share the visible GPUs)
     w, ctx = world(8)
     blocks = {r: HaloStencil(r, n, ctx[r][0], ctx[r][1], device=ctx[r][2]) for r in range(8)}
     w.run_ranks(lambda r: blocks[r].step())

@@ -76,6 +76,10 @@ int MPIXT_Selfchain(MPI_Comm c, float *prod, float *cons, int n, int iters, void
 int MPIXT_Halo_steps(int n, int steps, MPI_Comm *comms, void **streams, int *devices, float **u,
                      float **v, float **sbuf, float **rbuf, float w0, float w1, double *dev_s,
                      double *host_s);
+/* `iters` x {Isend + Irecv + Waitall_enqueue} of a self-message of `bytes`
+ * on the comm's stream (the benchmark's N=1 step, native loop). */
+int MPIXT_Loopback(MPI_Comm c, const void *src, void *dst, uint64_t bytes, int iters, void *stream,
+                   double *dev_s, double *host_s);
 /* `iters` back-to-back empty kernels launched from C++ (launch floor). */
 int MPIXT_Empty_loop(int iters, void *stream, double *dev_s, double *host_s);
 /* The Allreduce_enqueue reduce stage alone (no entry/exit barrier): rank

@@ -239,6 +239,37 @@ int MPIXT_Halo_steps(int n, int steps, MPI_Comm* comms, void** streams, int* dev
   return err.load();
 }
 
+// Loopback: `iters` x {Isend_enqueue + Irecv_enqueue + Waitall_enqueue} of a
+// self-message on one stream (the bench's N=1 step, any size).
+int MPIXT_Loopback(MPI_Comm c, const void* src, void* dst, uint64_t bytes, int iters, void* stream,
+                   double* dev_s, double* host_s) {
+  if (iters < 1) return MPIX_ERR_INVALID_ARG;
+  int me = 0;
+  MPI_Comm_rank(c, &me);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t a, b;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return MPIX_ERR_CUDA;
+  int err = 0;
+  cudaEventRecord(a, s);
+  double t0 = now_s();
+  for (int i = 0; i < iters && !err; ++i) {
+    MPI_Request r[2];
+    err |= MPIX_Isend_enqueue(src, (int)bytes, MPI_BYTE, me, 7, c, &r[0]);
+    err |= MPIX_Irecv_enqueue(dst, (int)bytes, MPI_BYTE, me, 7, c, &r[1]);
+    err |= MPIX_Waitall_enqueue(2, r, MPI_STATUSES_IGNORE);
+  }
+  cudaEventRecord(b, s);
+  double t1 = now_s();
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (dev_s) *dev_s = ms / 1e3;
+  if (host_s) *host_s = t1 - t0;
+  return err;
+}
+
 // Back-to-back empty kernels from C++ (the in-stream launch floor).
 int MPIXT_Empty_loop(int iters, void* stream, double* dev_s, double* host_s) {
   cudaStream_t s = (cudaStream_t)stream;

@@ -140,6 +140,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Pingpong": (I, [P, P, P, P, U64, I, P, P, I, I, P, P]),
         "MPIXT_Selfchain": (I, [P, P, P, I, I, P, P, P]),
         "MPIXT_Empty_loop": (I, [I, P, P, P]),
+        "MPIXT_Loopback": (I, [P, P, P, U64, I, P, P, P]),
         "MPIXT_Halo_steps": (I, [I, I, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P]),
         "MPIXT_Stream_create": (I, [I, C.POINTER(P)]),
         "MPIXT_Stream_destroy": (I, [P]),
@@ -570,6 +571,13 @@ class testing:
         if steps % 2:
             for b in blocks:
                 b.u, b.v = b.v, b.u
+        return ds.value, hs.value
+
+    @staticmethod
+    def loopback(c, src, dst, nbytes: int, iters: int, stream):
+        ds, hs = C.c_double(), C.c_double()
+        check(lib().MPIXT_Loopback(c.h, _ptr(src), _ptr(dst), nbytes, iters, _stream_handle(stream),
+                                   C.byref(ds), C.byref(hs)), "Loopback")
         return ds.value, hs.value
 
     @staticmethod

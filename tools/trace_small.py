@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2208_13707_b200 import mpix
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-w = mpix.World(1, [0]); s = torch.cuda.Stream()
+w = mpix.World(1, [0]); s = mpix.testing.new_stream(0)
 c = w.comm(0).stream_comm_create(mpix.Stream.from_cuda(s))
 src = torch.ones(max(S, 1), dtype=torch.uint8, device=0); dst = torch.zeros(max(S, 1), dtype=torch.uint8, device=0)
 for i in range(50):
