@@ -508,28 +508,37 @@ def extras_multirank(args, mpix, torch):
             sb = {r: torch.ones(cnt, dtype=tdt, device=ctx[r][2]) for r in range(P)}
             rb = {r: torch.empty(cnt, dtype=tdt, device=ctx[r][2]) for r in range(P)}
             iters = 10
-            ev = {r: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for r in range(P)}
-
-            def loop(r, k, timed):
-                # every rank enqueues all k calls from its own thread (no
-                # per-call thread spawn on the host path)
-                if timed:
-                    ev[r][0].record(ctx[r][0])
-                for _ in range(k):
-                    ctx[r][1].allreduce_enqueue(sb[r], rb[r], cnt, mdt)
-                if timed:
-                    ev[r][1].record(ctx[r][0])
-            w.run_ranks(lambda r: loop(r, 2, False))
+            cs = [ctx[r][1] for r in range(P)]
+            ss = [ctx[r][0] for r in range(P)]
+            ds = [ctx[r][2] for r in range(P)]
+            mpix.testing.allreduce_loop(cs, ss, ds, [sb[r] for r in range(P)],
+                                        [rb[r] for r in range(P)], cnt, mdt, 2)
+            dev_s, _ = mpix.testing.allreduce_loop(cs, ss, ds, [sb[r] for r in range(P)],
+                                                   [rb[r] for r in range(P)], cnt, mdt, iters)
             sync_all(ctx)
-            w.run_ranks(lambda r: loop(r, iters, True))
-            sync_all(ctx)
-            t = max(a.elapsed_time(b) for a, b in ev.values()) / 1e3 / iters
+            t = dev_s / iters
             algbw = nbytes / t / 1e9
             ar[f"{dt}_P{P}"] = {"ms": t * 1e3, "algbw_GBps": algbw,
                                 "busbw_GBps": algbw * 2 * (P - 1) / P,
                                 "ranks_per_gpu": -(-P // ndev),
                                 "check": float(rb[0][0]) == float(P)}
             del sb, rb
+        # small-message latency (one-shot <= 64 KiB), native driver
+        if P in (2, 8):
+            lat = {}
+            for nbytes in (8, 4096, 65536, 1 << 20):
+                cnt = max(1, nbytes // 4)
+                sb = [torch.ones(cnt, dtype=torch.float32, device=ctx[r][2]) for r in range(P)]
+                rb = [torch.empty(cnt, dtype=torch.float32, device=ctx[r][2]) for r in range(P)]
+                cs = [ctx[r][1] for r in range(P)]
+                ss = [ctx[r][0] for r in range(P)]
+                ds = [ctx[r][2] for r in range(P)]
+                mpix.testing.allreduce_loop(cs, ss, ds, sb, rb, cnt, mpix.MPI_FLOAT, 5)
+                dev_s, host_s = mpix.testing.allreduce_loop(cs, ss, ds, sb, rb, cnt, mpix.MPI_FLOAT, 200)
+                sync_all(ctx)
+                lat[str(nbytes)] = {"us": dev_s / 200 * 1e6, "host_us": host_s / 200 * 1e6,
+                                    "check": float(rb[0][0]) == float(P)}
+            ar[f"latency_f32_P{P}"] = lat
         w.finalize()
     out["allreduce_256MiB"] = ar
 

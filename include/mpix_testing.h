@@ -80,6 +80,11 @@ int MPIXT_Halo_steps(int n, int steps, MPI_Comm *comms, void **streams, int *dev
  * on the comm's stream (the benchmark's N=1 step, native loop). */
 int MPIXT_Loopback(MPI_Comm c, const void *src, void *dst, uint64_t bytes, int iters, void *stream,
                    double *dev_s, double *host_s);
+/* `iters` x Allreduce_enqueue per rank from one native thread per rank
+ * (arrays indexed by rank); *dev_s = max over ranks of event time. */
+int MPIXT_Allreduce_loop(int P, MPI_Comm *comms, void **streams, int *devices, void **sbufs,
+                         void **rbufs, int count, MPI_Datatype dt, MPI_Op op, int iters,
+                         double *dev_s, double *host_s);
 /* `iters` back-to-back empty kernels launched from C++ (launch floor). */
 int MPIXT_Empty_loop(int iters, void *stream, double *dev_s, double *host_s);
 /* The Allreduce_enqueue reduce stage alone (no entry/exit barrier): rank

@@ -270,6 +270,51 @@ int MPIXT_Loopback(MPI_Comm c, const void* src, void* dst, uint64_t bytes, int i
   return err;
 }
 
+// `iters` x MPIX_Allreduce_enqueue(sbuf[r] -> rbuf[r], count, dt, op) per
+// rank, one native thread per rank; *dev_s = max over ranks of event time.
+int MPIXT_Allreduce_loop(int P, MPI_Comm* comms, void** streams, int* devices, void** sbufs,
+                         void** rbufs, int count, MPI_Datatype dt, MPI_Op op, int iters,
+                         double* dev_s, double* host_s) {
+  if (P < 1 || iters < 1) return MPIX_ERR_INVALID_ARG;
+  std::vector<cudaEvent_t> e0(P), e1(P);
+  for (int r = 0; r < P; ++r) {
+    cudaSetDevice(devices[r]);
+    if (cudaEventCreate(&e0[r]) != cudaSuccess || cudaEventCreate(&e1[r]) != cudaSuccess)
+      return MPIX_ERR_CUDA;
+  }
+  std::atomic<int> err{0};
+  Spin go(P);
+  double t0 = 0, t1 = 0;
+  auto rank = [&](int r) {
+    cudaSetDevice(devices[r]);
+    MPIX_Rank_bind(r);
+    cudaEventRecord(e0[r], (cudaStream_t)streams[r]);
+    go.arrive_and_wait();
+    if (r == 0) t0 = now_s();
+    for (int i = 0; i < iters && !err.load(); ++i) {
+      int rc = MPIX_Allreduce_enqueue(sbufs[r], rbufs[r], count, dt, op, comms[r]);
+      if (rc) err.store(rc);
+    }
+    cudaEventRecord(e1[r], (cudaStream_t)streams[r]);
+  };
+  std::vector<std::thread> th;
+  for (int r = 0; r < P; ++r) th.emplace_back(rank, r);
+  for (auto& t : th) t.join();
+  t1 = now_s();
+  float mx = 0;
+  for (int r = 0; r < P; ++r) {
+    cudaEventSynchronize(e1[r]);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0[r], e1[r]);
+    mx = std::max(mx, ms);
+    cudaEventDestroy(e0[r]);
+    cudaEventDestroy(e1[r]);
+  }
+  if (dev_s) *dev_s = mx / 1e3;
+  if (host_s) *host_s = t1 - t0;
+  return err.load();
+}
+
 // Back-to-back empty kernels from C++ (the in-stream launch floor).
 int MPIXT_Empty_loop(int iters, void* stream, double* dev_s, double* host_s) {
   cudaStream_t s = (cudaStream_t)stream;

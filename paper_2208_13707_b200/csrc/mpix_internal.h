@@ -297,7 +297,7 @@ int launch_p2p(const P2PArgs& a, bool sys, bool inline_copy, uint64_t copy_grid,
 int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint64_t* err_word,
                  uint64_t spin_limit_ns, bool sys, cudaStream_t s, cudaEvent_t copy_ev0 = nullptr,
                  cudaEvent_t copy_ev1 = nullptr);
-int launch_allreduce(const ARArgs& a, bool sys, uint64_t reduce_grid, cudaStream_t s);
+int launch_allreduce(const ARArgs& a, bool sys, uint64_t reduce_grid, cudaStream_t s, bool fused);
 uint64_t p2p_copy_grid(uint64_t bytes);
 uint64_t ar_reduce_grid(uint64_t work_bytes, int P);
 int preload_kernels();

@@ -1464,6 +1464,67 @@ static ReduceKernel reduce_kernel(int dtype, int op) {
   }
 }
 
+// Small allreduce in ONE launch (bytes <= MPIX_ALLREDUCE_ONESHOT_MAX): one
+// CTA runs the entry barrier, my two-shot chunk (read it from every input,
+// fold in rank order, store it into every output — also correct in place),
+// and the exit barrier. Replaces entry + reduce + exit for latency-bound
+// sizes, where the host cost of three launches per rank dominated.
+template <bool SYS>
+__global__ void __launch_bounds__(kArThreads) k_ar_fused(const ARArgs a) {
+  using M = Scope<SYS>;
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint64_t s_sb[kMaxCollRanks], s_rb[kMaxCollRanks];
+  __shared__ int s_ok;
+  const int q = threadIdx.x;
+  const int P = a.P;
+  if (q == 0) s_ok = 1;
+  __syncthreads();
+  if (q < P) {
+    CollSlot* dst = a.peer_in[q];
+    M::st_rlx(&dst->sbuf, (uint64_t)a.sbuf);
+    M::st_rlx(&dst->rbuf, (uint64_t)a.rbuf);
+    M::st_rel(&dst->flag, a.epoch);
+    if (!spin_ge<SYS>(&a.my_in[q].flag, a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL))
+      s_ok = 0;
+    s_sb[q] = M::ld_rlx(&a.my_in[q].sbuf);
+    s_rb[q] = M::ld_rlx(&a.my_in[q].rbuf);
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  switch (a.dtype) {
+    case AR_F32:
+      if (a.op == AR_SUM) ar_tile<AR_F32, AR_SUM>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      else if (a.op == AR_MAX) ar_tile<AR_F32, AR_MAX>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      else ar_tile<AR_F32, AR_MIN>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      break;
+    case AR_BF16:
+      if (a.op == AR_SUM) ar_tile<AR_BF16, AR_SUM>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      else if (a.op == AR_MAX) ar_tile<AR_BF16, AR_MAX>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      else ar_tile<AR_BF16, AR_MIN>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      break;
+    case AR_I32:
+      if (a.op == AR_SUM) ar_tile<AR_I32, AR_SUM>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      else if (a.op == AR_MAX) ar_tile<AR_I32, AR_MAX>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      else ar_tile<AR_I32, AR_MIN>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      break;
+    default:
+      if (a.op == AR_SUM) ar_tile<AR_F64, AR_SUM>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      else if (a.op == AR_MAX) ar_tile<AR_F64, AR_MAX>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      else ar_tile<AR_F64, AR_MIN>(a, s_sb, s_rb, AR_TWOSHOT, 0, 1);
+      break;
+  }
+  __syncthreads();
+  if (P > 1) {
+    if (q == 0) M::fence_ar();
+    __syncthreads();
+    if (q < P) {
+      M::st_rlx(a.peer_exit[q], a.epoch);
+      spin_ge<SYS>(&a.my_exit[q], a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
+    }
+  }
+}
+
 // Exit: tell every peer I am done with its buffers; wait for all of them.
 template <bool SYS>
 __global__ void __launch_bounds__(32) k_ar_exit(const ARArgs a) {
@@ -1616,7 +1677,12 @@ uint64_t ar_reduce_grid(uint64_t work_bytes, int P) {
   return g < 1 ? 1 : g;
 }
 
-int launch_allreduce(const ARArgs& a, bool sys, uint64_t grid, cudaStream_t s) {
+int launch_allreduce(const ARArgs& a, bool sys, uint64_t grid, cudaStream_t s, bool fused) {
+  if (fused) {
+    cudaError_t e = sys ? launch_pdl(k_ar_fused<true>, 1, kArThreads, s, a)
+                        : launch_pdl(k_ar_fused<false>, 1, kArThreads, s, a);
+    return e == cudaSuccess ? 1 : -1;
+  }
   {
     cudaError_t e = sys ? launch_pdl(k_ar_entry<true>, 1, 32, s, a)
                         : launch_pdl(k_ar_entry<false>, 1, 32, s, a);
@@ -1673,6 +1739,7 @@ int preload_kernels() {
       (const void*)k_copy, (const void*)k_fin<true>, (const void*)k_fin<false>,
       (const void*)k_ar_entry<true>, (const void*)k_ar_entry<false>,
       (const void*)k_ar_exit<true>, (const void*)k_ar_exit<false>,
+      (const void*)k_ar_fused<true>, (const void*)k_ar_fused<false>,
       (const void*)k_batch<true, 4, 8>, (const void*)k_batch<false, 4, 8>,
       (const void*)k_batch<true, 16, 32>, (const void*)k_batch<false, 16, 32>,
       (const void*)k_batch<true, kBatchOps, kBatchWaits>,

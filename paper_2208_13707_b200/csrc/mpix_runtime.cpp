@@ -975,7 +975,9 @@ int allreduce_enqueue(const void* sbuf, void* rbuf, int count, MPI_Datatype dt, 
   StreamBatch& b = *static_cast<StreamBatch*>(c->batch);
   std::lock_guard<std::mutex> lk(b.mu);
   if (!b.ops.empty() && flush_locked(b, c->cu, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
-  int nk = launch_allreduce(a, sys, ar_reduce_grid(work, P), c->cu);
+  // latency-bound sizes: entry + reduce + exit in one single-CTA launch
+  const bool fused = bytes <= g_world->cfg.oneshot_max;
+  int nk = launch_allreduce(a, sys, ar_reduce_grid(work, P), c->cu, fused);
   if (nk < 0) return MPIX_ERR_CUDA;
   g_launches.fetch_add(nk);
   return MPI_SUCCESS;

@@ -141,6 +141,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Selfchain": (I, [P, P, P, I, I, P, P, P]),
         "MPIXT_Empty_loop": (I, [I, P, P, P]),
         "MPIXT_Loopback": (I, [P, P, P, U64, I, P, P, P]),
+        "MPIXT_Allreduce_loop": (I, [I, P, P, P, P, P, I, I, I, I, P, P]),
         "MPIXT_Halo_steps": (I, [I, I, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P]),
         "MPIXT_Stream_create": (I, [I, C.POINTER(P)]),
         "MPIXT_Stream_destroy": (I, [P]),
@@ -578,6 +579,19 @@ class testing:
         ds, hs = C.c_double(), C.c_double()
         check(lib().MPIXT_Loopback(c.h, _ptr(src), _ptr(dst), nbytes, iters, _stream_handle(stream),
                                    C.byref(ds), C.byref(hs)), "Loopback")
+        return ds.value, hs.value
+
+    @staticmethod
+    def allreduce_loop(comms, streams, devices, sbufs, rbufs, count: int, dt: int, iters: int,
+                       op: int = MPI_SUM):
+        P = len(comms)
+        VP = C.c_void_p
+        ds, hs = C.c_double(), C.c_double()
+        check(lib().MPIXT_Allreduce_loop(
+            P, (VP * P)(*[c.h for c in comms]), (VP * P)(*[_stream_handle(s) for s in streams]),
+            (C.c_int * P)(*devices), (VP * P)(*[_ptr(b) for b in sbufs]),
+            (VP * P)(*[_ptr(b) for b in rbufs]), count, dt, op, iters, C.byref(ds), C.byref(hs)),
+            "Allreduce_loop")
         return ds.value, hs.value
 
     @staticmethod

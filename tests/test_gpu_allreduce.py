@@ -148,3 +148,38 @@ def test_reduce_stage_alone_matches_oracle(dt, twoshot):
     for r in range(P):
         assert torch.equal(rb[r].cpu().view(torch.int16 if dt == "bf16" else torch.int32),
                            exp.view(torch.int16 if dt == "bf16" else torch.int32)), r
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+@pytest.mark.parametrize("case", ["plain", "in_place", "unaligned", "max_i32"])
+def test_fused_single_launch_allreduce(P, case, monkeypatch):
+    """The single-CTA allreduce (entry + two-shot chunk + exit in one launch),
+    forced up to large counts, bit-exact with the rank-ordered oracle."""
+    monkeypatch.setenv("MPIX_ALLREDUCE_ONESHOT_MAX", str(64 << 20))
+    count = 300001
+    dt = "i32" if case == "max_i32" else "f32"
+    op = mpix.MPI_MAX if case == "max_i32" else mpix.MPI_SUM
+    with gpu_world(P) as (w, ctx):
+        ins = make_inputs(P, count, dt, seed=P + 17)
+        off = 1 if case == "unaligned" else 0
+        sb = [torch.zeros(count + off, dtype=DT[dt][0], device=0) for _ in range(P)]
+        for r in range(P):
+            sb[r][off:] = ins[r].to(0)
+        rb = [torch.zeros(count + 2 * off, dtype=DT[dt][0], device=0) for _ in range(P)]
+        torch.cuda.synchronize()
+        l0 = mpix.launch_count()
+
+        def body(r):
+            if case == "in_place":
+                ctx[r].comm.allreduce_enqueue("in_place", sb[r], count, DT[dt][1], op)
+            else:
+                ctx[r].comm.allreduce_enqueue(sb[r][off:], rb[r][2 * off:], count, DT[dt][1], op)
+
+        w.run_ranks(body)
+        launches = mpix.launch_count() - l0
+        sync_all(ctx)
+        exp = oracle(ins, dt, op)
+        for r in range(P):
+            got = sb[r].cpu() if case == "in_place" else rb[r][2 * off:].cpu()
+            assert torch.equal(got, exp), r
+        assert launches == P  # one launch per rank
