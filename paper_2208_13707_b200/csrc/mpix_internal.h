@@ -249,6 +249,7 @@ constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch
 template <int NOPS, int NWAIT>
 struct BatchArgs {
   int n, nwait;
+  int n_static;  // ops[0, n_static): one CTA each; ops[n_static, n): dynamic, one CTA in order
   int early;  // no grouped copy follows: trigger the next (head) kernel at start
   uint64_t spin_limit_ns;
   uint64_t* err_word;

@@ -1113,13 +1113,26 @@ __global__ void __launch_bounds__(kThreads) k_batch(const BatchArgs<NOPS, NWAIT>
   __shared__ Decision s_dc;
   pdl_wait();
   if (b.early) pdl_trigger();  // no grouped copy behind me: the next head kernel may park
-  if ((int)blockIdx.x < b.n) {
-    __shared__ P2PArgs a;
+  __shared__ P2PArgs a;
+  if ((int)blockIdx.x < b.n_static) {
     const BatchOp& o = b.ops[blockIdx.x];
     if (threadIdx.x == 0) load_op(o, b.spin_limit_ns, a);
     __syncthreads();
     if (o.inl) proto_body<SYS, true>(a, s_dc);
     else proto_body<SYS, false>(a, s_dc);  // decision -> op record; triggers k_gcopy
+  } else if ((int)blockIdx.x == b.n_static && b.n > b.n_static) {
+    // Dynamic-matching operations run one after another in this CTA, in
+    // batch order: their matching is serialised by the receiver's lock and
+    // tickets anyway, and one CTA per stream (instead of one spinning CTA per
+    // operation) leaves the SMs to the other streams and ranks.
+    for (int i = b.n_static; i < b.n; ++i) {
+      const BatchOp& o = b.ops[i];
+      if (threadIdx.x == 0) load_op(o, b.spin_limit_ns, a);
+      __syncthreads();
+      if (o.inl) proto_body<SYS, true>(a, s_dc);
+      else proto_body<SYS, false>(a, s_dc);
+      __syncthreads();
+    }
   } else {
     wait_all<SYS>(b.w, b.nwait, b.err_word, b.spin_limit_ns);
   }
@@ -1610,22 +1623,30 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   b.nwait = nwait;
   b.spin_limit_ns = spin_limit_ns;
   b.err_word = err_word;
-  for (int i = 0; i < n; ++i) b.ops[i] = ops[i];
+  // static-matching operations first (one CTA each), then the dynamic ones
+  // (one sequential CTA), keeping batch order within each group
+  int k = 0;
+  for (int i = 0; i < n; ++i)
+    if (!ops[i].dyn) b.ops[k++] = ops[i];
+  b.n_static = k;
+  for (int i = 0; i < n; ++i)
+    if (ops[i].dyn) b.ops[k++] = ops[i];
+  const int head_ctas = b.n_static + (n > b.n_static ? 1 : 0);
   for (int i = 0; i < nwait; ++i) b.w[i] = w[i];
   GCopyArgs g;
   g.m = 0;
   uint64_t tiles = 0;
   for (int i = 0; i < n; ++i) {
-    if (ops[i].inl) continue;
+    if (b.ops[i].inl) continue;
     g.tile_start[g.m] = (uint32_t)tiles;
-    g.rec[g.m] = ops[i].rec;
-    tiles += p2p_copy_grid(ops[i].bytes);
+    g.rec[g.m] = b.ops[i].rec;
+    tiles += p2p_copy_grid(b.ops[i].bytes);
     ++g.m;
   }
   g.tile_start[g.m] = (uint32_t)tiles;
   for (int i = 0; i < n; ++i) b.ops[i].early = tiles <= kEarlyTriggerTiles;
   if (g.m == 0) {  // inline operations only: one launch, the wait included
-    const int grid = n + (nwait > 0 ? 1 : 0);
+    const int grid = head_ctas + (nwait > 0 ? 1 : 0);
     b.early = 1;
     cudaError_t e = sys ? launch_head(k_batch<true, NOPS, NWAIT>, grid, kThreads, s, b)
                         : launch_head(k_batch<false, NOPS, NWAIT>, grid, kThreads, s, b);
@@ -1636,8 +1657,8 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   b.nwait = 0;
   b.early = 0;
   {
-    cudaError_t e = sys ? launch_head(k_batch<true, NOPS, NWAIT>, n, kThreads, s, b)
-                        : launch_head(k_batch<false, NOPS, NWAIT>, n, kThreads, s, b);
+    cudaError_t e = sys ? launch_head(k_batch<true, NOPS, NWAIT>, head_ctas, kThreads, s, b)
+                        : launch_head(k_batch<false, NOPS, NWAIT>, head_ctas, kThreads, s, b);
     if (e != cudaSuccess) return -1;
   }
   b.nwait = nw;
