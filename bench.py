@@ -598,7 +598,7 @@ def extras_multirank(args, mpix, torch):
         torch.cuda.synchronize(d)
     out["msgrate_8B"] = {"ranks": P, "streams_per_rank": S, "window": W, **res,
                          "driver": "native C++ threads over the C ABI (MPIXT_Msgrate)",
-                         "launches_per_window": "1 coalesced k_batch + ceil(2W/64)-1 flushes"}
+                         "launches_per_window": "1 coalesced k_batch (2W = 128 operations + the Waitall)"}
     w.finalize()
 
     # the same under the dynamic (wildcard-capable) matching engine

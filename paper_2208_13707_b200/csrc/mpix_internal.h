@@ -243,7 +243,7 @@ struct BatchOp {
 };
 static_assert(sizeof(BatchOp) == 200, "BatchOp packing");
 
-constexpr int kBatchOps = 64;     // operations per coalesced launch
+constexpr int kBatchOps = 128;    // operations per coalesced launch (27.7 KB of parameters)
 constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch
 
 template <int NOPS, int NWAIT>

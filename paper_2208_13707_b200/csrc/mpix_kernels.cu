@@ -1680,6 +1680,9 @@ int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint6
     return launch_batch_t<4, 8>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s, ev0, ev1);
   if (n <= 16 && nwait <= 32)
     return launch_batch_t<16, 32>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s, ev0, ev1);
+  if (n <= 64 && nwait <= kBatchWaits)
+    return launch_batch_t<64, kBatchWaits>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s, ev0,
+                                           ev1);
   if (n <= kBatchOps && nwait <= kBatchWaits)
     return launch_batch_t<kBatchOps, kBatchWaits>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s,
                                                   ev0, ev1);
@@ -1763,6 +1766,8 @@ int preload_kernels() {
       (const void*)k_ar_fused<true>, (const void*)k_ar_fused<false>,
       (const void*)k_batch<true, 4, 8>, (const void*)k_batch<false, 4, 8>,
       (const void*)k_batch<true, 16, 32>, (const void*)k_batch<false, 16, 32>,
+      (const void*)k_batch<true, 64, kBatchWaits>, (const void*)k_batch<false, 64, kBatchWaits>,
+      (const void*)k_gfin<true, 64, kBatchWaits>, (const void*)k_gfin<false, 64, kBatchWaits>,
       (const void*)k_batch<true, kBatchOps, kBatchWaits>,
       (const void*)k_batch<false, kBatchOps, kBatchWaits>,
       (const void*)k_gfin<true, 4, 8>, (const void*)k_gfin<false, 4, 8>,
