@@ -247,6 +247,25 @@ int MPIX_Request_free(MPI_Request *request);
 int MPIX_Allreduce_enqueue(const void *sendbuf, void *recvbuf, int count,
                            MPI_Datatype datatype, MPI_Op op, MPI_Comm comm);
 
+/* More enqueued collectives ("The enqueue APIs can be
+ * extended to collectives"; no reference implementation). Same entry/exit
+ * barrier as MPIX_Allreduce_enqueue, same stream-order semantics; folds are
+ * rank-ordered (bit-exact with oracle/streamix_oracle.c orc_allreduce_*).
+ * Reduce: the result lands in the root's recvbuf; sendbuf may be
+ * MPI_IN_PLACE at the root. Reduce_scatter_block: rank r receives the fold
+ * of block r (recvcount elements) of every sendbuf (not in place).
+ * Bcast: the root's buffer is copied into every other member's buffer.
+ * Allgather: block q of every recvbuf = member q's sendbuf (MPI_IN_PLACE:
+ * my block is already in place). Barrier: entry + exit barrier only. */
+int MPIX_Reduce_enqueue(const void *sendbuf, void *recvbuf, int count, MPI_Datatype datatype,
+                        MPI_Op op, int root, MPI_Comm comm);
+int MPIX_Reduce_scatter_block_enqueue(const void *sendbuf, void *recvbuf, int recvcount,
+                                      MPI_Datatype datatype, MPI_Op op, MPI_Comm comm);
+int MPIX_Bcast_enqueue(void *buffer, int count, MPI_Datatype datatype, int root, MPI_Comm comm);
+int MPIX_Allgather_enqueue(const void *sendbuf, int sendcount, MPI_Datatype sendtype,
+                           void *recvbuf, int recvcount, MPI_Datatype recvtype, MPI_Comm comm);
+int MPIX_Barrier_enqueue(MPI_Comm comm);
+
 /* ------------------------------------------------------------------------ */
 /* Introspection (tests / bench)                                             */
 /* ------------------------------------------------------------------------ */

@@ -268,6 +268,24 @@ struct GCopyArgs {
 enum ARDtype : int { AR_I32 = 0, AR_F32 = 1, AR_BF16 = 2, AR_F64 = 3 };
 enum AROp : int { AR_SUM = 0, AR_MAX = 1, AR_MIN = 2 };
 enum ARAlgo : int { AR_ONESHOT = 0, AR_TWOSHOT = 1 };
+// Enqueued collectives sharing the entry/exit barrier of Allreduce_enqueue.
+enum CollKind : int {
+  CK_ALLREDUCE = 0,
+  CK_REDUCE = 1,          // fold at the root
+  CK_REDUCE_SCATTER = 2,  // block: rank r folds chunk r
+  CK_BCAST = 3,
+  CK_ALLGATHER = 4,
+  CK_BARRIER = 5,
+};
+// OpRecord.action of a collective after its entry barrier.
+enum : uint64_t {
+  COLL_FAILED = 0,
+  COLL_ONESHOT = 1,  // allreduce (AR_ONESHOT + 1)
+  COLL_TWOSHOT = 2,  // allreduce (AR_TWOSHOT + 1)
+  COLL_NOOP = 3,     // nothing to move on this rank (exit barrier only)
+  COLL_FOLD = 4,     // fold OpRecord.flags inputs coll[0..) into coll[16]
+  COLL_COPY = 5,     // OpRecord.flags segments coll[s] -> coll[16 + s]
+};
 
 struct ARArgs {
   const uint8_t* sbuf;
@@ -288,6 +306,9 @@ struct ARArgs {
   uint64_t opid;
   uint64_t* err_word;
   uint64_t spin_limit_ns;
+  int kind;              // CollKind
+  int root;              // REDUCE / BCAST
+  uint64_t chunk_bytes;  // ALLGATHER: bytes per rank; REDUCE_SCATTER: bytes of my block
 };
 
 // Launchers implemented in mpix_kernels.cu (host side). Each returns the
@@ -299,6 +320,8 @@ int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint6
                  uint64_t spin_limit_ns, bool sys, cudaStream_t s, cudaEvent_t copy_ev0 = nullptr,
                  cudaEvent_t copy_ev1 = nullptr);
 int launch_allreduce(const ARArgs& a, bool sys, uint64_t reduce_grid, cudaStream_t s, bool fused);
+// Reduce / Reduce_scatter / Bcast / Allgather / Barrier: entry -> work -> exit.
+int launch_collective(const ARArgs& a, bool sys, uint64_t work_grid, cudaStream_t s);
 uint64_t p2p_copy_grid(uint64_t bytes);
 uint64_t ar_reduce_grid(uint64_t work_bytes, int P);
 int preload_kernels();

@@ -1430,14 +1430,46 @@ __global__ void __launch_bounds__(32) k_ar_entry(const ARArgs a) {
     ok = spin_ge<SYS>(&a.my_in[q].flag, a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
     sb = M::ld_rlx(&a.my_in[q].sbuf);
     rb = M::ld_rlx(&a.my_in[q].rbuf);
-    rec->coll[q] = sb;
-    rec->coll[kMaxCollRanks + q] = rb;
+    switch (a.kind) {
+      case CK_REDUCE_SCATTER:  // fold chunk `me` of every input into my buffer
+        rec->coll[q] = sb + (uint64_t)a.me * a.chunk_bytes;
+        if (q == a.me) rec->coll[kMaxCollRanks] = (uint64_t)a.rbuf;
+        break;
+      case CK_REDUCE:          // the root folds every input into its buffer
+        rec->coll[q] = sb;
+        if (q == a.me) rec->coll[kMaxCollRanks] = (uint64_t)a.rbuf;
+        break;
+      case CK_BCAST:           // one segment: the root's buffer -> mine
+        if (q == a.root) rec->coll[0] = sb;
+        if (q == a.me) rec->coll[kMaxCollRanks] = (uint64_t)a.rbuf;
+        break;
+      case CK_ALLGATHER:       // segment q: rank q's block -> my buffer at q
+        rec->coll[q] = sb;
+        rec->coll[kMaxCollRanks + q] = (uint64_t)a.rbuf + (uint64_t)q * a.chunk_bytes;
+        break;
+      default:                 // allreduce: every member's buffers
+        rec->coll[q] = sb;
+        rec->coll[kMaxCollRanks + q] = rb;
+    }
   }
   ok = __all_sync(0xffffffffu, ok);
   // One-shot reads every peer's full buffer while peers write theirs: use
   // two-shot if any rank reduces in place.
   int inplace = __any_sync(0xffffffffu, q < P && sb == rb);
-  if (q == 0) rec->action = ok ? (uint64_t)((inplace && P > 1) ? AR_TWOSHOT : a.algo) + 1 : 0;
+  if (q == 0) {
+    uint64_t act = COLL_FAILED;
+    if (ok) {
+      switch (a.kind) {
+        case CK_ALLREDUCE: act = (uint64_t)((inplace && P > 1) ? AR_TWOSHOT : a.algo) + 1; break;
+        case CK_REDUCE: act = a.me == a.root ? COLL_FOLD : COLL_NOOP; rec->flags = P; break;
+        case CK_REDUCE_SCATTER: act = COLL_FOLD; rec->flags = P; break;
+        case CK_BCAST: act = a.me == a.root ? COLL_NOOP : COLL_COPY; rec->flags = 1; break;
+        case CK_ALLGATHER: act = COLL_COPY; rec->flags = P; break;
+        default: act = COLL_NOOP;
+      }
+    }
+    rec->action = act;
+  }
   pdl_trigger();
 }
 
@@ -1455,8 +1487,37 @@ __global__ void __launch_bounds__(kArThreads, (DT == AR_BF16 || DT == AR_F64) ? 
   if (threadIdx.x == 0) s_act = rec->action;
   __syncthreads();
   pdl_trigger();
-  if (s_act == 0) return;
-  ar_tile<DT, OP>(a, s_sb, s_rb, (int)s_act - 1, blockIdx.x, gridDim.x);
+  if (s_act == COLL_ONESHOT || s_act == COLL_TWOSHOT) {
+    ar_tile<DT, OP>(a, s_sb, s_rb, (int)s_act - 1, blockIdx.x, gridDim.x);
+  } else if (s_act == COLL_FOLD) {
+    // Reduce / Reduce_scatter: a one-shot fold of rec->flags inputs (rank
+    // order) into the single output coll[16]
+    ARArgs f = a;
+    f.P = (int)rec->flags;
+    f.me = 0;
+    if (threadIdx.x < f.P) {
+      s_sb[threadIdx.x] = rec->coll[threadIdx.x];
+      s_rb[threadIdx.x] = threadIdx.x == 0 ? rec->coll[kMaxCollRanks] : 0;
+    }
+    __syncthreads();
+    ar_tile<DT, OP>(f, s_sb, s_rb, AR_ONESHOT, blockIdx.x, gridDim.x);
+  }
+}
+
+// Bcast / Allgather (PDL behind k_ar_entry): rec->flags segments of
+// a.chunk_bytes, coll[s] -> coll[16 + s]; CTA b copies tile b % tps of
+// segment b / tps. In-place segments (src == dst) are skipped.
+__global__ void __launch_bounds__(kCopyThreads, 2) k_coll_copy(const ARArgs a) {
+  pdl_wait();
+  const OpRecord* rec = a.rec;
+  pdl_trigger();
+  if (rec->action != COLL_COPY) return;
+  const uint64_t tps = a.chunk_bytes ? (a.chunk_bytes + kTileVec * 16 - 1) / (kTileVec * 16) : 1;
+  const uint64_t seg = blockIdx.x / tps, t = blockIdx.x % tps;
+  if (seg >= rec->flags) return;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(rec->coll[seg]);
+  uint8_t* dst = reinterpret_cast<uint8_t*>(rec->coll[kMaxCollRanks + seg]);
+  tile_copy(dst, src, a.chunk_bytes, t, tps);
 }
 
 using ReduceKernel = void (*)(const ARArgs);
@@ -1692,6 +1753,30 @@ int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint6
 // One CTA per tile when it moves enough bytes (P inputs + outputs of
 // kArTileVec x 16 B each); with few ranks a CTA takes several tiles so CTA
 // launch does not dominate (P = 1: 4 tiles = 32 KiB in + 32 KiB out).
+int launch_collective(const ARArgs& a, bool sys, uint64_t work_grid, cudaStream_t s) {
+  {
+    cudaError_t e = sys ? launch_pdl(k_ar_entry<true>, 1, 32, s, a)
+                        : launch_pdl(k_ar_entry<false>, 1, 32, s, a);
+    if (e != cudaSuccess) return -1;
+  }
+  int nk = 1;
+  if (a.kind == CK_BCAST || a.kind == CK_ALLGATHER) {
+    if (launch_pdl(k_coll_copy, (int)work_grid, kCopyThreads, s, a) != cudaSuccess) return -1;
+    ++nk;
+  } else if (a.kind == CK_REDUCE || a.kind == CK_REDUCE_SCATTER) {
+    if (launch_pdl(reduce_kernel(a.dtype, a.op), (int)work_grid, kArThreads, s, a) != cudaSuccess)
+      return -1;
+    ++nk;
+  }
+  if (a.P > 1) {
+    cudaError_t e = sys ? launch_pdl(k_ar_exit<true>, 1, 32, s, a)
+                        : launch_pdl(k_ar_exit<false>, 1, 32, s, a);
+    if (e != cudaSuccess) return -1;
+    ++nk;
+  }
+  return nk;
+}
+
 uint64_t ar_reduce_grid(uint64_t work_bytes, int P) {
   const uint64_t tile = kArTileVec * 16;
   const uint64_t tiles = (work_bytes + tile - 1) / tile;
@@ -1763,7 +1848,7 @@ int preload_kernels() {
       (const void*)k_copy, (const void*)k_fin<true>, (const void*)k_fin<false>,
       (const void*)k_ar_entry<true>, (const void*)k_ar_entry<false>,
       (const void*)k_ar_exit<true>, (const void*)k_ar_exit<false>,
-      (const void*)k_ar_fused<true>, (const void*)k_ar_fused<false>,
+      (const void*)k_ar_fused<true>, (const void*)k_ar_fused<false>, (const void*)k_coll_copy,
       (const void*)k_batch<true, 4, 8>, (const void*)k_batch<false, 4, 8>,
       (const void*)k_batch<true, 16, 32>, (const void*)k_batch<false, 16, 32>,
       (const void*)k_batch<true, 64, kBatchWaits>, (const void*)k_batch<false, 64, kBatchWaits>,

@@ -115,6 +115,11 @@ def _declare(L: C.CDLL) -> None:
         "MPIX_Waitall_enqueue": (I, [I, C.POINTER(U64), P]),
         "MPIX_Request_free": (I, [C.POINTER(U64)]),
         "MPIX_Allreduce_enqueue": (I, [P, P, I, I, I, P]),
+        "MPIX_Reduce_enqueue": (I, [P, P, I, I, I, I, P]),
+        "MPIX_Reduce_scatter_block_enqueue": (I, [P, P, I, I, I, P]),
+        "MPIX_Bcast_enqueue": (I, [P, I, I, I, P]),
+        "MPIX_Allgather_enqueue": (I, [P, I, I, P, I, I, P]),
+        "MPIX_Barrier_enqueue": (I, [P]),
         "MPIX_Launch_count": (U64, []),
         "MPIX_Config_get": (I, [C.POINTER(U64), C.POINTER(I), C.POINTER(I), C.POINTER(U64)]),
         "MPIX_Comm_get_ctx": (I, [P, C.POINTER(U32)]),
@@ -396,6 +401,30 @@ class Comm:
         sb = 1 if sendbuf == "in_place" else _ptr(sendbuf)
         check(lib().MPIX_Allreduce_enqueue(sb, _ptr(recvbuf), count, dt, op, self.h),
               "MPIX_Allreduce_enqueue")
+
+    def reduce_enqueue(self, sendbuf, recvbuf, count: int, dt: int, op: int = MPI_SUM,
+                       root: int = 0) -> None:
+        sb = 1 if sendbuf == "in_place" else _ptr(sendbuf)
+        rb = _ptr(recvbuf) if recvbuf is not None else None
+        check(lib().MPIX_Reduce_enqueue(sb, rb, count, dt, op, root, self.h), "MPIX_Reduce_enqueue")
+
+    def reduce_scatter_block_enqueue(self, sendbuf, recvbuf, recvcount: int, dt: int,
+                                     op: int = MPI_SUM) -> None:
+        sb = 1 if sendbuf == "in_place" else _ptr(sendbuf)
+        check(lib().MPIX_Reduce_scatter_block_enqueue(sb, _ptr(recvbuf), recvcount, dt, op, self.h),
+              "MPIX_Reduce_scatter_block_enqueue")
+
+    def bcast_enqueue(self, buf, count: int, dt: int, root: int = 0) -> None:
+        check(lib().MPIX_Bcast_enqueue(_ptr(buf), count, dt, root, self.h), "MPIX_Bcast_enqueue")
+
+    def allgather_enqueue(self, sendbuf, recvbuf, count: int, dt: int) -> None:
+        """count elements per member; sendbuf may be "in_place"."""
+        sb = 1 if sendbuf == "in_place" else _ptr(sendbuf)
+        check(lib().MPIX_Allgather_enqueue(sb, count, dt, _ptr(recvbuf), count, dt, self.h),
+              "MPIX_Allgather_enqueue")
+
+    def barrier_enqueue(self) -> None:
+        check(lib().MPIX_Barrier_enqueue(self.h), "MPIX_Barrier_enqueue")
 
 
 def wait_enqueue(req: Request) -> None:
