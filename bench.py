@@ -542,6 +542,47 @@ def extras_multirank(args, mpix, torch):
         w.finalize()
     out["allreduce_256MiB"] = ar
 
+    # the other enqueued collectives at P = 8 (ranks share the visible GPUs),
+    # 256 MiB per rank of fp32: bcast of 256 MiB, allgather of 32 MiB blocks,
+    # reduce_scatter_block of 32 MiB blocks (256 MiB input per rank)
+    w, ctx = world(8)
+    P8 = 8
+    nb = 256 << 20
+    cnt = nb // 4
+    big = {r: torch.ones(cnt, dtype=torch.float32, device=ctx[r][2]) for r in range(P8)}
+    small = {r: torch.ones(cnt // P8, dtype=torch.float32, device=ctx[r][2]) for r in range(P8)}
+    colls = {
+        "bcast_256MiB": lambda r: ctx[r][1].bcast_enqueue(big[r], cnt, mpix.MPI_FLOAT, 0),
+        "allgather_8x32MiB": lambda r: ctx[r][1].allgather_enqueue(small[r], big[r], cnt // P8,
+                                                                   mpix.MPI_FLOAT),
+        "reduce_scatter_8x32MiB": lambda r: ctx[r][1].reduce_scatter_block_enqueue(
+            big[r], small[r], cnt // P8, mpix.MPI_FLOAT),
+    }
+    cres = {}
+    for name, fn in colls.items():
+        ev = {r: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for r in range(P8)}
+
+        def loop(r, k, timed, fn=fn, ev=ev):
+            if timed:
+                ev[r][0].record(ctx[r][0])
+            for _ in range(k):
+                fn(r)
+            if timed:
+                ev[r][1].record(ctx[r][0])
+        w.run_ranks(lambda r: loop(r, 1, False))
+        sync_all(ctx)
+        w.run_ranks(lambda r: loop(r, 5, True))
+        sync_all(ctx)
+        t = max(a.elapsed_time(b) for a, b in ev.values()) / 1e3 / 5
+        # bytes every rank receives (the algorithmic per-rank volume)
+        per_rank = {"bcast_256MiB": nb, "allgather_8x32MiB": nb * 7 // 8,
+                    "reduce_scatter_8x32MiB": nb}[name]
+        cres[name] = {"ms": t * 1e3, "GBps_per_rank": per_rank / t / 1e9, "ranks_per_gpu": -(-P8 // ndev)}
+    del big, small
+    w.finalize()
+    out["collectives_P8"] = cres
+
     # cfg5: 3-D halo stencil, 2x2x2 periodic, 512^3 fp32 per rank
     n = 512  # BASELINE cfg5: 512^3 fp32 per rank (8 ranks share the visible GPUs)
     w, ctx = world(8)
