@@ -209,7 +209,10 @@ int MPIX_Stream_comm_create_multiple(MPI_Comm parent, int count,
 /* proc_enqueue.cpp:8-28), launches one sm_100a kernel into the comm's CUDA  */
 /* stream and returns; it never blocks on the peer.            */
 /* Matching is MPI non-overtaking per (comm, source, dest, tag).             */
-/* v1 divergence: MPI_ANY_SOURCE / MPI_ANY_TAG receives give UNSUPPORTED.    */
+/* MPI_ANY_SOURCE / MPI_ANY_TAG receives need a dynamic-matching comm        */
+/* (MPIX_MATCHING=dynamic or the "mpix_matching" stream hint), else         */
+/* UNSUPPORTED. Non-blocking calls are coalesced into the stream's next      */
+/* ordering call.                                             */
 /* ------------------------------------------------------------------------ */
 
 /* PAPER.md:427. Blocking in the stream: later work in the stream sees the
@@ -238,6 +241,45 @@ int MPIX_Irecv_enqueue(void *buf, int count, MPI_Datatype datatype, int source,
 int MPIX_Wait_enqueue(MPI_Request *request, MPI_Status *status);
 int MPIX_Waitall_enqueue(int count, MPI_Request requests[],
                          MPI_Status statuses[]);
+
+/* ------------------------------------------------------------------------ */
+/* Conventional (host-thread) p2p on GPU buffers — Proc::isend/irecv/send/  */
+/* recv/wait/waitall (proc_p2p.cpp:96-212). Arguments are checked rank ->   */
+/* count -> tag (proc_p2p.cpp:9-23); a multiplex comm gives MULTIPLEX_COMM.  */
+/* The operation runs at once on the rank's internal CUDA stream with the   */
+/* same kernels and rings as the enqueue family, so a conventional send     */
+/* matches a peer's Recv_enqueue on the same comm (mixed mode). */
+/* MPI_Send is eager (returns once the payload is delivered or staged),     */
+/* MPI_Recv returns once the payload has landed. MPI_Wait/Waitall block the */
+/* host; a request can be waited once (INVALID_REQUEST after), and passing  */
+/* one to MPIX_Wait(all)_enqueue gives STREAM_MISMATCH (Appendix A6).       */
+/* ------------------------------------------------------------------------ */
+int MPI_Send(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm);
+int MPI_Recv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+             MPI_Status *status);
+int MPI_Isend(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+              MPI_Request *request);
+int MPI_Irecv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+              MPI_Request *request);
+int MPI_Wait(MPI_Request *request, MPI_Status *status);
+int MPI_Waitall(int count, MPI_Request requests[], MPI_Status statuses[]);
+
+/* Multiplex stream p2p — PAPER.md:484-487, Proc::stream_isend/irecv
+ * (proc_p2p.cpp:115-144). NOT_MULTIPLEX on a single-stream comm; indices
+ * are checked like the reference (INVALID_INDEX, WILDCARD_DST for an
+ * MPIX_ANY_INDEX destination). The operation runs on the CUDA stream of
+ * local stream src_idx (send) / dst_idx (receive), or on the rank's internal
+ * stream if that MPIX stream is not a GPU stream; the stream indices are
+ * part of the match. v1: MPIX_ANY_INDEX sources and dynamic-matching comms
+ * give UNSUPPORTED. The blocking forms synchronise that stream. */
+int MPIX_Stream_send(const void *buf, int count, MPI_Datatype datatype, int dest, int tag,
+                     MPI_Comm comm, int src_idx, int dst_idx);
+int MPIX_Stream_recv(void *buf, int count, MPI_Datatype datatype, int source, int tag,
+                     MPI_Comm comm, int src_idx, int dst_idx, MPI_Status *status);
+int MPIX_Stream_isend(const void *buf, int count, MPI_Datatype datatype, int dest, int tag,
+                      MPI_Comm comm, int src_idx, int dst_idx, MPI_Request *request);
+int MPIX_Stream_irecv(void *buf, int count, MPI_Datatype datatype, int source, int tag,
+                      MPI_Comm comm, int src_idx, int dst_idx, MPI_Request *request);
 int MPIX_Request_free(MPI_Request *request);
 
 /* New (absent from the reference): in-stream sum/max/min

@@ -138,6 +138,7 @@ struct RankState {
   uint64_t* h_err = nullptr;  // host-mapped error word
   uint64_t* d_err = nullptr;
   cudaStream_t aux = nullptr;      // setup work
+  cudaStream_t p2p = nullptr;      // conventional (host-thread) p2p of this rank
   cudaMemPool_t pool = nullptr;
   std::mutex mu;
   // Staging buffers for large blocking sends whose receive is not posted yet
@@ -164,6 +165,8 @@ struct RankState {
     cudaStream_t stream = nullptr;
     int source = -1, tag = -1;
     bool remote = false;  // the peer lives on another GPU (system scope)
+    bool conventional = false;  // MPI_Isend/Irecv or MPIX_Stream_isend/irecv (host-waited)
+    bool consumed = false;      // completed by MPI_Wait/Waitall (proc_p2p.cpp:147)
   };
   std::vector<ReqInfo> reqs;
 };
@@ -204,6 +207,8 @@ struct mpix_comm_s {
   cudaStream_t cu = nullptr;
   std::vector<uint64_t> send_pseq, recv_pseq;
   uint64_t recv_rseq = 0;  // dynamic matching: my receive ticket
+  std::mutex mu;           // conventional / multiplex use may come from several threads
+  std::unordered_map<uint64_t, uint32_t> idx_tagseq;  // multiplex: (dir, peer, tag, sidx, didx)
   void* batch = nullptr;   // the StreamBatch of cu (looked up once)
   bool any_remote = false; // some member lives on another GPU
   std::unordered_map<uint64_t, uint32_t> send_tagseq, recv_tagseq;
@@ -346,6 +351,7 @@ int rank_init(RankState& r, const Config& cfg) {
   memset(r.h_err, 0, 64);
   CK(cudaHostGetDevicePointer(&r.d_err, r.h_err, 0));
   CK(cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&r.p2p, cudaStreamNonBlocking));
   CK(cudaHostAlloc(&r.h_stage, kStageSlots * sizeof(uint64_t), cudaHostAllocMapped | cudaHostAllocPortable));
   memset(r.h_stage, 0, kStageSlots * sizeof(uint64_t));
   CK(cudaHostGetDevicePointer(&r.d_stage, r.h_stage, 0));
@@ -594,6 +600,10 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
 }
 
 uint64_t tagseq_key(int peer, int tag) { return ((uint64_t)(uint32_t)peer << 32) | (uint32_t)tag; }
+uint64_t idx_key(int dir, int peer, int tag, int sidx, int didx) {
+  return ((uint64_t)dir << 63) | ((uint64_t)(peer & 0x7fff) << 48) | ((uint64_t)(sidx & 0xff) << 40) |
+         ((uint64_t)(didx & 0xff) << 32) | (uint32_t)tag;
+}
 
 // check_args of proc_enqueue.cpp:8-20 (enqueue precedence: rank, tag, count).
 int check_args(const mpix_comm_s* c, int count, int peer, int tag, bool recv_side) {
@@ -615,7 +625,8 @@ struct Ticket {
   uint64_t gen;
 };
 
-Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remote) {
+Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remote,
+                  bool conventional) {
   uint64_t n = rs.req_next.fetch_add(1);
   uint64_t slot = n % kReqSlots;
   uint64_t gen = n / kReqSlots + 1;
@@ -625,6 +636,8 @@ Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remot
   ri.source = source;
   ri.tag = tag;
   ri.remote = remote;
+  ri.conventional = conventional;
+  ri.consumed = false;
   Ticket t;
   t.handle = ((uint64_t)(rs.rank + 1) << 48) | (n + 1);
   t.flag = rs.d_done + slot;
@@ -673,6 +686,18 @@ int acquire_staging(RankState& rs, uint64_t bytes, cudaStream_t s, uint8_t** p, 
 }
 
 // Point-to-point enqueue (send side and receive side).
+// How an operation reaches p2p_post: the enqueue family (the comm's stream),
+// conventional host-thread p2p (the rank's internal stream), or multiplex
+// stream p2p (the stream of local index sidx / didx).
+struct PostHow {
+  cudaStream_t stream = nullptr;
+  bool conventional = false;
+  int sidx = -2, didx = -2;  // IDX_NONE unless multiplex (types.hpp:14)
+};
+
+int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
+             bool is_recv, bool blocking, MPI_Request* req, const PostHow& how);
+
 int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
                 bool is_recv, bool blocking, MPI_Request* req) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
@@ -680,6 +705,82 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   if (!c->enqueue_ok) return MPIX_ERR_NOT_ENQUEUE_COMM;  // proc_enqueue.cpp:33-34
   int rc = check_args(c, count, peer, tag, is_recv);
   if (rc) return rc;
+  PostHow how;
+  how.stream = c->cu;
+  return p2p_post(c, buf, count, dt, peer, tag, is_recv, blocking, req, how);
+}
+
+// check_send_args / check_recv_args of proc_p2p.cpp:9-23 (conventional
+// precedence: rank, count, tag).
+int check_p2p_args(const mpix_comm_s* c, int count, int peer, int tag, bool recv_side) {
+  const int P = c->sh->P;
+  if (recv_side) {
+    if (peer != MPI_ANY_SOURCE && (peer < 0 || peer >= P)) return MPIX_ERR_INVALID_RANK;
+    if (count < 0) return MPIX_ERR_INVALID_COUNT;
+    if (tag != MPI_ANY_TAG && tag < 0) return MPIX_ERR_INVALID_TAG;
+  } else {
+    if (peer < 0 || peer >= P) return MPIX_ERR_INVALID_RANK;
+    if (count < 0) return MPIX_ERR_INVALID_COUNT;
+    if (tag < 0) return MPIX_ERR_INVALID_TAG;
+  }
+  return MPI_SUCCESS;
+}
+
+// Conventional p2p (Proc::isend/irecv, proc_p2p.cpp:96-113) on GPU buffers:
+// executed on the rank's internal stream, launched at once (no batching:
+// a posted conventional send must progress without a later MPI call).
+int conv_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
+              bool is_recv, bool blocking, MPI_Request* req) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!c) return MPIX_ERR_INVALID_COMM;
+  if (c->sh->multiplex) return MPIX_ERR_MULTIPLEX_COMM;
+  int rc = check_p2p_args(c, count, peer, tag, is_recv);
+  if (rc) return rc;
+  PostHow how;
+  how.stream = rank_of(c->rank).p2p;
+  how.conventional = true;
+  return p2p_post(c, buf, count, dt, peer, tag, is_recv, blocking, req, how);
+}
+
+// Multiplex stream p2p (Proc::stream_isend/irecv, proc_p2p.cpp:115-144):
+// runs on the CUDA stream of local stream src_idx (send) / dst_idx (recv),
+// or on the rank's internal stream when that MPIX stream is not a GPU stream.
+int stream_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
+                int src_idx, int dst_idx, bool is_recv, bool blocking, MPI_Request* req) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!c) return MPIX_ERR_INVALID_COMM;
+  if (!c->sh->multiplex) return MPIX_ERR_NOT_MULTIPLEX;
+  int rc = check_p2p_args(c, count, peer, tag, is_recv);
+  if (rc) return rc;
+  const auto& counts = c->sh->counts;
+  const int me = c->rank;
+  if (!is_recv) {
+    if (src_idx < 0 || src_idx >= counts[me]) return MPIX_ERR_INVALID_INDEX;
+    if (dst_idx < 0 || dst_idx >= counts[peer]) return MPIX_ERR_INVALID_INDEX;
+  } else {
+    if (dst_idx == MPIX_ANY_INDEX) return MPIX_ERR_WILDCARD_DST;
+    if (dst_idx < 0 || dst_idx >= counts[me]) return MPIX_ERR_INVALID_INDEX;
+    if (src_idx != MPIX_ANY_INDEX) {
+      if (src_idx < 0) return MPIX_ERR_INVALID_INDEX;
+      if (peer != MPI_ANY_SOURCE && src_idx >= counts[peer]) return MPIX_ERR_INVALID_INDEX;
+    }
+    // the index travels in the static key; a wildcard index would need the
+    // dynamic engine to filter on it (not implemented)
+    if (src_idx == MPIX_ANY_INDEX || c->sh->dyn) return MPIX_ERR_UNSUPPORTED;
+  }
+  if (!is_recv && c->sh->dyn) return MPIX_ERR_UNSUPPORTED;
+  const int local = is_recv ? dst_idx : src_idx;
+  mpix_stream_s* ls = c->local_streams[local];
+  PostHow how;
+  how.stream = ls && ls->kind == mpix_stream_s::cuda ? ls->cu : rank_of(me).p2p;
+  how.conventional = true;
+  how.sidx = src_idx;
+  how.didx = dst_idx;
+  return p2p_post(c, buf, count, dt, peer, tag, is_recv, blocking, req, how);
+}
+
+int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
+             bool is_recv, bool blocking, MPI_Request* req, const PostHow& how) {
   int esz = type_size(dt);
   if (!esz) return MPIX_ERR_TYPE;
   const bool dyn = c->sh->dyn;
@@ -693,6 +794,8 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   const int me = c->rank;
   RankState& rs = rank_of(me);
   const uint64_t bytes = (uint64_t)count * (uint64_t)esz;
+  const bool indexed = how.sidx >= 0;
+  std::lock_guard<std::mutex> clk(c->mu);
 
   P2PArgs a = {};
   a.is_recv = is_recv;
@@ -706,7 +809,8 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   uint32_t tseq;
   if (!is_recv) {
     const int d = peer;
-    tseq = c->send_tagseq[tagseq_key(d, tag)]++;
+    tseq = indexed ? c->idx_tagseq[idx_key(0, d, tag, how.sidx, how.didx)]++
+                   : c->send_tagseq[tagseq_key(d, tag)]++;
     a.pseq = c->send_pseq[d]++;
     a.post_ring = reinterpret_cast<SlotDesc*>(sh.base[d] + L.sr(me));
     a.post_mirror = reinterpret_cast<uint64_t*>(sh.base[me] + L.sr_free(d));
@@ -720,7 +824,8 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     a.mode = 0;
   } else {
     const int s = peer;
-    tseq = c->recv_tagseq[tagseq_key(s, tag)]++;
+    tseq = indexed ? c->idx_tagseq[idx_key(1, s, tag, how.sidx, how.didx)]++
+                   : c->recv_tagseq[tagseq_key(s, tag)]++;
     a.pseq = c->recv_pseq[s]++;
     a.post_ring = reinterpret_cast<SlotDesc*>(sh.base[s] + L.rr(me));
     a.post_mirror = reinterpret_cast<uint64_t*>(sh.base[me] + L.rr_free(s));
@@ -729,6 +834,9 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     a.mode = 0;
   }
   a.key = ((uint64_t)(uint32_t)tag << 32) | tseq;
+  if (indexed)  // multiplex: the stream indices are part of the match key (endpoint.hpp:26-32)
+    a.key = ((uint64_t)(uint32_t)tag << 32) | ((uint64_t)(how.sidx & 0xff) << 24) |
+            ((uint64_t)(how.didx & 0xff) << 16) | (tseq & 0xffff);
   if (dyn) {
     a.dyn = 1;
     a.P = sh.P;
@@ -741,10 +849,10 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   const bool sys = w.cfg.force_sys ||
                    (dyn ? c->any_remote : rank_of(peer).device != rs.device);
   CK(cudaSetDevice(rs.device));
-  cudaStream_t s = c->cu;
+  cudaStream_t s = how.stream;
   Ticket t{};
   if (!blocking || is_recv) {
-    t = new_ticket(rs, s, is_recv ? peer : me, tag, sys);
+    t = new_ticket(rs, s, is_recv ? peer : me, tag, sys, how.conventional);
     a.my_done = t.flag;
     a.my_gen = t.gen;
   }
@@ -770,7 +878,7 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   }
   bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
   bool post_only = false;
-  if (!inl && !blocking && peer == me && !dyn) {
+  if (!inl && !blocking && peer == me && !dyn && !how.conventional) {
     // Self-message whose counterpart has not been enqueued yet: it can only
     // be enqueued later on this same stream (an enqueue comm has one stream),
     // so it runs after this operation, which therefore only posts and never
@@ -784,8 +892,8 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
     a.rec = rs.d_rec + (op % kOpRecords);
     a.opid = op;
   }
-  if (!c->batch) c->batch = &batch_of(s, rs.device);  // one agent per comm
-  StreamBatch& b = *static_cast<StreamBatch*>(c->batch);
+  if (!c->batch && !how.conventional) c->batch = &batch_of(s, rs.device);
+  StreamBatch& b = how.conventional ? batch_of(s, rs.device) : *static_cast<StreamBatch*>(c->batch);
   std::lock_guard<std::mutex> lk(b.mu);
   if (w.cfg.batch && !a.trace) {
     // Join the stream's batch; a blocking operation closes it (it must have
@@ -838,7 +946,10 @@ int p2p_enqueue(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
       b.ops.push_back(pack_op(a, inl));
       b.sys |= sys;
     }
-    if (blocking && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
+    // a blocking operation closes the batch; conventional operations are
+    // launched at once
+    if ((blocking || how.conventional) && flush_locked(b, s, nullptr, 0, false, nullptr) < 0)
+      return MPIX_ERR_CUDA;
   } else {
     if (!b.ops.empty() && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -877,6 +988,8 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
     RankState& rs = rank_of(items[i].rank);
     auto& ri = rs.reqs[items[i].n % kReqSlots];
     cudaStream_t s = ri.gen == items[i].n / kReqSlots + 1 ? ri.stream : nullptr;
+    // a conventional request has no queue (proc_enqueue.cpp:124-126, Appendix A6)
+    if (ri.conventional) return MPIX_ERR_STREAM_MISMATCH;
     if (i == 0) {
       s0 = s;
       dev0 = rs.device;
@@ -932,6 +1045,80 @@ int reduce_op(MPI_Op op) {
 
 // Every enqueued collective: validate, fill the entry-barrier arguments,
 // order the stream's held operations first, launch.
+// MPI_Wait / MPI_Waitall on the host (Proc::wait/waitall, proc_p2p.cpp:
+// 146-181): a request may be waited once (consumed); the wait is a device
+// wait launched on the request's stream, then the host synchronises it.
+int host_waitall(int n, MPI_Request* reqs, MPI_Status* statuses) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (n < 0) return MPIX_ERR_INVALID_ARG;
+  if (n == 0) return MPI_SUCCESS;
+  if (!reqs) return MPIX_ERR_INVALID_REQUEST;
+  struct Item {
+    int rank;
+    uint64_t n;
+  };
+  std::vector<Item> items(n);
+  for (int i = 0; i < n; ++i) {
+    if (!decode_ticket(reqs[i], &items[i].rank, &items[i].n)) return MPIX_ERR_INVALID_REQUEST;
+    auto& ri = rank_of(items[i].rank).reqs[items[i].n % kReqSlots];
+    if (ri.gen != items[i].n / kReqSlots + 1 || ri.consumed) return MPIX_ERR_INVALID_REQUEST;
+  }
+  // group by stream: one device wait (and one synchronisation) per stream
+  std::map<cudaStream_t, std::vector<int>> by;
+  for (int i = 0; i < n; ++i) by[rank_of(items[i].rank).reqs[items[i].n % kReqSlots].stream].push_back(i);
+  for (auto& kv : by) {
+    cudaStream_t s = kv.first;
+    const int r0 = items[kv.second[0]].rank;
+    RankState& rs0 = rank_of(r0);
+    std::vector<WaitEntry> we;
+    bool sys = false;
+    for (int i : kv.second) {
+      RankState& rs = rank_of(items[i].rank);
+      uint64_t nn = items[i].n;
+      we.push_back({rs.d_done + (nn % kReqSlots), nn / kReqSlots + 1});
+      sys |= rs.reqs[nn % kReqSlots].remote;
+    }
+    CK(cudaSetDevice(rs0.device));
+    StreamBatch& b = batch_of(s, rs0.device);
+    {
+      std::lock_guard<std::mutex> lk(b.mu);
+      if (flush_locked(b, s, we.data(), (int)we.size(), sys, rs0.d_err) < 0) return MPIX_ERR_CUDA;
+    }
+    CK(cudaStreamSynchronize(s));
+  }
+  for (int i = 0; i < n; ++i) {
+    auto& ri = rank_of(items[i].rank).reqs[items[i].n % kReqSlots];
+    ri.consumed = true;
+    if (statuses) {
+      statuses[i].MPI_SOURCE = ri.source;
+      statuses[i].MPI_TAG = ri.tag;
+      statuses[i].MPI_ERROR = MPI_SUCCESS;
+      statuses[i].source_index = -2;
+      statuses[i].count_bytes = UINT64_MAX;
+      statuses[i].truncated = 0;
+    }
+    reqs[i] = MPI_REQUEST_NULL;
+  }
+  return MPI_SUCCESS;
+}
+
+// Blocking conventional / multiplex operation: post as a blocking device
+// operation (eager or staged send, waiting receive), then synchronise.
+int host_blocking(int rc, mpix_comm_s* c, cudaStream_t s, MPI_Status* status, int source, int tag) {
+  if (rc) return rc;
+  CK(cudaSetDevice(rank_of(c->rank).device));
+  CK(cudaStreamSynchronize(s));
+  if (status) {
+    status->MPI_SOURCE = source;
+    status->MPI_TAG = tag;
+    status->MPI_ERROR = MPI_SUCCESS;
+    status->source_index = -2;
+    status->count_bytes = UINT64_MAX;
+    status->truncated = 0;
+  }
+  return MPI_SUCCESS;
+}
+
 int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype dt, MPI_Op op,
                  int root, mpix_comm_s* c) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
@@ -1146,12 +1333,37 @@ int MPIX_World_init(int nranks, const int* devices) {
   sh->counts.assign(nranks, 1);
   sh->L = RegionLayout{nranks, w->cfg.ring_slots, w->cfg.eager_bytes};
   sh->base.assign(nranks, nullptr);
+  sh->dyn = w->cfg.dyn_match;
+  // The world comm carries conventional p2p (and the mixed mode of
+  // Appendix A7): every rank gets a region for it too.
+  for (int r = 0; r < nranks; ++r) {
+    RankState& rs = *w->ranks[r];
+    if (cudaSetDevice(rs.device) != cudaSuccess) return MPIX_ERR_CUDA;
+    uint8_t* region = nullptr;
+    if (cudaMallocFromPoolAsync((void**)&region, sh->L.total(), rs.pool, rs.aux) != cudaSuccess ||
+        cudaMemsetAsync(region, 0, sh->L.total(), rs.aux) != cudaSuccess)
+      return MPIX_ERR_CUDA;
+    sh->base[r] = region;
+  }
+  {
+    std::vector<uint64_t> bases(nranks);
+    for (int r = 0; r < nranks; ++r) bases[r] = (uint64_t)sh->base[r];
+    for (int r = 0; r < nranks; ++r) {
+      RankState& rs = *w->ranks[r];
+      cudaSetDevice(rs.device);
+      if (cudaMemcpyAsync(sh->base[r] + sh->L.bases(), bases.data(), 8ull * nranks,
+                          cudaMemcpyHostToDevice, rs.aux) != cudaSuccess ||
+          cudaStreamSynchronize(rs.aux) != cudaSuccess)
+        return MPIX_ERR_CUDA;
+    }
+  }
   for (int r = 0; r < nranks; ++r) {
     auto* c = new mpix_comm_s();
     c->sh = sh;
     c->rank = r;
     c->send_pseq.assign(nranks, 0);
     c->recv_pseq.assign(nranks, 0);
+    for (int q = 0; q < nranks; ++q) c->any_remote |= w->ranks[q]->device != w->ranks[r]->device;
     w->world_comms.push_back(c);
   }
   g_world = w.release();
@@ -1178,7 +1390,13 @@ int MPIX_World_finalize(void) {
     }
     delete c;
   }
-  for (auto* c : w->world_comms) delete c;
+  for (auto* c : w->world_comms) {
+    RankState& rs = *w->ranks[c->rank];
+    cudaSetDevice(rs.device);
+    if (c->sh->base[c->rank]) cudaFreeAsync(c->sh->base[c->rank], rs.aux);
+    c->sh->base[c->rank] = nullptr;
+    delete c;
+  }
   for (auto& rs : w->ranks) {
     cudaSetDevice(rs->device);
     for (auto& sb : rs->stage) cudaFreeAsync(sb.p, rs->aux);
@@ -1190,6 +1408,7 @@ int MPIX_World_finalize(void) {
     if (rs->d_trace) cudaFree(rs->d_trace);
     cudaFreeHost(rs->h_err);
     cudaStreamDestroy(rs->aux);
+    cudaStreamDestroy(rs->p2p);
     cudaFreeHost(rs->h_stage);
     if (rs->pool) cudaMemPoolDestroy(rs->pool);
   }
@@ -1470,6 +1689,73 @@ int MPIX_Wait_enqueue(MPI_Request* request, MPI_Status* status) {
 
 int MPIX_Waitall_enqueue(int count, MPI_Request requests[], MPI_Status statuses[]) {
   return waitall_enqueue(count, requests, statuses);
+}
+
+// --------------------------------------------------------------------------
+// Conventional p2p and multiplex stream p2p (host-thread semantics)
+// --------------------------------------------------------------------------
+int MPI_Isend(const void* buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+              MPI_Request* request) {
+  if (!request) return MPIX_ERR_INVALID_ARG;
+  return conv_post(comm, const_cast<void*>(buf), count, datatype, dest, tag, false, false, request);
+}
+
+int MPI_Irecv(void* buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+              MPI_Request* request) {
+  if (!request) return MPIX_ERR_INVALID_ARG;
+  return conv_post(comm, buf, count, datatype, source, tag, true, false, request);
+}
+
+int MPI_Send(const void* buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm) {
+  int rc = conv_post(comm, const_cast<void*>(buf), count, datatype, dest, tag, false, true, nullptr);
+  return rc ? rc : host_blocking(rc, comm, rank_of(comm->rank).p2p, nullptr, dest, tag);
+}
+
+int MPI_Recv(void* buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+             MPI_Status* status) {
+  int rc = conv_post(comm, buf, count, datatype, source, tag, true, true, nullptr);
+  return rc ? rc : host_blocking(rc, comm, rank_of(comm->rank).p2p, status, source, tag);
+}
+
+int MPI_Wait(MPI_Request* request, MPI_Status* status) {
+  if (!request) return MPIX_ERR_INVALID_REQUEST;
+  return host_waitall(1, request, status);
+}
+
+int MPI_Waitall(int count, MPI_Request requests[], MPI_Status statuses[]) {
+  return host_waitall(count, requests, statuses);
+}
+
+static cudaStream_t local_stream_of(MPI_Comm comm, int idx) {
+  mpix_stream_s* ls = comm->local_streams[idx];
+  return ls && ls->kind == mpix_stream_s::cuda ? ls->cu : rank_of(comm->rank).p2p;
+}
+
+int MPIX_Stream_isend(const void* buf, int count, MPI_Datatype datatype, int dest, int tag,
+                      MPI_Comm comm, int src_idx, int dst_idx, MPI_Request* request) {
+  if (!request) return MPIX_ERR_INVALID_ARG;
+  return stream_post(comm, const_cast<void*>(buf), count, datatype, dest, tag, src_idx, dst_idx,
+                     false, false, request);
+}
+
+int MPIX_Stream_irecv(void* buf, int count, MPI_Datatype datatype, int source, int tag,
+                      MPI_Comm comm, int src_idx, int dst_idx, MPI_Request* request) {
+  if (!request) return MPIX_ERR_INVALID_ARG;
+  return stream_post(comm, buf, count, datatype, source, tag, src_idx, dst_idx, true, false, request);
+}
+
+int MPIX_Stream_send(const void* buf, int count, MPI_Datatype datatype, int dest, int tag,
+                     MPI_Comm comm, int src_idx, int dst_idx) {
+  int rc = stream_post(comm, const_cast<void*>(buf), count, datatype, dest, tag, src_idx, dst_idx,
+                       false, true, nullptr);
+  return rc ? rc : host_blocking(rc, comm, local_stream_of(comm, src_idx), nullptr, dest, tag);
+}
+
+int MPIX_Stream_recv(void* buf, int count, MPI_Datatype datatype, int source, int tag,
+                     MPI_Comm comm, int src_idx, int dst_idx, MPI_Status* status) {
+  int rc = stream_post(comm, buf, count, datatype, source, tag, src_idx, dst_idx, true, true,
+                       nullptr);
+  return rc ? rc : host_blocking(rc, comm, local_stream_of(comm, dst_idx), status, source, tag);
 }
 
 int MPIX_Request_free(MPI_Request* request) {

@@ -27,6 +27,7 @@ MPI_BYTE, MPI_INT, MPI_DOUBLE, MPI_FLOAT, MPIX_BFLOAT16 = 1, 2, 3, 4, 5
 MPI_SUM, MPI_MAX, MPI_MIN = 1, 2, 3
 MPI_ANY_SOURCE = -1
 MPI_ANY_TAG = -1
+MPIX_ANY_INDEX = -1
 MPI_REQUEST_NULL = 0
 
 ERR_NAMES = [
@@ -120,6 +121,16 @@ def _declare(L: C.CDLL) -> None:
         "MPIX_Bcast_enqueue": (I, [P, I, I, I, P]),
         "MPIX_Allgather_enqueue": (I, [P, I, I, P, I, I, P]),
         "MPIX_Barrier_enqueue": (I, [P]),
+        "MPI_Send": (I, [P, I, I, I, I, P]),
+        "MPI_Recv": (I, [P, I, I, I, I, P, P]),
+        "MPI_Isend": (I, [P, I, I, I, I, P, C.POINTER(U64)]),
+        "MPI_Irecv": (I, [P, I, I, I, I, P, C.POINTER(U64)]),
+        "MPI_Wait": (I, [C.POINTER(U64), P]),
+        "MPI_Waitall": (I, [I, C.POINTER(U64), P]),
+        "MPIX_Stream_send": (I, [P, I, I, I, I, P, I, I]),
+        "MPIX_Stream_recv": (I, [P, I, I, I, I, P, I, I, P]),
+        "MPIX_Stream_isend": (I, [P, I, I, I, I, P, I, I, C.POINTER(U64)]),
+        "MPIX_Stream_irecv": (I, [P, I, I, I, I, P, I, I, C.POINTER(U64)]),
         "MPIX_Launch_count": (U64, []),
         "MPIX_Config_get": (I, [C.POINTER(U64), C.POINTER(I), C.POINTER(I), C.POINTER(U64)]),
         "MPIX_Comm_get_ctx": (I, [P, C.POINTER(U32)]),
@@ -426,10 +437,63 @@ class Comm:
     def barrier_enqueue(self) -> None:
         check(lib().MPIX_Barrier_enqueue(self.h), "MPIX_Barrier_enqueue")
 
+    # conventional (host-thread) p2p on GPU buffers ----------------------------
+    def send(self, buf, count: int, dt: int, dest: int, tag: int) -> None:
+        check(lib().MPI_Send(_ptr(buf), count, dt, dest, tag, self.h), "MPI_Send")
+
+    def recv(self, buf, count: int, dt: int, source: int, tag: int) -> None:
+        check(lib().MPI_Recv(_ptr(buf), count, dt, source, tag, self.h, None), "MPI_Recv")
+
+    def isend(self, buf, count: int, dt: int, dest: int, tag: int) -> Request:
+        r = C.c_uint64()
+        check(lib().MPI_Isend(_ptr(buf), count, dt, dest, tag, self.h, C.byref(r)), "MPI_Isend")
+        return Request(r.value)
+
+    def irecv(self, buf, count: int, dt: int, source: int, tag: int) -> Request:
+        r = C.c_uint64()
+        check(lib().MPI_Irecv(_ptr(buf), count, dt, source, tag, self.h, C.byref(r)), "MPI_Irecv")
+        return Request(r.value)
+
+    # multiplex stream p2p ----------------------------------
+    def stream_send(self, buf, count: int, dt: int, dest: int, tag: int, src_idx: int,
+                    dst_idx: int) -> None:
+        check(lib().MPIX_Stream_send(_ptr(buf), count, dt, dest, tag, self.h, src_idx, dst_idx),
+              "MPIX_Stream_send")
+
+    def stream_recv(self, buf, count: int, dt: int, source: int, tag: int, src_idx: int,
+                    dst_idx: int) -> None:
+        check(lib().MPIX_Stream_recv(_ptr(buf), count, dt, source, tag, self.h, src_idx, dst_idx,
+                                     None), "MPIX_Stream_recv")
+
+    def stream_isend(self, buf, count: int, dt: int, dest: int, tag: int, src_idx: int,
+                     dst_idx: int) -> Request:
+        r = C.c_uint64()
+        check(lib().MPIX_Stream_isend(_ptr(buf), count, dt, dest, tag, self.h, src_idx, dst_idx,
+                                      C.byref(r)), "MPIX_Stream_isend")
+        return Request(r.value)
+
+    def stream_irecv(self, buf, count: int, dt: int, source: int, tag: int, src_idx: int,
+                     dst_idx: int) -> Request:
+        r = C.c_uint64()
+        check(lib().MPIX_Stream_irecv(_ptr(buf), count, dt, source, tag, self.h, src_idx, dst_idx,
+                                      C.byref(r)), "MPIX_Stream_irecv")
+        return Request(r.value)
+
 
 def wait_enqueue(req: Request) -> None:
     h = C.c_uint64(req.h if req else 0)
     check(lib().MPIX_Wait_enqueue(C.byref(h), None), "MPIX_Wait_enqueue")
+
+
+def wait(req: Request) -> None:
+    """MPI_Wait (host): the request is consumed."""
+    h = C.c_uint64(req.h if req else 0)
+    check(lib().MPI_Wait(C.byref(h), None), "MPI_Wait")
+
+
+def waitall(reqs: Sequence[Optional[Request]]) -> None:
+    arr = (C.c_uint64 * max(1, len(reqs)))(*[(r.h if r else 0) for r in reqs])
+    check(lib().MPI_Waitall(len(reqs), arr, None), "MPI_Waitall")
 
 
 def waitall_enqueue(reqs: Sequence[Optional[Request]]) -> None:
