@@ -3,9 +3,8 @@ outcomes (tests/golden/enqueue_errors.json, produced by the compiled
 reference through oracle/ref_driver.cpp:199-315).
 
 Each case below is the reference probe's case k, issued through the C ABI
-of this library. Cases 1 and 4 exercise the reference's conventional
-(host-thread) p2p, which is not part of the enqueue path built here; they are
-checked against the oracle in tests/test_oracle.py instead.
+of this library (all 20; cases 1 and 4 go through the conventional
+host-thread p2p, MPI_Isend / MPI_Irecv on the world comm).
 """
 import json
 import os
@@ -38,6 +37,13 @@ def test_enqueue_error_codes_match_reference(monkeypatch):
         c0, c1 = ctx[0].comm, ctx[1].comm
         # 0: enqueue precedence rank -> tag -> count (proc_enqueue.cpp:8-20)
         got[0] = code_of(lambda: c0.send_enqueue(buf, -1, mpix.MPI_INT, 1, -1))
+        # 1: conventional p2p precedence rank -> count -> tag (proc_p2p.cpp:9-14)
+        got[1] = code_of(lambda: w.comm(0).isend(buf, -1, mpix.MPI_INT, 1, -1))
+        # 4: a conventional receive's request in an enqueue wait (no queue)
+        conv = w.comm(0).irecv(sink[32:], 4, mpix.MPI_INT, 1, 77)
+        got[4] = code_of(lambda: mpix.waitall_enqueue([conv]))
+        w.comm(1).send(buf, 4, mpix.MPI_INT, 0, 77)
+        mpix.wait(conv)
         # 2, 3: Waitall of nothing / of a null request (proc_enqueue.cpp:121-123)
         got[2] = code_of(lambda: mpix.waitall_enqueue([]))
         got[3] = code_of(lambda: mpix.waitall_enqueue([None]))
@@ -104,7 +110,7 @@ def test_enqueue_error_codes_match_reference(monkeypatch):
         assert int(sink[0]) == 0 and bool((sink[8:12] == 0).all())
     for k, name in got.items():
         assert name == GOLD[k], (k, name, GOLD[k])
-    assert sorted(got) == [0, 2, 3, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19]
+    assert sorted(got) == list(range(20))
 
 
 def test_wildcard_on_static_comm_is_unsupported(monkeypatch):
