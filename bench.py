@@ -365,6 +365,8 @@ def bench_world(args):
     }
     if not args.no_extras and P == 1:
         line["extras"] = extras(args, mpix, torch, w, ctx)
+    if not args.no_extras and P > 1:
+        line["extras"] = extras_ngpu(args, mpix, torch, w, ctx, dev)
     if rank0_cpu() and P == 1:  # the CPU baseline: rank 0 at N=1 only
         line["cpu_baseline"] = cpu_reference_selfmsg(S, args.cpu_seconds)
     sync()
@@ -454,6 +456,44 @@ def extras(args, mpix, torch, w, ctx):
     out["inloop_self_chain_us"] = dev / 1000 * 1e6
     out["inloop_self_chain_host_us"] = host / 1000 * 1e6
     out["inloop_self_chain_over_floor_us"] = (dev / 1000 - 4 * t_empty) * 1e6
+    return out
+
+
+def extras_ngpu(args, mpix, torch, w, ctx, dev):
+    """N > 1 (one rank per GPU): Allreduce_enqueue busbw over all N GPUs
+    (BASELINE cfg3 at N), and Send/Recv_enqueue ping-pong latency between
+    ranks 0 and 1 (cfg2 latency across NVLink)."""
+    out = {}
+    P = len(dev)
+    cs = [ctx[r][2] for r in range(P)]
+    ss = [ctx[r][0] for r in range(P)]
+    ar = {}
+    for name, tdt, mdt in (("f32", torch.float32, mpix.MPI_FLOAT), ("bf16", torch.bfloat16, mpix.MPIX_BFLOAT16)):
+        nbytes = 256 << 20
+        cnt = nbytes // torch.tensor([], dtype=tdt).element_size()
+        sb = [torch.ones(cnt, dtype=tdt, device=dev[r]) for r in range(P)]
+        rb = [torch.empty(cnt, dtype=tdt, device=dev[r]) for r in range(P)]
+        mpix.testing.allreduce_loop(cs, ss, dev, sb, rb, cnt, mdt, 2)
+        dev_s, _ = mpix.testing.allreduce_loop(cs, ss, dev, sb, rb, cnt, mdt, 10)
+        for d in set(dev):
+            torch.cuda.synchronize(d)
+        t = dev_s / 10
+        algbw = nbytes / t / 1e9
+        ar[name] = {"ms": t * 1e3, "algbw_GBps": algbw, "busbw_GBps": algbw * 2 * (P - 1) / P,
+                    "busbw_frac_of_770": algbw * 2 * (P - 1) / P / 770.0,
+                    "check": float(rb[0][0]) == float(P)}
+        del sb, rb
+    out["allreduce_256MiB"] = ar
+    pp = {}
+    for nb in (8, 4096, 65536, 1 << 20, 64 << 20):
+        b0 = torch.zeros(max(nb, 16), dtype=torch.uint8, device=dev[0])
+        b1 = torch.zeros(max(nb, 16), dtype=torch.uint8, device=dev[1])
+        iters = 200 if nb <= (1 << 20) else 20
+        mpix.testing.pingpong(cs[0], cs[1], b0, b1, nb, 10, ss[0], ss[1], dev[0], dev[1])
+        d, h = mpix.testing.pingpong(cs[0], cs[1], b0, b1, nb, iters, ss[0], ss[1], dev[0], dev[1])
+        pp[str(nb)] = {"half_rtt_us": d / (2 * iters) * 1e6,
+                       "GBps": nb / (d / (2 * iters)) / 1e9}
+    out["pingpong_rank0_rank1"] = pp
     return out
 
 

@@ -40,6 +40,11 @@ def gpu_world(P, devices=None, spread=False):
         yield w, ctxs
         for c in ctxs:
             c.stream.synchronize()
+        for d in set(devices):
+            torch.cuda.synchronize(d)
+        # no spinning kernel of this test gave up on its watchdog
+        errs = [mpix.rank_error(r) for r in range(P)]
+        assert not any(errs), f"device watchdog fired: rank error words {errs}"
     finally:
         for d in set(devices):
             torch.cuda.synchronize(d)

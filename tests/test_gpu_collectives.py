@@ -150,3 +150,35 @@ def test_collectives_error_codes():
         with pytest.raises(mpix.MPIXError) as e:
             w.comm(0).barrier_enqueue()
         assert e.value.name == "NOT_ENQUEUE_COMM"
+
+
+def test_collectives_system_scope(monkeypatch):
+    """The cross-GPU (system-scope) kernel instantiations, on one GPU
+    (MPIX_FORCE_SYS=1): every collective once, bit-exact."""
+    monkeypatch.setenv("MPIX_FORCE_SYS", "1")
+    P, rc = 4, 4097
+    with gpu_world(P) as (w, ctx):
+        ins = make_inputs(P, P * rc, "bf16", seed=99)
+        sb = [x.to(0) for x in ins]
+        red = [torch.zeros(P * rc, dtype=torch.bfloat16, device=0) for _ in range(P)]
+        rsb = [torch.zeros(rc, dtype=torch.bfloat16, device=0) for _ in range(P)]
+        bc = [sb[r].clone() for r in range(P)]
+        ag = [torch.zeros(P * P * rc, dtype=torch.bfloat16, device=0) for _ in range(P)]
+        torch.cuda.synchronize()
+
+        def body(r):
+            c = ctx[r].comm
+            c.reduce_enqueue(sb[r], red[r], P * rc, mpix.MPIX_BFLOAT16, mpix.MPI_SUM, 2)
+            c.reduce_scatter_block_enqueue(sb[r], rsb[r], rc, mpix.MPIX_BFLOAT16)
+            c.bcast_enqueue(bc[r], P * rc, mpix.MPIX_BFLOAT16, 3)
+            c.allgather_enqueue(sb[r], ag[r], P * rc, mpix.MPIX_BFLOAT16)
+            c.barrier_enqueue()
+
+        w.run_ranks(body)
+        sync_all(ctx)
+        full = oracle(ins, "bf16", mpix.MPI_SUM)
+        assert torch.equal(red[2].cpu(), full)
+        for r in range(P):
+            assert torch.equal(rsb[r].cpu(), full[r * rc:(r + 1) * rc])
+            assert torch.equal(bc[r].cpu(), ins[3])
+            assert torch.equal(ag[r].cpu(), torch.cat(ins))

@@ -181,3 +181,32 @@ def test_conventional_wildcard_receive_dynamic(monkeypatch):
 
         w.run_ranks(body)
         assert sorted(int(t[0]) for t in y) == [1, 2]
+
+
+def test_conventional_and_multiplex_system_scope(monkeypatch):
+    monkeypatch.setenv("MPIX_FORCE_SYS", "1")
+    n = 300_000
+    with gpu_world(2) as (w, ctx):
+        mux = {}
+
+        def mk(r):
+            mux[r] = w.comm(r).stream_comm_create_multiplex(
+                [mpix.Stream.from_cuda(mpix.testing.new_stream(0)) for _ in range(2)])
+
+        w.run_ranks(mk)
+        src = [rand_bytes(n, 40 + r) for r in range(2)]
+        dst = [torch.zeros(n, dtype=torch.uint8, device=0) for _ in range(2)]
+        dst2 = [torch.zeros(n, dtype=torch.uint8, device=0) for _ in range(2)]
+        torch.cuda.synchronize()
+
+        def body(r):
+            c = w.comm(r)
+            reqs = [c.irecv(dst[r], n, mpix.MPI_BYTE, 1 - r, 1), c.isend(src[r], n, mpix.MPI_BYTE, 1 - r, 1)]
+            reqs += [mux[r].stream_irecv(dst2[r], n, mpix.MPI_BYTE, 1 - r, 2, 0, 1),
+                     mux[r].stream_isend(src[r], n, mpix.MPI_BYTE, 1 - r, 2, 0, 1)]
+            mpix.waitall(reqs)
+
+        w.run_ranks(body)
+        for r in range(2):
+            assert torch.equal(dst[r].cpu(), src[1 - r].cpu())
+            assert torch.equal(dst2[r].cpu(), src[1 - r].cpu())
