@@ -275,9 +275,12 @@ struct Fin {
     if (p) { b_addr[nb] = (uint64_t)p; b_val[nb] = v; ++nb; }
   }
   template <bool SYS>
+  // One fence: the payload (written by the whole CTA or grid before this)
+  // and the slot frees must both be visible before any mirror or done word;
+  // nothing orders the frees against the payload (a freed slot is reused only
+  // after its mirror), so group A is stored before the fence.
   __device__ void run() const {
     using M = Scope<SYS>;
-    M::fence_ar();
     for (uint32_t k = 0; k < na; ++k) M::st_rlx(reinterpret_cast<uint64_t*>(a_addr[k]), a_val[k]);
     M::fence_ar();
     for (uint32_t k = 0; k < nb; ++k) M::st_rlx(reinterpret_cast<uint64_t*>(b_addr[k]), b_val[k]);
@@ -313,10 +316,10 @@ __device__ void post_desc(const P2PArgs& a, uint64_t addr, uint64_t bytes, uint6
 }
 
 template <bool SYS>
-__device__ bool wait_post_slot(const P2PArgs& a) {
+__device__ bool wait_post_slot(const P2PArgs& a, uint64_t prefetched = 0) {
   const int slot = (int)(a.pseq % (uint64_t)a.R);
   uint64_t need = a.pseq >= (uint64_t)a.R ? a.pseq - a.R + 1 : 0;
-  if (need == 0) return true;
+  if (need == 0 || prefetched >= need) return true;
   return spin_ge<SYS>(&a.post_mirror[slot], need, a.err_word, a.spin_limit_ns, ERRW_WAIT_SLOT);
 }
 
@@ -783,6 +786,11 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   const int lane = threadIdx.x & 31;
   __shared__ int s_phase;  // 0 decided, 1 eager copy then post, 2 posted, 3 claim staging
   if (warp == 0) {
+    // the free-mirror of my post slot, loaded alongside the ring scan (one
+    // round trip instead of two in steady state, pseq >= R)
+    uint64_t pre = 0;
+    if (lane == 0 && a.pseq >= (uint64_t)a.R)
+      pre = M::ld_acq(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)]);
     Snap sn;
     int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
     if (lane == 0) {
@@ -799,11 +807,11 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
         if (j >= 0) {
           // receive already posted: push (my slot is skipped, but only after
           // its previous occupant retired, so its mirror stays monotonic)
-          if (wait_post_slot<SYS>(a)) send_win(a, dc, j, sn, false, a.buf);
+          if (wait_post_slot<SYS>(a, pre)) send_win(a, dc, j, sn, false, a.buf);
         } else if (a.mode == MODE_STAGED) {
           dc.action = ACT_STAGE;
           if (!dc.stage_ptr) s_phase = 3;
-        } else if (wait_post_slot<SYS>(a)) {
+        } else if (wait_post_slot<SYS>(a, pre)) {
           if (a.mode == MODE_EAGER) {
             s_phase = 1;
           } else {  // MODE_ISEND: publish the user buffer
@@ -814,14 +822,14 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
       } else {
         if (j >= 0) {
           uint64_t want = st_word(sn.state >> 8, ST_POSTED);
-          if (!wait_post_slot<SYS>(a)) {
+          if (!wait_post_slot<SYS>(a, pre)) {
             // watchdog: leave the send descriptor for nobody
           } else if (M::cas(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN)) == want) {
             recv_win(a, dc, j, sn, false);
           } else if (a.err_word) {
             ScopeSys::st_rlx(a.err_word, ERRW_PROTOCOL);  // nobody else may take it
           }
-        } else if (wait_post_slot<SYS>(a)) {
+        } else if (wait_post_slot<SYS>(a, pre)) {
           post_desc<SYS>(a, (uint64_t)a.buf, a.bytes, (uint64_t)a.my_done, a.my_gen, false);
           s_phase = 2;
         }
