@@ -270,8 +270,9 @@ int MPI_Waitall(int count, MPI_Request requests[], MPI_Status statuses[]);
  * MPIX_ANY_INDEX destination). The operation runs on the CUDA stream of
  * local stream src_idx (send) / dst_idx (receive), or on the rank's internal
  * stream if that MPIX stream is not a GPU stream; the stream indices are
- * part of the match. v1: MPIX_ANY_INDEX sources and dynamic-matching comms
- * give UNSUPPORTED. The blocking forms synchronise that stream. */
+ * part of the match. MPIX_ANY_INDEX sources need a dynamic-matching comm
+ * (UNSUPPORTED on a static one). The blocking forms synchronise that
+ * stream. */
 int MPIX_Stream_send(const void *buf, int count, MPI_Datatype datatype, int dest, int tag,
                      MPI_Comm comm, int src_idx, int dst_idx);
 int MPIX_Stream_recv(void *buf, int count, MPI_Datatype datatype, int source, int tag,

@@ -24,7 +24,7 @@ namespace mpix {
 
 constexpr int kThreads = 512;          // threads per CTA for every op kernel
 constexpr int kMaxCollRanks = 16;      // max communicator size for Allreduce
-constexpr uint64_t kOpRecords = 16384; // op-record ring entries per rank
+constexpr uint64_t kOpRecords = 65536; // op-record ring entries per rank (32 MiB; bounds in-flight large ops)
 
 enum : uint64_t { ST_FREE = 0, ST_POSTED = 1, ST_TAKEN = 2 };
 
@@ -176,6 +176,7 @@ struct P2PArgs {
   // dynamic matching (dyn = 1): pseq is the receive ticket on the receive
   // side; peer / tag may be -1 (ANY_SOURCE / ANY_TAG) on receives
   int dyn, P, me, peer, tag;
+  int sidx, didx;         // multiplex stream indices (-2 none, -1 ANY source index)
   uint64_t* bases;        // region bases of the comm's members (in my region)
   // paired self-message (host-matched in a batch): this receive also carries
   // its send; no descriptors, only both ring slots' retirement and the copy
@@ -239,7 +240,9 @@ struct BatchOp {
   uint32_t E;
   int32_t peer, tag;      // dynamic matching (-1 = ANY on receives)
   uint16_t R, P, me;
-  uint8_t is_recv, mode, blocking, inl, early, dyn, paired, pad_[7];
+  uint8_t is_recv, mode, blocking, inl, early, dyn, paired;
+  int8_t sidx, didx;      // multiplex stream indices (-2 none, -1 ANY)
+  uint8_t pad_[5];
 };
 static_assert(sizeof(BatchOp) == 200, "BatchOp packing");
 

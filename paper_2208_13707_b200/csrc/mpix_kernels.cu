@@ -470,6 +470,16 @@ __device__ __forceinline__ void warp_argmin(uint64_t& v, int& idx) {
 
 __device__ __forceinline__ bool tag_ok(int32_t want, int32_t have) { return want < 0 || want == have; }
 
+// Multiplex stream indices in the dynamic engine (endpoint.hpp:26-32): a
+// send descriptor carries (src_idx, dst_idx) in key bits 24..31 / 16..23, a
+// posted receive its (src_idx filter, dst_idx) in pad[0]; encoded idx + 2
+// (-2 = none, -1 = ANY source index).
+__device__ __forceinline__ uint64_t idx_enc(int idx) { return (uint64_t)((idx + 2) & 0xff); }
+__device__ __forceinline__ bool idx_ok(uint64_t want_src, uint64_t want_dst, uint64_t have_src,
+                                       uint64_t have_dst) {
+  return want_dst == have_dst && (want_src == 1 /* ANY */ || want_src == have_src);
+}
+
 // Receive side (warp 0, lock held): the earliest-arrived POSTED send
 // descriptor from an acceptable source with an acceptable tag. Returns the
 // source (or -1) and the slot; every lane gets the result.
@@ -484,7 +494,8 @@ __device__ int dyn_scan_sends(const P2PArgs& a, uint8_t* my_base, const RegionLa
     for (int i = lane; i < a.R; i += 32) {
       uint64_t st, key;
       ld_pair<SYS>(&ring[i], st, key);
-      if ((st & 0xff) == ST_POSTED && tag_ok(a.tag, (int32_t)(key >> 32))) {
+      if ((st & 0xff) == ST_POSTED && tag_ok(a.tag, (int32_t)(key >> 32)) &&
+          idx_ok(idx_enc(a.sidx), idx_enc(a.didx), (key >> 24) & 0xff, (key >> 16) & 0xff)) {
         uint64_t arr = Scope<SYS>::ld_rlx(&ring[i].pad[0]);
         if (arr < best) {
           best = arr;
@@ -510,7 +521,11 @@ __device__ int dyn_scan_recvs(const P2PArgs& a, SlotDesc* pq) {
     uint64_t st, key;
     ld_pair<SYS>(&pq[i], st, key);
     const int32_t src = (int32_t)(key >> 32), tg = (int32_t)(uint32_t)key;
-    if ((st & 0xff) == ST_POSTED && (src < 0 || src == a.me) && tag_ok(tg, a.tag)) {
+    if ((st & 0xff) == ST_POSTED && (src < 0 || src == a.me) && tag_ok(tg, a.tag) &&
+        [&] {
+          const uint64_t f = Scope<SYS>::ld_rlx(&pq[i].pad[0]);
+          return idx_ok((f >> 8) & 0xff, f & 0xff, idx_enc(a.sidx), idx_enc(a.didx));
+        }()) {
       const uint64_t rseq = st >> 8;
       if (rseq < best) {
         best = rseq;
@@ -557,7 +572,8 @@ __device__ void dyn_send_post(const P2PArgs& a, const Dom& D, uint64_t addr, uin
   SlotDesc* d = &a.post_ring[slot];
   const uint64_t arr = M::ld_rlx(D.arrival);
   M::st_rlx(D.arrival, arr + 1);
-  M::st_rlx(&d->key, ((uint64_t)(uint32_t)a.tag << 32) | (eager ? 1u : 0u));
+  M::st_rlx(&d->key, ((uint64_t)(uint32_t)a.tag << 32) | (idx_enc(a.sidx) << 24) |
+                         (idx_enc(a.didx) << 16) | (eager ? 1u : 0u));
   M::st_rlx(&d->addr, addr);
   M::st_rlx(&d->bytes, a.bytes);
   M::st_rlx(&d->done_addr, done_addr);
@@ -688,6 +704,7 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
         } else {
           SlotDesc* e = &D.pq[qslot];
           M::st_rlx(&e->key, ((uint64_t)(uint32_t)a.peer << 32) | (uint32_t)a.tag);
+          M::st_rlx(&e->pad[0], (idx_enc(a.sidx) << 8) | idx_enc(a.didx));
           M::st_rlx(&e->addr, (uint64_t)a.buf);
           M::st_rlx(&e->bytes, a.bytes);
           M::st_rlx(&e->done_addr, (uint64_t)a.my_done);
@@ -1107,6 +1124,8 @@ __device__ void load_op(const BatchOp& o, uint64_t spin_limit_ns, P2PArgs& a) {
   a.me = o.me;
   a.peer = o.peer;
   a.tag = o.tag;
+  a.sidx = o.sidx;
+  a.didx = o.didx;
   a.bases = o.bases;
 }
 

@@ -101,6 +101,8 @@ BatchOp pack_op(const P2PArgs& a, bool inl) {
   o.P = (uint16_t)a.P;
   o.me = (uint16_t)a.me;
   o.dyn = (uint8_t)a.dyn;
+  o.sidx = (int8_t)a.sidx;
+  o.didx = (int8_t)a.didx;
   o.is_recv = (uint8_t)a.is_recv;
   o.mode = (uint8_t)a.mode;
   o.blocking = (uint8_t)a.blocking;
@@ -274,11 +276,10 @@ int stream_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
       if (src_idx < 0) return MPIX_ERR_INVALID_INDEX;
       if (peer != MPI_ANY_SOURCE && src_idx >= counts[peer]) return MPIX_ERR_INVALID_INDEX;
     }
-    // the index travels in the static key; a wildcard index would need the
-    // dynamic engine to filter on it (not implemented)
-    if (src_idx == MPIX_ANY_INDEX || c->sh->dyn) return MPIX_ERR_UNSUPPORTED;
+    // a wildcard index needs the dynamic engine (it filters on the indices);
+    // the static key carries concrete ones
+    if (src_idx == MPIX_ANY_INDEX && !c->sh->dyn) return MPIX_ERR_UNSUPPORTED;
   }
-  if (!is_recv && c->sh->dyn) return MPIX_ERR_UNSUPPORTED;
   const int local = is_recv ? dst_idx : src_idx;
   mpix_stream_s* ls = c->local_streams[local];
   PostHow how;
@@ -304,7 +305,7 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   const int me = c->rank;
   RankState& rs = rank_of(me);
   const uint64_t bytes = (uint64_t)count * (uint64_t)esz;
-  const bool indexed = how.sidx >= 0;
+  const bool indexed = how.sidx != -2;  // IDX_NONE (types.hpp:14) outside multiplex
   std::lock_guard<std::mutex> clk(c->mu);
 
   P2PArgs a = {};
@@ -353,6 +354,8 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
     a.me = me;
     a.peer = peer;  // -1 = ANY_SOURCE (receives)
     a.tag = tag;    // -1 = ANY_TAG (receives)
+    a.sidx = how.sidx;
+    a.didx = how.didx;
     a.bases = reinterpret_cast<uint64_t*>(sh.base[me] + L.bases());
   }
 

@@ -210,3 +210,58 @@ def test_conventional_and_multiplex_system_scope(monkeypatch):
         for r in range(2):
             assert torch.equal(dst[r].cpu(), src[1 - r].cpu())
             assert torch.equal(dst2[r].cpu(), src[1 - r].cpu())
+
+
+@pytest.mark.parametrize("matching", ["static", "dynamic"])
+def test_multiplex_indices_under_both_matching_modes(matching, monkeypatch):
+    """The (src_idx, dst_idx) selection holds in both engines; MPIX_ANY_INDEX
+    sources need the dynamic engine (UNSUPPORTED on a static comm)."""
+    monkeypatch.setenv("MPIX_MATCHING", matching)
+    n = 2048
+    with gpu_world(2) as (w, ctx):
+        mux = {}
+
+        def mk(r):
+            mux[r] = w.comm(r).stream_comm_create_multiplex(
+                [mpix.Stream.from_cuda(mpix.testing.new_stream(0)) for _ in range(2)])
+
+        w.run_ranks(mk)
+        src = {(i, j): rand_bytes(n, 200 + 2 * i + j) for i in range(2) for j in range(2)}
+        dst = {(i, j): torch.zeros(n, dtype=torch.uint8, device=0) for i in range(2) for j in range(2)}
+        torch.cuda.synchronize()
+
+        def body(r):
+            c = mux[r]
+            if r == 0:
+                reqs = [c.stream_isend(src[(i, j)], n, mpix.MPI_BYTE, 1, 4, i, j)
+                        for i in range(2) for j in range(2)]
+            else:
+                reqs = [c.stream_irecv(dst[(i, j)], n, mpix.MPI_BYTE, 0, 4, i, j)
+                        for j in range(2) for i in reversed(range(2))]
+            mpix.waitall(reqs)
+
+        w.run_ranks(body)
+        for k in src:
+            assert torch.equal(dst[k].cpu(), src[k].cpu()), k
+        t = torch.zeros(n, dtype=torch.uint8, device=0)
+        if matching == "static":
+            assert err(lambda: mux[1].stream_irecv(t, n, mpix.MPI_BYTE, 0, 4, mpix.MPIX_ANY_INDEX, 0)) \
+                == "UNSUPPORTED"
+            return
+        # ANY_INDEX: two receives on dst_idx 0 take the sends from src_idx 1 and 0
+        any_dst = [torch.zeros(n, dtype=torch.uint8, device=0) for _ in range(2)]
+        torch.cuda.synchronize()
+
+        def body2(r):
+            c = mux[r]
+            if r == 0:
+                reqs = [c.stream_isend(src[(i, 0)], n, mpix.MPI_BYTE, 1, 5, i, 0) for i in (1, 0)]
+            else:
+                reqs = [c.stream_irecv(any_dst[k], n, mpix.MPI_BYTE, 0, 5, mpix.MPIX_ANY_INDEX, 0)
+                        for k in range(2)]
+            mpix.waitall(reqs)
+
+        w.run_ranks(body2)
+        got = sorted(bytes(x.cpu().numpy()[:4]) for x in any_dst)
+        exp = sorted(bytes(src[(i, 0)].cpu().numpy()[:4]) for i in range(2))
+        assert got == exp
