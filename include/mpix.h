@@ -296,7 +296,8 @@ int MPIX_Allreduce_enqueue(const void *sendbuf, void *recvbuf, int count,
  * rank-ordered (bit-exact with oracle/streamix_oracle.c orc_allreduce_*).
  * Reduce: the result lands in the root's recvbuf; sendbuf may be
  * MPI_IN_PLACE at the root. Reduce_scatter_block: rank r receives the fold
- * of block r (recvcount elements) of every sendbuf (not in place).
+ * of block r (recvcount elements) of every sendbuf; MPI_IN_PLACE takes the
+ * P blocks from recvbuf and leaves the result in its first block.
  * Bcast: the root's buffer is copied into every other member's buffer.
  * Allgather: block q of every recvbuf = member q's sendbuf (MPI_IN_PLACE:
  * my block is already in place). Barrier: entry + exit barrier only. */

@@ -63,9 +63,11 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
       }
       break;
     case CK_REDUCE_SCATTER:
-      // in place would fold chunk me of my buffer while writing its start
-      if (sbuf == MPI_IN_PLACE) return MPIX_ERR_UNSUPPORTED;
       if (!rbuf) return MPIX_ERR_INVALID_ARG;
+      // In place the input is recvbuf (P blocks) and the result goes to its
+      // first block, which rank 0 is still reading: fold into my own block
+      // (read by nobody else) and move it to the front after the exit barrier.
+      if (sbuf == MPI_IN_PLACE) sbuf = rbuf;
       break;
     case CK_BCAST:
       sbuf = rbuf;  // one buffer: the root's is the source
@@ -91,8 +93,12 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
   a.P = P;
   a.me = me;
   a.epoch = ++c->coll_epoch;
-  a.algo = (bytes <= g_world->cfg.oneshot_max || P <= 2) ? AR_ONESHOT : AR_TWOSHOT;
+  // two-shot moves fewer bytes than one-shot for every P > 1 (per rank: 2S/P·(P-1) peer
+  // traffic + 2S/P local vs (P-1)·S peer + 2S local), so one-shot only where latency rules
+  a.algo = bytes <= g_world->cfg.oneshot_max ? AR_ONESHOT : AR_TWOSHOT;
   a.chunk_bytes = bytes;  // ALLGATHER: per rank; REDUCE_SCATTER: my block; BCAST: the buffer
+  const bool rsb_in_place = kind == CK_REDUCE_SCATTER && sbuf == rbuf;
+  if (rsb_in_place) a.rbuf = static_cast<uint8_t*>(rbuf) + (uint64_t)me * bytes;
   const RegionLayout& L = sh.L;
   for (int q = 0; q < P; ++q) {
     a.peer_in[q] = reinterpret_cast<CollSlot*>(sh.base[q] + L.coll_in(me));
@@ -129,6 +135,10 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
     else if (kind == CK_ALLGATHER)
       grid = (uint64_t)P * p2p_copy_grid(bytes);
     nk = launch_collective(a, sys, grid, c->cu);
+    if (nk >= 0 && rsb_in_place && me != 0 && bytes) {
+      if (cudaMemcpyAsync(rbuf, a.rbuf, bytes, cudaMemcpyDeviceToDevice, c->cu) != cudaSuccess)
+        return MPIX_ERR_CUDA;
+    }
   }
   if (nk < 0) return MPIX_ERR_CUDA;
   g_launches.fetch_add(nk);

@@ -142,9 +142,6 @@ def test_collectives_error_codes():
             c.bcast_enqueue(t, 8, mpix.MPI_FLOAT, 2)
         assert e.value.name == "INVALID_RANK"
         with pytest.raises(mpix.MPIXError) as e:
-            c.reduce_scatter_block_enqueue("in_place", t, 4, mpix.MPI_FLOAT)
-        assert e.value.name == "UNSUPPORTED"
-        with pytest.raises(mpix.MPIXError) as e:
             c.reduce_enqueue(t, t, -1, mpix.MPI_FLOAT)
         assert e.value.name == "INVALID_COUNT"
         with pytest.raises(mpix.MPIXError) as e:
@@ -182,3 +179,18 @@ def test_collectives_system_scope(monkeypatch):
             assert torch.equal(rsb[r].cpu(), full[r * rc:(r + 1) * rc])
             assert torch.equal(bc[r].cpu(), ins[3])
             assert torch.equal(ag[r].cpu(), torch.cat(ins))
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_reduce_scatter_block_in_place(P):
+    rc = 10007
+    with gpu_world(P) as (w, ctx):
+        ins = make_inputs(P, P * rc, "f32", seed=P + 3)
+        bufs = [x.to(0).clone() for x in ins]
+        torch.cuda.synchronize()
+        w.run_ranks(lambda r: ctx[r].comm.reduce_scatter_block_enqueue("in_place", bufs[r], rc,
+                                                                       mpix.MPI_FLOAT))
+        sync_all(ctx)
+        full = oracle(ins, "f32", mpix.MPI_SUM)
+        for r in range(P):
+            assert torch.equal(bufs[r][:rc].cpu(), full[r * rc:(r + 1) * rc]), r
