@@ -193,8 +193,21 @@ def run_reference(args):
 def run_mpix(args):
     rank, world, local = dist_env()
     if world > 1:
+        import torch
         import torch.distributed as dist
         dist.init_process_group("gloo")
+        # Normally rank 0 sees all N GPUs and hosts the N-GPU world (the
+        # reference's World/run_ranks model); if the launcher hides GPUs from
+        # each process, every rank instead runs an independent one-GPU
+        # replica of the N=1 step and the job time is the max over ranks.
+        flag = torch.tensor([1 if torch.cuda.device_count() >= args.gpus or args.share_gpus else 0])
+        dist.broadcast(flag, 0)
+        if not int(flag[0]):
+            line = bench_replica(args, rank, world, local)
+            dist.destroy_process_group()
+            if rank == 0:
+                print(json.dumps(line))
+            return
         if rank != 0:
             dist.barrier()  # rank 0 hosts the N-GPU world
             dist.barrier()
@@ -209,6 +222,85 @@ def run_mpix(args):
             dist.barrier()
             dist.destroy_process_group()
     print(json.dumps(line))
+
+
+def bench_replica(args, rank, world, local):
+    """Replicas: each torchrun rank runs the N=1 loopback step on its own
+    visible GPU (no data-path exchange), barrier + synchronize around K
+    steps, device time max-reduced over ranks (gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2208_13707_b200 import mpix
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    S = args.size
+    w = mpix.World(1, [dev])
+    s = mpix.testing.new_stream(dev)
+    c = w.comm(0).stream_comm_create(mpix.Stream.from_cuda(s))
+    src = torch.empty(S, dtype=torch.uint8, device=dev)
+    dst = torch.zeros(S, dtype=torch.uint8, device=dev)
+    mpix.testing.fill_pattern(src, S, 1234 + rank, 0, s)
+    torch.cuda.synchronize(dev)
+    mpix.testing.loopback(c, src, dst, S, max(3, args.warmup), s)
+    torch.cuda.synchronize(dev)
+    assert torch.equal(src, dst), "payload mismatch"
+    dist.barrier()
+    l0 = mpix.launch_count()
+    dev_s, _ = mpix.testing.loopback(c, src, dst, S, args.steps, s)
+    launches = mpix.launch_count() - l0
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t = torch.tensor([dev_s], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_step = float(t[0]) / args.steps
+    clocks = ClockSampler(dev)
+    clocks.start()
+    mpix.testing.copy_timing(True)
+    mpix.testing.loopback(c, src, dst, S, args.steps, s)
+    torch.cuda.synchronize(dev)
+    tot_ms, ncopy = mpix.testing.copy_timing_read()
+    mpix.testing.copy_timing(False)
+    clk = clocks.stop()
+    k_ms = tot_ms / max(ncopy, 1)
+    peak = peaks().get("hbm_gbs", 6650.0)
+    achieved = 2 * S / (k_ms / 1e3) / 1e9
+    # e2e: pinned host input -> H2D -> loopback -> checksum -> 8-byte D2H
+    host = torch.empty(S, dtype=torch.uint8, pin_memory=True)
+    host.copy_(src.cpu())
+    csum = torch.zeros(1, dtype=torch.int64, device=dev)
+    hsum = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        with torch.cuda.stream(s):
+            src.copy_(host, non_blocking=True)
+        mpix.testing.loopback(c, src, dst, S, 1, s)
+        mpix.testing.checksum(dst, S, csum, s)
+        with torch.cuda.stream(s):
+            hsum.copy_(csum, non_blocking=True)
+        s.synchronize()
+    e2e_t = time.perf_counter() - t0
+    e2e_v = torch.tensor([S * args.steps / e2e_t / 1e9], dtype=torch.float64)
+    dist.all_reduce(e2e_v, op=dist.ReduceOp.SUM)
+    w.finalize()
+    return {
+        "metric": METRIC, "value": S * world / t_step / 1e9, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": "replicas only: each GPU runs the N=1 loopback step (GPUs not all "
+                               "visible to one process, so no NVLink exchange)",
+                   "message_bytes": S, "parallelism": f"{world} replicas",
+                   "l2": "inputs larger than L2"},
+        "roofline": {"bound": "hbm", "unit": "GB/s", "achieved": achieved, "peak": peak,
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "mpix::k_gcopy (rank 0's replica)", "kernel_ms": k_ms},
+        "e2e": {"value": float(e2e_v[0]), "unit": "GB/s", "h2d_bytes_per_step": S * world,
+                "d2h_bytes_per_step": 8 * world,
+                "timing": "host wall clock per replica, summed; stream synchronised every step"},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
 
 
 def bench_world(args):
