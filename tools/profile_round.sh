@@ -29,4 +29,8 @@ $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
   --log-file "$OUT/launches_reduce_only.csv" python tools/profile_allreduce.py --P 4 --reduce-only --iters 3 > /dev/null 2>&1
 ncu -i "$OUT/k_ar_reduce.ncu-rep" --page raw --csv > "$OUT/k_ar_reduce_raw.csv" 2>/dev/null
 ncu -i "$OUT/k_ar_reduce.ncu-rep" --page details --csv > "$OUT/k_ar_reduce_details.csv" 2>/dev/null
+# keep the CSV exports only: the reports would overflow gpurun_out's 64 MiB
+for rep in "$OUT"/k_gcopy.ncu-rep "$OUT"/k_batch.ncu-rep "$OUT"/k_ar_reduce.ncu-rep; do
+  [ -f "$rep" ] && mv "$rep" /tmp/
+done
 ls -la "$OUT"
