@@ -290,6 +290,33 @@ int MPIX_Request_free(MPI_Request *request);
 int MPIX_Allreduce_enqueue(const void *sendbuf, void *recvbuf, int count,
                            MPI_Datatype datatype, MPI_Op op, MPI_Comm comm);
 
+/* ------------------------------------------------------------------------ */
+/* Symmetric heap for one-process-per-GPU use (csrc/mpix_heap.cpp). Every    */
+/* process reserves the same virtual range and maps each rank's slice at     */
+/* base + rank * slice, so heap pointers are valid in every process. The     */
+/* caller exchanges the POSIX file descriptors (e.g. SCM_RIGHTS over a Unix  */
+/* socket): rank 0 creates with base_hint 0, the others pass rank 0's base.  */
+/* MPIX_Alloc_mem returns heap memory (cudaMalloc without a heap).           */
+/* ------------------------------------------------------------------------ */
+/* Multi-process world: this process hosts rank `rank` of `nranks`
+ * (devices[q] = rank q's GPU). Collective host steps (communicator creation,
+ * barrier, free) call `allgather(in, bytes, out, ctx)`, which must gather
+ * `bytes` from every rank into out[rank * bytes] (e.g. torch.distributed over
+ * gloo) and return 0. The symmetric heap must already exist and be attached;
+ * enqueue receive buffers, Isend buffers and collective buffers must be heap
+ * memory (MPIX_Alloc_mem), everything else is unchanged. */
+typedef int (*MPIX_Allgather_fn)(const void *in, uint64_t bytes, void *out, void *ctx);
+int MPIX_World_init_mp(int rank, int nranks, const int *devices, MPIX_Allgather_fn allgather,
+                       void *ctx);
+int MPIX_World_local_rank(int *rank);
+int MPIX_Heap_create(int rank, int nranks, int device, uint64_t bytes_per_rank, uint64_t base_hint,
+                     uint64_t *base_out, uint64_t *slice_out, int *fd_out);
+int MPIX_Heap_attach(int peer, int fd);
+int MPIX_Heap_contains(const void *ptr, uint64_t bytes);
+int MPIX_Heap_destroy(void);
+int MPIX_Alloc_mem(uint64_t bytes, void **ptr);
+int MPIX_Free_mem(void *ptr);
+
 /* More enqueued collectives ("The enqueue APIs can be
  * extended to collectives"; no reference implementation). Same entry/exit
  * barrier as MPIX_Allreduce_enqueue, same stream-order semantics; folds are

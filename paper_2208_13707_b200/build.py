@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmpix.so")
-SOURCES = ["mpix_runtime.cpp", "mpix_p2p.cpp", "mpix_coll.cpp", "mpix_kernels.cu",
+SOURCES = ["mpix_runtime.cpp", "mpix_p2p.cpp", "mpix_coll.cpp", "mpix_heap.cpp", "mpix_kernels.cu",
            "mpix_testing.cu", "mpix_drivers.cpp"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 

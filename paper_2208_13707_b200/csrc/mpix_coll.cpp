@@ -80,6 +80,13 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
       break;
   }
   RankState& rs = rank_of(me);
+  // Multi-process mode: peers read send buffers and write receive buffers.
+  {
+    const uint64_t sb_bytes = kind == CK_REDUCE_SCATTER ? bytes * P : bytes;
+    const uint64_t rb_bytes = kind == CK_ALLGATHER ? bytes * P : bytes;
+    if ((sbuf && !peer_ok(sbuf, sb_bytes)) || (rbuf && !peer_ok(rbuf, rb_bytes)))
+      return MPIX_ERR_INVALID_ARG;
+  }
 
   ARArgs a = {};
   a.kind = kind;

@@ -306,6 +306,12 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   RankState& rs = rank_of(me);
   const uint64_t bytes = (uint64_t)count * (uint64_t)esz;
   const bool indexed = how.sidx != -2;  // IDX_NONE (types.hpp:14) outside multiplex
+  // Multi-process mode: a receive buffer is pushed into by the sender and an
+  // Isend buffer pulled by the receiver, so both must be heap memory; a
+  // blocking send reads its own buffer (eager or staged copies).
+  if ((is_recv || !blocking) && !peer_ok(buf, bytes)) return MPIX_ERR_INVALID_ARG;
+  if (mp_mode() && !is_recv && blocking && bytes > L.E && bytes > w.cfg.stage_chunk)
+    return MPIX_ERR_UNSUPPORTED;  // host staging buffers are not peer-visible
   std::lock_guard<std::mutex> clk(c->mu);
 
   P2PArgs a = {};

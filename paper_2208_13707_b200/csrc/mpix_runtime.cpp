@@ -15,6 +15,33 @@ namespace mpix {
 
 std::atomic<uint64_t> g_launches{0};
 CopyTiming g_copy_timing;
+
+bool mp_mode() { return g_world && g_world->mp; }
+
+int peer_visible_alloc(void** p, uint64_t bytes) {
+  if (mp_mode()) return MPIX_Alloc_mem(bytes, p);
+  return cudaMalloc(p, bytes) == cudaSuccess ? MPI_SUCCESS : MPIX_ERR_NO_MEM;
+}
+
+std::vector<CollMsg> comm_exchange(CommShared& sh, int me, uint64_t& seq, const CollMsg& m) {
+  if (!mp_mode()) return sh.rv.exchange(sh.P, me, seq++, m);
+  ++seq;
+  struct Wire {
+    int64_t i0, i1;
+    uint64_t u0, p0;
+  };
+  Wire in{m.i0, m.i1, m.u0, (uint64_t)m.p0};
+  std::vector<Wire> out(sh.P);
+  std::vector<CollMsg> v(sh.P);
+  if (g_world->ag(&in, sizeof(in), out.data(), g_world->ag_ctx) != 0) return {};
+  for (int q = 0; q < sh.P; ++q) {
+    v[q].i0 = out[q].i0;
+    v[q].i1 = out[q].i1;
+    v[q].u0 = out[q].u0;
+    v[q].p0 = (void*)out[q].p0;
+  }
+  return v;
+}
 std::mutex g_world_mu;
 World* g_world = nullptr;
 thread_local int t_bound_rank = -1;
@@ -71,7 +98,12 @@ int rank_init(RankState& r, const Config& cfg) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, r.device));
   r.sms = prop.multiProcessorCount;
-  CK(cudaMalloc(&r.d_done, kReqSlots * sizeof(uint64_t)));
+  {  // peers store into my completion words
+    int rc = mp_mode() ? MPIX_Alloc_mem(kReqSlots * sizeof(uint64_t), (void**)&r.d_done)
+                       : (cudaMalloc(&r.d_done, kReqSlots * sizeof(uint64_t)) == cudaSuccess
+                              ? MPI_SUCCESS : MPIX_ERR_NO_MEM);
+    if (rc) return rc;
+  }
   CK(cudaMemset(r.d_done, 0, kReqSlots * sizeof(uint64_t)));
   CK(cudaMalloc(&r.d_rec, kOpRecords * sizeof(OpRecord)));
   CK(cudaMemset(r.d_rec, 0, kOpRecords * sizeof(OpRecord)));
@@ -116,10 +148,16 @@ int rank_pool(World& w, RankState& r) {
     CK(cudaMemPoolSetAccess(r.pool, &ad, 1));
   }
   if (w.cfg.stage_slots > 0 && w.cfg.stage_chunk > 0) {
-    CK(cudaMallocFromPoolAsync((void**)&r.d_arena, (uint64_t)w.cfg.stage_slots * w.cfg.stage_chunk,
-                               r.pool, r.aux));
-    CK(cudaMallocFromPoolAsync((void**)&r.d_arena_state, (uint64_t)w.cfg.stage_slots * 8, r.pool,
-                               r.aux));
+    if (w.mp) {  // peers pull from my arena and release its slots
+      if (MPIX_Alloc_mem((uint64_t)w.cfg.stage_slots * w.cfg.stage_chunk, (void**)&r.d_arena) ||
+          MPIX_Alloc_mem((uint64_t)w.cfg.stage_slots * 8, (void**)&r.d_arena_state))
+        return MPIX_ERR_NO_MEM;
+    } else {
+      CK(cudaMallocFromPoolAsync((void**)&r.d_arena, (uint64_t)w.cfg.stage_slots * w.cfg.stage_chunk,
+                                 r.pool, r.aux));
+      CK(cudaMallocFromPoolAsync((void**)&r.d_arena_state, (uint64_t)w.cfg.stage_slots * 8, r.pool,
+                                 r.aux));
+    }
     CK(cudaMemsetAsync(r.d_arena_state, 0, (uint64_t)w.cfg.stage_slots * 8, r.aux));
     CK(cudaStreamSynchronize(r.aux));
   }
@@ -156,14 +194,15 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
     if (s && s->matching >= 0) want = s->matching;
   m1.i1 = want;
   if (me == 0) m1.u0 = w.alloc_ctx();
-  auto v1 = par->sh->rv.exchange(P, me, par->rv_seq++, m1);
+  auto v1 = comm_exchange(*par->sh, me, par->rv_seq, m1);
+  if ((int)v1.size() != P) return MPIX_ERR_CUDA;
   uint32_t ctx = (uint32_t)v1[0].u0;
   bool dyn = false;
   for (int q = 0; q < P; ++q) dyn |= v1[q].i1 != 0;
 
   // Shared state is created by the root and handed out in phase 2.
   std::shared_ptr<CommShared> sh;
-  if (me == 0) {
+  if (me == 0 || w.mp) {  // multi-process: every member builds its own copy
     sh = std::make_shared<CommShared>();
     sh->ctx = ctx;
     sh->dyn = dyn;
@@ -180,7 +219,11 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
   uint8_t* region = nullptr;
   {
     CK(cudaSetDevice(rs.device));
-    CK(cudaMallocFromPoolAsync((void**)&region, L.total(), rs.pool, rs.aux));
+    if (w.mp) {
+      if (MPIX_Alloc_mem(L.total(), (void**)&region)) return MPIX_ERR_NO_MEM;
+    } else {
+      CK(cudaMallocFromPoolAsync((void**)&region, L.total(), rs.pool, rs.aux));
+    }
     CK(cudaMemsetAsync(region, 0, L.total(), rs.aux));
     CK(cudaStreamSynchronize(rs.aux));
   }
@@ -188,11 +231,12 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
   CollMsg m2;
   m2.p0 = region;
   if (me == 0) m2.sp = sh;
-  auto v2 = par->sh->rv.exchange(P, me, par->rv_seq++, m2);
-  sh = std::static_pointer_cast<CommShared>(v2[0].sp);
+  auto v2 = comm_exchange(*par->sh, me, par->rv_seq, m2);
+  if ((int)v2.size() != P) return MPIX_ERR_CUDA;
+  if (!w.mp) sh = std::static_pointer_cast<CommShared>(v2[0].sp);
   {
     // every member writes the same values; guard with the rank mutex of root
-    std::lock_guard<std::mutex> lk(rank_of(0).mu);
+    std::lock_guard<std::mutex> lk(rank_of(w.mp ? me : 0).mu);
     for (int q = 0; q < P; ++q) sh->base[q] = static_cast<uint8_t*>(v2[q].p0);
   }
   // The member bases also go into my region (dynamic matching resolves
@@ -205,7 +249,7 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
     CK(cudaStreamSynchronize(rs.aux));
   }
   // Phase 3: nobody uses the comm until every member has filled the table.
-  par->sh->rv.exchange(P, me, par->rv_seq++, CollMsg{});
+  if ((int)comm_exchange(*par->sh, me, par->rv_seq, CollMsg{}).size() != P) return MPIX_ERR_CUDA;
 
   auto* c = new mpix_comm_s();
   c->sh = sh;
@@ -277,20 +321,16 @@ const char* MPIX_Error_string(int code) {
 // --------------------------------------------------------------------------
 // World
 // --------------------------------------------------------------------------
-int MPIX_World_init(int nranks, const int* devices) {
-  std::lock_guard<std::mutex> lk(g_world_mu);
-  if (g_world) return MPIX_ERR_IN_USE;
-  if (nranks < 1) return MPIX_ERR_INVALID_ARG;
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return MPIX_ERR_CUDA;
-  std::unique_ptr<World> w(new World());
-  w->cfg = Config::from_env();
+// Build the world: all ranks in this process (MPIX_World_init) or only
+// rank `w->local` with stubs for the others (MPIX_World_init_mp).
+static int world_build(World* w, int nranks, const int* devices, int ndev) {
   w->n = nranks;
   for (int r = 0; r < nranks; ++r) {
     auto rs = std::make_unique<RankState>();
     rs->rank = r;
     rs->device = devices ? devices[r] : r % ndev;
-    if (rs->device < 0 || rs->device >= ndev) return MPIX_ERR_INVALID_ARG;
+    rs->hosted = !w->mp || r == w->local;
+    if (rs->hosted && (rs->device < 0 || rs->device >= ndev)) return MPIX_ERR_INVALID_ARG;
     w->ranks.push_back(std::move(rs));
   }
   for (auto& rs : w->ranks) {
@@ -298,34 +338,39 @@ int MPIX_World_init(int nranks, const int* devices) {
     for (auto& o : w->ranks) per += o->device == rs->device;
     rs->per_device = per;
   }
-  // Peer access between every pair of distinct devices (NVLink / NVSwitch).
-  std::vector<int> devs;
-  for (auto& rs : w->ranks)
-    if (std::find(devs.begin(), devs.end(), rs->device) == devs.end()) devs.push_back(rs->device);
-  for (int i : devs) {
-    for (int j : devs) {
-      if (i == j) continue;
-      int can = 0;
-      cudaDeviceCanAccessPeer(&can, i, j);
-      if (!can) return MPIX_ERR_UNSUPPORTED;
-      cudaSetDevice(i);
-      cudaError_t e = cudaDeviceEnablePeerAccess(j, 0);
-      if (e == cudaErrorPeerAccessAlreadyEnabled)
-        cudaGetLastError();
-      else if (e != cudaSuccess)
-        return MPIX_ERR_CUDA;
+  if (!w->mp) {
+    // Peer access between every pair of distinct devices (NVLink / NVSwitch);
+    // in multi-process mode the heap mappings grant access instead.
+    std::vector<int> devs;
+    for (auto& rs : w->ranks)
+      if (std::find(devs.begin(), devs.end(), rs->device) == devs.end()) devs.push_back(rs->device);
+    for (int i : devs) {
+      for (int j : devs) {
+        if (i == j) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, i, j);
+        if (!can) return MPIX_ERR_UNSUPPORTED;
+        cudaSetDevice(i);
+        cudaError_t e = cudaDeviceEnablePeerAccess(j, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled)
+          cudaGetLastError();
+        else if (e != cudaSuccess)
+          return MPIX_ERR_CUDA;
+      }
     }
   }
   for (auto& rs : w->ranks) {
+    if (!rs->hosted) continue;
     int rc = rank_init(*rs, w->cfg);
     if (rc) return rc;
   }
   for (auto& rs : w->ranks) {
+    if (!rs->hosted) continue;
     int rc = rank_pool(*w, *rs);
     if (rc) return rc;
   }
   // Bootstrap world communicator, ctx 0 (world.cpp:61-76). It carries no
-  // stream, so enqueue on it is NOT_ENQUEUE_COMM; it has no region.
+  // stream, so enqueue on it is NOT_ENQUEUE_COMM.
   auto sh = std::make_shared<CommShared>();
   sh->ctx = 0;
   sh->P = nranks;
@@ -338,18 +383,31 @@ int MPIX_World_init(int nranks, const int* devices) {
   // Appendix A7): every rank gets a region for it too.
   for (int r = 0; r < nranks; ++r) {
     RankState& rs = *w->ranks[r];
+    if (!rs.hosted) continue;
     if (cudaSetDevice(rs.device) != cudaSuccess) return MPIX_ERR_CUDA;
     uint8_t* region = nullptr;
-    if (cudaMallocFromPoolAsync((void**)&region, sh->L.total(), rs.pool, rs.aux) != cudaSuccess ||
-        cudaMemsetAsync(region, 0, sh->L.total(), rs.aux) != cudaSuccess)
+    if (w->mp) {
+      if (MPIX_Alloc_mem(sh->L.total(), (void**)&region)) return MPIX_ERR_NO_MEM;
+    } else if (cudaMallocFromPoolAsync((void**)&region, sh->L.total(), rs.pool, rs.aux) != cudaSuccess) {
       return MPIX_ERR_CUDA;
+    }
+    if (cudaMemsetAsync(region, 0, sh->L.total(), rs.aux) != cudaSuccess) return MPIX_ERR_CUDA;
     sh->base[r] = region;
+  }
+  if (w->mp) {  // the other ranks' world regions, from their processes
+    CollMsg m;
+    m.p0 = sh->base[w->local];
+    uint64_t seq = 0;
+    auto v = comm_exchange(*sh, w->local, seq, m);
+    if ((int)v.size() != nranks) return MPIX_ERR_CUDA;
+    for (int r = 0; r < nranks; ++r) sh->base[r] = static_cast<uint8_t*>(v[r].p0);
   }
   {
     std::vector<uint64_t> bases(nranks);
     for (int r = 0; r < nranks; ++r) bases[r] = (uint64_t)sh->base[r];
     for (int r = 0; r < nranks; ++r) {
       RankState& rs = *w->ranks[r];
+      if (!rs.hosted) continue;
       cudaSetDevice(rs.device);
       if (cudaMemcpyAsync(sh->base[r] + sh->L.bases(), bases.data(), 8ull * nranks,
                           cudaMemcpyHostToDevice, rs.aux) != cudaSuccess ||
@@ -358,15 +416,65 @@ int MPIX_World_init(int nranks, const int* devices) {
     }
   }
   for (int r = 0; r < nranks; ++r) {
+    if (!w->ranks[r]->hosted) {
+      w->world_comms.push_back(nullptr);
+      continue;
+    }
     auto* c = new mpix_comm_s();
     c->sh = sh;
     c->rank = r;
     c->send_pseq.assign(nranks, 0);
     c->recv_pseq.assign(nranks, 0);
     for (int q = 0; q < nranks; ++q) c->any_remote |= w->ranks[q]->device != w->ranks[r]->device;
+    c->any_remote |= w->mp && nranks > 1;
     w->world_comms.push_back(c);
   }
+  return MPI_SUCCESS;
+}
+
+int MPIX_World_init(int nranks, const int* devices) {
+  std::lock_guard<std::mutex> lk(g_world_mu);
+  if (g_world) return MPIX_ERR_IN_USE;
+  if (nranks < 1) return MPIX_ERR_INVALID_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return MPIX_ERR_CUDA;
+  std::unique_ptr<World> w(new World());
+  w->cfg = Config::from_env();
+  int rc = world_build(w.get(), nranks, devices, ndev);
+  if (rc) return rc;
   g_world = w.release();
+  return MPI_SUCCESS;
+}
+
+int MPIX_World_init_mp(int rank, int nranks, const int* devices, MPIX_Allgather_fn allgather,
+                       void* ctx) {
+  std::lock_guard<std::mutex> lk(g_world_mu);
+  if (g_world) return MPIX_ERR_IN_USE;
+  if (nranks < 1 || rank < 0 || rank >= nranks || !devices || !allgather) return MPIX_ERR_INVALID_ARG;
+  if (nranks > 1 && !heap_live()) return MPIX_ERR_NOT_INITIALIZED;  // MPIX_Heap_create + attach first
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return MPIX_ERR_CUDA;
+  std::unique_ptr<World> w(new World());
+  w->cfg = Config::from_env();
+  w->mp = true;
+  w->local = rank;
+  w->ag = allgather;
+  w->ag_ctx = ctx;
+  w->cfg.force_sys = true;  // peers are other processes: system scope everywhere
+  g_world = w.get();        // comm_exchange during the build reads g_world
+  int rc = world_build(w.get(), nranks, devices, ndev);
+  if (rc) {
+    g_world = nullptr;
+    return rc;
+  }
+  w.release();
+  return MPI_SUCCESS;
+}
+
+int MPIX_World_local_rank(int* rank) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!rank) return MPIX_ERR_INVALID_ARG;
+  *rank = g_world->mp ? g_world->local : 0;
   return MPI_SUCCESS;
 }
 
@@ -378,32 +486,36 @@ int MPIX_World_finalize(void) {
   for (auto& kv : w->batches) held.push_back(kv.first);
   for (cudaStream_t s : held) flush_stream(s);
   for (auto& rs : w->ranks) {
+    if (!rs->hosted) continue;
     cudaSetDevice(rs->device);
     cudaDeviceSynchronize();
   }
+  // heap memory (multi-process mode) is released with the heap
   for (auto* c : w->all_comms) {
     RankState& rs = *w->ranks[c->rank];
     cudaSetDevice(rs.device);
-    if (c->sh && c->sh->base[c->rank]) {
-      cudaFreeAsync(c->sh->base[c->rank], rs.aux);
-      c->sh->base[c->rank] = nullptr;
-    }
+    if (c->sh && c->sh->base[c->rank] && !w->mp) cudaFreeAsync(c->sh->base[c->rank], rs.aux);
+    if (c->sh) c->sh->base[c->rank] = nullptr;
     delete c;
   }
   for (auto* c : w->world_comms) {
+    if (!c) continue;
     RankState& rs = *w->ranks[c->rank];
     cudaSetDevice(rs.device);
-    if (c->sh->base[c->rank]) cudaFreeAsync(c->sh->base[c->rank], rs.aux);
+    if (c->sh->base[c->rank] && !w->mp) cudaFreeAsync(c->sh->base[c->rank], rs.aux);
     c->sh->base[c->rank] = nullptr;
     delete c;
   }
   for (auto& rs : w->ranks) {
+    if (!rs->hosted) continue;
     cudaSetDevice(rs->device);
     for (auto& sb : rs->stage) cudaFreeAsync(sb.p, rs->aux);
-    if (rs->d_arena) cudaFreeAsync(rs->d_arena, rs->aux);
-    if (rs->d_arena_state) cudaFreeAsync(rs->d_arena_state, rs->aux);
+    if (!w->mp) {
+      if (rs->d_arena) cudaFreeAsync(rs->d_arena, rs->aux);
+      if (rs->d_arena_state) cudaFreeAsync(rs->d_arena_state, rs->aux);
+    }
     cudaStreamSynchronize(rs->aux);
-    cudaFree(rs->d_done);
+    if (!w->mp) cudaFree(rs->d_done);
     cudaFree(rs->d_rec);
     if (rs->d_trace) cudaFree(rs->d_trace);
     cudaFreeHost(rs->h_err);
@@ -425,7 +537,7 @@ int MPIX_World_size(int* n) {
 
 int MPIX_World_comm(int rank, MPI_Comm* comm) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
-  if (rank < 0 || rank >= g_world->n) return MPIX_ERR_INVALID_RANK;
+  if (rank < 0 || rank >= g_world->n || !g_world->world_comms[rank]) return MPIX_ERR_INVALID_RANK;
   *comm = g_world->world_comms[rank];
   return MPI_SUCCESS;
 }
@@ -459,7 +571,8 @@ int MPI_Comm_size(MPI_Comm comm, int* size) {
 int MPI_Barrier(MPI_Comm comm) {  // proc_comm.cpp:31-46 (host-side)
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
   if (!comm) return MPIX_ERR_INVALID_COMM;
-  comm->sh->rv.exchange(comm->sh->P, comm->rank, comm->rv_seq++, CollMsg{});
+  if ((int)comm_exchange(*comm->sh, comm->rank, comm->rv_seq, CollMsg{}).size() != comm->sh->P)
+    return MPIX_ERR_CUDA;
   return MPI_SUCCESS;
 }
 
@@ -477,6 +590,21 @@ int MPI_Comm_free(MPI_Comm* comm) {  // proc_comm.cpp:178-194
   cudaEvent_t ev = nullptr;
   if (c->cu && flush_stream(c->cu) < 0) return MPIX_ERR_CUDA;
   CK(cudaSetDevice(rs.device));
+  if (w.mp) {
+    // events do not cross processes: retire my work, then agree
+    CK(cudaStreamSynchronize(c->cu ? c->cu : rs.aux));
+    if ((int)comm_exchange(*c->sh, c->rank, c->rv_seq, CollMsg{}).size() != P) return MPIX_ERR_CUDA;
+    c->sh->base[c->rank] = nullptr;  // heap memory is released with the heap
+    for (auto* s : c->local_streams)
+      if (s) s->refcount.fetch_sub(1);
+    {
+      std::lock_guard<std::mutex> lk(w.comms_mu);
+      w.all_comms.erase(std::remove(w.all_comms.begin(), w.all_comms.end(), c), w.all_comms.end());
+    }
+    delete c;
+    *comm = MPI_COMM_NULL;
+    return MPI_SUCCESS;
+  }
   CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   CK(cudaEventRecord(ev, c->cu ? c->cu : rs.aux));
   CollMsg m;

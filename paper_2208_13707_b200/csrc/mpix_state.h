@@ -124,6 +124,7 @@ class Rendezvous {
 
 struct RankState {
   int rank = 0;
+  bool hosted = true;  // false: a stub for a rank of another process (multi-process mode)
   int device = 0;
   int sms = 148;
   int per_device = 1;  // ranks sharing this GPU
@@ -250,6 +251,14 @@ namespace mpix {
 
 struct World {
   Config cfg;
+  // Multi-process mode (MPIX_World_init_mp): this process hosts rank
+  // `local`; the other RankStates are stubs (device only); collective host
+  // steps go through the caller's allgather; device memory peers touch lives
+  // in the symmetric heap (mpix_heap.cpp), so raw pointers stay valid.
+  bool mp = false;
+  int local = 0;
+  MPIX_Allgather_fn ag = nullptr;
+  void* ag_ctx = nullptr;
   std::mutex batch_mu;
   std::unordered_map<cudaStream_t, std::unique_ptr<StreamBatch>> batches;
   int n = 0;
@@ -288,6 +297,18 @@ extern thread_local int t_bound_rank;
 
 // mpix_runtime.cpp
 int type_size(MPI_Datatype dt);
+// Collective host exchange over the members of a communicator: the in-process
+// rendezvous, or the allgather of multi-process mode.
+std::vector<CollMsg> comm_exchange(CommShared& sh, int me, uint64_t& seq, const CollMsg& m);
+// Device memory that peers read or write: the symmetric heap in
+// multi-process mode, cudaMalloc otherwise.
+int peer_visible_alloc(void** p, uint64_t bytes);
+bool mp_mode();
+bool heap_live();  // mpix_heap.cpp
+// Multi-process mode: memory a peer dereferences must be in the heap.
+inline bool peer_ok(const void* p, uint64_t bytes) {
+  return !mp_mode() || bytes == 0 || MPIX_Heap_contains(p, bytes);
+}
 std::string hex_encode(const void* bytes, size_t len);
 int hex_decode(const std::string& s, std::vector<uint8_t>& out);
 int rank_init(RankState& r, const Config& cfg);

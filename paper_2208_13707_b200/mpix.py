@@ -87,6 +87,14 @@ def _declare(L: C.CDLL) -> None:
     sig = {
         "MPIX_Error_string": (C.c_char_p, [I]),
         "MPIX_World_init": (I, [I, P]),
+        "MPIX_World_init_mp": (I, [I, I, P, P, P]),
+        "MPIX_World_local_rank": (I, [C.POINTER(I)]),
+        "MPIX_Heap_create": (I, [I, I, I, U64, U64, C.POINTER(U64), C.POINTER(U64), C.POINTER(I)]),
+        "MPIX_Heap_attach": (I, [I, I]),
+        "MPIX_Heap_contains": (I, [P, U64]),
+        "MPIX_Heap_destroy": (I, []),
+        "MPIX_Alloc_mem": (I, [U64, C.POINTER(P)]),
+        "MPIX_Free_mem": (I, [P]),
         "MPIX_World_finalize": (I, []),
         "MPIX_World_size": (I, [C.POINTER(I)]),
         "MPIX_World_comm": (I, [I, C.POINTER(P)]),
@@ -545,6 +553,130 @@ class World:
 
     def __exit__(self, *exc):
         self.finalize()
+
+
+# --- multi-process world (one process per GPU) ---------------------------------
+_AG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p)
+
+_TORCH_DTYPESTR = {}
+
+
+class _RawCuda:
+    """A raw device range exposed through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, numel: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
+class MPWorld:
+    """This process hosts one rank of a world of torch.distributed's size
+    (MPIX_World_init_mp): the symmetric heap is created and every peer's slice
+    mapped (file descriptors passed over Unix sockets), and the runtime's
+    collective host steps run over torch.distributed (gloo, CPU). Buffers
+    that peers touch must come from `alloc`."""
+
+    def __init__(self, heap_bytes: int = 2 << 30, device: Optional[int] = None):
+        import socket
+        import tempfile
+
+        import torch
+        import torch.distributed as dist
+        assert dist.is_initialized(), "call torch.distributed.init_process_group first"
+        self.dist, self.torch = dist, torch
+        self.rank, self.n = dist.get_rank(), dist.get_world_size()
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+        self.device = device
+        torch.cuda.set_device(device)
+        L = lib()
+        base, slc, fd = C.c_uint64(), C.c_uint64(), C.c_int()
+        ok = False
+        for k in range(32):  # a virtual range free in every process
+            cand = 0x600000000000 + (k << 40)
+            rc = L.MPIX_Heap_create(self.rank, self.n, device, heap_bytes, cand, C.byref(base),
+                                    C.byref(slc), C.byref(fd))
+            flag = torch.tensor([1 if rc == 0 else 0])
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag[0]):
+                ok = True
+                break
+            if rc == 0:
+                L.MPIX_Heap_destroy()
+        if not ok:
+            raise MPIXError(ERR["NO_MEM"], "MPIX_Heap_create: no common virtual range")
+        self.base, self.slice = base.value, slc.value
+        # pass every rank's heap file descriptor to every other rank
+        token = torch.randint(0, 2**31 - 1, (1,))
+        dist.broadcast(token, 0)
+        tmp = tempfile.gettempdir()
+        path = lambda q: os.path.join(tmp, f"mpix_heap_{int(token[0])}_{q}")
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(path(self.rank))
+        srv.listen(self.n)
+        dist.barrier()
+        for q in range(self.n):
+            if q != self.rank:
+                c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                c.connect(path(q))
+                socket.send_fds(c, [self.rank.to_bytes(4, "little")], [fd.value])
+                c.close()
+        for _ in range(self.n - 1):
+            conn, _ = srv.accept()
+            msg, fds, _, _ = socket.recv_fds(conn, 4, 1)
+            check(L.MPIX_Heap_attach(int.from_bytes(msg, "little"), fds[0]), "MPIX_Heap_attach")
+            os.close(fds[0])
+            conn.close()
+        srv.close()
+        os.unlink(path(self.rank))
+        os.close(fd.value)
+        dist.barrier()
+        devs = torch.zeros(self.n, dtype=torch.int64)
+        mine = torch.tensor([device], dtype=torch.int64)
+        parts = [torch.zeros(1, dtype=torch.int64) for _ in range(self.n)]
+        dist.all_gather(parts, mine)
+        devs = (C.c_int * self.n)(*[int(p[0]) for p in parts])
+
+        def _allgather(inp, nbytes, out, ctx):
+            try:
+                b = torch.frombuffer(bytearray(C.string_at(inp, nbytes)), dtype=torch.uint8)
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(self.n)]
+                dist.all_gather(outs, b)
+                joined = torch.cat(outs).numpy().tobytes()
+                C.memmove(out, joined, len(joined))
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        self._ag = _AG_FN(_allgather)  # keep the callback alive
+        check(L.MPIX_World_init_mp(self.rank, self.n, devs, self._ag, None), "MPIX_World_init_mp")
+
+    def comm(self) -> Comm:
+        """This rank's world communicator."""
+        h = C.c_void_p()
+        check(lib().MPIX_World_comm(self.rank, C.byref(h)), "MPIX_World_comm")
+        return Comm(h)
+
+    def alloc(self, numel: int, dtype=None):
+        """A torch tensor in this rank's slice of the symmetric heap."""
+        torch = self.torch
+        dtype = dtype or torch.uint8
+        esz = torch.tensor([], dtype=dtype).element_size()
+        p = C.c_void_p()
+        check(lib().MPIX_Alloc_mem(max(1, numel * esz), C.byref(p)), "MPIX_Alloc_mem")
+        typestr = {torch.uint8: "|u1", torch.int32: "<i4", torch.int64: "<i8",
+                   torch.float32: "<f4", torch.float64: "<f8", torch.bfloat16: "<V2"}[dtype]
+        if dtype is torch.bfloat16:  # no bfloat16 typestr: view int16 storage
+            t = torch.as_tensor(_RawCuda(p.value, numel, "<i2"), device=f"cuda:{self.device}")
+            return t.view(torch.bfloat16)
+        return torch.as_tensor(_RawCuda(p.value, numel, typestr), device=f"cuda:{self.device}")
+
+    def finalize(self) -> None:
+        self.torch.cuda.synchronize(self.device)
+        self.dist.barrier()
+        check(lib().MPIX_World_finalize(), "MPIX_World_finalize")
+        self.dist.barrier()  # no peer still maps my slice
+        check(lib().MPIX_Heap_destroy(), "MPIX_Heap_destroy")
 
 
 # --- test/bench helper kernels (include/mpix_testing.h) ---------------------------

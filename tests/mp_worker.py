@@ -1,0 +1,106 @@
+"""Worker for tests/test_gpu_mp.py: one rank per process (torchrun), the
+multi-process world (symmetric heap + MPIX_World_init_mp). Exercises the
+enqueue p2p, conventional p2p and collectives across processes and checks
+every result exactly; prints "MP OK <rank>" on success."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2208_13707_b200 import mpix  # noqa: E402
+
+
+def main():
+    dist.init_process_group("gloo")
+    w = mpix.MPWorld(heap_bytes=1 << 30)
+    r, n, dev = w.rank, w.n, w.device
+    peer = 1 - r if n == 2 else (r + 1) % n
+    left = (r + n - 1) % n
+    s = mpix.testing.new_stream(dev)
+    c = w.comm().stream_comm_create(mpix.Stream.from_cuda(s))
+    g = torch.Generator().manual_seed(1234)
+    # deterministic per-rank payloads known to every rank
+    pay = {q: torch.randint(0, 256, (6 << 20,), dtype=torch.uint8, generator=g) for q in range(n)}
+    src = w.alloc(6 << 20)
+    dst = w.alloc(6 << 20)
+    src.copy_(pay[r].to(dev))
+    torch.cuda.synchronize(dev)
+    # 1. ring exchange of several sizes: Isend to the right, Irecv from the left
+    for nb in (0, 8, 4096, 70000, 1 << 20, 6 << 20):
+        dst.zero_()
+        torch.cuda.synchronize(dev)
+        rr = c.irecv_enqueue(dst, nb, mpix.MPI_BYTE, left, 3)
+        rs = c.isend_enqueue(src, nb, mpix.MPI_BYTE, (r + 1) % n, 3)
+        mpix.waitall_enqueue([rr, rs])
+        s.synchronize()
+        assert torch.equal(dst[:nb].cpu(), pay[left][:nb]), ("ring", nb)
+    # 2. blocking ping-pong between ranks 0 and 1 (eager and staged sends)
+    if r < 2 and n >= 2:
+        for nb in (16, 100000, 3 << 20):
+            for it in range(3):
+                if r == 0:
+                    c.send_enqueue(src, nb, mpix.MPI_BYTE, 1, 10 + it)
+                    c.recv_enqueue(dst, nb, mpix.MPI_BYTE, 1, 20 + it)
+                else:
+                    c.recv_enqueue(dst, nb, mpix.MPI_BYTE, 0, 10 + it)
+                    c.send_enqueue(dst, nb, mpix.MPI_BYTE, 0, 20 + it)
+            s.synchronize()
+            if r == 0:
+                assert torch.equal(dst[:nb].cpu(), pay[0][:nb]), ("pingpong", nb)
+    dist.barrier()
+    # 3. allreduce (fp32, exactly representable inputs: any order is exact)
+    cnt = (1 << 20) + 5
+    x = w.alloc(cnt, torch.float32)
+    y = w.alloc(cnt, torch.float32)
+    vals = [(torch.arange(cnt, dtype=torch.float32) % 1000 - 500 + q) / 4 for q in range(n)]
+    x.copy_(vals[r].to(dev))
+    torch.cuda.synchronize(dev)
+    c.allreduce_enqueue(x, y, cnt, mpix.MPI_FLOAT)
+    s.synchronize()
+    exp = vals[0].clone()
+    for q in range(1, n):
+        exp += vals[q]
+    assert torch.equal(y.cpu(), exp), "allreduce"
+    # small (fused single-launch) allreduce
+    c.allreduce_enqueue(x, y, 100, mpix.MPI_FLOAT)
+    s.synchronize()
+    assert torch.equal(y[:100].cpu(), exp[:100]), "allreduce small"
+    # 4. bcast from the last rank and allgather
+    b = w.alloc(1 << 20)
+    b.copy_(pay[r][: 1 << 20].to(dev))
+    torch.cuda.synchronize(dev)
+    c.bcast_enqueue(b, 1 << 20, mpix.MPI_BYTE, n - 1)
+    s.synchronize()
+    assert torch.equal(b.cpu(), pay[n - 1][: 1 << 20]), "bcast"
+    ag = w.alloc(n * 4096)
+    c.allgather_enqueue(src, ag, 4096, mpix.MPI_BYTE)
+    s.synchronize()
+    assert torch.equal(ag.cpu(), torch.cat([pay[q][:4096] for q in range(n)])), "allgather"
+    # 5. conventional p2p on the world comm
+    wc = w.comm()
+    if r < 2 and n >= 2:
+        t = w.alloc(5000)
+        if r == 0:
+            wc.send(src, 5000, mpix.MPI_BYTE, 1, 7)
+        else:
+            wc.recv(t, 5000, mpix.MPI_BYTE, 0, 7)
+            assert torch.equal(t.cpu(), pay[0][:5000]), "conventional"
+    # 6. a non-heap receive buffer is rejected in multi-process mode
+    plain = torch.zeros(64, dtype=torch.uint8, device=dev)
+    try:
+        c.irecv_enqueue(plain, 64, mpix.MPI_BYTE, left, 99)
+        raise AssertionError("non-heap receive buffer accepted")
+    except mpix.MPIXError as e:
+        assert e.name == "INVALID_ARG", e.name
+    assert mpix.rank_error(r) == 0
+    c.free()
+    w.finalize()
+    os.write(1, f"MP OK {r}\n".encode())  # one write: lines of ranks do not interleave
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
