@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--share-gpus", action="store_true",
                     help="validation only: map rank r to GPU r %% ndev (ranks share GPUs)")
+    ap.add_argument("--single-process", action="store_true",
+                    help="N>1: rank 0 drives all N GPUs in one process (the reference's World "
+                         "model) instead of one process per GPU")
     return ap.parse_args()
 
 
@@ -201,7 +204,14 @@ def run_mpix(args):
         # each process, every rank instead runs an independent one-GPU
         # replica of the N=1 step and the job time is the max over ranks.
         flag = torch.tensor([1 if torch.cuda.device_count() >= args.gpus or args.share_gpus else 0])
-        dist.broadcast(flag, 0)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag[0]) and not args.single_process:
+            # one process per GPU: the multi-process world over the symmetric heap
+            line = bench_mp(args, rank, world, local)
+            dist.destroy_process_group()
+            if rank == 0:
+                print(json.dumps(line))
+            return
         if not int(flag[0]):
             line = bench_replica(args, rank, world, local)
             dist.destroy_process_group()
@@ -222,6 +232,175 @@ def run_mpix(args):
             dist.barrier()
             dist.destroy_process_group()
     print(json.dumps(line))
+
+
+def bench_mp(args, rank, world, local):
+    """N > 1, one process per GPU (MPIX_World_init_mp over the symmetric
+    heap): GPU pairs (0,1),(2,3).. each move one S-byte message per step
+    (Isend_enqueue on the even rank, Irecv_enqueue + Wait on the odd rank);
+    K steps between barriers, device time max over ranks (gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2208_13707_b200 import mpix
+    S = args.size
+    ndev = torch.cuda.device_count()
+    dev = local % ndev
+    w = mpix.MPWorld(heap_bytes=3 * S + (4 << 30), device=dev)  # bump heap: bench + extras buffers
+    s = mpix.testing.new_stream(dev)
+    c = w.comm().stream_comm_create(mpix.Stream.from_cuda(s))
+    src, dst = w.alloc(S), w.alloc(S)
+    mpix.testing.fill_pattern(src, S, 1234 + rank, 0, s)
+    s.synchronize()
+    pairs = world // 2
+    active = rank < 2 * pairs
+    sender = active and rank % 2 == 0
+    peer = rank + 1 if sender else rank - 1
+    tag = [0]
+
+    def step():
+        if not active:
+            return
+        tag[0] = (tag[0] + 1) % 30000
+        if sender:
+            mpix.wait_enqueue(c.isend_enqueue(src, S, mpix.MPI_BYTE, peer, tag[0]))
+        else:
+            mpix.wait_enqueue(c.irecv_enqueue(dst, S, mpix.MPI_BYTE, peer, tag[0]))
+
+    step()
+    s.synchronize()
+    if active and not sender:  # the payload is the sender's pattern
+        exp = w.alloc(S)
+        mpix.testing.fill_pattern(exp, S, 1234 + peer, 0, s)
+        s.synchronize()
+        assert torch.equal(dst, exp), "payload mismatch"
+    for _ in range(args.warmup):
+        step()
+    s.synchronize()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = mpix.launch_count()
+    e0.record(s)
+    for _ in range(args.steps):
+        step()
+    e1.record(s)
+    s.synchronize()
+    launches = mpix.launch_count() - l0
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_step = float(t[0]) / args.steps
+    nl = torch.tensor([launches], dtype=torch.int64)
+    dist.all_reduce(nl, op=dist.ReduceOp.SUM)
+    # dominant kernel: the copy grid of each message (receiver pulls or sender
+    # pushes, whichever arrives second); longest average over ranks
+    mpix.testing.copy_timing(True)
+    for _ in range(args.steps):
+        step()
+    s.synchronize()
+    tot, ncopy = mpix.testing.copy_timing_read()
+    mpix.testing.copy_timing(False)
+    kt = torch.tensor([tot / max(ncopy, 1) if ncopy else 0.0], dtype=torch.float64)
+    dist.all_reduce(kt, op=dist.ReduceOp.MAX)
+    k_ms = float(kt[0])
+    clk = clocks.stop()
+    same_gpu = ndev < world
+    peak = peaks().get("hbm_gbs", 6650.0) / 2 if same_gpu else 770.0
+    achieved = S / (k_ms / 1e3) / 1e9 if k_ms else 0.0
+    # e2e: the sender's pinned host input -> H2D -> Isend; the receiver's
+    # Irecv -> checksum -> 8-byte D2H; both synchronise every step
+    host = torch.empty(S, dtype=torch.uint8, pin_memory=True)
+    host.copy_(src.cpu())
+    csum = torch.zeros(1, dtype=torch.int64, device=dev)
+    hsum = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        if active:
+            tag[0] = (tag[0] + 1) % 30000
+            if sender:
+                with torch.cuda.stream(s):
+                    src.copy_(host, non_blocking=True)
+                mpix.wait_enqueue(c.isend_enqueue(src, S, mpix.MPI_BYTE, peer, tag[0]))
+            else:
+                mpix.wait_enqueue(c.irecv_enqueue(dst, S, mpix.MPI_BYTE, peer, tag[0]))
+                mpix.testing.checksum(dst, S, csum, s)
+                with torch.cuda.stream(s):
+                    hsum.copy_(csum, non_blocking=True)
+        s.synchronize()
+    e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    extras = {}
+    if not args.no_extras:
+        extras = extras_mp(args, mpix, torch, dist, w, c, s, rank, world, dev)
+    c.free()
+    w.finalize()
+    return {
+        "metric": METRIC, "value": S * pairs / t_step / 1e9, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": f"{pairs} GPU pair(s), one process per GPU (multi-process world, "
+                               "symmetric heap): Isend_enqueue -> Irecv_enqueue + Wait",
+                   "message_bytes": S, "ranks": world, "parallelism": "one process per GPU",
+                   "l2": "inputs larger than L2",
+                   "baseline_config": "BASELINE.json configs[1] (SURVEY.md §8d cfg2) at N GPUs",
+                   **({"note": "GPUs shared by ranks: not an NVLink measurement"} if same_gpu else {})},
+        "roofline": {"bound": "hbm" if same_gpu else "nvlink", "unit": "GB/s", "achieved": achieved,
+                     "peak": peak, "frac": achieved / peak if peak else 0.0, "traffic": None,
+                     "peak_source": ("half the measured HBM copy bandwidth (read + write on one GPU)"
+                                     if same_gpu else
+                                     "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"),
+                     "kernel": "mpix::k_gcopy (the copy grid of each message)", "kernel_ms": k_ms,
+                     "algorithmic_bytes_per_launch": S},
+        "e2e": {"value": S * pairs * args.steps / float(e2e_t[0]) / 1e9, "unit": "GB/s",
+                "h2d_bytes_per_step": S * pairs, "d2h_bytes_per_step": 8 * pairs,
+                "timing": "host wall clock, max over ranks, streams synchronised every step"},
+        "gpu_launches": int(nl[0]),
+        "clocks": clk,
+        "extras": extras,
+    }
+
+
+def extras_mp(args, mpix, torch, dist, w, c, s, rank, world, dev):
+    """Multi-process N > 1: Allreduce_enqueue 256 MiB over all N (busbw) and
+    the ranks 0 <-> 1 ping-pong half round trip, device time max over ranks."""
+    out = {}
+    ar = {}
+    for name, tdt, mdt in (("f32", torch.float32, mpix.MPI_FLOAT), ("bf16", torch.bfloat16, mpix.MPIX_BFLOAT16)):
+        nbytes = 256 << 20
+        cnt = nbytes // torch.tensor([], dtype=tdt).element_size()
+        sb, rb = w.alloc(cnt, tdt), w.alloc(cnt, tdt)
+        sb.fill_(1)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        mpix.testing.allreduce_loop([c], [s], [dev], [sb], [rb], cnt, mdt, 2)
+        dist.barrier()
+        d, _ = mpix.testing.allreduce_loop([c], [s], [dev], [sb], [rb], cnt, mdt, 10)
+        t = torch.tensor([d / 10], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        algbw = nbytes / float(t[0]) / 1e9
+        ar[name] = {"ms": float(t[0]) * 1e3, "algbw_GBps": algbw,
+                    "busbw_GBps": algbw * 2 * (world - 1) / world,
+                    "check": float(rb[0]) == float(world)}
+    out["allreduce_256MiB"] = ar
+    pp = {}
+    buf = w.alloc(64 << 20)
+    for nb in (8, 4096, 65536, 1 << 20, 64 << 20):
+        iters = 200 if nb <= (1 << 20) else 20
+        dist.barrier()
+        d = 0.0
+        if rank < 2:
+            mpix.testing.pingpong_side(c, buf, nb, 10, 1 - rank, rank == 0, s)
+            d = mpix.testing.pingpong_side(c, buf, nb, iters, 1 - rank, rank == 0, s)
+        t = torch.tensor([d], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        half = float(t[0]) / (2 * iters)
+        pp[str(nb)] = {"half_rtt_us": half * 1e6, "GBps": nb / half / 1e9}
+    out["pingpong_rank0_rank1"] = pp
+    return out
 
 
 def bench_replica(args, rank, world, local):

@@ -65,6 +65,10 @@ int MPIXT_Msgrate(int P, int S, int W, int batches, MPI_Comm *comms, void **stre
  * Send+Recv / Recv+Send, `iters` round trips; *dev_s = event time on s0. */
 int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void *b0, void *b1, uint64_t bytes, int iters,
                    void *s0, void *s1, int dev0, int dev1, double *dev_s, double *host_s);
+/* One side of a blocking ping-pong with `peer` (multi-process mode, one
+ * process per rank): the initiator sends then receives. */
+int MPIXT_Pingpong_side(MPI_Comm c, void *buf, uint64_t bytes, int iters, int peer, int initiator,
+                        void *stream, double *dev_s);
 /* producer kernel -> Send_enqueue -> Recv_enqueue -> consumer kernel (self
  * messages of n floats on one stream), `iters` times. */
 int MPIXT_Selfchain(MPI_Comm c, float *prod, float *cons, int n, int iters, void *stream,

@@ -138,6 +138,37 @@ int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void* b0, void* b1, uint64_t bytes,
   return err.load();
 }
 
+// One side of a blocking ping-pong (multi-process mode: each process drives
+// its own rank): the initiator sends then receives, the other side receives
+// then sends; *dev_s = event time on this side's stream.
+int MPIXT_Pingpong_side(MPI_Comm c, void* buf, uint64_t bytes, int iters, int peer, int initiator,
+                        void* stream, double* dev_s) {
+  if (iters < 1) return MPIX_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t a, b;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return MPIX_ERR_CUDA;
+  const int count = (int)bytes;
+  int err = 0;
+  cudaEventRecord(a, s);
+  for (int i = 0; i < iters && !err; ++i) {
+    if (initiator) {
+      err |= MPIX_Send_enqueue(buf, count, MPI_BYTE, peer, 1, c);
+      err |= MPIX_Recv_enqueue(buf, count, MPI_BYTE, peer, 2, c, MPI_STATUS_IGNORE);
+    } else {
+      err |= MPIX_Recv_enqueue(buf, count, MPI_BYTE, peer, 1, c, MPI_STATUS_IGNORE);
+      err |= MPIX_Send_enqueue(buf, count, MPI_BYTE, peer, 2, c);
+    }
+  }
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (dev_s) *dev_s = ms / 1e3;
+  return err;
+}
+
 // producer kernel -> Send_enqueue -> Recv_enqueue -> consumer kernel, all on
 // one stream (self messages), `iters` times.
 int MPIXT_Selfchain(MPI_Comm c, float* prod, float* cons, int n, int iters, void* stream,

@@ -461,6 +461,10 @@ int MPIX_World_init_mp(int rank, int nranks, const int* devices, MPIX_Allgather_
   w->ag = allgather;
   w->ag_ctx = ctx;
   w->cfg.force_sys = true;  // peers are other processes: system scope everywhere
+  // Host staging buffers are not peer-visible: staged blocking sends use the
+  // device arena only, so give it larger slots (1 GiB of heap by default).
+  if (!std::getenv("MPIX_STAGE_CHUNK")) w->cfg.stage_chunk = 64ull << 20;
+  if (!std::getenv("MPIX_STAGE_SLOTS")) w->cfg.stage_slots = 16;
   g_world = w.get();        // comm_exchange during the build reads g_world
   int rc = world_build(w.get(), nranks, devices, ndev);
   if (rc) {

@@ -162,6 +162,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Preload": (I, []),
         "MPIXT_Msgrate": (I, [I, I, I, I, P, P, P, P, P, P, P]),
         "MPIXT_Pingpong": (I, [P, P, P, P, U64, I, P, P, I, I, P, P]),
+        "MPIXT_Pingpong_side": (I, [P, P, U64, I, I, I, P, P]),
         "MPIXT_Selfchain": (I, [P, P, P, I, I, P, P, P]),
         "MPIXT_Empty_loop": (I, [I, P, P, P]),
         "MPIXT_Loopback": (I, [P, P, P, U64, I, P, P, P]),
@@ -576,7 +577,7 @@ class MPWorld:
     collective host steps run over torch.distributed (gloo, CPU). Buffers
     that peers touch must come from `alloc`."""
 
-    def __init__(self, heap_bytes: int = 2 << 30, device: Optional[int] = None):
+    def __init__(self, heap_bytes: int = 4 << 30, device: Optional[int] = None):
         import socket
         import tempfile
 
@@ -752,6 +753,13 @@ class testing:
                                    _stream_handle(s0), _stream_handle(s1), dev0, dev1,
                                    C.byref(ds), C.byref(hs)), "Pingpong")
         return ds.value, hs.value
+
+    @staticmethod
+    def pingpong_side(c, buf, nbytes: int, iters: int, peer: int, initiator: bool, stream):
+        ds = C.c_double()
+        check(lib().MPIXT_Pingpong_side(c.h, _ptr(buf), nbytes, iters, peer, int(initiator),
+                                        _stream_handle(stream), C.byref(ds)), "Pingpong_side")
+        return ds.value
 
     @staticmethod
     def selfchain(c, prod, cons, n: int, iters: int, stream):

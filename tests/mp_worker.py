@@ -15,7 +15,7 @@ from paper_2208_13707_b200 import mpix  # noqa: E402
 
 def main():
     dist.init_process_group("gloo")
-    w = mpix.MPWorld(heap_bytes=1 << 30)
+    w = mpix.MPWorld(heap_bytes=3 << 30)  # arena (1 GiB) + buffers
     r, n, dev = w.rank, w.n, w.device
     peer = 1 - r if n == 2 else (r + 1) % n
     left = (r + n - 1) % n
