@@ -33,6 +33,18 @@ int MPIXT_Stream_create(int device, void **stream);
 int MPIXT_Stream_destroy(void *stream);
 /* One empty kernel (launch-floor measurement). */
 int MPIXT_Empty(void *stream);
+/* Replay-dependent data for CUDA-Graph tests: x[i] = (*iter + 1) * a + b * (i % 7);
+ * check counts mismatches into *bad_dev; bump advances *iter (all in-stream). */
+int MPIXT_Iter_fill(float *x, uint64_t n, const uint32_t *iter, float a, float b, void *stream);
+int MPIXT_Iter_check(const float *x, uint64_t n, const uint32_t *iter, float a, float b,
+                     uint64_t *bad_dev, void *stream);
+int MPIXT_Iter_bump(uint32_t *iter, void *stream);
+/* CUDA-Graph capture of one stream (thread-local capture mode), instantiate,
+ * replay, destroy. */
+int MPIXT_Graph_begin(void *stream);
+int MPIXT_Graph_end(void *stream, void **exec);
+int MPIXT_Graph_launch(void *exec, void *stream);
+int MPIXT_Graph_destroy(void *exec);
 /* fill float buffer: x[i] = value */
 int MPIXT_Fill_f32(float *x, uint64_t n, float value, void *stream);
 

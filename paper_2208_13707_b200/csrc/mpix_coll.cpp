@@ -115,7 +115,26 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
   a.my_exit = reinterpret_cast<uint64_t*>(sh.base[me] + L.coll_exit(0));
   a.err_word = rs.d_err;
   a.spin_limit_ns = g_world->cfg.spin_limit_ns;
+  // CUDA-Graph capture: only graph-capturable comms (device epoch counter,
+  // a decision record of its own); elsewhere the epoch would repeat on replay
+  bool capturing = false;
   {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(c->cu, &cs) != cudaSuccess) return MPIX_ERR_CUDA;
+    capturing = cs != cudaStreamCaptureStatusNone;
+    if (capturing && !c->graph) return MPIX_ERR_UNSUPPORTED;
+  }
+  if (c->graph) {
+    a.gseq = c->d_gseq + 2 * P;
+    const bool fused = kind == CK_ALLREDUCE && bytes <= g_world->cfg.oneshot_max;
+    a.gbump = (fused || P > 1) ? GB_EXIT : GB_ENTRY;  // the chain's last epoch reader
+  }
+  if (capturing) {
+    uint64_t k = rs.grec_next.fetch_add(1);
+    if (k >= kGraphRecs) return MPIX_ERR_NO_MEM;
+    a.rec = rs.d_grec + k;
+    a.opid = k;
+  } else {
     uint64_t opid = rs.op_next.fetch_add(1);
     a.rec = rs.d_rec + (opid % kOpRecords);
     a.opid = opid;

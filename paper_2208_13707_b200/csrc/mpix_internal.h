@@ -54,6 +54,10 @@ struct alignas(32) CollSlot {
 };
 
 // Layout of one rank's per-communicator region.
+// Per-(direction, peer, tag) match-sequence counters a graph-capturable
+// communicator may use (distinct (peer, tag) keys over its lifetime).
+constexpr uint32_t kGraphTagCounters = 1024;
+
 struct RegionLayout {
   int P;       // communicator size
   int R;       // ring slots per ordered pair
@@ -93,8 +97,13 @@ struct RegionLayout {
   __host__ __device__ uint64_t dom_arrival() const { return dom() + 16; }
   __host__ __device__ uint64_t dom_next_spost(int q) const { return dom() + 64 + 8ull * q; }
   __host__ __device__ uint64_t pq() const { return (dom_next_spost(P) + 63) & ~63ull; }
+  // Device sequence counters (graph-capturable communicators, DESIGN.md
+  // §3b): [0,P) send pair sequences, [P,2P) receive pair sequences, 2P the
+  // collective epoch, then kGraphTagCounters per-(direction, peer, tag)
+  // match sequences. Only my own kernels touch them.
+  __host__ __device__ uint64_t gseq() const { return (pq() + ring_bytes() + 63) & ~63ull; }
   __host__ __device__ uint64_t eager_base() const {
-    return (pq() + ring_bytes() + 255) & ~255ull;
+    return (gseq() + 8ull * (2ull * P + 1 + kGraphTagCounters) + 255) & ~255ull;
   }
   // eager payload ring of messages q -> me
   __host__ __device__ uint64_t eager(int q) const {
@@ -187,6 +196,7 @@ struct P2PArgs {
   uint64_t pair_gen;
   uint64_t* pair_mirror;
   uint64_t pair_pseq;
+  int greset;             // captured blocking receive: zero my_done before posting
 };
 
 // Copy grids up to this many CTAs may be launched (and park at
@@ -196,8 +206,10 @@ constexpr uint64_t kEarlyTriggerTiles = 64;
 
 struct WaitEntry {
   uint64_t* flag;
-  uint64_t gen;
+  uint64_t gen;  // kWaitConsume: captured request, wait for 1 then reset to 0
 };
+constexpr uint64_t kWaitConsume = 1ull << 63;
+enum : uint8_t { G_ON = 1, G_LASTP = 2, G_LASTT = 4, G_RESET = 8 };
 
 // One operation of a coalesced batch (k_batch): the P2PArgs fields of an
 // operation, packed (200 B) because the batch travels as kernel parameters.
@@ -242,7 +254,14 @@ struct BatchOp {
   uint16_t R, P, me;
   uint8_t is_recv, mode, blocking, inl, early, dyn, paired;
   int8_t sidx, didx;      // multiplex stream indices (-2 none, -1 ANY)
-  uint8_t pad_[5];
+  // Graph-capturable communicator (G_ON): pseq and the key's match sequence
+  // are relative to the device counters bases[gp] / bases[gt] (`bases`
+  // points at the counter block; dynamic matching is excluded), which the
+  // last CTA of the launch chain advances (G_LASTP / G_LASTT: this is the
+  // batch's last operation on that counter). G_RESET: a captured blocking
+  // receive zeroes its completion word before posting.
+  uint8_t gflags;
+  uint16_t gp, gt;
 };
 static_assert(sizeof(BatchOp) == 200, "BatchOp packing");
 
@@ -252,6 +271,7 @@ constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch
 template <int NOPS, int NWAIT>
 struct BatchArgs {
   int n, nwait;
+  uint32_t* arrive;  // graph counters: CTAs of this (final) launch that have finished; null = none
   int n_static;  // ops[0, n_static): one CTA each; ops[n_static, n): dynamic, one CTA in order
   int early;  // no grouped copy follows: trigger the next (head) kernel at start
   uint64_t spin_limit_ns;
@@ -312,7 +332,12 @@ struct ARArgs {
   int kind;              // CollKind
   int root;              // REDUCE / BCAST
   uint64_t chunk_bytes;  // ALLGATHER: bytes per rank; REDUCE_SCATTER: bytes of my block
+  // graph-capturable communicator: epoch = *gseq + 1, read after
+  // griddepcontrol.wait; the kernel named by gbump advances *gseq at its end
+  uint64_t* gseq;
+  int gbump;             // GB_NONE / GB_ENTRY (P = 1) / GB_EXIT (exit or fused)
 };
+enum : int { GB_NONE = 0, GB_ENTRY = 1, GB_EXIT = 2 };
 
 // Launchers implemented in mpix_kernels.cu (host side). Each returns the
 // number of kernels launched, or -1 on a CUDA error. `sys` selects
@@ -321,7 +346,7 @@ int launch_p2p(const P2PArgs& a, bool sys, bool inline_copy, uint64_t copy_grid,
                cudaEvent_t copy_ev0 = nullptr, cudaEvent_t copy_ev1 = nullptr);
 int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint64_t* err_word,
                  uint64_t spin_limit_ns, bool sys, cudaStream_t s, cudaEvent_t copy_ev0 = nullptr,
-                 cudaEvent_t copy_ev1 = nullptr);
+                 cudaEvent_t copy_ev1 = nullptr, uint32_t* arrive = nullptr);
 int launch_allreduce(const ARArgs& a, bool sys, uint64_t reduce_grid, cudaStream_t s, bool fused);
 // Reduce / Reduce_scatter / Bcast / Allgather / Barrier: entry -> work -> exit.
 int launch_collective(const ARArgs& a, bool sys, uint64_t work_grid, cudaStream_t s);

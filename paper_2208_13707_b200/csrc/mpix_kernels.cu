@@ -939,6 +939,13 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
     a.trace->g0 = globaltimer();
     a.trace->t[0] = clock64();
   }
+  if (a.greset) {  // captured blocking receive: its completion word is reused every replay
+    if (threadIdx.x == 0) {
+      *reinterpret_cast<volatile uint64_t*>(a.my_done) = 0;
+      __threadfence();
+    }
+    __syncthreads();
+  }
   if (a.paired) decide_paired<SYS>(a, s_dc);
   else if (a.dyn) decide_dyn<SYS>(a, s_dc);
   else decide<SYS>(a, s_dc);
@@ -1080,6 +1087,14 @@ __device__ void load_op(const BatchOp& o, uint64_t spin_limit_ns, P2PArgs& a) {
   a.R = o.R;
   a.key = o.key;
   a.pseq = o.pseq;
+  a.greset = 0;
+  if (o.gflags & G_ON) {  // graph-capturable comm: sequences relative to the device counters
+    const volatile uint64_t* g = o.bases;
+    a.pseq = g[o.gp] + o.pseq;
+    const uint32_t t = (uint32_t)g[o.gt] + (uint32_t)o.key;
+    a.key = (o.key & 0xffffffff00000000ull) | t;
+    a.greset = (o.gflags & G_RESET) ? 1 : 0;
+  }
   a.post_ring = o.post_ring;
   a.post_mirror = o.post_mirror;
   a.scan_ring = o.scan_ring;
@@ -1131,8 +1146,35 @@ __device__ void load_op(const BatchOp& o, uint64_t spin_limit_ns, P2PArgs& a) {
 
 template <bool SYS>
 __device__ void wait_all(const WaitEntry* w, int nwait, uint64_t* err_word, uint64_t spin_limit_ns) {
-  for (int i = threadIdx.x; i < nwait; i += blockDim.x)
-    if (!spin_ge<SYS>(w[i].flag, w[i].gen, err_word, spin_limit_ns, ERRW_WAIT_DONE)) break;
+  for (int i = threadIdx.x; i < nwait; i += blockDim.x) {
+    if (w[i].gen & kWaitConsume) {  // captured request: consume the completion (1 -> 0)
+      if (!spin_ge<SYS>(w[i].flag, 1, err_word, spin_limit_ns, ERRW_WAIT_DONE)) break;
+      Scope<SYS>::st_rlx(w[i].flag, 0);
+    } else if (!spin_ge<SYS>(w[i].flag, w[i].gen, err_word, spin_limit_ns, ERRW_WAIT_DONE)) {
+      break;
+    }
+  }
+}
+
+// Graph-capturable comms: the last CTA of a batch's final launch to finish
+// advances the device sequence counters by the batch's per-counter counts
+// (every CTA read them in load_op before, and the next launch of the stream
+// reads them only after griddepcontrol.wait, i.e. after this grid).
+template <int NOPS, int NWAIT>
+__device__ void graph_advance(const BatchArgs<NOPS, NWAIT>& b) {
+  if (!b.arrive || threadIdx.x != 0) return;
+  __threadfence();
+  if (atomicAdd(b.arrive, 1u) != gridDim.x - 1) return;
+  __threadfence();
+  for (int i = 0; i < b.n; ++i) {
+    const BatchOp& o = b.ops[i];
+    if (!(o.gflags & G_ON)) continue;
+    volatile uint64_t* g = o.bases;
+    if (o.gflags & G_LASTP) g[o.gp] = g[o.gp] + o.pseq + 1;
+    if (o.gflags & G_LASTT) g[o.gt] = g[o.gt] + (uint32_t)o.key + 1;
+  }
+  *reinterpret_cast<volatile uint32_t*>(b.arrive) = 0;
+  __threadfence();
 }
 
 template <bool SYS, int NOPS, int NWAIT>
@@ -1163,6 +1205,7 @@ __global__ void __launch_bounds__(kThreads) k_batch(const BatchArgs<NOPS, NWAIT>
   } else {
     wait_all<SYS>(b.w, b.nwait, b.err_word, b.spin_limit_ns);
   }
+  graph_advance(b);
 }
 
 // Grouped copy (PDL behind k_batch): CTA t finds its operation in the tile
@@ -1193,14 +1236,16 @@ __global__ void __launch_bounds__(kThreads) k_gfin(const BatchArgs<NOPS, NWAIT> 
   __shared__ Decision s_dc;
   if ((int)blockIdx.x < b.n) {
     const BatchOp& o = b.ops[blockIdx.x];
-    if (o.inl) return;
-    __shared__ P2PArgs a;
-    if (threadIdx.x == 0) load_op(o, b.spin_limit_ns, a);
-    __syncthreads();
-    fin_body<SYS>(a, s_dc);
+    if (!o.inl) {
+      __shared__ P2PArgs a;
+      if (threadIdx.x == 0) load_op(o, b.spin_limit_ns, a);
+      __syncthreads();
+      fin_body<SYS>(a, s_dc);
+    }
   } else {
     wait_all<SYS>(b.w, b.nwait, b.err_word, b.spin_limit_ns);
   }
+  graph_advance(b);
 }
 
 // ---------------------------------------------------------------------------
@@ -1439,10 +1484,27 @@ __device__ void ar_tile(const ARArgs& a, const uint64_t* sb, const uint64_t* rb,
   for (uint64_t e = p.e0 + gt; e < p.e1; e += gn) reduce_elem<DT, OP>(sb, outs, p.nout, a.P, e);
 }
 
+// Collective epoch: host-assigned, or (graph-capturable comm) the device
+// counter + 1, read after griddepcontrol.wait.
+__device__ __forceinline__ uint64_t coll_epoch(const ARArgs& a) {
+  return a.gseq ? *reinterpret_cast<volatile uint64_t*>(a.gseq) + 1 : a.epoch;
+}
+// ... advanced by the chain's last epoch reader (one thread, after the CTA
+// has read it).
+__device__ __forceinline__ void coll_advance(const ARArgs& a, int where) {
+  __syncthreads();
+  if (a.gseq && a.gbump == where && threadIdx.x == 0) {
+    volatile uint64_t* g = a.gseq;
+    *g = *g + 1;
+    __threadfence();
+  }
+}
+
 // Entry: publish my buffers to every peer, wait for theirs, record them.
 template <bool SYS>
 __global__ void __launch_bounds__(32) k_ar_entry(const ARArgs a) {
   pdl_wait();
+  const uint64_t epoch = coll_epoch(a);
   using M = Scope<SYS>;
   const int q = threadIdx.x;
   const int P = a.P;
@@ -1453,8 +1515,8 @@ __global__ void __launch_bounds__(32) k_ar_entry(const ARArgs a) {
     CollSlot* dst = a.peer_in[q];
     M::st_rlx(&dst->sbuf, (uint64_t)a.sbuf);
     M::st_rlx(&dst->rbuf, (uint64_t)a.rbuf);
-    M::st_rel(&dst->flag, a.epoch);
-    ok = spin_ge<SYS>(&a.my_in[q].flag, a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
+    M::st_rel(&dst->flag, epoch);
+    ok = spin_ge<SYS>(&a.my_in[q].flag, epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
     sb = M::ld_rlx(&a.my_in[q].sbuf);
     rb = M::ld_rlx(&a.my_in[q].rbuf);
     switch (a.kind) {
@@ -1497,6 +1559,7 @@ __global__ void __launch_bounds__(32) k_ar_entry(const ARArgs a) {
     }
     rec->action = act;
   }
+  coll_advance(a, GB_ENTRY);
   pdl_trigger();
 }
 
@@ -1575,6 +1638,7 @@ __global__ void __launch_bounds__(kArThreads) k_ar_fused(const ARArgs a) {
   using M = Scope<SYS>;
   pdl_wait();
   pdl_trigger();
+  const uint64_t epoch = coll_epoch(a);
   __shared__ uint64_t s_sb[kMaxCollRanks], s_rb[kMaxCollRanks];
   __shared__ int s_ok;
   const int q = threadIdx.x;
@@ -1585,8 +1649,8 @@ __global__ void __launch_bounds__(kArThreads) k_ar_fused(const ARArgs a) {
     CollSlot* dst = a.peer_in[q];
     M::st_rlx(&dst->sbuf, (uint64_t)a.sbuf);
     M::st_rlx(&dst->rbuf, (uint64_t)a.rbuf);
-    M::st_rel(&dst->flag, a.epoch);
-    if (!spin_ge<SYS>(&a.my_in[q].flag, a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL))
+    M::st_rel(&dst->flag, epoch);
+    if (!spin_ge<SYS>(&a.my_in[q].flag, epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL))
       s_ok = 0;
     s_sb[q] = M::ld_rlx(&a.my_in[q].sbuf);
     s_rb[q] = M::ld_rlx(&a.my_in[q].rbuf);
@@ -1620,10 +1684,11 @@ __global__ void __launch_bounds__(kArThreads) k_ar_fused(const ARArgs a) {
     if (q == 0) M::fence_ar();
     __syncthreads();
     if (q < P) {
-      M::st_rlx(a.peer_exit[q], a.epoch);
-      spin_ge<SYS>(&a.my_exit[q], a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
+      M::st_rlx(a.peer_exit[q], epoch);
+      spin_ge<SYS>(&a.my_exit[q], epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
     }
   }
+  coll_advance(a, GB_EXIT);
 }
 
 // Exit: tell every peer I am done with its buffers; wait for all of them.
@@ -1634,11 +1699,13 @@ __global__ void __launch_bounds__(32) k_ar_exit(const ARArgs a) {
   using M = Scope<SYS>;
   const int q = threadIdx.x;
   if (a.rec->action == 0) return;
+  const uint64_t epoch = coll_epoch(a);
   M::fence_ar();
   if (q < a.P) {
-    M::st_rlx(a.peer_exit[q], a.epoch);
-    spin_ge<SYS>(&a.my_exit[q], a.epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
+    M::st_rlx(a.peer_exit[q], epoch);
+    spin_ge<SYS>(&a.my_exit[q], epoch, a.err_word, a.spin_limit_ns, ERRW_WAIT_COLL);
   }
+  coll_advance(a, GB_EXIT);
 }
 
 // ---------------------------------------------------------------------------
@@ -1705,8 +1772,9 @@ int launch_p2p(const P2PArgs& a, bool sys, bool inl, uint64_t grid, cudaStream_t
 template <int NOPS, int NWAIT>
 static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwait,
                           uint64_t* err_word, uint64_t spin_limit_ns, bool sys, cudaStream_t s,
-                          cudaEvent_t ev0, cudaEvent_t ev1) {
+                          cudaEvent_t ev0, cudaEvent_t ev1, uint32_t* arrive) {
   BatchArgs<NOPS, NWAIT> b;
+  b.arrive = arrive;  // graph counters: advanced by the final launch
   b.n = n;
   b.nwait = nwait;
   b.spin_limit_ns = spin_limit_ns;
@@ -1744,12 +1812,14 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   const int nw = b.nwait;
   b.nwait = 0;
   b.early = 0;
+  b.arrive = nullptr;  // the counters advance in k_gfin
   {
     cudaError_t e = sys ? launch_head(k_batch<true, NOPS, NWAIT>, head_ctas, kThreads, s, b)
                         : launch_head(k_batch<false, NOPS, NWAIT>, head_ctas, kThreads, s, b);
     if (e != cudaSuccess) return -1;
   }
   b.nwait = nw;
+  b.arrive = arrive;
   if (ev0) cudaEventRecord(ev0, s);  // timing probe (bench roofline) only
   if (launch_pdl(k_gcopy, (int)tiles, kCopyThreads, s, g) != cudaSuccess) return -1;
   if (ev1) cudaEventRecord(ev1, s);
@@ -1762,18 +1832,19 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
 // Parameter-size classes: the whole struct is copied into the launch, so
 // small batches use the small instantiations.
 int launch_batch(const BatchOp* ops, int n, const WaitEntry* w, int nwait, uint64_t* err_word,
-                 uint64_t spin_limit_ns, bool sys, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+                 uint64_t spin_limit_ns, bool sys, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                 uint32_t* arrive) {
   if (n <= 0 && nwait <= 0) return 0;
   if (n <= 4 && nwait <= 8)
-    return launch_batch_t<4, 8>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s, ev0, ev1);
+    return launch_batch_t<4, 8>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s, ev0, ev1, arrive);
   if (n <= 16 && nwait <= 32)
-    return launch_batch_t<16, 32>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s, ev0, ev1);
+    return launch_batch_t<16, 32>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s, ev0, ev1, arrive);
   if (n <= 64 && nwait <= kBatchWaits)
     return launch_batch_t<64, kBatchWaits>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s, ev0,
-                                           ev1);
+                                           ev1, arrive);
   if (n <= kBatchOps && nwait <= kBatchWaits)
     return launch_batch_t<kBatchOps, kBatchWaits>(ops, n, w, nwait, err_word, spin_limit_ns, sys, s,
-                                                  ev0, ev1);
+                                                  ev0, ev1, arrive);
   return -1;
 }
 

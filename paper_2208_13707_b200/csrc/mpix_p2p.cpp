@@ -26,6 +26,19 @@ int flush_locked(StreamBatch& b, cudaStream_t s, const WaitEntry* w, int nwait, 
   int n = (int)b.ops.size();
   int wi = 0;
   uint64_t* err = b.err_word ? b.err_word : w_err;
+  // graph-capturable comms: mark each device counter's last operation (the
+  // final launch advances the counter past it)
+  uint32_t* arrive = nullptr;
+  if (!b.grel.empty()) {
+    arrive = b.d_arrive;
+    std::unordered_set<const uint64_t*> seen;
+    for (int i = n - 1; i >= 0; --i) {
+      BatchOp& o = b.ops[i];
+      if (!(o.gflags & G_ON)) continue;
+      if (seen.insert(o.bases + o.gp).second) o.gflags |= G_LASTP;
+      if (seen.insert(o.bases + o.gt).second) o.gflags |= G_LASTT;
+    }
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_copy_timing.on.load()) {
     bool large_recv = false;
@@ -40,7 +53,7 @@ int flush_locked(StreamBatch& b, cudaStream_t s, const WaitEntry* w, int nwait, 
   do {
     int m = std::min(nwait - wi, kBatchWaits);
     int rc = launch_batch(b.ops.data(), n, w + wi, m, err, cfg.spin_limit_ns, b.sys || wsys, s,
-                          e0, e1);
+                          e0, e1, n ? arrive : nullptr);
     e0 = e1 = nullptr;
     if (rc < 0) return -1;
     launches += rc;
@@ -48,6 +61,7 @@ int flush_locked(StreamBatch& b, cudaStream_t s, const WaitEntry* w, int nwait, 
     b.ops.clear();
     b.first_large_pseq.clear();
     b.post_only.clear();
+    b.grel.clear();
     wi += m;
   } while (wi < nwait);
   b.sys = false;
@@ -157,14 +171,38 @@ Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remot
   return t;
 }
 
-bool decode_ticket(uint64_t h, int* rank, uint64_t* n) {
+// A request created while its stream is captured into a CUDA graph: a
+// completion word of its own, set to 1 by the completion and consumed
+// (reset to 0) by the captured wait, so every replay sees a fresh request.
+constexpr uint64_t kGraphTicket = 1ull << 47;
+
+int new_graph_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remote, Ticket* t) {
+  uint64_t n = rs.gdone_next.fetch_add(1);
+  if (n >= kGraphReqs) return MPIX_ERR_NO_MEM;
+  auto& ri = rs.greqs[n];
+  ri.gen = 1;
+  ri.stream = s;
+  ri.source = source;
+  ri.tag = tag;
+  ri.remote = remote;
+  ri.conventional = false;
+  ri.consumed = false;
+  t->handle = ((uint64_t)(rs.rank + 1) << 48) | kGraphTicket | (n + 1);
+  t->flag = rs.d_gdone + n;
+  t->gen = 1;
+  return MPI_SUCCESS;
+}
+
+bool decode_ticket(uint64_t h, int* rank, uint64_t* n, bool* graph = nullptr) {
   if (h == 0) return false;
   int r = (int)(h >> 48) - 1;
   if (r < 0 || !g_world || r >= g_world->n) return false;
-  uint64_t v = h & ((1ull << 48) - 1);
-  if (v == 0) return false;
+  const bool g = (h & kGraphTicket) != 0;
+  uint64_t v = h & (kGraphTicket - 1);
+  if (v == 0 || (g && v > kGraphReqs)) return false;
   *rank = r;
   *n = v - 1;
+  if (graph) *graph = g;
   return true;
 }
 
@@ -238,6 +276,13 @@ int check_p2p_args(const mpix_comm_s* c, int count, int peer, int tag, bool recv
   return MPI_SUCCESS;
 }
 
+// The stream conventional operations of comm c run on: the rank's internal
+// stream, or — graph-capturable comm, whose device counters must be read
+// and advanced in one stream order — the comm's own stream.
+cudaStream_t conv_stream(const mpix_comm_s* c) {
+  return c->graph && c->cu ? c->cu : rank_of(c->rank).p2p;
+}
+
 // Conventional p2p (Proc::isend/irecv, proc_p2p.cpp:96-113) on GPU buffers:
 // executed on the rank's internal stream, launched at once (no batching:
 // a posted conventional send must progress without a later MPI call).
@@ -249,7 +294,7 @@ int conv_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, i
   int rc = check_p2p_args(c, count, peer, tag, is_recv);
   if (rc) return rc;
   PostHow how;
-  how.stream = rank_of(c->rank).p2p;
+  how.stream = conv_stream(c);
   how.conventional = true;
   return p2p_post(c, buf, count, dt, peer, tag, is_recv, blocking, req, how);
 }
@@ -312,6 +357,20 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   if ((is_recv || !blocking) && !peer_ok(buf, bytes)) return MPIX_ERR_INVALID_ARG;
   if (mp_mode() && !is_recv && blocking && bytes > L.E && bytes > w.cfg.stage_chunk)
     return MPIX_ERR_UNSUPPORTED;  // host staging buffers are not peer-visible
+  // CUDA-Graph capture: a graph-capturable comm takes its
+  // sequence numbers from device counters; any other comm would replay
+  // stale ones (checked here for blocking operations and at the wait, off
+  // the non-blocking fast path).
+  const bool gr = c->graph;
+  bool capturing = false;
+  if (gr || blocking) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(how.stream, &cs) != cudaSuccess) return MPIX_ERR_CUDA;
+    capturing = cs != cudaStreamCaptureStatusNone;
+    if (capturing && !gr) return MPIX_ERR_UNSUPPORTED;
+  }
+  if (capturing && !is_recv && blocking && bytes > L.E && bytes > w.cfg.stage_chunk)
+    return MPIX_ERR_UNSUPPORTED;  // host staging buffers are reclaimed by the host
   std::lock_guard<std::mutex> clk(c->mu);
 
   P2PArgs a = {};
@@ -365,13 +424,32 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
     a.bases = reinterpret_cast<uint64_t*>(sh.base[me] + L.bases());
   }
 
+  // graph-capturable: the pair-sequence counter and the (direction, peer,
+  // tag) match-sequence counter of this operation
+  uint16_t gp = 0, gt = 0;
+  if (gr) {
+    gp = (uint16_t)(is_recv ? sh.P + peer : peer);
+    const uint64_t tk = ((uint64_t)is_recv << 63) | ((uint64_t)(uint32_t)peer << 32) | (uint32_t)tag;
+    auto it = c->gtag.find(tk);
+    if (it == c->gtag.end()) {
+      if (c->gtag.size() >= kGraphTagCounters) return MPIX_ERR_UNSUPPORTED;
+      it = c->gtag.emplace(tk, (uint16_t)(2 * sh.P + 1 + c->gtag.size())).first;
+    }
+    gt = it->second;
+  }
+
   const bool sys = w.cfg.force_sys ||
                    (dyn ? c->any_remote : rank_of(peer).device != rs.device);
   CK(cudaSetDevice(rs.device));
   cudaStream_t s = how.stream;
   Ticket t{};
   if (!blocking || is_recv) {
-    t = new_ticket(rs, s, is_recv ? peer : me, tag, sys, how.conventional);
+    if (capturing) {
+      int rc2 = new_graph_ticket(rs, s, is_recv ? peer : me, tag, sys, &t);
+      if (rc2) return rc2;
+    } else {
+      t = new_ticket(rs, s, is_recv ? peer : me, tag, sys, how.conventional);
+    }
     a.my_done = t.flag;
     a.my_gen = t.gen;
   }
@@ -386,7 +464,7 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
       if (rc2) return rc2;
     }
   }
-  if (rs.d_trace) {
+  if (rs.d_trace && !gr) {
     uint64_t n = rs.trace_next.fetch_add(1);
     a.trace = rs.d_trace + (n % kTraceRecs);
     TraceRec head = {};
@@ -397,7 +475,7 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   }
   bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
   bool post_only = false;
-  if (!inl && !blocking && peer == me && !dyn && !how.conventional) {
+  if (!inl && !blocking && peer == me && !dyn && !how.conventional && !gr) {
     // Self-message whose counterpart has not been enqueued yet: it can only
     // be enqueued later on this same stream (an enqueue comm has one stream),
     // so it runs after this operation, which therefore only posts and never
@@ -406,7 +484,12 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
     auto it = other.find(tagseq_key(me, tag));
     if (it == other.end() || it->second <= tseq) inl = post_only = true;
   }
-  if (!inl) {
+  if (!inl && capturing) {  // a decision record no later operation reuses
+    uint64_t k = rs.grec_next.fetch_add(1);
+    if (k >= kGraphRecs) return MPIX_ERR_NO_MEM;
+    a.rec = rs.d_grec + k;
+    a.opid = k;
+  } else if (!inl) {
     uint64_t op = rs.op_next.fetch_add(1);
     a.rec = rs.d_rec + (op % kOpRecords);
     a.opid = op;
@@ -414,14 +497,14 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   if (!c->batch && !how.conventional) c->batch = &batch_of(s, rs.device);
   StreamBatch& b = how.conventional ? batch_of(s, rs.device) : *c->batch;
   std::lock_guard<std::mutex> lk(b.mu);
-  if (w.cfg.batch && !a.trace) {
+  if ((w.cfg.batch || gr) && !a.trace) {
     // Join the stream's batch; a blocking operation closes it (it must have
     // completed before anything behind it in the stream runs).
     // A self-message whose counterpart is held post-only in this batch: the
     // host has matched them (same comm, same key, static matching), so the
     // two become one paired operation — no descriptors, one copy.
     int pk = -1;
-    if (!dyn && peer == me && (!blocking || is_recv) && a.mode != MODE_STAGED) {
+    if (!dyn && !gr && peer == me && (!blocking || is_recv) && a.mode != MODE_STAGED) {
       for (size_t k = 0; k < b.post_only.size(); ++k) {
         const auto& po = b.post_only[k];
         if (po.comm == c && po.key == a.key && po.is_recv != is_recv) pk = (int)k;
@@ -454,20 +537,50 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
       b.ops[j] = m;
       b.sys |= sys;
     } else {
+      // graph-capturable: sequences relative to the batch's start (the
+      // kernels add the device counters)
+      const uint64_t* pc = c->d_gseq + gp;
+      const uint64_t* tc = c->d_gseq + gt;
+      auto relative = [&] {
+        a.pseq = b.grel[pc];
+        a.key = ((uint64_t)(uint32_t)tag << 32) | b.grel[tc];
+      };
+      if (gr) relative();
       bool flush_first = (int)b.ops.size() >= kBatchOps;
       auto fl = b.first_large_pseq.find(a.post_mirror);
       flush_first |= fl != b.first_large_pseq.end() && a.pseq >= fl->second + (uint64_t)a.R;
       for (auto& po : b.post_only) flush_first |= po.comm == c && po.key == a.key;
-      if (flush_first && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
+      // graph-capturable comm (no host pairing): a blocking self-receive
+      // whose send is in this batch could wait in k_batch for the send's
+      // push, which only the k_gcopy behind it performs — launch the send first
+      flush_first |= gr && blocking && is_recv && peer == me && !b.ops.empty();
+      if (gr && !b.d_arrive) {
+        uint32_t k = rs.arrive_next.fetch_add(1);
+        if (k >= kArriveWords) return MPIX_ERR_NO_MEM;
+        b.d_arrive = rs.d_arrive + k;
+      }
+      if (flush_first) {
+        if (flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
+        if (gr) relative();
+      }
       if (b.ops.empty()) b.err_word = rs.d_err;
       if (!inl && a.post_mirror) b.first_large_pseq.emplace(a.post_mirror, a.pseq);
       if (post_only) b.post_only.push_back({c, a.key, b.ops.size(), (bool)is_recv});
       b.ops.push_back(pack_op(a, inl));
+      if (gr) {
+        BatchOp& o = b.ops.back();
+        o.bases = c->d_gseq;
+        o.gp = gp;
+        o.gt = gt;
+        o.gflags = G_ON | ((capturing && blocking && is_recv) ? G_RESET : 0);
+        b.grel[pc] += 1;
+        b.grel[tc] += 1;
+      }
       b.sys |= sys;
     }
     // a blocking operation closes the batch; conventional operations are
     // launched at once
-    if ((blocking || how.conventional) && flush_locked(b, s, nullptr, 0, false, nullptr) < 0)
+    if ((blocking || how.conventional || !w.cfg.batch) && flush_locked(b, s, nullptr, 0, false, nullptr) < 0)
       return MPIX_ERR_CUDA;
   } else {
     if (!b.ops.empty() && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
@@ -495,18 +608,26 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
   struct Item {
     int rank;
     uint64_t n;
+    bool graph;
   };
   std::vector<Item> items(n);
+  int ngraph = 0;
   for (int i = 0; i < n; ++i) {  // proc_enqueue.cpp:122-123
-    if (!decode_ticket(reqs[i], &items[i].rank, &items[i].n)) return MPIX_ERR_INVALID_REQUEST;
+    if (!decode_ticket(reqs[i], &items[i].rank, &items[i].n, &items[i].graph))
+      return MPIX_ERR_INVALID_REQUEST;
+    ngraph += items[i].graph;
   }
+  auto info = [&](const Item& it) -> RankState::ReqInfo& {
+    RankState& rs = rank_of(it.rank);
+    return it.graph ? rs.greqs[it.n] : rs.reqs[it.n % kReqSlots];
+  };
   cudaStream_t s0 = nullptr;
   int dev0 = -1;
   bool sys = false;
   for (int i = 0; i < n; ++i) {  // proc_enqueue.cpp:124-126
     RankState& rs = rank_of(items[i].rank);
-    auto& ri = rs.reqs[items[i].n % kReqSlots];
-    cudaStream_t s = ri.gen == items[i].n / kReqSlots + 1 ? ri.stream : nullptr;
+    auto& ri = info(items[i]);
+    cudaStream_t s = items[i].graph || ri.gen == items[i].n / kReqSlots + 1 ? ri.stream : nullptr;
     // a conventional request has no queue (proc_enqueue.cpp:124-126, Appendix A6)
     if (ri.conventional) return MPIX_ERR_STREAM_MISMATCH;
     if (i == 0) {
@@ -516,10 +637,15 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
     if (s != s0 || rs.device != dev0) return MPIX_ERR_STREAM_MISMATCH;
     sys |= ri.remote;
   }
+  {  // captured requests are waited inside their capture, the others outside
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s0, &cs) != cudaSuccess) return MPIX_ERR_CUDA;
+    const bool capturing = cs != cudaStreamCaptureStatusNone;
+    if (capturing ? ngraph != n : ngraph != 0) return MPIX_ERR_UNSUPPORTED;
+  }
   if (statuses) {
     for (int i = 0; i < n; ++i) {
-      RankState& rs = rank_of(items[i].rank);
-      auto& ri = rs.reqs[items[i].n % kReqSlots];
+      auto& ri = info(items[i]);
       statuses[i].MPI_SOURCE = ri.source;
       statuses[i].MPI_TAG = ri.tag;
       statuses[i].MPI_ERROR = MPI_SUCCESS;
@@ -533,8 +659,13 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
   for (int k = 0; k < n; ++k) {
     RankState& rs = rank_of(items[k].rank);
     uint64_t nn = items[k].n;
-    we[k].flag = rs.d_done + (nn % kReqSlots);
-    we[k].gen = nn / kReqSlots + 1;
+    if (items[k].graph) {
+      we[k].flag = rs.d_gdone + nn;
+      we[k].gen = kWaitConsume;
+    } else {
+      we[k].flag = rs.d_done + (nn % kReqSlots);
+      we[k].gen = nn / kReqSlots + 1;
+    }
   }
   // The wait closes the stream's batch: one launch for the window.
   StreamBatch& b = batch_of(s0, dev0);
@@ -559,7 +690,9 @@ int host_waitall(int n, MPI_Request* reqs, MPI_Status* statuses) {
   };
   std::vector<Item> items(n);
   for (int i = 0; i < n; ++i) {
-    if (!decode_ticket(reqs[i], &items[i].rank, &items[i].n)) return MPIX_ERR_INVALID_REQUEST;
+    bool graph = false;
+    if (!decode_ticket(reqs[i], &items[i].rank, &items[i].n, &graph)) return MPIX_ERR_INVALID_REQUEST;
+    if (graph) return MPIX_ERR_UNSUPPORTED;  // a captured request is waited in its graph
     auto& ri = rank_of(items[i].rank).reqs[items[i].n % kReqSlots];
     if (ri.gen != items[i].n / kReqSlots + 1 || ri.consumed) return MPIX_ERR_INVALID_REQUEST;
   }
@@ -685,13 +818,13 @@ int MPI_Irecv(void* buf, int count, MPI_Datatype datatype, int source, int tag, 
 
 int MPI_Send(const void* buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm) {
   int rc = conv_post(comm, const_cast<void*>(buf), count, datatype, dest, tag, false, true, nullptr);
-  return rc ? rc : host_blocking(rc, comm, rank_of(comm->rank).p2p, nullptr, dest, tag);
+  return rc ? rc : host_blocking(rc, comm, conv_stream(comm), nullptr, dest, tag);
 }
 
 int MPI_Recv(void* buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
              MPI_Status* status) {
   int rc = conv_post(comm, buf, count, datatype, source, tag, true, true, nullptr);
-  return rc ? rc : host_blocking(rc, comm, rank_of(comm->rank).p2p, status, source, tag);
+  return rc ? rc : host_blocking(rc, comm, conv_stream(comm), status, source, tag);
 }
 
 int MPI_Wait(MPI_Request* request, MPI_Status* status) {

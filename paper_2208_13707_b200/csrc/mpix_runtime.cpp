@@ -107,6 +107,18 @@ int rank_init(RankState& r, const Config& cfg) {
   CK(cudaMemset(r.d_done, 0, kReqSlots * sizeof(uint64_t)));
   CK(cudaMalloc(&r.d_rec, kOpRecords * sizeof(OpRecord)));
   CK(cudaMemset(r.d_rec, 0, kOpRecords * sizeof(OpRecord)));
+  {  // captured requests' completion words (peers store into them too)
+    int rc = mp_mode() ? MPIX_Alloc_mem(kGraphReqs * sizeof(uint64_t), (void**)&r.d_gdone)
+                       : (cudaMalloc(&r.d_gdone, kGraphReqs * sizeof(uint64_t)) == cudaSuccess
+                              ? MPI_SUCCESS : MPIX_ERR_NO_MEM);
+    if (rc) return rc;
+  }
+  CK(cudaMemset(r.d_gdone, 0, kGraphReqs * sizeof(uint64_t)));
+  CK(cudaMalloc(&r.d_grec, kGraphRecs * sizeof(OpRecord)));
+  CK(cudaMemset(r.d_grec, 0, kGraphRecs * sizeof(OpRecord)));
+  CK(cudaMalloc(&r.d_arrive, kArriveWords * sizeof(uint32_t)));
+  CK(cudaMemset(r.d_arrive, 0, kArriveWords * sizeof(uint32_t)));
+  r.greqs.resize(kGraphReqs);
   if (cfg.trace) {
     CK(cudaMalloc(&r.d_trace, kTraceRecs * sizeof(TraceRec)));
     CK(cudaMemset(r.d_trace, 0, kTraceRecs * sizeof(TraceRec)));
@@ -264,6 +276,15 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
   c->cu = c->enqueue_ok ? streams[0]->cu : nullptr;
   c->send_pseq.assign(P, 0);
   c->recv_pseq.assign(P, 0);
+  // graph-capturable: this rank's choice alone (the device counters count
+  // exactly what the host counters would), static matching only
+  {
+    int g = w.cfg.graph ? 1 : 0;
+    for (auto* s : streams)
+      if (s && s->graph >= 0) g = s->graph;
+    c->graph = g && c->enqueue_ok && !sh->dyn;
+    c->d_gseq = reinterpret_cast<uint64_t*>(region + L.gseq());
+  }
   for (int q = 0; q < P; ++q) c->any_remote |= rank_of(q).device != rs.device;
   {
     std::lock_guard<std::mutex> lk(w.comms_mu);
@@ -521,6 +542,9 @@ int MPIX_World_finalize(void) {
     cudaStreamSynchronize(rs->aux);
     if (!w->mp) cudaFree(rs->d_done);
     cudaFree(rs->d_rec);
+    if (!w->mp) cudaFree(rs->d_gdone);
+    cudaFree(rs->d_grec);
+    cudaFree(rs->d_arrive);
     if (rs->d_trace) cudaFree(rs->d_trace);
     cudaFreeHost(rs->h_err);
     cudaStreamDestroy(rs->aux);
@@ -717,6 +741,15 @@ int MPIX_Stream_create(MPI_Info info, MPIX_Stream* stream) {
       s->cu = cs;
       s->device = dev;
       s->exclusive = false;  // proc_stream.cpp:23-24
+    }
+    auto mg = info->entries.find("mpix_graph");  // this library's hint
+    if (mg != info->entries.end()) {
+      if (mg->second == "1" || mg->second == "true")
+        s->graph = 1;
+      else if (mg->second == "0" || mg->second == "false")
+        s->graph = 0;
+      else
+        return MPIX_ERR_BAD_HINT;
     }
     auto mm = info->entries.find("mpix_matching");  // this library's hint
     if (mm != info->entries.end()) {

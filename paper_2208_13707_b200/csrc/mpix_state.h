@@ -16,6 +16,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <unordered_set>
 #include <queue>
 #include <string>
 #include <unordered_map>
@@ -42,6 +43,7 @@ struct Config {
   bool dyn_match = false;            // MPIX_MATCHING=dynamic: device matching engine, wildcards
   int stage_slots = 64;              // MPIX_STAGE_SLOTS: device staging arena slots per rank
   uint64_t stage_chunk = 4ull << 20; // MPIX_STAGE_CHUNK: bytes per arena slot
+  bool graph = false;                // MPIX_GRAPH=1: every enqueue comm is graph-capturable
 
   static Config from_env() {
     Config c;
@@ -66,6 +68,7 @@ struct Config {
     c.stage_slots = (int)geti("MPIX_STAGE_SLOTS", c.stage_slots);
     if (c.stage_slots > 1024) c.stage_slots = 1024;
     c.stage_chunk = (geti("MPIX_STAGE_CHUNK", c.stage_chunk) + 255) & ~255ull;
+    c.graph = geti("MPIX_GRAPH", 0) != 0;
     return c;
   }
 };
@@ -168,7 +171,21 @@ struct RankState {
     bool consumed = false;      // completed by MPI_Wait/Waitall (proc_p2p.cpp:147)
   };
   std::vector<ReqInfo> reqs;
+  // CUDA-Graph capture: requests created while a stream is
+  // being captured get completion words of their own (zeroed, never reused:
+  // a graph may be replayed at any time), as do their decision records;
+  // each captured stream batch gets an arrival word.
+  uint64_t* d_gdone = nullptr;
+  std::atomic<uint64_t> gdone_next{0};
+  std::vector<ReqInfo> greqs;
+  OpRecord* d_grec = nullptr;
+  std::atomic<uint64_t> grec_next{0};
+  uint32_t* d_arrive = nullptr;
+  std::atomic<uint32_t> arrive_next{0};
 };
+constexpr uint64_t kGraphReqs = 1ull << 16;   // captured requests per rank (lifetime)
+constexpr uint64_t kGraphRecs = 4096;         // captured large operations per rank (lifetime)
+constexpr uint32_t kArriveWords = 4096;       // streams with graph-capturable batches per rank
 
 struct CommShared {
   uint32_t ctx = 0;
@@ -211,6 +228,11 @@ struct StreamBatch {
     bool is_recv;
   };
   std::vector<PostOnly> post_only;
+  // graph-capturable comms: operations of this batch per device counter so
+  // far (the next operation's relative sequence), and the arrival word of
+  // the final launch, which advances the counters
+  std::unordered_map<const uint64_t*, uint32_t> grel;
+  uint32_t* d_arrive = nullptr;
 };
 
 }  // namespace mpix
@@ -227,6 +249,7 @@ struct mpix_stream_s {
   int device = -1;
   bool exclusive = true;
   int matching = -1;  // info "mpix_matching": 0 static, 1 dynamic, -1 default
+  int graph = -1;     // info "mpix_graph": 1 graph-capturable comms, 0 not, -1 default
   std::atomic<int> refcount{0};
 };
 
@@ -245,6 +268,12 @@ struct mpix_comm_s {
   std::unordered_map<uint64_t, uint32_t> send_tagseq, recv_tagseq;
   uint64_t coll_epoch = 0;
   uint64_t rv_seq = 0;
+  // Graph-capturable: sequence numbers come from device
+  // counters in my region (RegionLayout::gseq), so a captured operation is
+  // correct on every replay; gtag maps (direction, peer, tag) to a counter.
+  bool graph = false;
+  uint64_t* d_gseq = nullptr;
+  std::unordered_map<uint64_t, uint16_t> gtag;
 };
 
 namespace mpix {

@@ -86,6 +86,25 @@ __global__ void k_delay(uint64_t ns) {
 
 __global__ void k_empty() {}
 
+// Replay-dependent data for CUDA-Graph tests: the iteration comes from a
+// device word the graph itself advances, so every replay moves new values.
+__global__ void k_iter_fill(float* x, uint64_t n, const uint32_t* iter, float a, float b) {
+  const float it = (float)(*iter + 1);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    x[i] = it * a + b * (float)(i % 7);
+}
+__global__ void k_iter_check(const float* x, uint64_t n, const uint32_t* iter, float a, float b,
+                             unsigned long long* bad) {
+  const float it = (float)(*iter + 1);
+  unsigned long long c = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    c += x[i] != it * a + b * (float)(i % 7);
+  if (c) atomicAdd(bad, c);
+}
+__global__ void k_iter_bump(uint32_t* iter) { *iter += 1; }
+
 __global__ void k_fill_f32(float* x, uint64_t n, float v) {
   uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
@@ -253,6 +272,49 @@ int MPIXT_Stencil7(const float* u, float* out, int nx, int ny, int nz, float w0,
   return done(cudaGetLastError());
 }
 
+int MPIXT_Iter_fill(float* x, uint64_t n, const uint32_t* iter, float a, float b, void* stream) {
+  k_iter_fill<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, n, iter, a, b);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Iter_check(const float* x, uint64_t n, const uint32_t* iter, float a, float b,
+                     uint64_t* bad_dev, void* stream) {
+  k_iter_check<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      x, n, iter, a, b, reinterpret_cast<unsigned long long*>(bad_dev));
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Iter_bump(uint32_t* iter, void* stream) {
+  k_iter_bump<<<1, 1, 0, (cudaStream_t)stream>>>(iter);
+  return done(cudaGetLastError());
+}
+
+// CUDA-Graph capture of one stream (thread-local mode: other threads keep
+// launching while this one captures).
+int MPIXT_Graph_begin(void* stream) {
+  return cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal) ==
+                 cudaSuccess ? 0 : 100;
+}
+
+int MPIXT_Graph_end(void* stream, void** exec) {
+  cudaGraph_t g = nullptr;
+  if (cudaStreamEndCapture((cudaStream_t)stream, &g) != cudaSuccess || !g) return 100;
+  cudaGraphExec_t e = nullptr;
+  cudaError_t rc = cudaGraphInstantiate(&e, g, 0);
+  cudaGraphDestroy(g);
+  if (rc != cudaSuccess) return 100;
+  *exec = (void*)e;
+  return 0;
+}
+
+int MPIXT_Graph_launch(void* exec, void* stream) {
+  return cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream) == cudaSuccess ? 0 : 100;
+}
+
+int MPIXT_Graph_destroy(void* exec) {
+  return cudaGraphExecDestroy((cudaGraphExec_t)exec) == cudaSuccess ? 0 : 100;
+}
+
 int MPIXT_Copy_to_host(void* host, const void* dev, uint64_t bytes) {
   return cudaMemcpy(host, dev, bytes, cudaMemcpyDefault) == cudaSuccess ? 0 : 100;
 }
@@ -261,7 +323,8 @@ int MPIXT_Preload(void) {
   cudaFuncAttributes fa;
   const void* ks[] = {(const void*)k_fill_pattern, (const void*)k_checksum, (const void*)k_saxpy,
                       (const void*)k_delay,        (const void*)k_empty,    (const void*)k_fill_f32,
-                      (const void*)k_halo,         (const void*)k_stencil7};
+                      (const void*)k_halo,         (const void*)k_stencil7, (const void*)k_iter_fill,
+                      (const void*)k_iter_check,   (const void*)k_iter_bump};
   int rc = 0;
   for (const void* k : ks)
     if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) rc = 100;

@@ -154,6 +154,13 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Saxpy": (I, [I, C.c_float, P, P, P]),
         "MPIXT_Delay": (I, [U64, P]),
         "MPIXT_Empty": (I, [P]),
+        "MPIXT_Iter_fill": (I, [P, U64, P, C.c_float, C.c_float, P]),
+        "MPIXT_Iter_check": (I, [P, U64, P, C.c_float, C.c_float, P, P]),
+        "MPIXT_Iter_bump": (I, [P, P]),
+        "MPIXT_Graph_begin": (I, [P]),
+        "MPIXT_Graph_end": (I, [P, C.POINTER(P)]),
+        "MPIXT_Graph_launch": (I, [P, P]),
+        "MPIXT_Graph_destroy": (I, [P]),
         "MPIXT_Fill_f32": (I, [P, U64, C.c_float, P]),
         "MPIXT_Halo_pack": (I, [P, I, I, I, I, P, P]),
         "MPIXT_Halo_unpack": (I, [P, I, I, I, I, P, P]),
@@ -713,6 +720,40 @@ class testing:
     @staticmethod
     def empty(stream) -> None:
         check(lib().MPIXT_Empty(_stream_handle(stream)))
+
+    # --- CUDA-Graph helpers: replay-dependent data and raw stream capture ---
+    @staticmethod
+    def iter_fill(x, n: int, it_dev, a: float, b: float, stream) -> None:
+        """x[i] = (*it_dev + 1) * a + b * (i % 7), in-stream."""
+        check(lib().MPIXT_Iter_fill(_ptr(x), n, _ptr(it_dev), a, b, _stream_handle(stream)))
+
+    @staticmethod
+    def iter_check(x, n: int, it_dev, a: float, b: float, bad_dev, stream) -> None:
+        """Adds the number of i with x[i] != (*it_dev + 1) * a + b * (i % 7) to *bad_dev."""
+        check(lib().MPIXT_Iter_check(_ptr(x), n, _ptr(it_dev), a, b, _ptr(bad_dev),
+                                     _stream_handle(stream)))
+
+    @staticmethod
+    def iter_bump(it_dev, stream) -> None:
+        check(lib().MPIXT_Iter_bump(_ptr(it_dev), _stream_handle(stream)))
+
+    @staticmethod
+    def graph_begin(stream) -> None:
+        check(lib().MPIXT_Graph_begin(_stream_handle(stream)), "cudaStreamBeginCapture")
+
+    @staticmethod
+    def graph_end(stream) -> int:
+        h = C.c_void_p()
+        check(lib().MPIXT_Graph_end(_stream_handle(stream), C.byref(h)), "cudaStreamEndCapture")
+        return h.value
+
+    @staticmethod
+    def graph_launch(exec_h: int, stream) -> None:
+        check(lib().MPIXT_Graph_launch(exec_h, _stream_handle(stream)), "cudaGraphLaunch")
+
+    @staticmethod
+    def graph_destroy(exec_h: int) -> None:
+        check(lib().MPIXT_Graph_destroy(exec_h), "cudaGraphExecDestroy")
 
     @staticmethod
     def fill_f32(x, n: int, v: float, stream) -> None:

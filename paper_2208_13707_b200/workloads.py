@@ -85,3 +85,117 @@ def msgrate(world, ctxs, S: int, W: int, batches: int, bufs) -> dict:
             sb.append(bufs[r][k][0])
             rb.append(bufs[r][k][1])
     return mpix.testing.msgrate(comms, streams, sb, rb, devs, P, S, W, batches)
+
+
+def graph_latency(G: int = 64, R: int = 20) -> dict:
+    """Latency-bound patterns enqueued eagerly vs captured into a CUDA graph
+    (DESIGN.md §3b). G iterations are enqueued (or captured once and replayed),
+    R times. Device time comes from CUDA events on each rank's stream, taking
+    the max over ranks. Graph-capturable comms are used for both arms, so the
+    kernels are the same and only the host launch path differs.
+    - loopback_8B: Isend + Irecv + Waitall_enqueue of an 8-byte self-message.
+    - pingpong_8B: Send/Recv_enqueue between 2 ranks sharing GPU 0 (half RTT).
+    - allreduce_4KiB_P2: Allreduce_enqueue (fused single launch), 2 ranks.
+    """
+    import torch
+
+    def world(P):
+        w = mpix.World(P, [0] * P)
+        ctx = {}
+
+        def setup(r):
+            s = mpix.testing.new_stream(0)
+            ctx[r] = (s, w.comm(r).stream_comm_create(mpix.Stream.from_cuda(s, mpix_graph="1")))
+        w.run_ranks(setup)
+        return w, ctx
+
+    def timed(w, ctx, step, P):
+        """step(r, k): enqueue k iterations on rank r's stream. Returns the max
+        over ranks of the stream time for R*G iterations (seconds)."""
+        ev = {r: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for r in range(P)}
+
+        def run(r):
+            s = ctx[r][0]
+            ev[r][0].record(s)
+            for _ in range(R):
+                step(r, G)
+            ev[r][1].record(s)
+        w.run_ranks(lambda r: step(r, 4))  # warm-up
+        for r in range(P):
+            ctx[r][0].synchronize()
+        w.run_ranks(run)
+        for r in range(P):
+            ctx[r][0].synchronize()
+        return max(ev[r][0].elapsed_time(ev[r][1]) for r in range(P)) / 1e3
+
+    def both(w, ctx, P, enqueue):
+        """enqueue(r, k) enqueues k iterations; returns (eager_us, graph_us)."""
+        t_eager = timed(w, ctx, enqueue, P)
+        execs = {}
+
+        def cap(r):
+            s = ctx[r][0]
+            s.synchronize()
+            mpix.testing.graph_begin(s)
+            try:
+                enqueue(r, G)
+            finally:
+                execs[r] = mpix.testing.graph_end(s)
+        w.run_ranks(cap)
+
+        def replay(r, k):
+            s = ctx[r][0]
+            for _ in range(max(1, k // G)):
+                mpix.testing.graph_launch(execs[r], s)
+        t_graph = timed(w, ctx, replay, P)
+        for e in execs.values():
+            mpix.testing.graph_destroy(e)
+        n = R * G
+        return t_eager / n * 1e6, t_graph / n * 1e6
+
+    out = {"iterations_per_graph": G, "replays": R}
+    w, ctx = world(1)
+    a = torch.zeros(8, dtype=torch.uint8, device=0)
+    b = torch.zeros(8, dtype=torch.uint8, device=0)
+    c0 = ctx[0][1]
+
+    def loop(r, k):
+        for _ in range(k):
+            rq = [c0.isend_enqueue(a, 8, mpix.MPI_BYTE, 0, 1),
+                  c0.irecv_enqueue(b, 8, mpix.MPI_BYTE, 0, 1)]
+            mpix.waitall_enqueue(rq)
+    e, g = both(w, ctx, 1, loop)
+    out["loopback_8B"] = {"eager_us": e, "graph_us": g}
+    w.finalize()
+
+    w, ctx = world(2)
+    bufs = {r: (torch.zeros(8, dtype=torch.uint8, device=0),
+                torch.zeros(8, dtype=torch.uint8, device=0)) for r in range(2)}
+
+    def pp(r, k):
+        c = ctx[r][1]
+        sb, rb = bufs[r]
+        for _ in range(k):
+            if r == 0:
+                c.send_enqueue(sb, 8, mpix.MPI_BYTE, 1, 2)
+                c.recv_enqueue(rb, 8, mpix.MPI_BYTE, 1, 3)
+            else:
+                c.recv_enqueue(rb, 8, mpix.MPI_BYTE, 0, 2)
+                c.send_enqueue(sb, 8, mpix.MPI_BYTE, 0, 3)
+    e, g = both(w, ctx, 2, pp)
+    out["pingpong_8B_half_rtt"] = {"eager_us": e / 2, "graph_us": g / 2}
+
+    xs = {r: (torch.ones(1024, device=0), torch.zeros(1024, device=0)) for r in range(2)}
+
+    def ar(r, k):
+        c = ctx[r][1]
+        x, y = xs[r]
+        for _ in range(k):
+            c.allreduce_enqueue(x, y, 1024, mpix.MPI_FLOAT)
+    e, g = both(w, ctx, 2, ar)
+    out["allreduce_4KiB_P2"] = {"eager_us": e, "graph_us": g}
+    for r in range(2):
+        ctx[r][0].synchronize()
+    w.finalize()
+    return out
