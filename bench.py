@@ -971,6 +971,11 @@ def extras_multirank(args, mpix, torch):
             os.environ.pop("MPIX_MATCHING", None)
         else:
             os.environ["MPIX_MATCHING"] = prev
+
+    # CUDA-Graph capture: the same latency-bound patterns enqueued eagerly
+    # from Python vs captured once and replayed (graph-capturable comms)
+    from paper_2208_13707_b200.workloads import graph_latency
+    out["graph_replay"] = graph_latency()
     return out
 
 
