@@ -95,6 +95,34 @@ def main():
         raise AssertionError("non-heap receive buffer accepted")
     except mpix.MPIXError as e:
         assert e.name == "INVALID_ARG", e.name
+    # 7. CUDA-Graph capture across processes: a graph-capturable comm, a
+    #    captured ring exchange + allreduce, replayed with device-side checks
+    s2 = mpix.testing.new_stream(dev)
+    gc = w.comm().stream_comm_create(mpix.Stream.from_cuda(s2, mpix_graph="1"))
+    m = 70000
+    gx = w.alloc(m, torch.float32)
+    gy = w.alloc(m, torch.float32)
+    gz = w.alloc(m, torch.float32)
+    it = torch.zeros(1, dtype=torch.int32, device=dev)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    mpix.testing.graph_begin(s2)
+    mpix.testing.iter_fill(gx, m, it, float(r + 1), 1.0, s2)
+    rq = [gc.irecv_enqueue(gy, m, mpix.MPI_FLOAT, left, 4),
+          gc.isend_enqueue(gx, m, mpix.MPI_FLOAT, (r + 1) % n, 4)]
+    mpix.waitall_enqueue(rq)
+    mpix.testing.iter_check(gy, m, it, float(left + 1), 1.0, bad, s2)
+    gc.allreduce_enqueue(gx, gz, m, mpix.MPI_FLOAT)
+    mpix.testing.iter_check(gz, m, it, n * (n + 1) / 2, float(n), bad, s2)
+    mpix.testing.iter_bump(it, s2)
+    gexec = mpix.testing.graph_end(s2)
+    for _ in range(6):
+        mpix.testing.graph_launch(gexec, s2)
+    s2.synchronize()
+    mpix.testing.graph_destroy(gexec)
+    assert it.item() == 6 and bad.item() == 0, ("graph", it.item(), bad.item())
+    gc.free()
     assert mpix.rank_error(r) == 0
     c.free()
     w.finalize()
