@@ -242,8 +242,13 @@ __device__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
         sn.bytes = M::ld_rlx(&s->bytes);
         sn.done_addr = M::ld_rlx(&s->done_addr);
         sn.done_val = M::ld_rlx(&s->done_val);
-        M::fence_ar();
-        ok = ((sn.state & 0xff) == ST_POSTED) && sn.key == key && M::ld_rlx(&s->state) == sn.state;
+        // No re-validation: a state moves POSTED(pseq) -> TAKEN -> FREE ->
+        // POSTED(pseq + R) only, and the fields change only with a new post,
+        // so they belong to this post as long as the state does — which the
+        // snapshot's user either proves by CAS on exactly sn.state (taking a
+        // send descriptor) or owns (a receive descriptor only its one
+        // matching sender reads).
+        ok = ((sn.state & 0xff) == ST_POSTED) && sn.key == key;
       }
       ok = __shfl_sync(0xffffffffu, ok, src);
       if (ok) {
@@ -310,7 +315,10 @@ __device__ void post_desc(const P2PArgs& a, uint64_t addr, uint64_t bytes, uint6
   M::st_rlx(&d->bytes, bytes);
   M::st_rlx(&d->done_addr, done_addr);
   M::st_rlx(&d->done_val, done_val);
-  if (others_wrote) M::fence_ar();  // payload written by other threads/CTAs
+  // Payload written by other threads of the CTA (others_wrote): ordered by
+  // the CTA barrier before this call plus the release store's fence (one
+  // MEMBAR; a separate fence here would emit a second).
+  (void)others_wrote;
   M::st_rel(&d->state, st_word(a.pseq, ST_POSTED));
   M::fence_sc();  // Dekker: my post is visible before I rescan
 }
