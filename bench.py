@@ -944,8 +944,13 @@ def extras_multirank(args, mpix, torch):
     w.run_ranks(setup)
     bufs = [[(torch.zeros(2, dtype=torch.int32, device=devs[r]),
               torch.zeros((W, 2), dtype=torch.int32, device=devs[r])) for _ in range(S)] for r in range(P)]
+    # host-bound (enqueue threads): warm up twice, report the median of 3 runs
     msgrate(w, ctxs, S, W, 1, bufs)
-    res = msgrate(w, ctxs, S, W, B, bufs)
+    for _ in range(2):
+        msgrate(w, ctxs, S, W, B, bufs)
+    runs = sorted((msgrate(w, ctxs, S, W, B, bufs) for _ in range(3)), key=lambda x: x["msgs_per_s"])
+    res = dict(runs[1])
+    res["runs_msgs_per_s"] = [x["msgs_per_s"] for x in runs]
     for d in range(ndev):
         torch.cuda.synchronize(d)
     out["msgrate_8B"] = {"ranks": P, "streams_per_rank": S, "window": W, **res,

@@ -71,6 +71,14 @@ namespace mpix {
                    : "memory");                                                                   \
       return o;                                                                                   \
     }                                                                                             \
+    static __device__ __forceinline__ uint64_t cas_acq(uint64_t* p, uint64_t c, uint64_t v) {     \
+      uint64_t o;                                                                                 \
+      asm volatile("atom.acquire." SC ".global.cas.b64 %0, [%1], %2, %3;"                       \
+                   : "=l"(o)                                                                      \
+                   : "l"(p), "l"(c), "l"(v)                                                       \
+                   : "memory");                                                                   \
+      return o;                                                                                   \
+    }                                                                                             \
     static __device__ __forceinline__ void fence_sc() { asm volatile("fence.sc." SC ";" ::: "memory"); } \
     static __device__ __forceinline__ void fence_ar() {                                           \
       asm volatile("fence.acq_rel." SC ";" ::: "memory");                                        \
@@ -447,7 +455,9 @@ __device__ bool dom_lock(uint64_t* lock, const P2PArgs& a) {
   using M = Scope<SYS>;
   const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
   unsigned ns = 32;
-  while (M::cas(lock, 0, 1) != 0) {
+  // acquire only: everything of the previous holder is published by its
+  // release (dom_unlock); nothing of mine precedes the lock
+  while (M::cas_acq(lock, 0, 1) != 0) {
     __nanosleep(ns);
     if (ns < 512) ns <<= 1;
     if (a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
@@ -621,14 +631,13 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
     if (s_stage == 1) {  // eager: payload into my slot of the receiver's eager ring first
       const int slot = (int)(a.pseq % (uint64_t)a.R);
       cta_copy(a.eager_ring + (uint64_t)slot * a.E, a.buf, a.bytes);
-      __syncthreads();
-      if (threadIdx.x == 0) M::fence_ar();
+      __syncthreads();  // published by the unlock's release (after the CTA barrier)
     }
     if (warp == 0 && s_stage != 0) {
       int got = lane == 0 ? (int)dom_lock<SYS>(D.lock, a) : 0;
       got = __shfl_sync(0xffffffffu, got, 0);
       if (got) {
-        M::fence_ar();
+        __syncwarp();  // lane 0's acquire orders the other lanes' scan loads
         const int j = dyn_scan_recvs<SYS>(a, D.pq);
         if (lane == 0) {
           if (j >= 0) {
@@ -674,7 +683,7 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
     }
     got = __shfl_sync(0xffffffffu, got, 0);
     if (got) {
-      M::fence_ar();
+      __syncwarp();  // lane 0's acquire orders the other lanes' scan loads
       int sslot = 0;
       const int q = dyn_scan_sends<SYS>(a, my_base, L, &sslot);
       if (lane == 0) {
@@ -744,7 +753,7 @@ __device__ void stage_publish_dyn(const P2PArgs& a, Decision& dc) {
     got = __shfl_sync(0xffffffffu, got, 0);
     if (lane == 0) s_push = 0;
     if (got) {
-      M::fence_ar();
+      __syncwarp();  // lane 0's acquire orders the other lanes' scan loads
       const int j = dyn_scan_recvs<SYS>(a, D.pq);
       if (lane == 0) {
         if (j >= 0) {
