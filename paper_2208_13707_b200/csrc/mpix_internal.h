@@ -284,8 +284,16 @@ struct BatchArgs {
 // [tile_start[j], tile_start[j+1]) belong to large operation j.
 struct GCopyArgs {
   int m;
+  // direct: every large operation is a host-paired self-message, so its copy
+  // (src, dst, bytes) is known at launch — the grid copies without waiting
+  // for k_batch's decisions (k_batch triggers it at once; CTA 0 waits for
+  // k_batch after its tile, so k_gfin still runs after both)
+  int direct;
   uint32_t tile_start[kBatchOps + 1];
   OpRecord* rec[kBatchOps];
+  const uint8_t* src[kBatchOps];
+  uint8_t* dst[kBatchOps];
+  uint64_t nbytes[kBatchOps];
 };
 
 enum ARDtype : int { AR_I32 = 0, AR_F32 = 1, AR_BF16 = 2, AR_F64 = 3 };

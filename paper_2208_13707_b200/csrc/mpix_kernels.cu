@@ -1228,13 +1228,22 @@ __global__ void __launch_bounds__(kThreads) k_batch(const BatchArgs<NOPS, NWAIT>
 // Grouped copy (PDL behind k_batch): CTA t finds its operation in the tile
 // prefix table and streams one tile of it.
 __global__ void __launch_bounds__(kCopyThreads, 2) k_gcopy(const GCopyArgs g) {
-  pdl_wait();
+  if (!g.direct) pdl_wait();
   const uint32_t t = blockIdx.x;
   int lo = 0, hi = g.m - 1;
   while (lo < hi) {  // last j with tile_start[j] <= t
     const int mid = (lo + hi + 1) >> 1;
     if (g.tile_start[mid] <= t) lo = mid;
     else hi = mid - 1;
+  }
+  if (g.direct) {
+    // launched once k_batch passed its own griddepcontrol.wait: everything
+    // before k_batch in the stream is complete, so the sources are ready
+    tile_copy(g.dst[lo], g.src[lo], g.nbytes[lo], t - g.tile_start[lo],
+              g.tile_start[lo + 1] - g.tile_start[lo]);
+    if (blockIdx.x == 0) pdl_wait();  // this grid completes after k_batch
+    pdl_trigger();
+    return;
   }
   const OpRecord* rec = g.rec[lo];
   const uint64_t action = rec->action;
@@ -1808,12 +1817,18 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   for (int i = 0; i < nwait; ++i) b.w[i] = w[i];
   GCopyArgs g;
   g.m = 0;
+  g.direct = 1;
   uint64_t tiles = 0;
   for (int i = 0; i < n; ++i) {
-    if (b.ops[i].inl) continue;
+    const BatchOp& o = b.ops[i];
+    if (o.inl) continue;
     g.tile_start[g.m] = (uint32_t)tiles;
-    g.rec[g.m] = b.ops[i].rec;
-    tiles += p2p_copy_grid(b.ops[i].bytes);
+    g.rec[g.m] = o.rec;
+    g.direct &= o.paired ? 1 : 0;
+    g.src[g.m] = o.paired ? o.pr.src : nullptr;
+    g.dst[g.m] = o.buf;
+    g.nbytes[g.m] = o.paired ? (o.pr.bytes < o.bytes ? o.pr.bytes : o.bytes) : 0;
+    tiles += p2p_copy_grid(o.bytes);
     ++g.m;
   }
   g.tile_start[g.m] = (uint32_t)tiles;
@@ -1828,7 +1843,7 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   // decisions (the wait moves to k_gfin) -> grouped copy -> completions + wait
   const int nw = b.nwait;
   b.nwait = 0;
-  b.early = 0;
+  b.early = g.direct;  // a direct copy grid starts as soon as k_batch has waited
   b.arrive = nullptr;  // the counters advance in k_gfin
   {
     cudaError_t e = sys ? launch_head(k_batch<true, NOPS, NWAIT>, head_ctas, kThreads, s, b)
