@@ -1180,18 +1180,20 @@ __device__ void wait_all(const WaitEntry* w, int nwait, uint64_t* err_word, uint
 template <int NOPS, int NWAIT>
 __device__ void graph_advance(const BatchArgs<NOPS, NWAIT>& b) {
   if (!b.arrive || threadIdx.x != 0) return;
-  __threadfence();
+  __threadfence();  // my counter reads (load_op) before my arrival
   if (atomicAdd(b.arrive, 1u) != gridDim.x - 1) return;
-  __threadfence();
+  // Fire-and-forget reductions (no round trip each): the next reader is a
+  // later launch of this stream, ordered behind this grid's completion.
   for (int i = 0; i < b.n; ++i) {
     const BatchOp& o = b.ops[i];
     if (!(o.gflags & G_ON)) continue;
-    volatile uint64_t* g = o.bases;
-    if (o.gflags & G_LASTP) g[o.gp] = g[o.gp] + o.pseq + 1;
-    if (o.gflags & G_LASTT) g[o.gt] = g[o.gt] + (uint32_t)o.key + 1;
+    if (o.gflags & G_LASTP)
+      atomicAdd(reinterpret_cast<unsigned long long*>(o.bases + o.gp), o.pseq + 1);
+    if (o.gflags & G_LASTT)
+      atomicAdd(reinterpret_cast<unsigned long long*>(o.bases + o.gt),
+                (unsigned long long)(uint32_t)o.key + 1);
   }
   *reinterpret_cast<volatile uint32_t*>(b.arrive) = 0;
-  __threadfence();
 }
 
 template <bool SYS, int NOPS, int NWAIT>
@@ -1519,11 +1521,8 @@ __device__ __forceinline__ uint64_t coll_epoch(const ARArgs& a) {
 // has read it).
 __device__ __forceinline__ void coll_advance(const ARArgs& a, int where) {
   __syncthreads();
-  if (a.gseq && a.gbump == where && threadIdx.x == 0) {
-    volatile uint64_t* g = a.gseq;
-    *g = *g + 1;
-    __threadfence();
-  }
+  if (a.gseq && a.gbump == where && threadIdx.x == 0)  // read by a later launch only
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.gseq), 1ull);
 }
 
 // Entry: publish my buffers to every peer, wait for theirs, record them.

@@ -167,6 +167,22 @@ def graph_latency(G: int = 64, R: int = 20) -> dict:
             mpix.waitall_enqueue(rq)
     e, g = both(w, ctx, 1, loop)
     out["loopback_8B"] = {"eager_us": e, "graph_us": g}
+
+    # in-stream chain: producer kernel -> Send_enqueue -> Recv_enqueue ->
+    # consumer kernel (8 B self-message, one stream)
+    x = torch.zeros(2, dtype=torch.float32, device=0)
+    y = torch.zeros(2, dtype=torch.float32, device=0)
+    s0 = ctx[0][0]
+
+    def chain(r, k):
+        for _ in range(k):
+            mpix.testing.fill_f32(x, 2, 1.0, s0)
+            c0.send_enqueue(x, 2, mpix.MPI_FLOAT, 0, 3)
+            c0.recv_enqueue(y, 2, mpix.MPI_FLOAT, 0, 3)
+            mpix.testing.saxpy(2, 1.0, y, x, s0)
+    e, g = both(w, ctx, 1, chain)
+    out["self_chain_8B"] = {"eager_us": e, "graph_us": g,
+                            "kernels": "producer + send + recv + consumer"}
     w.finalize()
 
     w, ctx = world(2)
