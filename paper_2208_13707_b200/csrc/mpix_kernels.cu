@@ -509,16 +509,28 @@ __device__ int dyn_scan_sends(const P2PArgs& a, uint8_t* my_base, const RegionLa
   const int q0 = a.peer >= 0 ? a.peer : 0, q1 = a.peer >= 0 ? a.peer + 1 : a.P;
   for (int q = q0; q < q1; ++q) {
     SlotDesc* ring = reinterpret_cast<SlotDesc*>(my_base + L.sr(q));
-    for (int i = lane; i < a.R; i += 32) {
-      uint64_t st, key;
-      ld_pair<SYS>(&ring[i], st, key);
-      if ((st & 0xff) == ST_POSTED && tag_ok(a.tag, (int32_t)(key >> 32)) &&
-          idx_ok(idx_enc(a.sidx), idx_enc(a.didx), (key >> 24) & 0xff, (key >> 16) & 0xff)) {
-        uint64_t arr = Scope<SYS>::ld_rlx(&ring[i].pad[0]);
-        if (arr < best) {
-          best = arr;
-          best_idx = q * a.R + i;
-        }
+    // every load of this source's ring first (one round trip, not one per
+    // slot): under the lock no descriptor can become POSTED meanwhile
+    uint64_t st[kMaxScanPerLane], ky[kMaxScanPerLane], ar[kMaxScanPerLane];
+#pragma unroll
+    for (int k = 0; k < kMaxScanPerLane; ++k) {
+      const int i = k * 32 + lane;
+      st[k] = 0;
+      ky[k] = 0;
+      ar[k] = ~0ull;
+      if (i < a.R) {
+        ld_pair<SYS>(&ring[i], st[k], ky[k]);
+        ar[k] = Scope<SYS>::ld_rlx(&ring[i].pad[0]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxScanPerLane; ++k) {
+      const int i = k * 32 + lane;
+      if (i < a.R && (st[k] & 0xff) == ST_POSTED && tag_ok(a.tag, (int32_t)(ky[k] >> 32)) &&
+          idx_ok(idx_enc(a.sidx), idx_enc(a.didx), (ky[k] >> 24) & 0xff, (ky[k] >> 16) & 0xff) &&
+          ar[k] < best) {
+        best = ar[k];
+        best_idx = q * a.R + i;
       }
     }
   }
@@ -535,16 +547,25 @@ __device__ int dyn_scan_recvs(const P2PArgs& a, SlotDesc* pq) {
   const int lane = threadIdx.x & 31;
   uint64_t best = ~0ull;
   int best_idx = 0x7fffffff;
-  for (int i = lane; i < a.R; i += 32) {
-    uint64_t st, key;
-    ld_pair<SYS>(&pq[i], st, key);
-    const int32_t src = (int32_t)(key >> 32), tg = (int32_t)(uint32_t)key;
-    if ((st & 0xff) == ST_POSTED && (src < 0 || src == a.me) && tag_ok(tg, a.tag) &&
-        [&] {
-          const uint64_t f = Scope<SYS>::ld_rlx(&pq[i].pad[0]);
-          return idx_ok((f >> 8) & 0xff, f & 0xff, idx_enc(a.sidx), idx_enc(a.didx));
-        }()) {
-      const uint64_t rseq = st >> 8;
+  uint64_t st[kMaxScanPerLane], ky[kMaxScanPerLane], fl[kMaxScanPerLane];
+#pragma unroll
+  for (int k = 0; k < kMaxScanPerLane; ++k) {  // all loads first (lock held)
+    const int i = k * 32 + lane;
+    st[k] = 0;
+    ky[k] = 0;
+    fl[k] = 0;
+    if (i < a.R) {
+      ld_pair<SYS>(&pq[i], st[k], ky[k]);
+      fl[k] = Scope<SYS>::ld_rlx(&pq[i].pad[0]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxScanPerLane; ++k) {
+    const int i = k * 32 + lane;
+    const int32_t src = (int32_t)(ky[k] >> 32), tg = (int32_t)(uint32_t)ky[k];
+    if (i < a.R && (st[k] & 0xff) == ST_POSTED && (src < 0 || src == a.me) && tag_ok(tg, a.tag) &&
+        idx_ok((fl[k] >> 8) & 0xff, fl[k] & 0xff, idx_enc(a.sidx), idx_enc(a.didx))) {
+      const uint64_t rseq = st[k] >> 8;
       if (rseq < best) {
         best = rseq;
         best_idx = i;
