@@ -214,7 +214,14 @@ int acquire_staging(RankState& rs, uint64_t bytes, cudaStream_t s, uint8_t** p, 
   int best = -1;
   for (size_t b = 0; b < rs.stage.size(); ++b) {
     auto& sb = rs.stage[b];
-    bool free = *reinterpret_cast<volatile uint64_t*>(&rs.h_stage[b]) >= sb.gen;
+    uint64_t rel = 0;  // the buffer's release word
+    if (mp_mode()) {   // in heap memory (a peer process releases it)
+      if (cudaMemcpy(&rel, rs.d_stage + b, sizeof(rel), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return MPIX_ERR_CUDA;
+    } else {
+      rel = *reinterpret_cast<volatile uint64_t*>(&rs.h_stage[b]);
+    }
+    bool free = rel >= sb.gen;
     if (free && sb.size >= bytes && (best < 0 || sb.size < rs.stage[best].size)) best = (int)b;
   }
   if (best < 0) {
@@ -222,7 +229,11 @@ int acquire_staging(RankState& rs, uint64_t bytes, cudaStream_t s, uint8_t** p, 
     uint64_t size = 1ull << 20;
     while (size < bytes) size <<= 1;
     RankState::StageBuf sb;
-    if (cudaMallocFromPoolAsync((void**)&sb.p, size, rs.pool, s) != cudaSuccess) return MPIX_ERR_NO_MEM;
+    if (mp_mode()) {  // the receiver (another process) pulls from it
+      if (MPIX_Alloc_mem(size, (void**)&sb.p)) return MPIX_ERR_NO_MEM;
+    } else if (cudaMallocFromPoolAsync((void**)&sb.p, size, rs.pool, s) != cudaSuccess) {
+      return MPIX_ERR_NO_MEM;
+    }
     sb.size = size;
     rs.stage.push_back(sb);
     best = (int)rs.stage.size() - 1;
@@ -355,8 +366,6 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   // Isend buffer pulled by the receiver, so both must be heap memory; a
   // blocking send reads its own buffer (eager or staged copies).
   if ((is_recv || !blocking) && !peer_ok(buf, bytes)) return MPIX_ERR_INVALID_ARG;
-  if (mp_mode() && !is_recv && blocking && bytes > L.E && bytes > w.cfg.stage_chunk)
-    return MPIX_ERR_UNSUPPORTED;  // host staging buffers are not peer-visible
   // CUDA-Graph capture: a graph-capturable comm takes its
   // sequence numbers from device counters; any other comm would replay
   // stale ones (checked here for blocking operations and at the wait, off

@@ -130,7 +130,14 @@ int rank_init(RankState& r, const Config& cfg) {
   CK(cudaStreamCreateWithFlags(&r.p2p, cudaStreamNonBlocking));
   CK(cudaHostAlloc(&r.h_stage, kStageSlots * sizeof(uint64_t), cudaHostAllocMapped | cudaHostAllocPortable));
   memset(r.h_stage, 0, kStageSlots * sizeof(uint64_t));
-  CK(cudaHostGetDevicePointer(&r.d_stage, r.h_stage, 0));
+  if (mp_mode()) {
+    // a peer process releases my staging buffers: the flags must be heap
+    // memory (host-mapped memory of this process is not visible to it)
+    if (MPIX_Alloc_mem(kStageSlots * sizeof(uint64_t), (void**)&r.d_stage)) return MPIX_ERR_NO_MEM;
+    CK(cudaMemset(r.d_stage, 0, kStageSlots * sizeof(uint64_t)));
+  } else {
+    CK(cudaHostGetDevicePointer(&r.d_stage, r.h_stage, 0));
+  }
   r.reqs.resize(kReqSlots);
   if (preload_kernels() != 0) return MPIX_ERR_CUDA;
   MPIXT_Preload();
@@ -534,7 +541,8 @@ int MPIX_World_finalize(void) {
   for (auto& rs : w->ranks) {
     if (!rs->hosted) continue;
     cudaSetDevice(rs->device);
-    for (auto& sb : rs->stage) cudaFreeAsync(sb.p, rs->aux);
+    if (!w->mp)  // multi-process: heap memory, released with the heap
+      for (auto& sb : rs->stage) cudaFreeAsync(sb.p, rs->aux);
     if (!w->mp) {
       if (rs->d_arena) cudaFreeAsync(rs->d_arena, rs->aux);
       if (rs->d_arena_state) cudaFreeAsync(rs->d_arena_state, rs->aux);

@@ -50,6 +50,24 @@ def main():
             s.synchronize()
             if r == 0:
                 assert torch.equal(dst[:nb].cpu(), pay[0][:nb]), ("pingpong", nb)
+    # 2b. a blocking send larger than an arena slot (64 MiB) before its
+    #     receive is posted: staged through a heap staging buffer
+    big = 80 << 20
+    ref = pay[0].repeat(big // (6 << 20) + 1)[:big]
+    if r < 2:
+        bs = w.alloc(big)
+        br = w.alloc(big)
+        bs.copy_(ref.to(dev))
+        torch.cuda.synchronize(dev)
+    dist.barrier()
+    if r == 0:
+        c.send_enqueue(bs, big, mpix.MPI_BYTE, 1, 30)
+        s.synchronize()  # completes before the receive exists: staged
+    dist.barrier()
+    if r == 1:
+        c.recv_enqueue(br, big, mpix.MPI_BYTE, 0, 30)
+        s.synchronize()
+        assert torch.equal(br.cpu(), ref), "staged send > 64 MiB"
     dist.barrier()
     # 3. allreduce (fp32, exactly representable inputs: any order is exact)
     cnt = (1 << 20) + 5
