@@ -129,6 +129,9 @@ int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void* b0, void* b1, uint64_t bytes,
   side(0);
   t.join();
   cudaEventSynchronize(b);
+  cudaSetDevice(dev1);
+  cudaStreamSynchronize((cudaStream_t)s1);  // rank 1's last send retired too
+  cudaSetDevice(dev0);
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
   cudaEventDestroy(a);
