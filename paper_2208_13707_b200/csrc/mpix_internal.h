@@ -272,7 +272,9 @@ template <int NOPS, int NWAIT>
 struct BatchArgs {
   int n, nwait;
   uint32_t* arrive;  // graph counters: CTAs of this (final) launch that have finished; null = none
-  int n_static;  // ops[0, n_static): one CTA each; ops[n_static, n): dynamic, one CTA in order
+  int n_static;  // ops[0, n_static): one CTA each; then dynamic ops, in order:
+  int n_drecv;   // receives [n_static, n_drecv) in one CTA, sends [n_drecv, n) in another
+                 // (a batch closed by a blocking receive: all of them in one CTA, in order)
   int early;  // no grouped copy follows: trigger the next (head) kernel at start
   uint64_t spin_limit_ns;
   uint64_t* err_word;

@@ -1229,21 +1229,36 @@ __global__ void __launch_bounds__(kThreads) k_batch(const BatchArgs<NOPS, NWAIT>
     __syncthreads();
     if (o.inl) proto_body<SYS, true>(a, s_dc);
     else proto_body<SYS, false>(a, s_dc);  // decision -> op record; triggers k_gcopy
-  } else if ((int)blockIdx.x == b.n_static && b.n > b.n_static) {
-    // Dynamic-matching operations run one after another in this CTA, in
-    // batch order: their matching is serialised by the receiver's lock and
-    // tickets anyway, and one CTA per stream (instead of one spinning CTA per
-    // operation) leaves the SMs to the other streams and ranks.
-    for (int i = b.n_static; i < b.n; ++i) {
-      const BatchOp& o = b.ops[i];
-      if (threadIdx.x == 0) load_op(o, b.spin_limit_ns, a);
-      __syncthreads();
-      if (o.inl) proto_body<SYS, true>(a, s_dc);
-      else proto_body<SYS, false>(a, s_dc);
-      __syncthreads();
-    }
   } else {
-    wait_all<SYS>(b.w, b.nwait, b.err_word, b.spin_limit_ns);
+    // Dynamic-matching operations: the receives one after another in one
+    // CTA, the sends in another, each in batch order. Matching serialises
+    // them on the receiver's lock and tickets anyway, and receive tickets
+    // (post order) and send tickets (per-destination order) only order ops
+    // of one kind; one CTA per kind (instead of one spinning CTA per
+    // operation) leaves the SMs to the other streams and ranks, and each
+    // CTA holds at most one lock at a time.
+    const int k = (int)blockIdx.x - b.n_static;
+    const bool has_r = b.n_drecv > b.n_static, has_s = b.n > b.n_drecv;
+    int lo = -1, hi = -1;
+    if (has_r && k == 0) {
+      lo = b.n_static;
+      hi = b.n_drecv;
+    } else if (has_s && k == (has_r ? 1 : 0)) {
+      lo = b.n_drecv;
+      hi = b.n;
+    }
+    if (lo >= 0) {
+      for (int i = lo; i < hi; ++i) {
+        const BatchOp& o = b.ops[i];
+        if (threadIdx.x == 0) load_op(o, b.spin_limit_ns, a);
+        __syncthreads();
+        if (o.inl) proto_body<SYS, true>(a, s_dc);
+        else proto_body<SYS, false>(a, s_dc);
+        __syncthreads();
+      }
+    } else {
+      wait_all<SYS>(b.w, b.nwait, b.err_word, b.spin_limit_ns);
+    }
   }
   graph_advance(b);
 }
@@ -1831,9 +1846,19 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   for (int i = 0; i < n; ++i)
     if (!ops[i].dyn) b.ops[k++] = ops[i];
   b.n_static = k;
+  // Dynamic receives, then dynamic sends, batch order in each — unless a
+  // blocking receive closes the batch: it may wait in k_batch for a push
+  // that its send, had it run second in the other CTA, would leave to the
+  // k_gcopy behind it; in batch order in one CTA the earlier sends run
+  // first and the receive pulls instead.
+  bool blocking_recv = false;
+  for (int i = 0; i < n; ++i) blocking_recv |= ops[i].dyn && ops[i].is_recv && ops[i].blocking;
   for (int i = 0; i < n; ++i)
-    if (ops[i].dyn) b.ops[k++] = ops[i];
-  const int head_ctas = b.n_static + (n > b.n_static ? 1 : 0);
+    if (ops[i].dyn && (blocking_recv || ops[i].is_recv)) b.ops[k++] = ops[i];
+  b.n_drecv = k;
+  for (int i = 0; i < n; ++i)
+    if (ops[i].dyn && !blocking_recv && !ops[i].is_recv) b.ops[k++] = ops[i];
+  const int head_ctas = b.n_static + (b.n_drecv > b.n_static ? 1 : 0) + (n > b.n_drecv ? 1 : 0);
   for (int i = 0; i < nwait; ++i) b.w[i] = w[i];
   GCopyArgs g;
   g.m = 0;
