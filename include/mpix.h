@@ -327,7 +327,9 @@ int MPIX_Free_mem(void *ptr);
  * P blocks from recvbuf and leaves the result in its first block.
  * Bcast: the root's buffer is copied into every other member's buffer.
  * Allgather: block q of every recvbuf = member q's sendbuf (MPI_IN_PLACE:
- * my block is already in place). Barrier: entry + exit barrier only. */
+ * my block is already in place). Alltoall: block q of member r's sendbuf
+ * lands in block r of member q's recvbuf (no MPI_IN_PLACE). Barrier: entry +
+ * exit barrier only. */
 int MPIX_Reduce_enqueue(const void *sendbuf, void *recvbuf, int count, MPI_Datatype datatype,
                         MPI_Op op, int root, MPI_Comm comm);
 int MPIX_Reduce_scatter_block_enqueue(const void *sendbuf, void *recvbuf, int recvcount,
@@ -335,6 +337,8 @@ int MPIX_Reduce_scatter_block_enqueue(const void *sendbuf, void *recvbuf, int re
 int MPIX_Bcast_enqueue(void *buffer, int count, MPI_Datatype datatype, int root, MPI_Comm comm);
 int MPIX_Allgather_enqueue(const void *sendbuf, int sendcount, MPI_Datatype sendtype,
                            void *recvbuf, int recvcount, MPI_Datatype recvtype, MPI_Comm comm);
+int MPIX_Alltoall_enqueue(const void *sendbuf, int sendcount, MPI_Datatype sendtype,
+                          void *recvbuf, int recvcount, MPI_Datatype recvtype, MPI_Comm comm);
 int MPIX_Barrier_enqueue(MPI_Comm comm);
 
 /* ------------------------------------------------------------------------ */

@@ -72,6 +72,10 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
     case CK_BCAST:
       sbuf = rbuf;  // one buffer: the root's is the source
       break;
+    case CK_ALLTOALL:
+      // in place, a peer would read my blocks while I overwrite them
+      if (!rbuf || !sbuf || sbuf == MPI_IN_PLACE) return MPIX_ERR_INVALID_ARG;
+      break;
     case CK_ALLGATHER:
       if (!rbuf) return MPIX_ERR_INVALID_ARG;
       if (sbuf == MPI_IN_PLACE) sbuf = static_cast<uint8_t*>(rbuf) + (uint64_t)me * bytes;
@@ -82,8 +86,8 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
   RankState& rs = rank_of(me);
   // Multi-process mode: peers read send buffers and write receive buffers.
   {
-    const uint64_t sb_bytes = kind == CK_REDUCE_SCATTER ? bytes * P : bytes;
-    const uint64_t rb_bytes = kind == CK_ALLGATHER ? bytes * P : bytes;
+    const uint64_t sb_bytes = (kind == CK_REDUCE_SCATTER || kind == CK_ALLTOALL) ? bytes * P : bytes;
+    const uint64_t rb_bytes = (kind == CK_ALLGATHER || kind == CK_ALLTOALL) ? bytes * P : bytes;
     if ((sbuf && !peer_ok(sbuf, sb_bytes)) || (rbuf && !peer_ok(rbuf, rb_bytes)))
       return MPIX_ERR_INVALID_ARG;
   }
@@ -158,7 +162,7 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
       grid = ar_reduce_grid(bytes, P);
     else if (kind == CK_BCAST && me != root)
       grid = p2p_copy_grid(bytes);
-    else if (kind == CK_ALLGATHER)
+    else if (kind == CK_ALLGATHER || kind == CK_ALLTOALL)
       grid = (uint64_t)P * p2p_copy_grid(bytes);
     nk = launch_collective(a, sys, grid, c->cu);
     if (nk >= 0 && rsb_in_place && me != 0 && bytes) {
@@ -202,6 +206,13 @@ int MPIX_Allgather_enqueue(const void* sendbuf, int sendcount, MPI_Datatype send
       (uint64_t)sendcount * type_size(sendtype) != (uint64_t)recvcount * type_size(recvtype))
     return MPIX_ERR_INVALID_COUNT;
   return coll_enqueue(CK_ALLGATHER, sendbuf, recvbuf, recvcount, recvtype, MPI_SUM, 0, comm);
+}
+
+int MPIX_Alltoall_enqueue(const void* sendbuf, int sendcount, MPI_Datatype sendtype, void* recvbuf,
+                          int recvcount, MPI_Datatype recvtype, MPI_Comm comm) {
+  if ((uint64_t)sendcount * type_size(sendtype) != (uint64_t)recvcount * type_size(recvtype))
+    return MPIX_ERR_INVALID_COUNT;
+  return coll_enqueue(CK_ALLTOALL, sendbuf, recvbuf, recvcount, recvtype, MPI_SUM, 0, comm);
 }
 
 int MPIX_Barrier_enqueue(MPI_Comm comm) {

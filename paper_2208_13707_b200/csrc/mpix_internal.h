@@ -309,6 +309,7 @@ enum CollKind : int {
   CK_BCAST = 3,
   CK_ALLGATHER = 4,
   CK_BARRIER = 5,
+  CK_ALLTOALL = 6,        // block q of my sendbuf -> rank q's recvbuf at block me
 };
 // OpRecord.action of a collective after its entry barrier.
 enum : uint64_t {

@@ -1597,6 +1597,10 @@ __global__ void __launch_bounds__(32) k_ar_entry(const ARArgs a) {
         rec->coll[q] = sb;
         rec->coll[kMaxCollRanks + q] = (uint64_t)a.rbuf + (uint64_t)q * a.chunk_bytes;
         break;
+      case CK_ALLTOALL:        // segment q: block me of rank q's sendbuf -> my buffer at q
+        rec->coll[q] = sb + (uint64_t)a.me * a.chunk_bytes;
+        rec->coll[kMaxCollRanks + q] = (uint64_t)a.rbuf + (uint64_t)q * a.chunk_bytes;
+        break;
       default:                 // allreduce: every member's buffers
         rec->coll[q] = sb;
         rec->coll[kMaxCollRanks + q] = rb;
@@ -1615,6 +1619,7 @@ __global__ void __launch_bounds__(32) k_ar_entry(const ARArgs a) {
         case CK_REDUCE_SCATTER: act = COLL_FOLD; rec->flags = P; break;
         case CK_BCAST: act = a.me == a.root ? COLL_NOOP : COLL_COPY; rec->flags = 1; break;
         case CK_ALLGATHER: act = COLL_COPY; rec->flags = P; break;
+        case CK_ALLTOALL: act = COLL_COPY; rec->flags = P; break;
         default: act = COLL_NOOP;
       }
     }
@@ -1935,7 +1940,7 @@ int launch_collective(const ARArgs& a, bool sys, uint64_t work_grid, cudaStream_
     if (e != cudaSuccess) return -1;
   }
   int nk = 1;
-  if (a.kind == CK_BCAST || a.kind == CK_ALLGATHER) {
+  if (a.kind == CK_BCAST || a.kind == CK_ALLGATHER || a.kind == CK_ALLTOALL) {
     if (launch_pdl(k_coll_copy, (int)work_grid, kCopyThreads, s, a) != cudaSuccess) return -1;
     ++nk;
   } else if (a.kind == CK_REDUCE || a.kind == CK_REDUCE_SCATTER) {

@@ -128,6 +128,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIX_Reduce_scatter_block_enqueue": (I, [P, P, I, I, I, P]),
         "MPIX_Bcast_enqueue": (I, [P, I, I, I, P]),
         "MPIX_Allgather_enqueue": (I, [P, I, I, P, I, I, P]),
+        "MPIX_Alltoall_enqueue": (I, [P, I, I, P, I, I, P]),
         "MPIX_Barrier_enqueue": (I, [P]),
         "MPI_Send": (I, [P, I, I, I, I, P]),
         "MPI_Recv": (I, [P, I, I, I, I, P, P]),
@@ -449,6 +450,11 @@ class Comm:
         sb = 1 if sendbuf == "in_place" else _ptr(sendbuf)
         check(lib().MPIX_Allgather_enqueue(sb, count, dt, _ptr(recvbuf), count, dt, self.h),
               "MPIX_Allgather_enqueue")
+
+    def alltoall_enqueue(self, sendbuf, recvbuf, count: int, dt: int) -> None:
+        """count elements per (sender, receiver) block."""
+        check(lib().MPIX_Alltoall_enqueue(_ptr(sendbuf), count, dt, _ptr(recvbuf), count, dt,
+                                          self.h), "MPIX_Alltoall_enqueue")
 
     def barrier_enqueue(self) -> None:
         check(lib().MPIX_Barrier_enqueue(self.h), "MPIX_Barrier_enqueue")

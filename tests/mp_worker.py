@@ -97,6 +97,12 @@ def main():
     c.allgather_enqueue(src, ag, 4096, mpix.MPI_BYTE)
     s.synchronize()
     assert torch.equal(ag.cpu(), torch.cat([pay[q][:4096] for q in range(n)])), "allgather"
+    # alltoall: block q of rank r's sendbuf -> block r of rank q's recvbuf
+    blk = 70000
+    at = w.alloc(n * blk)
+    c.alltoall_enqueue(src, at, blk, mpix.MPI_BYTE)
+    s.synchronize()
+    assert torch.equal(at.cpu(), torch.cat([pay[q][r * blk:(r + 1) * blk] for q in range(n)])), "alltoall"
     # 5. conventional p2p on the world comm
     wc = w.comm()
     if r < 2 and n >= 2:

@@ -109,6 +109,45 @@ def test_allgather(P, n, in_place):
             assert torch.equal(rb[r].cpu(), exp), r
 
 
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+@pytest.mark.parametrize("nb", [12, 4096, (1 << 20) + 4], ids=["12B", "4KiB", "1MiB+4"])
+def test_alltoall(P, nb):
+    """Block q of rank r's sendbuf lands in block r of rank q's recvbuf, byte-exact
+    (blocks of any size, including ones that are not multiples of 16 B)."""
+    with gpu_world(P) as (w, ctx):
+        src = [torch.randint(0, 256, (P * nb,), dtype=torch.uint8,
+                             generator=torch.Generator().manual_seed(40 + r)) for r in range(P)]
+        sb = [x.to(0) for x in src]
+        rb = [torch.zeros(P * nb, dtype=torch.uint8, device=0) for _ in range(P)]
+        torch.cuda.synchronize()
+        for _ in range(2):  # twice: the epoch and the op records are reused correctly
+            w.run_ranks(lambda r: ctx[r].comm.alltoall_enqueue(sb[r], rb[r], nb, mpix.MPI_BYTE))
+        sync_all(ctx)
+        for q in range(P):
+            exp = torch.cat([src[r][q * nb:(q + 1) * nb] for r in range(P)])
+            assert torch.equal(rb[q].cpu(), exp), q
+
+
+def test_alltoall_errors():
+    with gpu_world(2) as (w, ctx):
+        x = torch.zeros(64, dtype=torch.int32, device=0)
+        codes = {}
+
+        def body(r):
+            c = ctx[r].comm
+            out = []
+            for fn in (lambda: mpix.lib().MPIX_Alltoall_enqueue(1, 8, mpix.MPI_INT, x.data_ptr(), 8,
+                                                                mpix.MPI_INT, c.h),
+                       lambda: mpix.lib().MPIX_Alltoall_enqueue(x.data_ptr(), 8, mpix.MPI_INT,
+                                                                x.data_ptr() + 256, 4,
+                                                                mpix.MPI_INT, c.h)):
+                out.append(mpix.error_string(fn()))
+            codes[r] = out
+
+        w.run_ranks(body)
+        assert codes[0] == ["INVALID_ARG", "INVALID_COUNT"], codes
+
+
 def test_barrier_orders_streams():
     """Rank 0 delays, then writes; Barrier_enqueue on every rank; every rank
     then reads rank 0's buffer through a Bcast: the write is visible."""

@@ -268,6 +268,37 @@ def test_captured_bcast_and_allgather(graph_env):
             rp.close()
 
 
+def test_captured_alltoall(graph_env):
+    P, n = 3, 2048
+    with gpu_world(P) as (w, ctx):
+        reps = [Replay(c) for c in ctx]
+        sb = [torch.zeros(P * n, device=0) for _ in ctx]
+        rb = [torch.zeros(P * n, device=0) for _ in ctx]
+
+        def cap(r):
+            c, rp = ctx[r], reps[r]
+
+            def body():
+                for q in range(P):  # block q, for rank q: (it+1)(10r+q+1) + i%7
+                    mpix.testing.iter_fill(sb[r][q * n:(q + 1) * n], n, rp.it,
+                                           float(10 * r + q + 1), 1.0, c.stream)
+                c.comm.alltoall_enqueue(sb[r], rb[r], n, mpix.MPI_FLOAT)
+                for q in range(P):  # block q of mine came from rank q
+                    mpix.testing.iter_check(rb[r][q * n:(q + 1) * n], n, rp.it,
+                                            float(10 * q + r + 1), 1.0, rp.bad, c.stream)
+                mpix.testing.iter_bump(rp.it, c.stream)
+
+            rp.capture(body)
+
+        w.run_ranks(cap)
+        w.run_ranks(lambda r: reps[r].launch(K))
+        sync_all(ctx)
+        assert [rp.bad.item() for rp in reps] == [0] * P
+        assert all(rp.it.item() == K for rp in reps)
+        for rp in reps:
+            rp.close()
+
+
 def test_graph_hint_and_capture_rules():
     """The "mpix_graph" stream hint makes one comm graph-capturable; on a
     comm without it, capture is refused (UNSUPPORTED) rather than replaying
