@@ -877,12 +877,15 @@ def extras_multirank(args, mpix, torch):
     cnt = nb // 4
     big = {r: torch.ones(cnt, dtype=torch.float32, device=ctx[r][2]) for r in range(P8)}
     small = {r: torch.ones(cnt // P8, dtype=torch.float32, device=ctx[r][2]) for r in range(P8)}
+    big2 = {r: torch.empty(cnt, dtype=torch.float32, device=ctx[r][2]) for r in range(P8)}
     colls = {
         "bcast_256MiB": lambda r: ctx[r][1].bcast_enqueue(big[r], cnt, mpix.MPI_FLOAT, 0),
         "allgather_8x32MiB": lambda r: ctx[r][1].allgather_enqueue(small[r], big[r], cnt // P8,
                                                                    mpix.MPI_FLOAT),
         "reduce_scatter_8x32MiB": lambda r: ctx[r][1].reduce_scatter_block_enqueue(
             big[r], small[r], cnt // P8, mpix.MPI_FLOAT),
+        "alltoall_8x32MiB": lambda r: ctx[r][1].alltoall_enqueue(big[r], big2[r], cnt // P8,
+                                                                 mpix.MPI_FLOAT),
     }
     cres = {}
     for name, fn in colls.items():
@@ -903,9 +906,9 @@ def extras_multirank(args, mpix, torch):
         t = max(a.elapsed_time(b) for a, b in ev.values()) / 1e3 / 5
         # bytes every rank receives (the algorithmic per-rank volume)
         per_rank = {"bcast_256MiB": nb, "allgather_8x32MiB": nb * 7 // 8,
-                    "reduce_scatter_8x32MiB": nb}[name]
+                    "reduce_scatter_8x32MiB": nb, "alltoall_8x32MiB": nb * 7 // 8}[name]
         cres[name] = {"ms": t * 1e3, "GBps_per_rank": per_rank / t / 1e9, "ranks_per_gpu": -(-P8 // ndev)}
-    del big, small
+    del big, small, big2
     w.finalize()
     out["collectives_P8"] = cres
 
