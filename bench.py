@@ -386,6 +386,26 @@ def extras_mp(args, mpix, torch, dist, w, c, s, rank, world, dev):
                     "busbw_GBps": algbw * 2 * (world - 1) / world,
                     "check": float(rb[0]) == float(world)}
     out["allreduce_256MiB"] = ar
+    # Alltoall_enqueue: 32 MiB blocks per (sender, receiver) pair; busbw counts
+    # the (N-1)/N of each rank's buffer that crosses to peers
+    blk = 32 << 20
+    asb, arb = w.alloc(world * blk), w.alloc(world * blk)
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    with torch.cuda.stream(s):
+        c.alltoall_enqueue(asb, arb, blk, mpix.MPI_BYTE)
+    s.synchronize()
+    dist.barrier()
+    ev0.record(s)
+    for _ in range(5):
+        c.alltoall_enqueue(asb, arb, blk, mpix.MPI_BYTE)
+    ev1.record(s)
+    s.synchronize()
+    t = torch.tensor([ev0.elapsed_time(ev1) / 1e3 / 5], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    out["alltoall_32MiB_blocks"] = {"ms": float(t[0]) * 1e3,
+                                    "busbw_GBps": world * blk * (world - 1) / world / float(t[0]) / 1e9}
     pp = {}
     buf = w.alloc(64 << 20)
     for nb in (8, 4096, 65536, 1 << 20, 64 << 20):
