@@ -117,7 +117,7 @@ __device__ __noinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_
   unsigned ns = 32;
   while (M::ld_acq(p) < target) {
     __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
+    if (ns < 64) ns <<= 1;  // short cap: the poll's own round trip dominates (256: +0.3-0.5 us latency)
     if (limit_ns && globaltimer() - t0 > limit_ns) {
       if (err_word) ScopeSys::st_rlx(err_word, code);
       return false;
