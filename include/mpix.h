@@ -115,6 +115,17 @@ typedef struct {
 #define MPIX_ERR_TYPE 104          /* unknown datatype                      */
 #define MPIX_ERR_OP 105            /* unknown / unsupported reduction op    */
 #define MPIX_ERR_NO_MEM 106
+/* A device-side watchdog (MPIX_SPIN_TIMEOUT_MS) expired in one of the rank's
+ * kernels: a flag wait never saw its peer. The rank's communication state is
+ * undefined from then on, so the condition is STICKY: every later call that
+ * names the rank (enqueue, conventional p2p, waits, collectives,
+ * MPIX_Comm_check) returns it. The reference reports every failure through
+ * Result<Err> (result.hpp:36-45); an unbounded spin has no Err there, so the
+ * code is new. */
+#define MPIX_ERR_TIMEOUT 107
+/* A device-side protocol check failed (a descriptor another agent must not
+ * have taken was taken). Sticky like MPIX_ERR_TIMEOUT. */
+#define MPIX_ERR_DEVICE 108
 
 /* Name of an error code, e.g. "NOT_ENQUEUE_COMM" (result.cpp:5-32). */
 const char *MPIX_Error_string(int code);
@@ -363,6 +374,11 @@ int MPIX_Type_size(MPI_Datatype datatype);
  * recorded (1 slot wait, 2 completion wait, 3 collective barrier, 4 protocol)
  * before exiting instead of hanging. Reading clears nothing. */
 int MPIX_Rank_error(int rank, uint64_t *code);
+/* Health of this member of comm without blocking: MPI_SUCCESS, or the
+ * sticky MPIX_ERR_TIMEOUT / MPIX_ERR_DEVICE once a kernel of the rank hit its
+ * watchdog (see MPIX_ERR_TIMEOUT). Work already enqueued is not waited for:
+ * synchronise the stream first to check it. */
+int MPIX_Comm_check(MPI_Comm comm);
 /* Tracing (MPIX_TRACE=1 at MPIX_World_init): copies up to max_records
  * 128-byte per-operation records (struct TraceRec in csrc/mpix_internal.h:
  * op sequence, kind/mode/decision, bytes, key, clock64 stamps of the

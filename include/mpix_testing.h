@@ -23,6 +23,10 @@ int MPIXT_Fill_pattern(void *buf, uint64_t nbytes, uint32_t seed, uint32_t iter,
 /* *out_dev (device uint64) = order-independent checksum of nbytes
  * (oracle: orc_checksum64). Zeroes *out_dev first. */
 int MPIXT_Checksum(const void *buf, uint64_t nbytes, uint64_t *out_dev, void *stream);
+/* cfg3 inputs of rank `rank`: count elements of dt (MPI_FLOAT or
+ * MPIX_BFLOAT16) from value set 0 (exact) or 1 (uniform(-1,1)); oracle:
+ * orc_value_f32 / orc_value_bf16. */
+int MPIXT_Fill_values(void *buf, uint64_t count, int dt, int set, uint32_t rank, void *stream);
 /* y[i] = a * x[i] + y[i] (fp32) — PAPER.md Listing 2 */
 int MPIXT_Saxpy(int n, float a, const float *x, float *y, void *stream);
 /* Busy-wait `ns` nanoseconds inside the stream (peer-delay tests). */

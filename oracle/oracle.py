@@ -68,6 +68,14 @@ def orc() -> C.CDLL:
         L.orc_stencil7.argtypes = [P, P, I, I, I, C.c_float, C.c_float]
         L.orc_halo_pack.argtypes = [P, I, I, I, I, P]
         L.orc_halo_unpack.argtypes = [P, I, I, I, I, P]
+        L.orc_value_f32.restype = C.c_float
+        L.orc_value_f32.argtypes = [U64, C.c_uint32, I]
+        L.orc_value_bf16.restype = C.c_uint16
+        L.orc_value_bf16.argtypes = [U64, C.c_uint32, I]
+        L.orc_gen_checksum.restype = U64
+        L.orc_gen_checksum.argtypes = [C.c_uint32, U64, I, I]
+        L.orc_allreduce_gen.restype = U64
+        L.orc_allreduce_gen.argtypes = [I, U64, I, I, I, I, P, P]
         L.orc_loopback_message.restype = U64
         L.orc_loopback_message.argtypes = [P, U64, P, U64, P]
         _orc = L
@@ -215,6 +223,32 @@ def exact_inputs(P: int, count: int, dt: str) -> list:
             f = ((h % 256).astype(np.int64) - 128).astype(np.float32) / np.float32(16)
             out.append((f.view(np.uint32) >> 16).astype(np.uint16))  # exact in bf16
     return out
+
+
+_GEN_DT = {"f32": (1, np.float32), "bf16": (2, np.uint16)}
+
+
+def value(i: int, r: int, dt: str, value_set: int):
+    """One generated cfg3 input element (bf16 as uint16 bits)."""
+    if dt == "f32":
+        return np.float32(orc().orc_value_f32(i, r, value_set))
+    return np.uint16(orc().orc_value_bf16(i, r, value_set))
+
+
+def gen_checksum(r: int, count: int, dt: str, value_set: int) -> int:
+    """checksum64 of rank r's generated input (count elements)."""
+    return int(orc().orc_gen_checksum(r, count, _GEN_DT[dt][0], value_set))
+
+
+def allreduce_gen(P: int, count: int, dt: str, value_set: int, op: int = 1, samples=()):
+    """Rank-ordered allreduce of P generated inputs without materialising
+    them: (checksum64 of the output, the output at `samples`)."""
+    code, npdt = _GEN_DT[dt]
+    idx = np.ascontiguousarray(np.asarray(samples, dtype=np.uint64))
+    out = np.zeros(max(1, idx.size), dtype=npdt)
+    cs = orc().orc_allreduce_gen(P, count, code, value_set, op, idx.size, _p(idx) if idx.size else None,
+                                 _p(out))
+    return int(cs), out[:idx.size]
 
 
 def _hash32_np(i: np.ndarray, r: int) -> np.ndarray:

@@ -398,3 +398,86 @@ uint64_t orc_loopback_message(const void *src, uint64_t len, void *dst, uint64_t
   if (n) memcpy(dst, f + 36, n);
   return n;
 }
+
+/* ---- cfg3 at full size ----------------------------
+ * Inputs are generated per (element, rank) instead of materialised, so the
+ * rank-ordered fold of P x 256 MiB runs in host memory of one chunk.
+ *   set 0 "exact":           f32 (h%2048-1024)/256, bf16 (h%256-128)/16
+ *   set 1 "order-sensitive": uniform(-1,1) = (h >> 8) * 2^-23 - 1 (exact in
+ *                            f32; bf16 = its RNE rounding)
+ * The device generator (MPIXT_Fill_values, mpix_testing.cu) computes the
+ * same bits. */
+float orc_value_f32(uint64_t i, uint32_t r, int set) {
+  if (set == 0) return orc_exact_f32(i, r);
+  return (float)(orc_hash32(i, r) >> 8) * (1.0f / 8388608.0f) - 1.0f;
+}
+
+uint16_t orc_value_bf16(uint64_t i, uint32_t r, int set) {
+  if (set == 0) return orc_exact_bf16(i, r);
+  return orc_f32_to_bf16_rne(orc_value_f32(i, r, 1));
+}
+
+/* checksum64 of bytes [0, nbytes) of a buffer whose 8-byte word 0 is word
+ * `w0` of the whole buffer (nbytes a multiple of 8 except at the end). */
+static uint64_t checksum_part(const uint8_t *b, uint64_t nbytes, uint64_t w0) {
+  uint64_t nw = nbytes / 8, acc = 0;
+  for (uint64_t i = 0; i < nw; ++i) {
+    uint64_t v;
+    memcpy(&v, b + 8 * i, 8);
+    acc += mix64(v ^ ((w0 + i) * 0x9E3779B97F4A7C15ull));
+  }
+  if (nbytes & 7) {
+    uint64_t v = 0;
+    for (uint64_t k = nw * 8; k < nbytes; ++k) v |= (uint64_t)b[k] << (8 * (k - nw * 8));
+    acc += mix64(v ^ ((w0 + nw) * 0x9E3779B97F4A7C15ull));
+  }
+  return acc;
+}
+
+uint64_t orc_gen_checksum(uint32_t r, uint64_t count, int dt, int set) {
+  const uint64_t chunk = 1u << 20; /* elements, a multiple of 4 */
+  const int es = dt == 1 ? 4 : 2;
+  uint8_t *buf = (uint8_t *)malloc(chunk * es);
+  uint64_t acc = 0;
+  for (uint64_t c0 = 0; c0 < count; c0 += chunk) {
+    uint64_t n = count - c0 < chunk ? count - c0 : chunk;
+    for (uint64_t k = 0; k < n; ++k) {
+      if (dt == 1) { float v = orc_value_f32(c0 + k, r, set); memcpy(buf + 4 * k, &v, 4); }
+      else { uint16_t v = orc_value_bf16(c0 + k, r, set); memcpy(buf + 2 * k, &v, 2); }
+    }
+    acc += checksum_part(buf, n * es, c0 * es / 8);
+  }
+  free(buf);
+  return acc;
+}
+
+uint64_t orc_allreduce_gen(int P, uint64_t count, int dt, int set, int op, int ns,
+                           const uint64_t *sample_idx, void *sample_out) {
+  const uint64_t chunk = 1u << 20;
+  const int es = dt == 1 ? 4 : 2;
+  uint8_t *buf = (uint8_t *)malloc(chunk * es);
+  uint64_t acc = 0;
+  for (uint64_t c0 = 0; c0 < count; c0 += chunk) {
+    uint64_t n = count - c0 < chunk ? count - c0 : chunk;
+    for (uint64_t k = 0; k < n; ++k) {
+      const uint64_t i = c0 + k;
+      if (dt == 1) { /* same fold as orc_allreduce_f32 */
+        volatile float a = orc_value_f32(i, 0, set);
+        for (int q = 1; q < P; ++q) a = FOLD(a, orc_value_f32(i, (uint32_t)q, set), op);
+        float v = a;
+        memcpy(buf + 4 * k, &v, 4);
+      } else { /* same fold as orc_allreduce_bf16 */
+        volatile float a = bf16_to_f32(orc_value_bf16(i, 0, set));
+        for (int q = 1; q < P; ++q) a = FOLD(a, bf16_to_f32(orc_value_bf16(i, (uint32_t)q, set)), op);
+        uint16_t v = orc_f32_to_bf16_rne(a);
+        memcpy(buf + 2 * k, &v, 2);
+      }
+    }
+    for (int s = 0; s < ns; ++s)
+      if (sample_idx[s] >= c0 && sample_idx[s] < c0 + n)
+        memcpy((uint8_t *)sample_out + (size_t)s * es, buf + (sample_idx[s] - c0) * es, es);
+    acc += checksum_part(buf, n * es, c0 * es / 8);
+  }
+  free(buf);
+  return acc;
+}

@@ -39,6 +39,7 @@ def build(force=False, verbose=False):
     os.makedirs(odir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
               "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+    cmds = []
     for src in SOURCES:
         obj = os.path.join(odir, src + ".o")
         cmd = [nvcc(), ARCH, *common, "-c", os.path.join(CSRC, src), "-o", obj]
@@ -46,8 +47,14 @@ def build(force=False, verbose=False):
             cmd += ["-Xptxas", "-v"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        cmds.append(cmd)
         objs.append(obj)
+    # translation units compile in parallel (the kernels TU dominates)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c), cmds)):
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
     tmp = LIB + ".tmp"
     cmd = [nvcc(), ARCH, "-shared", "-o", tmp, *objs, "-lpthread",
            "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map")]

@@ -30,6 +30,7 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
   if (!c) return MPIX_ERR_INVALID_COMM;
   if (!c->enqueue_ok) return MPIX_ERR_NOT_ENQUEUE_COMM;
+  if (int h = rank_health(rank_of(c->rank))) return h;  // sticky watchdog state
   if (count < 0) return MPIX_ERR_INVALID_COUNT;
   CommShared& sh = *c->sh;
   const int P = sh.P;

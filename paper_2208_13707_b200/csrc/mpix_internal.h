@@ -25,8 +25,22 @@ namespace mpix {
 constexpr int kThreads = 512;          // threads per CTA for every op kernel
 constexpr int kMaxCollRanks = 16;      // max communicator size for Allreduce
 constexpr uint64_t kOpRecords = 65536; // op-record ring entries per rank (32 MiB; bounds in-flight large ops)
+// Completion pool of a rank: kReqSlots reusable request words, then
+// kGraphReqs words of captured requests (never reused), then two status
+// planes at a fixed byte offset from any completion word w: w + kStatusOff =
+// delivered bytes | truncated << 63, w + 2 * kStatusOff = source << 32 | tag,
+// written by whoever completes a receive (the reference's Status,
+// request.hpp:13-19, filled by deliver, endpoint.cpp:17-24).
+constexpr uint64_t kReqSlots = 1ull << 20;
+constexpr uint64_t kGraphReqs = 1ull << 16;
+constexpr uint64_t kDoneWords = kReqSlots + kGraphReqs;
+constexpr uint64_t kStatusOff = kDoneWords * 8;
+constexpr uint64_t kTruncBit = 1ull << 63;
 
 enum : uint64_t { ST_FREE = 0, ST_POSTED = 1, ST_TAKEN = 2 };
+// Codes a kernel stores in the rank's watchdog word before giving up
+// (the host turns any of them into the sticky MPIX_ERR_TIMEOUT / _DEVICE).
+enum : uint64_t { ERRW_WAIT_SLOT = 1, ERRW_WAIT_DONE = 2, ERRW_WAIT_COLL = 3, ERRW_PROTOCOL = 4 };
 
 __host__ __device__ inline uint64_t st_word(uint64_t pseq, uint64_t st) {
   return (pseq << 8) | st;
@@ -127,6 +141,7 @@ struct alignas(64) OpRecord {
   uint64_t coll[2 * kMaxCollRanks];  // allreduce: peers' sbuf / rbuf
   uint64_t flags;
   uint64_t stage_ptr, stage_done, stage_gen;  // staged send: buffer + release
+  uint64_t stat_addr, stat_bytes, stat_srctag; // status of the completed receive (kStatusOff)
 };
 
 enum : uint64_t { ACT_NONE = 0, ACT_COPY = 1, ACT_STAGE = 2 };

@@ -103,8 +103,6 @@ __device__ __forceinline__ uint64_t globaltimer() {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
-enum : uint64_t { ERRW_WAIT_SLOT = 1, ERRW_WAIT_DONE = 2, ERRW_WAIT_COLL = 3, ERRW_PROTOCOL = 4 };
-
 // Spin until *p >= target. Returns false on watchdog expiry after recording
 // `code` in the rank's host-mapped error word (the kernel then exits rather
 // than hanging the GPU).
@@ -280,20 +278,34 @@ struct Fin {
   uint32_t na, nb;
   uint64_t a_addr[2], a_val[2];
   uint64_t b_addr[5], b_val[5];
-  __device__ void clear() { na = nb = 0; }
+  // the completed receive's status (its completion word's status planes)
+  uint64_t s_addr, s_bytes, s_srctag;
+  __device__ void clear() { na = nb = 0; s_addr = 0; }
   __device__ void add_a(void* p, uint64_t v) {
     if (p) { a_addr[na] = (uint64_t)p; a_val[na] = v; ++na; }
   }
   __device__ void add_b(void* p, uint64_t v) {
     if (p) { b_addr[nb] = (uint64_t)p; b_val[nb] = v; ++nb; }
   }
+  // deliver's status (endpoint.cpp:17-24): bytes = min(len, cap), truncated = len > cap
+  // sidx_enc: the sender's multiplex stream index + 2 (0 = none)
+  __device__ void status(void* done, uint64_t len, uint64_t cap, int src, int tag, uint64_t sidx_enc) {
+    if (!done) return;
+    s_addr = (uint64_t)done;
+    s_bytes = (len < cap ? len : cap) | (len > cap ? kTruncBit : 0);
+    s_srctag = ((uint64_t)(src & 0xffffff) << 40) | ((sidx_enc & 0xff) << 32) | (uint32_t)tag;
+  }
   template <bool SYS>
   // One fence: the payload (written by the whole CTA or grid before this)
   // and the slot frees must both be visible before any mirror or done word;
   // nothing orders the frees against the payload (a freed slot is reused only
-  // after its mirror), so group A is stored before the fence.
+  // after its mirror), so group A (and the status) is stored before the fence.
   __device__ void run() const {
     using M = Scope<SYS>;
+    if (s_addr) {
+      M::st_rlx(reinterpret_cast<uint64_t*>(s_addr + kStatusOff), s_bytes);
+      M::st_rlx(reinterpret_cast<uint64_t*>(s_addr + 2 * kStatusOff), s_srctag);
+    }
     for (uint32_t k = 0; k < na; ++k) M::st_rlx(reinterpret_cast<uint64_t*>(a_addr[k]), a_val[k]);
     M::fence_ar();
     for (uint32_t k = 0; k < nb; ++k) M::st_rlx(reinterpret_cast<uint64_t*>(b_addr[k]), b_val[k]);
@@ -358,6 +370,8 @@ __device__ void send_win(const P2PArgs& a, Decision& dc, int j, const Snap& r, b
   dc.fin.add_b(reinterpret_cast<void*>(r.done_addr), r.done_val);
   dc.fin.add_b(a.my_done, a.my_gen);
   if (a.mode == MODE_STAGED && dc.stage_done) dc.fin.add_b(dc.stage_done, dc.stage_gen);
+  dc.fin.status(reinterpret_cast<void*>(r.done_addr), a.bytes, r.bytes, a.me, (int)(a.key >> 32),
+                (uint64_t)(a.sidx + 2));
 }
 
 // Receiver wins (send descriptor already TAKEN by me): pull.
@@ -375,6 +389,7 @@ __device__ void recv_win(const P2PArgs& a, Decision& dc, int j, const Snap& s, b
   dc.fin.add_b(&a.post_mirror[slot], a.pseq + 1);  // consumed either way
   dc.fin.add_b(reinterpret_cast<void*>(s.done_addr), s.done_val);
   dc.fin.add_b(a.my_done, a.my_gen);
+  dc.fin.status(a.my_done, s.bytes, a.bytes, a.peer, (int)(s.key >> 32), (uint64_t)(a.sidx + 2));
 }
 
 // Claim a slot of the rank's device staging arena (warp 0, all lanes). A
@@ -599,6 +614,7 @@ __device__ void dyn_send_take(const P2PArgs& a, Decision& dc, SlotDesc* pq, int 
   dc.fin.add_b(reinterpret_cast<void*>(done_addr), done_val);
   dc.fin.add_b(a.my_done, a.my_gen);
   if (a.mode == MODE_STAGED && dc.stage_done) dc.fin.add_b(dc.stage_done, dc.stage_gen);
+  dc.fin.status(reinterpret_cast<void*>(done_addr), a.bytes, cap, a.me, a.tag, idx_enc(a.sidx));
 }
 
 // Sender posts its descriptor (lock held, lane 0), stamped with the arrival.
@@ -739,6 +755,7 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
           }
           dc.fin.add_b(reinterpret_cast<void*>(done_addr), done_val);
           dc.fin.add_b(a.my_done, a.my_gen);
+          dc.fin.status(a.my_done, len, a.bytes, q, (int32_t)(key >> 32), (key >> 24) & 0xff);
         } else {
           SlotDesc* e = &D.pq[qslot];
           M::st_rlx(&e->key, ((uint64_t)(uint32_t)a.peer << 32) | (uint32_t)a.tag);
@@ -827,6 +844,7 @@ __device__ void decide_paired(const P2PArgs& a, Decision& dc) {
       dc.fin.add_b(&a.pair_mirror[sslot], a.pair_pseq + 1);
       dc.fin.add_b(a.pair_done, a.pair_gen);
       dc.fin.add_b(a.my_done, a.my_gen);
+      dc.fin.status(a.my_done, a.pair_bytes, a.bytes, a.me, (int)(a.key >> 32), 0);
     }
   }
   __syncthreads();
@@ -1014,6 +1032,9 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
       rec->stage_ptr = (uint64_t)s_dc.stage_ptr;
       rec->stage_done = (uint64_t)s_dc.stage_done;
       rec->stage_gen = s_dc.stage_gen;
+      rec->stat_addr = s_dc.fin.s_addr;
+      rec->stat_bytes = s_dc.fin.s_bytes;
+      rec->stat_srctag = s_dc.fin.s_srctag;
       for (uint32_t k = 0; k < s_dc.fin.na; ++k) {
         rec->fin_addr[k] = s_dc.fin.a_addr[k];
         rec->fin_val[k] = s_dc.fin.a_val[k];
@@ -1085,6 +1106,9 @@ __device__ void fin_body(const P2PArgs& a, Decision& s_dc) {
       Fin f;
       f.na = rec->nfin & 0xff;
       f.nb = rec->nfin >> 8;
+      f.s_addr = rec->stat_addr;
+      f.s_bytes = rec->stat_bytes;
+      f.s_srctag = rec->stat_srctag;
       for (uint32_t k = 0; k < f.na; ++k) { f.a_addr[k] = rec->fin_addr[k]; f.a_val[k] = rec->fin_val[k]; }
       for (uint32_t k = 0; k < f.nb; ++k) { f.b_addr[k] = rec->fin_addr[2 + k]; f.b_val[k] = rec->fin_val[2 + k]; }
       f.run<SYS>();

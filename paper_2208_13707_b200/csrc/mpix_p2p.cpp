@@ -4,6 +4,8 @@
 // multiplex stream p2p (proj/src/proc_p2p.cpp:96-212), and the waits.
 #include "mpix_state.h"
 
+#include <chrono>
+
 namespace mpix {
 
 StreamBatch& batch_of(cudaStream_t s, int device) {
@@ -66,6 +68,7 @@ int flush_locked(StreamBatch& b, cudaStream_t s, const WaitEntry* w, int nwait, 
   } while (wi < nwait);
   b.sys = false;
   b.err_word = nullptr;
+  b.t_first = 0;
   g_launches.fetch_add(launches);
   return launches;
 }
@@ -83,6 +86,101 @@ int flush_stream(cudaStream_t s) {
   if (b->ops.empty()) return 0;
   if (cudaSetDevice(b->device) != cudaSuccess) return -1;
   return flush_locked(*b, s, nullptr, 0, false, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// Flusher thread: the progress guarantee of held batches. A non-blocking
+// operation held in a stream's batch is normally launched by that stream's
+// next ordering call; the reference instead registers I-operations at their
+// own queue position (proc_enqueue.cpp:67-114), so a program that never
+// makes such a call (e.g. Isend_enqueue on stream A, then a host wait on
+// stream B for the matching receive) must still progress: any batch held
+// longer than cfg.flush_ns is launched here.
+// ---------------------------------------------------------------------------
+static uint64_t now_ns() {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+void batch_note_held(StreamBatch& b) {
+  if (b.t_first) return;
+  b.t_first = now_ns();
+  World& w = *g_world;
+  if (w.cfg.flush_ns && !w.fl_armed.exchange(true)) {
+    std::lock_guard<std::mutex> lk(w.fl_mu);
+    w.fl_cv.notify_one();
+  }
+}
+
+// Launch every batch older than flush_ns; returns the ns until the next one
+// is due (0: nothing held).
+static uint64_t flush_due(World& w) {
+  std::vector<std::pair<cudaStream_t, StreamBatch*>> v;
+  {
+    std::lock_guard<std::mutex> lk(w.batch_mu);
+    v.reserve(w.batches.size());
+    for (auto& kv : w.batches) v.emplace_back(kv.first, kv.second.get());
+  }
+  uint64_t next = 0;
+  for (auto& e : v) {
+    StreamBatch& b = *e.second;
+    std::unique_lock<std::mutex> lk(b.mu, std::try_to_lock);
+    if (!lk.owns_lock()) {  // its owner is working on it right now
+      next = next ? std::min(next, w.cfg.flush_ns) : w.cfg.flush_ns;
+      continue;
+    }
+    if (b.ops.empty()) continue;
+    const uint64_t age = now_ns() - b.t_first;
+    if (age < w.cfg.flush_ns) {
+      const uint64_t d = w.cfg.flush_ns - age;
+      next = next ? std::min(next, d) : d;
+      continue;
+    }
+    // a batch of a stream being captured stays with its capture (its wait,
+    // inside the capture, launches it)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(e.first, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      continue;
+    }
+    if (cudaSetDevice(b.device) == cudaSuccess) flush_locked(b, e.first, nullptr, 0, false, nullptr);
+  }
+  return next;
+}
+
+static void flusher_main(World* w) {
+  std::unique_lock<std::mutex> lk(w->fl_mu);
+  while (!w->fl_stop) {
+    if (!w->fl_armed.load()) {
+      w->fl_cv.wait(lk, [&] { return w->fl_stop || w->fl_armed.load(); });
+      continue;
+    }
+    w->fl_armed.store(false);  // before the scan: a batch started after it re-arms
+    lk.unlock();
+    const uint64_t next = flush_due(*w);
+    lk.lock();
+    if (next) {
+      w->fl_armed.store(true);
+      w->fl_cv.wait_for(lk, std::chrono::nanoseconds(next), [&] { return w->fl_stop; });
+    }
+  }
+}
+
+void flusher_start(World& w) {
+  if (!w.cfg.flush_ns || !w.cfg.batch) return;
+  w.fl_stop = false;
+  w.flusher = std::thread(flusher_main, &w);
+}
+
+void flusher_stop(World& w) {
+  if (!w.flusher.joinable()) return;
+  {
+    std::lock_guard<std::mutex> lk(w.fl_mu);
+    w.fl_stop = true;
+  }
+  w.fl_cv.notify_all();
+  w.flusher.join();
 }
 
 BatchOp pack_op(const P2PArgs& a, bool inl) {
@@ -152,7 +250,7 @@ struct Ticket {
 };
 
 Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remote,
-                  bool conventional) {
+                  bool conventional, bool is_recv, int me, uint64_t bytes) {
   uint64_t n = rs.req_next.fetch_add(1);
   uint64_t slot = n % kReqSlots;
   uint64_t gen = n / kReqSlots + 1;
@@ -164,6 +262,10 @@ Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remot
   ri.remote = remote;
   ri.conventional = conventional;
   ri.consumed = false;
+  ri.is_recv = is_recv;
+  ri.me = me;
+  ri.bytes = bytes;
+  ri.comm = nullptr;
   Ticket t;
   t.handle = ((uint64_t)(rs.rank + 1) << 48) | (n + 1);
   t.flag = rs.d_done + slot;
@@ -176,7 +278,8 @@ Ticket new_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remot
 // (reset to 0) by the captured wait, so every replay sees a fresh request.
 constexpr uint64_t kGraphTicket = 1ull << 47;
 
-int new_graph_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remote, Ticket* t) {
+int new_graph_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool remote, bool is_recv,
+                     int me, uint64_t bytes, Ticket* t) {
   uint64_t n = rs.gdone_next.fetch_add(1);
   if (n >= kGraphReqs) return MPIX_ERR_NO_MEM;
   auto& ri = rs.greqs[n];
@@ -187,6 +290,10 @@ int new_graph_ticket(RankState& rs, cudaStream_t s, int source, int tag, bool re
   ri.remote = remote;
   ri.conventional = false;
   ri.consumed = false;
+  ri.is_recv = is_recv;
+  ri.me = me;
+  ri.bytes = bytes;
+  ri.comm = nullptr;
   t->handle = ((uint64_t)(rs.rank + 1) << 48) | kGraphTicket | (n + 1);
   t->flag = rs.d_gdone + n;
   t->gen = 1;
@@ -254,6 +361,7 @@ struct PostHow {
   cudaStream_t stream = nullptr;
   bool conventional = false;
   int sidx = -2, didx = -2;  // IDX_NONE unless multiplex (types.hpp:14)
+  uint64_t* ticket = nullptr; // out: the operation's ticket (blocking receives too)
 };
 
 int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
@@ -298,7 +406,7 @@ cudaStream_t conv_stream(const mpix_comm_s* c) {
 // executed on the rank's internal stream, launched at once (no batching:
 // a posted conventional send must progress without a later MPI call).
 int conv_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
-              bool is_recv, bool blocking, MPI_Request* req) {
+              bool is_recv, bool blocking, MPI_Request* req, uint64_t* ticket = nullptr) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
   if (!c) return MPIX_ERR_INVALID_COMM;
   if (c->sh->multiplex) return MPIX_ERR_MULTIPLEX_COMM;
@@ -307,6 +415,7 @@ int conv_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, i
   PostHow how;
   how.stream = conv_stream(c);
   how.conventional = true;
+  how.ticket = ticket;
   return p2p_post(c, buf, count, dt, peer, tag, is_recv, blocking, req, how);
 }
 
@@ -314,7 +423,8 @@ int conv_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, i
 // runs on the CUDA stream of local stream src_idx (send) / dst_idx (recv),
 // or on the rank's internal stream when that MPIX stream is not a GPU stream.
 int stream_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
-                int src_idx, int dst_idx, bool is_recv, bool blocking, MPI_Request* req) {
+                int src_idx, int dst_idx, bool is_recv, bool blocking, MPI_Request* req,
+                uint64_t* ticket = nullptr) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
   if (!c) return MPIX_ERR_INVALID_COMM;
   if (!c->sh->multiplex) return MPIX_ERR_NOT_MULTIPLEX;
@@ -343,11 +453,13 @@ int stream_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer,
   how.conventional = true;
   how.sidx = src_idx;
   how.didx = dst_idx;
+  how.ticket = ticket;
   return p2p_post(c, buf, count, dt, peer, tag, is_recv, blocking, req, how);
 }
 
 int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, int tag,
              bool is_recv, bool blocking, MPI_Request* req, const PostHow& how) {
+  if (int h = rank_health(rank_of(c->rank))) return h;  // sticky watchdog state
   int esz = type_size(dt);
   if (!esz) return MPIX_ERR_TYPE;
   const bool dyn = c->sh->dyn;
@@ -422,14 +534,14 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   if (indexed)  // multiplex: the stream indices are part of the match key (endpoint.hpp:26-32)
     a.key = ((uint64_t)(uint32_t)tag << 32) | ((uint64_t)(how.sidx & 0xff) << 24) |
             ((uint64_t)(how.didx & 0xff) << 16) | (tseq & 0xffff);
+  a.me = me;      // the status source of a receive this operation completes
+  a.peer = peer;  // -1 = ANY_SOURCE (receives, dynamic matching)
+  a.tag = tag;    // -1 = ANY_TAG (receives, dynamic matching)
+  a.sidx = how.sidx;  // multiplex stream indices (-2 none)
+  a.didx = how.didx;
   if (dyn) {
     a.dyn = 1;
     a.P = sh.P;
-    a.me = me;
-    a.peer = peer;  // -1 = ANY_SOURCE (receives)
-    a.tag = tag;    // -1 = ANY_TAG (receives)
-    a.sidx = how.sidx;
-    a.didx = how.didx;
     a.bases = reinterpret_cast<uint64_t*>(sh.base[me] + L.bases());
   }
 
@@ -454,10 +566,23 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   Ticket t{};
   if (!blocking || is_recv) {
     if (capturing) {
-      int rc2 = new_graph_ticket(rs, s, is_recv ? peer : me, tag, sys, &t);
+      int rc2 = new_graph_ticket(rs, s, is_recv ? peer : me, tag, sys, is_recv, me, bytes, &t);
       if (rc2) return rc2;
     } else {
-      t = new_ticket(rs, s, is_recv ? peer : me, tag, sys, how.conventional);
+      t = new_ticket(rs, s, is_recv ? peer : me, tag, sys, how.conventional, is_recv, me, bytes);
+      if (how.conventional && is_recv) {  // MPI_Comm_free's PENDING_OPS check
+        auto& v = c->conv_recvs;
+        if (v.size() >= 256) {  // drop the ones already waited
+          v.erase(std::remove_if(v.begin(), v.end(),
+                                 [&](const std::pair<uint64_t*, uint64_t>& e) {
+                                   auto& r = rs.reqs[(uint64_t)(e.first - rs.d_done) % kReqSlots];
+                                   return r.consumed || r.gen != e.second;
+                                 }),
+                  v.end());
+        }
+        v.emplace_back(t.flag, t.gen);
+        rs.reqs[(uint64_t)(t.flag - rs.d_done)].comm = c;
+      }
     }
     a.my_done = t.flag;
     a.my_gen = t.gen;
@@ -589,8 +714,11 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
     }
     // a blocking operation closes the batch; conventional operations are
     // launched at once
-    if ((blocking || how.conventional || !w.cfg.batch) && flush_locked(b, s, nullptr, 0, false, nullptr) < 0)
-      return MPIX_ERR_CUDA;
+    if (blocking || how.conventional || !w.cfg.batch) {
+      if (flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
+    } else if (!b.ops.empty()) {
+      batch_note_held(b);  // the flusher launches it if no ordering call comes
+    }
   } else {
     if (!b.ops.empty() && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -605,7 +733,11 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
     if (nk < 0) return MPIX_ERR_CUDA;
     g_launches.fetch_add(nk);
   }
+  if (s != c->cu &&
+      std::find(c->side_streams.begin(), c->side_streams.end(), s) == c->side_streams.end())
+    c->side_streams.push_back(s);
   if (req) *req = (!blocking) ? t.handle : MPI_REQUEST_NULL;
+  if (how.ticket) *how.ticket = t.handle;
   return MPI_SUCCESS;
 }
 
@@ -626,6 +758,7 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
       return MPIX_ERR_INVALID_REQUEST;
     ngraph += items[i].graph;
   }
+  if (int h = rank_health(rank_of(items[0].rank))) return h;  // sticky watchdog state
   auto info = [&](const Item& it) -> RankState::ReqInfo& {
     RankState& rs = rank_of(it.rank);
     return it.graph ? rs.greqs[it.n] : rs.reqs[it.n % kReqSlots];
@@ -683,8 +816,33 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
   return MPI_SUCCESS;
 }
 
-// Every enqueued collective: validate, fill the entry-barrier arguments,
-// order the stream's held operations first, launch.
+// The status of a completed request (host side, after its stream was
+// synchronised): a receive reads the status planes its completion wrote
+// (source, tag, stream index, bytes, truncated: deliver, endpoint.cpp:17-24);
+// a send reports (me, tag, bytes) as post_send does (proc_p2p.cpp:54-58).
+int read_status(RankState& rs, uint64_t n, MPI_Status* st) {
+  const auto& ri = rs.reqs[n % kReqSlots];
+  st->MPI_ERROR = MPI_SUCCESS;
+  if (!ri.is_recv) {
+    st->MPI_SOURCE = ri.me;
+    st->MPI_TAG = ri.tag;
+    st->source_index = -2;
+    st->count_bytes = ri.bytes;
+    st->truncated = 0;
+    return MPI_SUCCESS;
+  }
+  const uint64_t* w = rs.d_done + (n % kReqSlots);
+  uint64_t v[2];
+  CK(cudaMemcpy(&v[0], reinterpret_cast<const uint8_t*>(w) + kStatusOff, 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&v[1], reinterpret_cast<const uint8_t*>(w) + 2 * kStatusOff, 8, cudaMemcpyDeviceToHost));
+  st->count_bytes = v[0] & ~kTruncBit;
+  st->truncated = (v[0] & kTruncBit) ? 1 : 0;
+  st->MPI_SOURCE = (int)((v[1] >> 40) & 0xffffff);
+  st->source_index = (int)((v[1] >> 32) & 0xff) - 2;
+  st->MPI_TAG = (int)(uint32_t)v[1];
+  return MPI_SUCCESS;
+}
+
 // MPI_Wait / MPI_Waitall on the host (Proc::wait/waitall, proc_p2p.cpp:
 // 146-181): a request may be waited once (consumed); the wait is a device
 // wait launched on the request's stream, then the host synchronises it.
@@ -704,6 +862,7 @@ int host_waitall(int n, MPI_Request* reqs, MPI_Status* statuses) {
     if (graph) return MPIX_ERR_UNSUPPORTED;  // a captured request is waited in its graph
     auto& ri = rank_of(items[i].rank).reqs[items[i].n % kReqSlots];
     if (ri.gen != items[i].n / kReqSlots + 1 || ri.consumed) return MPIX_ERR_INVALID_REQUEST;
+    if (int h = rank_health(rank_of(items[i].rank))) return h;
   }
   // group by stream: one device wait (and one synchronisation) per stream
   std::map<cudaStream_t, std::vector<int>> by;
@@ -728,16 +887,16 @@ int host_waitall(int n, MPI_Request* reqs, MPI_Status* statuses) {
     }
     CK(cudaStreamSynchronize(s));
   }
+  // a watchdog expiry while waiting: the requests did not complete
+  for (int i = 0; i < n; ++i)
+    if (int h = rank_health(rank_of(items[i].rank))) return h;
   for (int i = 0; i < n; ++i) {
-    auto& ri = rank_of(items[i].rank).reqs[items[i].n % kReqSlots];
+    RankState& rs = rank_of(items[i].rank);
+    auto& ri = rs.reqs[items[i].n % kReqSlots];
     ri.consumed = true;
     if (statuses) {
-      statuses[i].MPI_SOURCE = ri.source;
-      statuses[i].MPI_TAG = ri.tag;
-      statuses[i].MPI_ERROR = MPI_SUCCESS;
-      statuses[i].source_index = -2;
-      statuses[i].count_bytes = UINT64_MAX;
-      statuses[i].truncated = 0;
+      CK(cudaSetDevice(rs.device));
+      if (int rc = read_status(rs, items[i].n, &statuses[i])) return rc;
     }
     reqs[i] = MPI_REQUEST_NULL;
   }
@@ -745,14 +904,22 @@ int host_waitall(int n, MPI_Request* reqs, MPI_Status* statuses) {
 }
 
 // Blocking conventional / multiplex operation: post as a blocking device
-// operation (eager or staged send, waiting receive), then synchronise.
-int host_blocking(int rc, mpix_comm_s* c, cudaStream_t s, MPI_Status* status, int source, int tag) {
+// operation (eager or staged send, waiting receive), then synchronise and
+// report the operation's status (its ticket).
+int host_blocking(int rc, mpix_comm_s* c, cudaStream_t s, MPI_Status* status, uint64_t ticket) {
   if (rc) return rc;
-  CK(cudaSetDevice(rank_of(c->rank).device));
+  RankState& rs = rank_of(c->rank);
+  CK(cudaSetDevice(rs.device));
   CK(cudaStreamSynchronize(s));
-  if (status) {
-    status->MPI_SOURCE = source;
-    status->MPI_TAG = tag;
+  if (int h = rank_health(rs)) return h;
+  int r = 0;
+  uint64_t n = 0;
+  if (ticket && decode_ticket(ticket, &r, &n)) {
+    rs.reqs[n % kReqSlots].consumed = true;
+    if (status) return read_status(rs, n, status);
+  } else if (status) {  // a blocking send carries no completion word
+    status->MPI_SOURCE = c->rank;
+    status->MPI_TAG = -1;
     status->MPI_ERROR = MPI_SUCCESS;
     status->source_index = -2;
     status->count_bytes = UINT64_MAX;
@@ -827,13 +994,14 @@ int MPI_Irecv(void* buf, int count, MPI_Datatype datatype, int source, int tag, 
 
 int MPI_Send(const void* buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm) {
   int rc = conv_post(comm, const_cast<void*>(buf), count, datatype, dest, tag, false, true, nullptr);
-  return rc ? rc : host_blocking(rc, comm, conv_stream(comm), nullptr, dest, tag);
+  return rc ? rc : host_blocking(rc, comm, conv_stream(comm), nullptr, 0);
 }
 
 int MPI_Recv(void* buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
              MPI_Status* status) {
-  int rc = conv_post(comm, buf, count, datatype, source, tag, true, true, nullptr);
-  return rc ? rc : host_blocking(rc, comm, conv_stream(comm), status, source, tag);
+  uint64_t t = 0;
+  int rc = conv_post(comm, buf, count, datatype, source, tag, true, true, nullptr, &t);
+  return rc ? rc : host_blocking(rc, comm, conv_stream(comm), status, t);
 }
 
 int MPI_Wait(MPI_Request* request, MPI_Status* status) {
@@ -867,14 +1035,15 @@ int MPIX_Stream_send(const void* buf, int count, MPI_Datatype datatype, int dest
                      MPI_Comm comm, int src_idx, int dst_idx) {
   int rc = stream_post(comm, const_cast<void*>(buf), count, datatype, dest, tag, src_idx, dst_idx,
                        false, true, nullptr);
-  return rc ? rc : host_blocking(rc, comm, local_stream_of(comm, src_idx), nullptr, dest, tag);
+  return rc ? rc : host_blocking(rc, comm, local_stream_of(comm, src_idx), nullptr, 0);
 }
 
 int MPIX_Stream_recv(void* buf, int count, MPI_Datatype datatype, int source, int tag,
                      MPI_Comm comm, int src_idx, int dst_idx, MPI_Status* status) {
+  uint64_t t = 0;
   int rc = stream_post(comm, buf, count, datatype, source, tag, src_idx, dst_idx, true, true,
-                       nullptr);
-  return rc ? rc : host_blocking(rc, comm, local_stream_of(comm, dst_idx), status, source, tag);
+                       nullptr, &t);
+  return rc ? rc : host_blocking(rc, comm, local_stream_of(comm, dst_idx), status, t);
 }
 
 int MPIX_Request_free(MPI_Request* request) {

@@ -98,22 +98,16 @@ int rank_init(RankState& r, const Config& cfg) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, r.device));
   r.sms = prop.multiProcessorCount;
-  {  // peers store into my completion words
-    int rc = mp_mode() ? MPIX_Alloc_mem(kReqSlots * sizeof(uint64_t), (void**)&r.d_done)
-                       : (cudaMalloc(&r.d_done, kReqSlots * sizeof(uint64_t)) == cudaSuccess
-                              ? MPI_SUCCESS : MPIX_ERR_NO_MEM);
+  {  // peers store into my completion words and status planes (kStatusOff)
+    const uint64_t nb = 3 * kDoneWords * sizeof(uint64_t);
+    int rc = mp_mode() ? MPIX_Alloc_mem(nb, (void**)&r.d_done)
+                       : (cudaMalloc(&r.d_done, nb) == cudaSuccess ? MPI_SUCCESS : MPIX_ERR_NO_MEM);
     if (rc) return rc;
+    CK(cudaMemset(r.d_done, 0, nb));
+    r.d_gdone = r.d_done + kReqSlots;  // captured requests' words (never reused)
   }
-  CK(cudaMemset(r.d_done, 0, kReqSlots * sizeof(uint64_t)));
   CK(cudaMalloc(&r.d_rec, kOpRecords * sizeof(OpRecord)));
   CK(cudaMemset(r.d_rec, 0, kOpRecords * sizeof(OpRecord)));
-  {  // captured requests' completion words (peers store into them too)
-    int rc = mp_mode() ? MPIX_Alloc_mem(kGraphReqs * sizeof(uint64_t), (void**)&r.d_gdone)
-                       : (cudaMalloc(&r.d_gdone, kGraphReqs * sizeof(uint64_t)) == cudaSuccess
-                              ? MPI_SUCCESS : MPIX_ERR_NO_MEM);
-    if (rc) return rc;
-  }
-  CK(cudaMemset(r.d_gdone, 0, kGraphReqs * sizeof(uint64_t)));
   CK(cudaMalloc(&r.d_grec, kGraphRecs * sizeof(OpRecord)));
   CK(cudaMemset(r.d_grec, 0, kGraphRecs * sizeof(OpRecord)));
   CK(cudaMalloc(&r.d_arrive, kArriveWords * sizeof(uint32_t)));
@@ -342,6 +336,8 @@ const char* MPIX_Error_string(int code) {
     case MPIX_ERR_TYPE: return "INVALID_TYPE";
     case MPIX_ERR_OP: return "INVALID_OP";
     case MPIX_ERR_NO_MEM: return "NO_MEM";
+    case MPIX_ERR_TIMEOUT: return "TIMEOUT";
+    case MPIX_ERR_DEVICE: return "DEVICE_PROTOCOL";
     default: return "UNKNOWN";
   }
 }
@@ -471,6 +467,7 @@ int MPIX_World_init(int nranks, const int* devices) {
   int rc = world_build(w.get(), nranks, devices, ndev);
   if (rc) return rc;
   g_world = w.release();
+  flusher_start(*g_world);
   return MPI_SUCCESS;
 }
 
@@ -500,6 +497,7 @@ int MPIX_World_init_mp(int rank, int nranks, const int* devices, MPIX_Allgather_
     return rc;
   }
   w.release();
+  flusher_start(*g_world);
   return MPI_SUCCESS;
 }
 
@@ -514,6 +512,7 @@ int MPIX_World_finalize(void) {
   std::lock_guard<std::mutex> lk(g_world_mu);
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
   World* w = g_world;
+  flusher_stop(*w);
   std::vector<cudaStream_t> held;
   for (auto& kv : w->batches) held.push_back(kv.first);
   for (cudaStream_t s : held) flush_stream(s);
@@ -550,7 +549,6 @@ int MPIX_World_finalize(void) {
     cudaStreamSynchronize(rs->aux);
     if (!w->mp) cudaFree(rs->d_done);
     cudaFree(rs->d_rec);
-    if (!w->mp) cudaFree(rs->d_gdone);
     cudaFree(rs->d_grec);
     cudaFree(rs->d_arrive);
     if (rs->d_trace) cudaFree(rs->d_trace);
@@ -620,15 +618,35 @@ int MPI_Comm_free(MPI_Comm* comm) {  // proc_comm.cpp:178-194
   World& w = *g_world;
   RankState& rs = rank_of(c->rank);
   const int P = c->sh->P;
+  // proc_comm.cpp:182-184: a receive posted on this comm and not yet
+  // delivered keeps it alive (checked locally, before the rendezvous).
+  // Conventional receives are host-waited, so they are checked here from
+  // their completion words; enqueue operations are ordered by the streams.
+  {
+    std::lock_guard<std::mutex> clk(c->mu);
+    for (auto& e : c->conv_recvs) {
+      auto& ri = rs.reqs[(uint64_t)(e.first - rs.d_done) % kReqSlots];
+      if (ri.consumed || ri.gen != e.second) continue;
+      uint64_t v = 0;
+      CK(cudaSetDevice(rs.device));
+      CK(cudaMemcpy(&v, e.first, 8, cudaMemcpyDeviceToHost));
+      if (v < e.second) return MPIX_ERR_PENDING_OPS;
+    }
+  }
   // Every member's outstanding work on this comm must retire before any
-  // region is released: exchange one event per member and make each aux
-  // stream wait on all of them.
+  // region is released: the member's release point follows its enqueue
+  // stream and every other stream it launched on (conventional p2p on the
+  // rank's internal stream, multiplex p2p on the local streams); members
+  // exchange those events and each aux stream waits on all of them.
   cudaEvent_t ev = nullptr;
   if (c->cu && flush_stream(c->cu) < 0) return MPIX_ERR_CUDA;
+  for (cudaStream_t s2 : c->side_streams)
+    if (flush_stream(s2) < 0) return MPIX_ERR_CUDA;
   CK(cudaSetDevice(rs.device));
   if (w.mp) {
     // events do not cross processes: retire my work, then agree
     CK(cudaStreamSynchronize(c->cu ? c->cu : rs.aux));
+    for (cudaStream_t s2 : c->side_streams) CK(cudaStreamSynchronize(s2));
     if ((int)comm_exchange(*c->sh, c->rank, c->rv_seq, CollMsg{}).size() != P) return MPIX_ERR_CUDA;
     c->sh->base[c->rank] = nullptr;  // heap memory is released with the heap
     for (auto* s : c->local_streams)
@@ -641,8 +659,19 @@ int MPI_Comm_free(MPI_Comm* comm) {  // proc_comm.cpp:178-194
     *comm = MPI_COMM_NULL;
     return MPI_SUCCESS;
   }
+  {  // my side streams first: aux follows them, then my enqueue stream
+    std::vector<cudaStream_t> mine = c->side_streams;
+    if (c->cu) mine.push_back(c->cu);
+    for (cudaStream_t s2 : mine) {
+      cudaEvent_t e2 = nullptr;
+      CK(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      CK(cudaEventRecord(e2, s2));
+      CK(cudaStreamWaitEvent(rs.aux, e2, 0));
+      CK(cudaEventDestroy(e2));
+    }
+  }
   CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  CK(cudaEventRecord(ev, c->cu ? c->cu : rs.aux));
+  CK(cudaEventRecord(ev, rs.aux));
   CollMsg m;
   m.p0 = ev;
   auto v = c->sh->rv.exchange(P, c->rank, c->rv_seq++, m);
@@ -855,6 +884,12 @@ int MPIX_Rank_error(int rank, uint64_t* code) {
   if (rank < 0 || rank >= g_world->n || !code) return MPIX_ERR_INVALID_RANK;
   *code = *reinterpret_cast<volatile uint64_t*>(g_world->ranks[rank]->h_err);
   return MPI_SUCCESS;
+}
+
+int MPIX_Comm_check(MPI_Comm comm) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (!comm) return MPIX_ERR_INVALID_COMM;
+  return rank_health(rank_of(comm->rank));
 }
 
 int MPIX_Trace_read(int rank, void* out, int max_records, int* n_records) {

@@ -19,6 +19,7 @@
 #include <unordered_set>
 #include <queue>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -44,6 +45,8 @@ struct Config {
   int stage_slots = 64;              // MPIX_STAGE_SLOTS: device staging arena slots per rank
   uint64_t stage_chunk = 4ull << 20; // MPIX_STAGE_CHUNK: bytes per arena slot
   bool graph = false;                // MPIX_GRAPH=1: every enqueue comm is graph-capturable
+  uint64_t flush_ns = 100000;        // MPIX_FLUSH_US: a held batch older than this is launched by
+                                     // the flusher thread (progress guarantee); 0 = no flusher
 
   static Config from_env() {
     Config c;
@@ -69,11 +72,11 @@ struct Config {
     if (c.stage_slots > 1024) c.stage_slots = 1024;
     c.stage_chunk = (geti("MPIX_STAGE_CHUNK", c.stage_chunk) + 255) & ~255ull;
     c.graph = geti("MPIX_GRAPH", 0) != 0;
+    c.flush_ns = geti("MPIX_FLUSH_US", 100) * 1000ull;
     return c;
   }
 };
 
-constexpr uint64_t kReqSlots = 1ull << 20;  // completion words per rank
 constexpr uint64_t kStageSlots = 4096;      // staging buffers per rank
 
 extern std::atomic<uint64_t> g_launches;  // kernels launched (MPIX_Launch_count)
@@ -169,6 +172,10 @@ struct RankState {
     bool remote = false;  // the peer lives on another GPU (system scope)
     bool conventional = false;  // MPI_Isend/Irecv or MPIX_Stream_isend/irecv (host-waited)
     bool consumed = false;      // completed by MPI_Wait/Waitall (proc_p2p.cpp:147)
+    bool is_recv = false;
+    int me = -1;                // the issuing comm rank (a send's status source)
+    uint64_t bytes = 0;         // send: payload bytes (its status, proc_p2p.cpp:54-58)
+    const void* comm = nullptr; // conventional receive: its comm (MPI_Comm_free PENDING_OPS)
   };
   std::vector<ReqInfo> reqs;
   // CUDA-Graph capture: requests created while a stream is
@@ -183,7 +190,6 @@ struct RankState {
   uint32_t* d_arrive = nullptr;
   std::atomic<uint32_t> arrive_next{0};
 };
-constexpr uint64_t kGraphReqs = 1ull << 16;   // captured requests per rank (lifetime)
 constexpr uint64_t kGraphRecs = 4096;         // captured large operations per rank (lifetime)
 constexpr uint32_t kArriveWords = 4096;       // streams with graph-capturable batches per rank
 
@@ -233,6 +239,9 @@ struct StreamBatch {
   // the final launch, which advances the counters
   std::unordered_map<const uint64_t*, uint32_t> grel;
   uint32_t* d_arrive = nullptr;
+  // steady-clock ns when the first held operation joined (0 = empty): the
+  // flusher thread launches a batch nobody ordered within cfg.flush_ns
+  uint64_t t_first = 0;
 };
 
 }  // namespace mpix
@@ -274,6 +283,13 @@ struct mpix_comm_s {
   bool graph = false;
   uint64_t* d_gseq = nullptr;
   std::unordered_map<uint64_t, uint16_t> gtag;
+  // Conventional receives not yet waited (completion word, generation):
+  // MPI_Comm_free returns PENDING_OPS while one is incomplete
+  // (proc_comm.cpp:184, c.pending counts receives until delivery).
+  std::vector<std::pair<uint64_t*, uint64_t>> conv_recvs;
+  // Streams other than cu this member launched on (conventional and
+  // multiplex p2p): MPI_Comm_free orders the region release after them.
+  std::vector<cudaStream_t> side_streams;
 };
 
 namespace mpix {
@@ -298,6 +314,12 @@ struct World {
   std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<>> retired;
   std::mutex comms_mu;
   std::vector<mpix_comm_s*> all_comms;
+  // Flusher thread (progress guarantee for held batches, mpix_p2p.cpp)
+  std::thread flusher;
+  std::mutex fl_mu;
+  std::condition_variable fl_cv;
+  bool fl_stop = false;
+  std::atomic<bool> fl_armed{false};
 
   uint32_t alloc_ctx() {  // world.cpp:43-51: retired ids recycled lowest-first
     std::lock_guard<std::mutex> lk(ctx_mu);
@@ -317,6 +339,16 @@ struct World {
 extern std::mutex g_world_mu;
 extern World* g_world;
 extern thread_local int t_bound_rank;
+
+// Sticky watchdog state (MPIX_ERR_TIMEOUT / MPIX_ERR_DEVICE): a kernel of
+// the rank gave up a flag wait and recorded why in the rank's host-mapped
+// error word; from then on every call naming the rank reports it.
+inline int rank_health(const RankState& rs) {
+  if (!rs.h_err) return MPI_SUCCESS;  // a stub rank of another process
+  const uint64_t v = *reinterpret_cast<volatile uint64_t*>(rs.h_err);
+  if (!v) return MPI_SUCCESS;
+  return v == ERRW_PROTOCOL ? MPIX_ERR_DEVICE : MPIX_ERR_TIMEOUT;
+}
 
 #define CK(call)                                 \
   do {                                           \
@@ -352,6 +384,9 @@ StreamBatch& batch_of(cudaStream_t s, int device);
 int flush_locked(StreamBatch& b, cudaStream_t s, const WaitEntry* w, int nwait, bool wsys,
                  uint64_t* w_err);
 int flush_stream(cudaStream_t s);
+void flusher_start(World& w);
+void flusher_stop(World& w);
+void batch_note_held(StreamBatch& b);  // caller holds b.mu, b.ops non-empty
 
 // mpix_coll.cpp
 int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype dt, MPI_Op op,

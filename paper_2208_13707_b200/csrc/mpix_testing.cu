@@ -105,6 +105,37 @@ __global__ void k_iter_check(const float* x, uint64_t n, const uint32_t* iter, f
 }
 __global__ void k_iter_bump(uint32_t* iter) { *iter += 1; }
 
+// cfg3 value sets (oracle: orc_value_f32 / orc_value_bf16): set 0 exact,
+// set 1 uniform(-1,1) = (h >> 8) * 2^-23 - 1; bf16 = RNE of the fp32 value.
+__device__ __forceinline__ uint32_t hash32(uint64_t i, uint32_t r) {
+  uint64_t z = i * 0x9E3779B97F4A7C15ull + (uint64_t)r * 0xD1B54A32D192ED03ull + 1;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return (uint32_t)(z ^ (z >> 31));
+}
+__device__ __forceinline__ float value_f32(uint64_t i, uint32_t r, int set, int bf) {
+  const uint32_t h = hash32(i, r);
+  if (set == 0)
+    return bf ? __fdiv_rn((float)((int)(h % 256u) - 128), 16.0f)
+              : __fdiv_rn((float)((int)(h % 2048u) - 1024), 256.0f);
+  return __fsub_rn(__fmul_rn((float)(h >> 8), 1.0f / 8388608.0f), 1.0f);
+}
+__global__ void k_fill_values(void* buf, uint64_t n, int bf, int set, uint32_t r) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = t; i < n; i += nt) {
+    const float v = value_f32(i, r, set, bf);
+    if (bf) {
+      // RNE as orc_f32_to_bf16_rne (no NaNs occur)
+      uint32_t u = __float_as_uint(v);
+      u += 0x7fffu + ((u >> 16) & 1u);
+      reinterpret_cast<uint16_t*>(buf)[i] = (uint16_t)(u >> 16);
+    } else {
+      reinterpret_cast<float*>(buf)[i] = v;
+    }
+  }
+}
+
 __global__ void k_fill_f32(float* x, uint64_t n, float v) {
   uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
@@ -205,6 +236,13 @@ int MPIXT_Checksum(const void* buf, uint64_t nbytes, uint64_t* out_dev, void* st
   if (cudaMemsetAsync(out_dev, 0, 8, s) != cudaSuccess) return 100;
   k_checksum<<<grid_for(nbytes / 8 + 1, 256), 256, 0, s>>>((const uint8_t*)buf, nbytes,
                                                            (unsigned long long*)out_dev);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Fill_values(void* buf, uint64_t count, int dt, int set, uint32_t rank, void* stream) {
+  if (dt != MPI_FLOAT && dt != MPIX_BFLOAT16) return 103;
+  k_fill_values<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(buf, count, dt == MPIX_BFLOAT16,
+                                                                       set, rank);
   return done(cudaGetLastError());
 }
 
@@ -321,7 +359,7 @@ int MPIXT_Copy_to_host(void* host, const void* dev, uint64_t bytes) {
 
 int MPIXT_Preload(void) {
   cudaFuncAttributes fa;
-  const void* ks[] = {(const void*)k_fill_pattern, (const void*)k_checksum, (const void*)k_saxpy,
+  const void* ks[] = {(const void*)k_fill_pattern, (const void*)k_checksum, (const void*)k_fill_values, (const void*)k_saxpy,
                       (const void*)k_delay,        (const void*)k_empty,    (const void*)k_fill_f32,
                       (const void*)k_halo,         (const void*)k_stencil7, (const void*)k_iter_fill,
                       (const void*)k_iter_check,   (const void*)k_iter_bump};

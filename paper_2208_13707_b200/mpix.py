@@ -39,7 +39,8 @@ ERR_NAMES = [
 ]
 ERR = {n: i for i, n in enumerate(ERR_NAMES)}
 ERR.update({"CUDA_ERROR": 100, "NOT_INITIALIZED": 101, "UNSUPPORTED": 102,
-            "INVALID_ARG": 103, "INVALID_TYPE": 104, "INVALID_OP": 105, "NO_MEM": 106})
+            "INVALID_ARG": 103, "INVALID_TYPE": 104, "INVALID_OP": 105, "NO_MEM": 106,
+            "TIMEOUT": 107, "DEVICE_PROTOCOL": 108})
 
 _TORCH_DT = {}
 
@@ -54,6 +55,11 @@ class MPIXError(RuntimeError):
 class MPIStatus(C.Structure):
     _fields_ = [("MPI_SOURCE", C.c_int), ("MPI_TAG", C.c_int), ("MPI_ERROR", C.c_int),
                 ("source_index", C.c_int), ("count_bytes", C.c_uint64), ("truncated", C.c_int)]
+
+    def as_dict(self) -> dict:
+        """The reference's Status (request.hpp:13-19) fields."""
+        return {"source": self.MPI_SOURCE, "tag": self.MPI_TAG, "source_index": self.source_index,
+                "bytes": self.count_bytes, "truncated": bool(self.truncated)}
 
 
 _lib = None
@@ -147,12 +153,14 @@ def _declare(L: C.CDLL) -> None:
         "MPIX_Type_size": (I, [I]),
         "MPIX_Version": (C.c_char_p, []),
         "MPIX_Rank_error": (I, [I, C.POINTER(U64)]),
+        "MPIX_Comm_check": (I, [P]),
         "MPIX_Comm_region": (I, [P, C.POINTER(P), C.POINTER(U64)]),
         "MPIX_Trace_read": (I, [I, P, I, C.POINTER(I)]),
         "MPIXT_Copy_to_host": (I, [P, P, U64]),
         "MPIXT_Fill_pattern": (I, [P, U64, U32, U32, P]),
         "MPIXT_Checksum": (I, [P, U64, P, P]),
         "MPIXT_Saxpy": (I, [I, C.c_float, P, P, P]),
+        "MPIXT_Fill_values": (I, [P, U64, I, I, U32, P]),
         "MPIXT_Delay": (I, [U64, P]),
         "MPIXT_Empty": (I, [P]),
         "MPIXT_Iter_fill": (I, [P, U64, P, C.c_float, C.c_float, P]),
@@ -463,8 +471,15 @@ class Comm:
     def send(self, buf, count: int, dt: int, dest: int, tag: int) -> None:
         check(lib().MPI_Send(_ptr(buf), count, dt, dest, tag, self.h), "MPI_Send")
 
-    def recv(self, buf, count: int, dt: int, source: int, tag: int) -> None:
-        check(lib().MPI_Recv(_ptr(buf), count, dt, source, tag, self.h, None), "MPI_Recv")
+    def recv(self, buf, count: int, dt: int, source: int, tag: int) -> dict:
+        st = MPIStatus()
+        check(lib().MPI_Recv(_ptr(buf), count, dt, source, tag, self.h, C.byref(st)), "MPI_Recv")
+        return st.as_dict()
+
+    def check(self) -> None:
+        """MPIX_Comm_check: raises MPIXError(TIMEOUT) once a kernel of this
+        member's rank hit its watchdog (sticky)."""
+        check(lib().MPIX_Comm_check(self.h), "MPIX_Comm_check")
 
     def isend(self, buf, count: int, dt: int, dest: int, tag: int) -> Request:
         r = C.c_uint64()
@@ -483,9 +498,11 @@ class Comm:
               "MPIX_Stream_send")
 
     def stream_recv(self, buf, count: int, dt: int, source: int, tag: int, src_idx: int,
-                    dst_idx: int) -> None:
+                    dst_idx: int) -> dict:
+        st = MPIStatus()
         check(lib().MPIX_Stream_recv(_ptr(buf), count, dt, source, tag, self.h, src_idx, dst_idx,
-                                     None), "MPIX_Stream_recv")
+                                     C.byref(st)), "MPIX_Stream_recv")
+        return st.as_dict()
 
     def stream_isend(self, buf, count: int, dt: int, dest: int, tag: int, src_idx: int,
                      dst_idx: int) -> Request:
@@ -507,15 +524,19 @@ def wait_enqueue(req: Request) -> None:
     check(lib().MPIX_Wait_enqueue(C.byref(h), None), "MPIX_Wait_enqueue")
 
 
-def wait(req: Request) -> None:
-    """MPI_Wait (host): the request is consumed."""
+def wait(req: Request) -> dict:
+    """MPI_Wait (host): the request is consumed; returns its status."""
     h = C.c_uint64(req.h if req else 0)
-    check(lib().MPI_Wait(C.byref(h), None), "MPI_Wait")
+    st = MPIStatus()
+    check(lib().MPI_Wait(C.byref(h), C.byref(st)), "MPI_Wait")
+    return st.as_dict()
 
 
-def waitall(reqs: Sequence[Optional[Request]]) -> None:
+def waitall(reqs: Sequence[Optional[Request]]) -> list:
     arr = (C.c_uint64 * max(1, len(reqs)))(*[(r.h if r else 0) for r in reqs])
-    check(lib().MPI_Waitall(len(reqs), arr, None), "MPI_Waitall")
+    sts = (MPIStatus * max(1, len(reqs)))()
+    check(lib().MPI_Waitall(len(reqs), arr, sts), "MPI_Waitall")
+    return [sts[i].as_dict() for i in range(len(reqs))]
 
 
 def waitall_enqueue(reqs: Sequence[Optional[Request]]) -> None:
@@ -710,6 +731,11 @@ class testing:
     @staticmethod
     def fill_pattern(buf, nbytes: int, seed: int, it: int, stream) -> None:
         check(lib().MPIXT_Fill_pattern(_ptr(buf), nbytes, seed, it, _stream_handle(stream)))
+
+    @staticmethod
+    def fill_values(buf, count: int, dt: int, value_set: int, rank: int, stream) -> None:
+        check(lib().MPIXT_Fill_values(_ptr(buf), count, dt, value_set, rank, _stream_handle(stream)),
+              "MPIXT_Fill_values")
 
     @staticmethod
     def checksum(buf, nbytes: int, out_dev, stream) -> None:

@@ -182,3 +182,24 @@ def test_live_cross_check_with_reference():
         out = np.zeros_like(ins)
         R.ref_allreduce(P, 301, 2, 1, ins.ctypes.data, out.ctypes.data, 1)
         assert out[0].tobytes() == O.allreduce(list(ins), "f32").tobytes()
+
+
+def test_generated_allreduce_oracle_equals_materialised_fold():
+    """orc_allreduce_gen (cfg3 at full size, inputs generated per element)
+    computes the same fold as orc_allreduce_f32/bf16 over materialised inputs,
+    and its "exact" set is the exact_inputs value set."""
+    for dt, npdt in (("f32", np.float32), ("bf16", np.uint16)):
+        for vs in (0, 1):
+            n, P = 4099, 3
+            ins = [np.array([O.value(i, r, dt, vs) for i in range(n)], dtype=npdt) for r in range(P)]
+            exp = O.allreduce(ins, dt)
+            cs, samp = O.allreduce_gen(P, n, dt, vs, 1, [0, 7, n - 1])
+            assert cs == O.checksum64(exp)
+            assert samp.view(np.uint8).tobytes() == exp[[0, 7, n - 1]].view(np.uint8).tobytes()
+            assert O.gen_checksum(2, n, dt, vs) == O.checksum64(ins[2])
+            if vs == 0:
+                for a, b in zip(O.exact_inputs(P, n, dt), ins):
+                    assert a.view(np.uint8).tobytes() == b.view(np.uint8).tobytes()
+            else:  # uniform(-1, 1), order-sensitive: not every sum is exact
+                f = ins[0].astype(np.float32) if dt == "f32" else (ins[0].astype(np.uint32) << 16).view(np.float32)
+                assert f.min() >= -1.0 and f.max() <= 1.0  # bf16 RNE may reach 1.0
