@@ -118,6 +118,27 @@ class ClockSampler:
 # --------------------------------------------------------------------------
 # reference arm / cpu baseline
 # --------------------------------------------------------------------------
+def host_cpus():
+    """The host cores this process may run on (the CPU arm is pinned to them
+    and they are stated in the line: nproc and the affinity list)."""
+    try:
+        aff = sorted(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = list(range(os.cpu_count() or 1))
+    return {"nproc": os.cpu_count(), "affinity": aff}
+
+
+def pin_cpu_arm():
+    """Pin the CPU arm to an explicit core list (the whole affinity mask, in
+    order) so the reference's worker threads stay on the stated cores."""
+    h = host_cpus()
+    try:
+        os.sched_setaffinity(0, h["affinity"])
+    except (AttributeError, OSError):
+        pass
+    return h
+
+
 def cpu_reference_selfmsg(size, budget_s, min_msgs=3):
     """The unmodified reference (oracle/_ref) on the loopback workload: one
     exec queue, isend+irecv+waitall_enqueue of `size` bytes per message."""
@@ -126,6 +147,7 @@ def cpu_reference_selfmsg(size, budget_s, min_msgs=3):
     R = O.ref()
     if R is None:
         return None
+    h = pin_cpu_arm()
     src = np.random.default_rng(0).integers(0, 255, size, dtype=np.uint8)
     dst = np.zeros_like(src)
     R.ref_selfmsg(src.ctypes.data, dst.ctypes.data, size, 1, 0)  # warm
@@ -135,9 +157,55 @@ def cpu_reference_selfmsg(size, budget_s, min_msgs=3):
         msgs += 2
     assert (dst == src).all()
     return {"value": size * msgs / t / 1e9, "unit": "GB/s", "cores": 2, "kind": "reference",
+            "threads": 2, "host": h,
             "sample": f"{msgs} x {size >> 20} MiB self-messages (isend+irecv+waitall_enqueue) "
-                      f"through the compiled reference, 1 rank = driver thread + queue worker, "
-                      f"{t:.1f} s"}
+                      f"through the compiled reference, 1 rank = driver thread + queue worker "
+                      f"(2 threads on the {h['nproc']}-core host), {t:.1f} s"}
+
+
+def cpu_reference_configs():
+    """The reference's own CPU path (oracle/_ref) on cfg1, cfg3 and cfg4 in
+    the same run, on this host's cores (SURVEY.md §8(d) "CPU reference timed
+    beside it"); bounded samples, sizes stated."""
+    import numpy as np
+    from oracle import oracle as O
+    R = O.ref()
+    if R is None:
+        return None
+    h = pin_cpu_arm()
+    out = {"host": h, "kind": "reference (unmodified streamix compiled from its sources)"}
+    # cfg1: 2 ranks, Send/Recv_enqueue ping-pong of 1 MiB fp32, 200 round trips
+    n = 262144
+    x = ((np.arange(n) % 1024).astype(np.float32) * np.float32(0.5))
+    f0, f1 = C.c_uint64(), C.c_uint64()
+    R.ref_pingpong(x.ctypes.data, 4 * n, 5, C.byref(f0), C.byref(f1))
+    t = R.ref_pingpong(x.ctypes.data, 4 * n, 200, C.byref(f0), C.byref(f1))
+    out["cfg1_pingpong_1MiB"] = {"round_trips": 200, "half_rtt_us": t / 400 * 1e6,
+                                 "GBps": 4 * n / (t / 400) / 1e9, "fnv1a64_rank0": f0.value,
+                                 "threads": 4}
+    for nb, it in ((8, 2000), (4096, 2000)):
+        b = np.zeros(nb, dtype=np.uint8)
+        t = R.ref_pingpong(b.ctypes.data, nb, it, C.byref(f0), C.byref(f1))
+        out[f"pingpong_{nb}B_half_rtt_us"] = t / (2 * it) * 1e6
+    # cfg3: the composed allreduce (irecv/isend/waitall_enqueue + queued rank-ordered fold)
+    ar = {}
+    cnt = 16 << 20  # 64 MiB fp32 per rank (the 256 MiB config scaled to fit the sample budget)
+    for P in (2, 4, 8):
+        ins = np.ones(P * cnt, dtype=np.float32)
+        outb = np.zeros_like(ins)
+        t = R.ref_allreduce(P, cnt, 2, 1, ins.ctypes.data, outb.ctypes.data, 1)
+        algbw = 4 * cnt / t / 1e9
+        ar[f"f32_P{P}"] = {"bytes_per_rank": 4 * cnt, "s": t, "algbw_GBps": algbw,
+                           "busbw_GBps": algbw * 2 * (P - 1) / P, "threads": 2 * P,
+                           "check": bool(outb[0] == P)}
+    out["cfg3_allreduce_64MiB"] = ar
+    # cfg4: 8 ranks x 4 streams, 8-B messages, window 64 (bench.hpp:22)
+    msgs = C.c_uint64()
+    R.ref_msgrate(8, 4, 64, 5, C.byref(msgs))
+    t = R.ref_msgrate(8, 4, 64, 100, C.byref(msgs))
+    out["cfg4_msgrate_8B"] = {"ranks": 8, "streams_per_rank": 4, "window": 64, "batches": 100,
+                              "msgs_per_s": msgs.value / t, "threads": 8 + 8 * 4}
+    return out
 
 
 def run_reference(args):
@@ -152,6 +220,7 @@ def run_reference(args):
         return
     size = args.size
     n = args.gpus
+    host = pin_cpu_arm()
     src = np.random.default_rng(0).integers(0, 255, size, dtype=np.uint8)
     dst = np.zeros_like(src)
     if n == 1:
@@ -184,6 +253,7 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": workload, "message_bytes": size, "host": "CPU (reference streamix)"},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "threads": cores, "host": host,
                          "sample": f"{args.steps} steps of {workload}"},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -246,7 +316,7 @@ def bench_mp(args, rank, world, local):
     S = args.size
     ndev = torch.cuda.device_count()
     dev = local % ndev
-    w = mpix.MPWorld(heap_bytes=3 * S + (4 << 30), device=dev)  # bump heap: bench + extras buffers
+    w = mpix.MPWorld(heap_bytes=3 * S + (6 << 30), device=dev)  # bump heap: bench + extras buffers
     s = mpix.testing.new_stream(dev)
     c = w.comm().stream_comm_create(mpix.Stream.from_cuda(s))
     src, dst = w.alloc(S), w.alloc(S)
@@ -294,21 +364,30 @@ def bench_mp(args, rank, world, local):
     t_step = float(t[0]) / args.steps
     nl = torch.tensor([launches], dtype=torch.int64)
     dist.all_reduce(nl, op=dist.ReduceOp.SUM)
-    # dominant kernel: the copy grid of each message (receiver pulls or sender
-    # pushes, whichever arrives second); longest average over ranks
+    # dominant kernel: the copy grid of each message. Both sides launch one;
+    # the second arriver's copies (a sender pushes into a posted receive, a
+    # receiver pulls a posted send), the other is empty. The runtime times
+    # both and counts only grids whose decision records say they copied.
     mpix.testing.copy_timing(True)
     for _ in range(args.steps):
         step()
     s.synchronize()
-    tot, ncopy = mpix.testing.copy_timing_read()
+    tot, ncopy, moved = mpix.testing.copy_timing_read()
     mpix.testing.copy_timing(False)
-    kt = torch.tensor([tot / max(ncopy, 1) if ncopy else 0.0], dtype=torch.float64)
-    dist.all_reduce(kt, op=dist.ReduceOp.MAX)
-    k_ms = float(kt[0])
+    agg = torch.tensor([tot, float(ncopy), float(moved)], dtype=torch.float64)
+    dist.all_reduce(agg, op=dist.ReduceOp.SUM)
+    k_ms = float(agg[0]) / max(float(agg[1]), 1.0)       # per copying grid, over all pairs
+    k_bytes = float(agg[2]) / max(float(agg[1]), 1.0)    # bytes per copying grid
+    n_copy = int(agg[1])
     clk = clocks.stop()
     same_gpu = ndev < world
-    peak = peaks().get("hbm_gbs", 6650.0) / 2 if same_gpu else 770.0
-    achieved = S / (k_ms / 1e3) / 1e9 if k_ms else 0.0
+    achieved = k_bytes / (k_ms / 1e3) / 1e9 if k_ms else 0.0
+    if same_gpu:  # ranks share a GPU: an HBM copy (read + write) on one device
+        peak = peaks().get("hbm_gbs", 6650.0) / 2
+        peak_src = "half the measured HBM copy bandwidth (read + write on one GPU)"
+    else:
+        peak = 770.0
+        peak_src = "measured peer copy 770 GB/s per direction (B200_PROFILING.md); nominal 900"
     # e2e: the sender's pinned host input -> H2D -> Isend; the receiver's
     # Irecv -> checksum -> 8-byte D2H; both synchronise every step
     host = torch.empty(S, dtype=torch.uint8, pin_memory=True)
@@ -350,11 +429,12 @@ def bench_mp(args, rank, world, local):
                    **({"note": "GPUs shared by ranks: not an NVLink measurement"} if same_gpu else {})},
         "roofline": {"bound": "hbm" if same_gpu else "nvlink", "unit": "GB/s", "achieved": achieved,
                      "peak": peak, "frac": achieved / peak if peak else 0.0, "traffic": None,
-                     "peak_source": ("half the measured HBM copy bandwidth (read + write on one GPU)"
-                                     if same_gpu else
-                                     "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"),
-                     "kernel": "mpix::k_gcopy (the copy grid of each message)", "kernel_ms": k_ms,
-                     "algorithmic_bytes_per_launch": S},
+                     "peak_source": peak_src,
+                     **({} if same_gpu else {"frac_of_nominal_900": achieved / 900.0}),
+                     "kernel": "mpix::k_gcopy (the second arriver's copy grid of each message)",
+                     "kernel_ms": k_ms, "kernel_launches_timed": n_copy,
+                     "algorithmic_bytes_per_launch": k_bytes,
+                     "step_frac": S / t_step / 1e9 / peak if peak else 0.0},
         "e2e": {"value": S * pairs * args.steps / float(e2e_t[0]) / 1e9, "unit": "GB/s",
                 "h2d_bytes_per_step": S * pairs, "d2h_bytes_per_step": 8 * pairs,
                 "timing": "host wall clock, max over ranks, streams synchronised every step"},
@@ -364,10 +444,87 @@ def bench_mp(args, rank, world, local):
     }
 
 
+SWEEP = [8, 64, 512, 4096, 32768, 262144, 2 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30]
+SWEEP_CAP = 1 << 30  # bytes of receive slots per window
+
+
+def tmax(torch, dist, v):
+    t = torch.tensor([float(v)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def stream_sweep_mp(mpix, torch, dist, c, s, rank, big_src, big_dst):
+    """cfg2 bandwidth: rank 0 -> rank 1 unidirectional
+    streaming, windows of 16 Isend_enqueue / Irecv_enqueue + Waitall_enqueue
+    (fewer slots above 64 MiB: a window's receives fit 1 GiB), native driver;
+    device time max over the pair."""
+    out = {}
+    for nb in SWEEP:
+        W = 16 if nb * 16 <= SWEEP_CAP else max(1, SWEEP_CAP // nb)
+        reps = int(min(200, max(3, (2 << 30) // (nb * W))))
+        buf = big_src if rank == 0 else big_dst
+        dist.barrier()
+        if rank < 2:
+            mpix.testing.stream_window(c, buf, nb, W, 2, 1 - rank, rank == 0, s)
+            s.synchronize()
+        dist.barrier()
+        d = 0.0
+        if rank < 2:
+            d, _ = mpix.testing.stream_window(c, buf, nb, W, reps, 1 - rank, rank == 0, s)
+        t = tmax(torch, dist, d)
+        g = nb * W * reps / t / 1e9
+        out[str(nb)] = {"window": W, "reps": reps, "GBps": g, "frac_of_770": g / 770.0,
+                        "frac_of_900": g / 900.0}
+    return out
+
+
+def round_robin(n, rnd, me):
+    """Partner of `me` in round `rnd` of the circle method (n even)."""
+    m = n - 1
+    if me == m:
+        return rnd
+    if me == rnd:
+        return m
+    return (2 * rnd - me) % m
+
+
+def all_pairs_mp(mpix, torch, dist, c, s, rank, world, big_src, big_dst):
+    """Every GPU pair at 64 MiB (SURVEY.md §8(d) "all 28 pairs ... for
+    uniformity"): n-1 rounds of n/2 disjoint pairs; in each pair the lower
+    rank streams 3 windows of 4 x 64 MiB to the higher; per-pair device time
+    is the max of its two ranks."""
+    nb, W, reps = 64 << 20, 4, 3
+    pairs = {}
+    for rnd in range(world - 1):
+        q = round_robin(world, rnd, rank)
+        sender = rank < q
+        buf = big_src if sender else big_dst
+        dist.barrier()
+        mpix.testing.stream_window(c, buf, nb, W, 1, q, sender, s)
+        s.synchronize()
+        dist.barrier()
+        d, _ = mpix.testing.stream_window(c, buf, nb, W, reps, q, sender, s)
+        ts = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(ts, torch.tensor([float(q), d], dtype=torch.float64))
+        for i in range(world):
+            j = int(ts[i][0])
+            if i < j:
+                t = max(float(ts[i][1]), float(ts[j][1]))
+                pairs[f"{i}-{j}"] = nb * W * reps / t / 1e9
+    v = sorted(pairs.values())
+    return {"message_bytes": nb, "pairs": pairs, "n_pairs": len(v), "min_GBps": v[0],
+            "median_GBps": v[len(v) // 2], "max_GBps": v[-1], "min_over_max": v[0] / v[-1],
+            "min_frac_of_770": v[0] / 770.0}
+
+
 def extras_mp(args, mpix, torch, dist, w, c, s, rank, world, dev):
     """Multi-process N > 1: Allreduce_enqueue 256 MiB over all N (busbw) and
     the ranks 0 <-> 1 ping-pong half round trip, device time max over ranks."""
     out = {}
+    big_src, big_dst = w.alloc(SWEEP_CAP), w.alloc(SWEEP_CAP)
+    out["stream_bw_rank0_to_rank1"] = stream_sweep_mp(mpix, torch, dist, c, s, rank, big_src, big_dst)
+    out["all_pairs_64MiB"] = all_pairs_mp(mpix, torch, dist, c, s, rank, world, big_src, big_dst)
     ar = {}
     for name, tdt, mdt in (("f32", torch.float32, mpix.MPI_FLOAT), ("bf16", torch.bfloat16, mpix.MPIX_BFLOAT16)):
         nbytes = 256 << 20
@@ -458,12 +615,12 @@ def bench_replica(args, rank, world, local):
     mpix.testing.copy_timing(True)
     mpix.testing.loopback(c, src, dst, S, args.steps, s)
     torch.cuda.synchronize(dev)
-    tot_ms, ncopy = mpix.testing.copy_timing_read()
+    tot_ms, ncopy, moved = mpix.testing.copy_timing_read()
     mpix.testing.copy_timing(False)
     clk = clocks.stop()
     k_ms = tot_ms / max(ncopy, 1)
     peak = peaks().get("hbm_gbs", 6650.0)
-    achieved = 2 * S / (k_ms / 1e3) / 1e9
+    achieved = 2 * (moved / max(ncopy, 1)) / (k_ms / 1e3) / 1e9
     # e2e: pinned host input -> H2D -> loopback -> checksum -> 8-byte D2H
     host = torch.empty(S, dtype=torch.uint8, pin_memory=True)
     host.copy_(src.cpu())
@@ -595,28 +752,31 @@ def bench_world(args):
     t_step = ms / 1e3 / args.steps
     value = S * len(pairs) / t_step / 1e9
 
-    # dominant kernel: the receive-side copy grid (k_copy), timed with CUDA
-    # events the runtime records around each launch on the launching stream
-    # (MPIXT_Copy_timing), over K more steps of the same workload
+    # dominant kernel: the copy grid (k_gcopy), timed with CUDA events the
+    # runtime records around each launch on the launching stream
+    # (MPIXT_Copy_timing; only grids that copied are counted), over K more
+    # steps of the same workload
     mpix.testing.copy_timing(True)
     for k in range(args.steps):
         step()
     sync()
-    tot_ms, ncopy = mpix.testing.copy_timing_read()
+    tot_ms, ncopy, moved = mpix.testing.copy_timing_read()
     mpix.testing.copy_timing(False)
     k_ms = tot_ms / max(ncopy, 1)
+    k_bytes = moved / max(ncopy, 1)  # message bytes one copying grid moved
 
-    # roofline of the dominant kernel (the receive kernel that moves the payload)
+    # roofline of the dominant kernel (the copy grid that moves the payload)
     if P == 1:
-        alg_bytes = 2 * S
+        alg_bytes = 2 * k_bytes  # read + write of the message on one GPU
         peak = pk.get("hbm_gbs", 6650.0)
         roof = {"bound": "hbm", "unit": "GB/s", "peak_source": "MEASURED_PEAKS.json hbm_gbs"
                 if "hbm_gbs" in pk else "fallback 6650 GB/s (B200_PROFILING.md)"}
     else:
-        alg_bytes = S
+        alg_bytes = k_bytes
         peak = 770.0
         roof = {"bound": "nvlink", "unit": "GB/s",
-                "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"}
+                "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md); "
+                               "nominal 900"}
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
@@ -626,10 +786,11 @@ def bench_world(args):
         except Exception:
             traffic = None
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
-                 "kernel": "mpix::k_copy (receive-side pull of the payload)",
+                 "kernel": "mpix::k_gcopy (the copy grid of the message; the second arriver's)",
                  "kernel_ms": k_ms, "kernel_launches_timed": ncopy,
                  "algorithmic_bytes_per_launch": alg_bytes,
-                 "step_frac": alg_bytes * len(pairs) / t_step / 1e9 / peak,
+                 "step_frac": (2 * S if P == 1 else S) * len(pairs) / t_step / 1e9 / peak,
+                 **({} if P == 1 else {"frac_of_nominal_900": achieved / 900.0}),
                  "step_note": "whole step (all launches: post, decide, copy, complete, wait) "
                               "against the same roofline"})
 
@@ -660,6 +821,8 @@ def bench_world(args):
         line["extras"] = extras_ngpu(args, mpix, torch, w, ctx, dev)
     if rank0_cpu() and P == 1:  # the CPU baseline: rank 0 at N=1 only
         line["cpu_baseline"] = cpu_reference_selfmsg(S, args.cpu_seconds)
+        if not args.no_extras:
+            line["cpu_reference_configs"] = cpu_reference_configs()
     sync()
     w.finalize()
     if not args.no_extras and P == 1:

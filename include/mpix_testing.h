@@ -87,6 +87,11 @@ int MPIXT_Pingpong_side(MPI_Comm c, void *buf, uint64_t bytes, int iters, int pe
                         void *stream, double *dev_s);
 /* producer kernel -> Send_enqueue -> Recv_enqueue -> consumer kernel (self
  * messages of n floats on one stream), `iters` times. */
+/* cfg2 streaming bandwidth, one side of a pair: reps windows of W (<= 64)
+ * Isend/Irecv_enqueue of `bytes` + Waitall_enqueue; receive i of a window
+ * lands at buf + i * bytes. Device seconds of the windows. */
+int MPIXT_Stream_window(MPI_Comm c, void *buf, uint64_t bytes, int W, int reps, int peer, int sender,
+                        void *stream, double *dev_s, double *host_s);
 int MPIXT_Selfchain(MPI_Comm c, float *prod, float *cons, int n, int iters, void *stream,
                     double *dev_s, double *host_s);
 /* cfg5: `steps` halo steps of the 2x2x2 periodic 8-rank decomposition (pack
@@ -115,10 +120,12 @@ int MPIXT_Empty_loop(int iters, void *stream, double *dev_s, double *host_s);
 int MPIXT_Reduce_only(int P, int me, void **sendbufs, void **recvbufs, int count,
                       MPI_Datatype datatype, MPI_Op op, int twoshot, void *stream);
 /* Timing probe for the benchmark's roofline: while enabled, the runtime
- * records CUDA events around every receive-side copy grid (k_copy) it
- * launches; read returns their summed duration and count. Enabling clears. */
+ * records CUDA events around every copy grid (k_gcopy / k_copy) it launches,
+ * on both sides of a message; read returns the summed duration, count and
+ * bytes of the grids whose decision records say they copied (the second
+ * arriver's; the other side's grid is empty). Enabling clears. */
 int MPIXT_Copy_timing(int enable);
-int MPIXT_Copy_timing_read(double *total_ms, int *n);
+int MPIXT_Copy_timing_read(double *total_ms, int *n, uint64_t *bytes);
 /* Number of helper kernels launched so far. */
 uint64_t MPIXT_Launch_count(void);
 

@@ -172,6 +172,44 @@ int MPIXT_Pingpong_side(MPI_Comm c, void* buf, uint64_t bytes, int iters, int pe
   return err;
 }
 
+// cfg2 streaming bandwidth, one side of a pair ("window of
+// 16 Isend/Irecv_enqueue + Waitall_enqueue"): `reps` windows of W messages
+// of `bytes`; the sender sends every message from buf, the receiver
+// receives message i of a window at buf + i * bytes. Device time of the
+// windows on the stream.
+int MPIXT_Stream_window(MPI_Comm c, void* buf, uint64_t bytes, int W, int reps, int peer, int sender,
+                        void* stream, double* dev_s, double* host_s) {
+  if (W < 1 || W > 64 || reps < 1) return MPIX_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t a, b;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return MPIX_ERR_CUDA;
+  const int count = (int)bytes;
+  int err = 0;
+  MPI_Request reqs[64];
+  cudaEventRecord(a, s);
+  const double t0 = now_s();
+  for (int k = 0; k < reps && !err; ++k) {
+    for (int i = 0; i < W && !err; ++i) {
+      if (sender)
+        err |= MPIX_Isend_enqueue(buf, count, MPI_BYTE, peer, 100 + i, c, &reqs[i]);
+      else
+        err |= MPIX_Irecv_enqueue(static_cast<uint8_t*>(buf) + (uint64_t)i * bytes, count, MPI_BYTE, peer,
+                                  100 + i, c, &reqs[i]);
+    }
+    if (!err) err |= MPIX_Waitall_enqueue(W, reqs, MPI_STATUSES_IGNORE);
+  }
+  cudaEventRecord(b, s);
+  const double t1 = now_s();
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (dev_s) *dev_s = ms / 1e3;
+  if (host_s) *host_s = t1 - t0;
+  return err;
+}
+
 // producer kernel -> Send_enqueue -> Recv_enqueue -> consumer kernel, all on
 // one stream (self messages), `iters` times.
 int MPIXT_Selfchain(MPI_Comm c, float* prod, float* cons, int n, int iters, void* stream,

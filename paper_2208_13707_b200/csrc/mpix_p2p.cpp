@@ -43,13 +43,14 @@ int flush_locked(StreamBatch& b, cudaStream_t s, const WaitEntry* w, int nwait, 
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_copy_timing.on.load()) {
-    bool large_recv = false;
-    for (auto& o : b.ops) large_recv |= !o.inl && o.is_recv;
-    if (large_recv) {
+    std::vector<OpRecord*> recs;
+    for (auto& o : b.ops)
+      if (!o.inl) recs.push_back(o.rec);
+    if (!recs.empty()) {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       std::lock_guard<std::mutex> tl(g_copy_timing.mu);
-      g_copy_timing.ev.emplace_back(e0, e1);
+      g_copy_timing.ev.push_back({e0, e1, b.device, std::move(recs)});
     }
   }
   do {
@@ -722,11 +723,11 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   } else {
     if (!b.ops.empty() && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (!inl && is_recv && g_copy_timing.on.load()) {
+    if (!inl && g_copy_timing.on.load()) {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       std::lock_guard<std::mutex> tl(g_copy_timing.mu);
-      g_copy_timing.ev.emplace_back(e0, e1);
+      g_copy_timing.ev.push_back({e0, e1, rs.device, {a.rec}});
     }
     a.early_trigger = p2p_copy_grid(bytes) <= kEarlyTriggerTiles;
     int nk = launch_p2p(a, sys, inl, inl ? 1 : p2p_copy_grid(bytes), s, e0, e1);

@@ -918,25 +918,38 @@ int MPIX_Comm_region(MPI_Comm comm, void** base, uint64_t* bytes) {
 int MPIXT_Copy_timing(int enable) {
   std::lock_guard<std::mutex> tl(g_copy_timing.mu);
   for (auto& p : g_copy_timing.ev) {
-    cudaEventDestroy(p.first);
-    cudaEventDestroy(p.second);
+    cudaEventDestroy(p.e0);
+    cudaEventDestroy(p.e1);
   }
   g_copy_timing.ev.clear();
   g_copy_timing.on.store(enable != 0);
   return MPI_SUCCESS;
 }
 
-int MPIXT_Copy_timing_read(double* total_ms, int* n) {
+int MPIXT_Copy_timing_read(double* total_ms, int* n, uint64_t* bytes) {
   std::lock_guard<std::mutex> tl(g_copy_timing.mu);
   double tot = 0;
+  int cnt = 0;
+  uint64_t moved = 0;
   for (auto& p : g_copy_timing.ev) {
-    if (cudaEventSynchronize(p.second) != cudaSuccess) return MPIX_ERR_CUDA;
+    if (cudaEventSynchronize(p.e1) != cudaSuccess) return MPIX_ERR_CUDA;
+    uint64_t b = 0;
+    CK(cudaSetDevice(p.device));
+    for (OpRecord* r : p.recs) {  // did this grid copy? (the second arriver's did)
+      uint64_t f[5];
+      CK(cudaMemcpy(f, &r->action, sizeof(f), cudaMemcpyDeviceToHost));  // action, src, dst, bytes
+      if (f[0] == ACT_COPY || f[0] == ACT_STAGE) b += f[3];
+    }
+    if (!b) continue;
     float ms = 0;
-    cudaEventElapsedTime(&ms, p.first, p.second);
+    cudaEventElapsedTime(&ms, p.e0, p.e1);
     tot += ms;
+    moved += b;
+    ++cnt;
   }
   if (total_ms) *total_ms = tot;
-  if (n) *n = (int)g_copy_timing.ev.size();
+  if (n) *n = cnt;
+  if (bytes) *bytes = moved;
   return MPI_SUCCESS;
 }
 

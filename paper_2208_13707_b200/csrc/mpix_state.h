@@ -82,11 +82,18 @@ constexpr uint64_t kStageSlots = 4096;      // staging buffers per rank
 extern std::atomic<uint64_t> g_launches;  // kernels launched (MPIX_Launch_count)
 
 // Timing probe for the bench's roofline (MPIXT_Copy_timing): CUDA events
-// around every receive-side copy grid while enabled.
+// around every copy grid (both sides of a message) while enabled, with the
+// decision records of its operations: only a grid whose records say it
+// copied (the second arriver's) is counted, with the bytes it moved.
 struct CopyTiming {
+  struct Entry {
+    cudaEvent_t e0, e1;
+    int device;
+    std::vector<OpRecord*> recs;
+  };
   std::mutex mu;
   std::atomic<bool> on{false};
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<Entry> ev;
 };
 extern CopyTiming g_copy_timing;
 

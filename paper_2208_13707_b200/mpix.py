@@ -180,6 +180,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Pingpong": (I, [P, P, P, P, U64, I, P, P, I, I, P, P]),
         "MPIXT_Pingpong_side": (I, [P, P, U64, I, I, I, P, P]),
         "MPIXT_Selfchain": (I, [P, P, P, I, I, P, P, P]),
+        "MPIXT_Stream_window": (I, [P, P, U64, I, I, I, I, P, P, P]),
         "MPIXT_Empty_loop": (I, [I, P, P, P]),
         "MPIXT_Loopback": (I, [P, P, P, U64, I, P, P, P]),
         "MPIXT_Allreduce_loop": (I, [I, P, P, P, P, P, I, I, I, I, P, P]),
@@ -188,7 +189,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Stream_destroy": (I, [P]),
         "MPIXT_Reduce_only": (I, [I, I, P, P, I, I, I, I, P]),
         "MPIXT_Copy_timing": (I, [I]),
-        "MPIXT_Copy_timing_read": (I, [C.POINTER(C.c_double), C.POINTER(I)]),
+        "MPIXT_Copy_timing_read": (I, [C.POINTER(C.c_double), C.POINTER(I), C.POINTER(U64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -835,6 +836,15 @@ class testing:
         return ds.value
 
     @staticmethod
+    def stream_window(c, buf, nbytes: int, window: int, reps: int, peer: int, sender: bool, stream):
+        """One side of the cfg2 streaming-bandwidth loop; (device s, host s)."""
+        d, h = C.c_double(), C.c_double()
+        check(lib().MPIXT_Stream_window(c.h, _ptr(buf), nbytes, window, reps, peer, int(sender),
+                                        _stream_handle(stream), C.byref(d), C.byref(h)),
+              "MPIXT_Stream_window")
+        return d.value, h.value
+
+    @staticmethod
     def selfchain(c, prod, cons, n: int, iters: int, stream):
         ds, hs = C.c_double(), C.c_double()
         check(lib().MPIXT_Selfchain(c.h, _ptr(prod), _ptr(cons), n, iters, _stream_handle(stream),
@@ -854,9 +864,11 @@ class testing:
 
     @staticmethod
     def copy_timing_read():
-        ms, n = C.c_double(), C.c_int()
-        check(lib().MPIXT_Copy_timing_read(C.byref(ms), C.byref(n)))
-        return ms.value, n.value
+        """(summed ms, count, bytes moved) of the timed copy grids that
+        actually copied (the second arriver's grid of each message)."""
+        ms, n, b = C.c_double(), C.c_int(), C.c_uint64()
+        check(lib().MPIXT_Copy_timing_read(C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value, b.value
 
     @staticmethod
     def halo_steps(blocks, steps: int, devices):

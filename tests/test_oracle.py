@@ -203,3 +203,35 @@ def test_generated_allreduce_oracle_equals_materialised_fold():
             else:  # uniform(-1, 1), order-sensitive: not every sum is exact
                 f = ins[0].astype(np.float32) if dt == "f32" else (ins[0].astype(np.uint32) << 16).view(np.float32)
                 assert f.min() >= -1.0 and f.max() <= 1.0  # bf16 RNE may reach 1.0
+
+
+def test_model_check_enumeration_and_matching_follow_the_reference_matcher():
+    """tests/model_check.py (the GPU bounded model check of SPEC.md:437):
+    the enumeration size, and its expected pairs equal the reference
+    matcher's (orc_match_reference, pinned to the reference in
+    tests/golden/matching.json) on every program, per communicator, for the
+    rank-0-first interleaving of each program's operations."""
+    from tests import model_check as M
+    progs = list(M.programs(2))
+    done = [p for p, _ in progs if M.completes(p)]
+    assert (len(progs), len(done)) == (9856, 6864)
+    for prog in done[::7]:
+        exp = M.expected_pairs(prog)
+        for comm in (0, 1):
+            rank_ops = [[], []]
+            where = [[], []]
+            for r in (0, 1):
+                for pos, (kind, peer, tag, _) in enumerate(prog.get((r, comm), [])):
+                    rank_ops[r].append((1 if kind in ("Send", "Isend") else 0, peer, tag))
+                    where[r].append(pos)
+            if not rank_ops[0] and not rank_ops[1]:
+                continue
+            order = [0] * len(rank_ops[0]) + [1] * len(rank_ops[1])
+            pairs = O.match_reference(rank_ops, order)
+            for r in (0, 1):
+                for i, (is_send, _, _) in enumerate(rank_ops[r]):
+                    if is_send:
+                        continue
+                    s = int(pairs[r][i])
+                    sr, si = s >> 16, s & 0xFFFF
+                    assert exp[(r, comm, where[r][i])] == (sr, comm, where[sr][si])
