@@ -1099,35 +1099,30 @@ def extras_multirank(args, mpix, torch):
     n = 512  # BASELINE cfg5: 512^3 fp32 per rank (8 ranks share the visible GPUs)
     w, ctx = world(8)
     blocks = {r: HaloStencil(r, n, ctx[r][0], ctx[r][1], device=ctx[r][2]) for r in range(8)}
-    w.run_ranks(lambda r: blocks[r].step())
+    w.run_ranks(lambda r: blocks[r].step())  # the Python step (pipelined), warm-up
     sync_all(ctx)
-    steps = 5
-    e = {r: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for r in range(8)}
-    for r in range(8):
-        e[r][0].record(ctx[r][0])
-    w.run_ranks(lambda r: [blocks[r].step() for _ in range(steps)])
-    for r in range(8):
-        e[r][1].record(ctx[r][0])
-    sync_all(ctx)
-    t_step = max(a.elapsed_time(b) for a, b in e.values()) / 1e3 / steps
-    # the same steps from one native thread per rank (MPIXT_Halo_steps)
-    mpix.testing.halo_steps(list(blocks.values()), 2, [ctx[r][2] for r in range(8)])
-    nat_dev, nat_host = mpix.testing.halo_steps(list(blocks.values()), 20, [ctx[r][2] for r in range(8)])
-    for r in range(8):
-        e[r][0].record(ctx[r][0])
-    for r in range(8):
-        for _ in range(steps):
-            mpix.testing.stencil7(blocks[r].u, blocks[r].v, n, n, n, 0.5, 0.1, ctx[r][0])
-    for r in range(8):
-        e[r][1].record(ctx[r][0])
-    sync_all(ctx)
-    t_comp = max(a.elapsed_time(b) for a, b in e.values()) / 1e3 / steps
-    out["halo3d"] = {"block": f"{n}^3 fp32 per rank, 8 ranks 2x2x2 periodic",
-                     "ranks_per_gpu": -(-8 // ndev), "step_ms": t_step * 1e3,
-                     "stencil_only_ms": t_comp * 1e3, "comm_overhead_ms": (t_step - t_comp) * 1e3,
-                     "native_step_ms": nat_dev / 20 * 1e3, "native_host_ms": nat_host / 20 * 1e3,
-                     "native_comm_overhead_ms": (nat_dev / 20 - t_comp) * 1e3,
-                     "face_bytes": n * n * 4}
+    devs8 = [ctx[r][2] for r in range(8)]
+    T = mpix.testing
+    halo = {"block": f"{n}^3 fp32 per rank, 8 ranks 2x2x2 periodic", "ranks_per_gpu": -(-8 // ndev),
+            "face_bytes": n * n * 4, "driver": "native (one host thread per rank, MPIXT_Halo_steps)"}
+    steps = 10
+    for name, mode in (("seq", T.HALO_SEQ), ("pipe", T.HALO_PIPE), ("compute", T.HALO_COMPUTE),
+                       ("exchange", T.HALO_EXCHANGE)):
+        T.halo_steps(list(blocks.values()), 2, devs8, mode)
+        d, h = T.halo_steps(list(blocks.values()), steps, devs8, mode)
+        halo[f"{name}_step_ms"] = d / steps * 1e3
+    t_seq, t_pipe = halo["seq_step_ms"], halo["pipe_step_ms"]
+    t_comp, t_x = halo["compute_step_ms"], halo["exchange_step_ms"]
+    # stencil roofline: every rank reads u once and writes its n^3 interior once
+    sb = 8 * 2 * n ** 3 * 4
+    halo["stencil_hbm_GBps"] = sb / (t_comp / 1e3) / 1e9 / max(1, ndev)
+    halo["stencil_frac_of_hbm"] = halo["stencil_hbm_GBps"] / peaks().get("hbm_gbs", 6650.0)
+    # exposed communication and overlap efficiency:
+    # the share of the exchange hidden behind the stencil
+    halo["exposed_comm_ms_seq"] = t_seq - t_comp
+    halo["exposed_comm_ms_pipe"] = t_pipe - t_comp
+    halo["overlap_efficiency"] = max(0.0, min(1.0, 1 - (t_pipe - t_comp) / t_x)) if t_x > 0 else None
+    out["halo3d"] = halo
     del blocks
     w.finalize()
 

@@ -62,6 +62,18 @@ int MPIXT_Halo_unpack(float *u, int nx, int ny, int nz, int face, const float *b
  * w1*(sum of 6 neighbours); out's halo untouched. */
 int MPIXT_Stencil7(const float *u, float *out, int nx, int ny, int nz, float w0, float w1,
                    void *stream);
+/* The same update restricted to the box [x0,x1]x[y0,y1]x[z0,z1] (1-based
+ * interior coordinates; an empty box is a no-op), and to the boundary shell
+ * (every point with a coordinate 1 or n: exactly the points that read a
+ * halo). Interior box [2,n-1]^3 + shell = the whole update, so a pipelined
+ * step runs the interior while the faces are in flight. */
+int MPIXT_Stencil7_box(const float *u, float *out, int nx, int ny, int nz, int x0, int x1, int y0,
+                       int y1, int z0, int z1, float w0, float w1, void *stream);
+int MPIXT_Stencil7_shell(const float *u, float *out, int nx, int ny, int nz, float w0, float w1,
+                         void *stream);
+/* All six faces in one launch: bufs[face] for face 0..5. */
+int MPIXT_Halo_pack6(const float *u, int nx, int ny, int nz, float *const *bufs, void *stream);
+int MPIXT_Halo_unpack6(float *u, int nx, int ny, int nz, float *const *bufs, void *stream);
 /* Debug: device->host copy (synchronous), and the base/size of rank
  * `comm`'s peer-mapped region of that communicator. */
 int MPIXT_Copy_to_host(void *host, const void *dev, uint64_t bytes);
@@ -97,8 +109,10 @@ int MPIXT_Selfchain(MPI_Comm c, float *prod, float *cons, int n, int iters, void
 /* cfg5: `steps` halo steps of the 2x2x2 periodic 8-rank decomposition (pack
  * 6 faces, 6 Irecv + 6 Isend_enqueue, Waitall_enqueue, unpack, stencil),
  * one native thread per rank. Arrays are indexed by rank (u, v, comms,
- * streams, devices) or rank*6+face (sbuf, rbuf). u and v swap every step. */
-int MPIXT_Halo_steps(int n, int steps, MPI_Comm *comms, void **streams, int *devices, float **u,
+ * streams, devices) or rank*6+face (sbuf, rbuf). u and v swap every step
+ * (not in HALO_EXCHANGE). Modes: */
+enum { HALO_SEQ = 0, HALO_PIPE = 1, HALO_COMPUTE = 2, HALO_EXCHANGE = 3 };
+int MPIXT_Halo_steps(int n, int steps, int mode, MPI_Comm *comms, void **streams, int *devices, float **u,
                      float **v, float **sbuf, float **rbuf, float w0, float w1, double *dev_s,
                      double *host_s);
 /* `iters` x {Isend + Irecv + Waitall_enqueue} of a self-message of `bytes`

@@ -242,14 +242,21 @@ int MPIXT_Selfchain(MPI_Comm c, float* prod, float* cons, int n, int iters, void
 }
 
 // cfg5: `steps` halo-exchange steps of a 2x2x2 periodic decomposition, one
-// host thread per rank (8 ranks): pack 6 faces -> 6 Irecv + 6 Isend_enqueue ->
-// Waitall_enqueue -> unpack -> 7-point stencil, all in the rank's stream
-// (the structure of workloads.HaloStencil.step). u/v[r] are the rank's two
-// (n+2)^3 blocks (swapped each step), sbuf/rbuf[r*6+d] its n*n face buffers.
-int MPIXT_Halo_steps(int n, int steps, MPI_Comm* comms, void** streams, int* devices, float** u,
-                     float** v, float** sbuf, float** rbuf, float w0, float w1, double* dev_s,
-                     double* host_s) {
+// host thread per rank (8 ranks), all in the rank's stream (the structure of
+// workloads.HaloStencil.step). u/v[r] are the rank's two (n+2)^3 blocks
+// (swapped each step), sbuf/rbuf[r*6+d] its n*n face buffers. mode:
+//   HALO_SEQ       pack6 -> 6 Irecv + 6 Isend_enqueue -> Waitall_enqueue ->
+//                  unpack6 -> stencil (the whole block)
+//   HALO_PIPE      the interior [2,n-1]^3 runs on a second stream while the
+//                  faces are packed, exchanged and unpacked; the boundary
+//                  shell runs after the unpack (same results, bit for bit)
+//   HALO_COMPUTE   the stencil alone (no exchange)
+//   HALO_EXCHANGE  pack6 -> exchange -> unpack6 alone (no stencil)
+int MPIXT_Halo_steps(int n, int steps, int mode, MPI_Comm* comms, void** streams, int* devices,
+                     float** u, float** v, float** sbuf, float** rbuf, float w0, float w1,
+                     double* dev_s, double* host_s) {
   const int P = 8;
+  if (mode < HALO_SEQ || mode > HALO_EXCHANGE) return MPIX_ERR_INVALID_ARG;
   static const int opp[6] = {1, 0, 3, 2, 5, 4};
   auto neighbour = [](int r, int d) {
     int c[3] = {r & 1, (r >> 1) & 1, (r >> 2) & 1};
@@ -257,10 +264,14 @@ int MPIXT_Halo_steps(int n, int steps, MPI_Comm* comms, void** streams, int* dev
     c[axis] = (c[axis] + ((d & 1) ? 1 : -1) + 2) % 2;
     return c[0] | (c[1] << 1) | (c[2] << 2);
   };
-  std::vector<cudaEvent_t> e0(P), e1(P);
+  std::vector<cudaEvent_t> e0(P), e1(P), ea(P), eb(P);
+  std::vector<cudaStream_t> s2(P, nullptr);
   for (int r = 0; r < P; ++r) {
     cudaSetDevice(devices[r]);
-    if (cudaEventCreate(&e0[r]) != cudaSuccess || cudaEventCreate(&e1[r]) != cudaSuccess)
+    if (cudaEventCreate(&e0[r]) != cudaSuccess || cudaEventCreate(&e1[r]) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ea[r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&eb[r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s2[r], cudaStreamNonBlocking) != cudaSuccess)
       return MPIX_ERR_CUDA;
   }
   std::atomic<int> err{0};
@@ -278,17 +289,30 @@ int MPIXT_Halo_steps(int n, int steps, MPI_Comm* comms, void** streams, int* dev
     MPI_Request reqs[12];
     for (int it = 0; it < steps && !err.load(); ++it) {
       int rc = 0;
-      for (int d = 0; d < 6; ++d) rc |= MPIXT_Halo_pack(a, n, n, n, d, sbuf[r * 6 + d], s);
-      for (int d = 0; d < 6; ++d)
-        rc |= MPIX_Irecv_enqueue(rbuf[r * 6 + d], n * n, MPI_FLOAT, neighbour(r, d), opp[d],
-                                 comms[r], &reqs[d]);
-      for (int d = 0; d < 6; ++d)
-        rc |= MPIX_Isend_enqueue(sbuf[r * 6 + d], n * n, MPI_FLOAT, neighbour(r, d), d, comms[r],
-                                 &reqs[6 + d]);
-      rc |= MPIX_Waitall_enqueue(12, reqs, MPI_STATUSES_IGNORE);
-      for (int d = 0; d < 6; ++d) rc |= MPIXT_Halo_unpack(a, n, n, n, d, rbuf[r * 6 + d], s);
-      rc |= MPIXT_Stencil7(a, b, n, n, n, w0, w1, s);
-      std::swap(a, b);
+      if (mode == HALO_PIPE) {  // interior on s2, behind everything before this step
+        cudaEventRecord(ea[r], (cudaStream_t)s);
+        cudaStreamWaitEvent(s2[r], ea[r], 0);
+        rc |= MPIXT_Stencil7_box(a, b, n, n, n, 2, n - 1, 2, n - 1, 2, n - 1, w0, w1, s2[r]);
+        cudaEventRecord(eb[r], s2[r]);
+      }
+      if (mode != HALO_COMPUTE) {
+        rc |= MPIXT_Halo_pack6(a, n, n, n, sbuf + r * 6, s);
+        for (int d = 0; d < 6; ++d)
+          rc |= MPIX_Irecv_enqueue(rbuf[r * 6 + d], n * n, MPI_FLOAT, neighbour(r, d), opp[d],
+                                   comms[r], &reqs[d]);
+        for (int d = 0; d < 6; ++d)
+          rc |= MPIX_Isend_enqueue(sbuf[r * 6 + d], n * n, MPI_FLOAT, neighbour(r, d), d, comms[r],
+                                   &reqs[6 + d]);
+        rc |= MPIX_Waitall_enqueue(12, reqs, MPI_STATUSES_IGNORE);
+        rc |= MPIXT_Halo_unpack6(a, n, n, n, rbuf + r * 6, s);
+      }
+      if (mode == HALO_PIPE) {
+        rc |= MPIXT_Stencil7_shell(a, b, n, n, n, w0, w1, s);
+        cudaStreamWaitEvent((cudaStream_t)s, eb[r], 0);
+      } else if (mode != HALO_EXCHANGE) {
+        rc |= MPIXT_Stencil7(a, b, n, n, n, w0, w1, s);
+      }
+      if (mode != HALO_EXCHANGE) std::swap(a, b);
       if (rc) err.store(rc);
     }
     cudaEventRecord(e1[r], (cudaStream_t)s);
@@ -305,6 +329,10 @@ int MPIXT_Halo_steps(int n, int steps, MPI_Comm* comms, void** streams, int* dev
     mx = std::max(mx, ms);
     cudaEventDestroy(e0[r]);
     cudaEventDestroy(e1[r]);
+    cudaStreamSynchronize(s2[r]);
+    cudaEventDestroy(ea[r]);
+    cudaEventDestroy(eb[r]);
+    cudaStreamDestroy(s2[r]);
   }
   if (dev_s) *dev_s = mx / 1e3;
   if (host_s) *host_s = t1 - t0;

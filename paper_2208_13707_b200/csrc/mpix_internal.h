@@ -379,6 +379,12 @@ int launch_collective(const ARArgs& a, bool sys, uint64_t work_grid, cudaStream_
 uint64_t p2p_copy_grid(uint64_t bytes);
 uint64_t ar_reduce_grid(uint64_t work_bytes, int P);
 int preload_kernels();
+// Registry of CUDA streams this library created (MPIXT_Stream_create) or saw
+// destroyed through it (MPIXT_Stream_destroy): the analogue of the
+// reference's live exec-queue registry (proj/src/exec_queue.cpp:82-103).
+// state: 1 live (created here), 0 destroyed here, -1 unknown (foreign).
+void stream_registry_note(void* stream, int live);
+int stream_registry_state(void* stream);
 int launch_reduce_only(const uint64_t* sb, const uint64_t* rb, int P, int me, uint64_t count,
                        int esize, int dtype, int op, int algo, OpRecord* rec, cudaStream_t s);
 

@@ -9,6 +9,10 @@
 // queue worker thread is gone, every enqueue call validates, assigns
 // matching sequence numbers, and launches sm_100a kernels (mpix_kernels.cu)
 // into the user's cudaStream_t.
+#include <cuda.h>
+#include <dlfcn.h>
+#include <stdio.h>
+
 #include "mpix_state.h"
 
 namespace mpix {
@@ -17,6 +21,61 @@ std::atomic<uint64_t> g_launches{0};
 CopyTiming g_copy_timing;
 
 bool mp_mode() { return g_world && g_world->mp; }
+
+static std::mutex g_streams_mu;
+static std::unordered_map<void*, int> g_streams;  // handle -> 1 live / 0 destroyed
+
+void stream_registry_note(void* stream, int live) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  g_streams[stream] = live ? 1 : 0;
+}
+
+int stream_registry_state(void* stream) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  auto it = g_streams.find(stream);
+  return it == g_streams.end() ? -1 : it->second;
+}
+
+// CUDA multiplexes streams onto CUDA_DEVICE_MAX_CONNECTIONS hardware queues
+// (default 8), read when a device's primary context is created. A stream
+// whose head is a spinning wait blocks every later kernel of the streams
+// sharing its queue, including the peers it waits for. Raise
+// it to 32 while no context exists; warn when a context already does.
+static void hw_queue_check() {
+  const char* v = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+  if (v && atoi(v) >= 32) return;
+  // driver entry points through dlopen (the library does not link libcuda)
+  int active_any = 0, ndev = 0;
+  void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+  if (h) {
+    auto init = reinterpret_cast<decltype(&cuInit)>(dlsym(h, "cuInit"));
+    auto count = reinterpret_cast<decltype(&cuDeviceGetCount)>(dlsym(h, "cuDeviceGetCount"));
+    auto get = reinterpret_cast<decltype(&cuDeviceGet)>(dlsym(h, "cuDeviceGet"));
+    auto state = reinterpret_cast<decltype(&cuDevicePrimaryCtxGetState)>(
+        dlsym(h, "cuDevicePrimaryCtxGetState"));
+    if (init && count && get && state && init(0) == CUDA_SUCCESS && count(&ndev) == CUDA_SUCCESS) {
+      for (int d = 0; d < ndev; ++d) {
+        CUdevice dev;
+        unsigned flags = 0;
+        int active = 0;
+        if (get(&dev, d) == CUDA_SUCCESS && state(dev, &flags, &active) == CUDA_SUCCESS && active)
+          active_any = 1;
+      }
+    }
+  }
+  if (!active_any) {
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 1);
+    return;
+  }
+  static std::atomic<bool> warned{false};
+  if (!warned.exchange(true))
+    fprintf(stderr,
+            "mpix: warning: a CUDA context already exists with CUDA_DEVICE_MAX_CONNECTIONS=%s "
+            "(< 32 hardware queues); more concurrently waiting MPIX streams per GPU than queues "
+            "can stall until the watchdog (set it to 32 before the first CUDA call)\n",
+            v ? v : "unset (8)");
+}
 
 int peer_visible_alloc(void** p, uint64_t bytes) {
   if (mp_mode()) return MPIX_Alloc_mem(bytes, p);
@@ -460,6 +519,7 @@ int MPIX_World_init(int nranks, const int* devices) {
   std::lock_guard<std::mutex> lk(g_world_mu);
   if (g_world) return MPIX_ERR_IN_USE;
   if (nranks < 1) return MPIX_ERR_INVALID_ARG;
+  hw_queue_check();
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return MPIX_ERR_CUDA;
   std::unique_ptr<World> w(new World());
@@ -477,6 +537,7 @@ int MPIX_World_init_mp(int rank, int nranks, const int* devices, MPIX_Allgather_
   if (g_world) return MPIX_ERR_IN_USE;
   if (nranks < 1 || rank < 0 || rank >= nranks || !devices || !allgather) return MPIX_ERR_INVALID_ARG;
   if (nranks > 1 && !heap_live()) return MPIX_ERR_NOT_INITIALIZED;  // MPIX_Heap_create + attach first
+  hw_queue_check();
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return MPIX_ERR_CUDA;
   std::unique_ptr<World> w(new World());
@@ -769,6 +830,10 @@ int MPIX_Stream_create(MPI_Info info, MPIX_Stream* stream) {
       if (bytes.size() != sizeof(cudaStream_t)) return MPIX_ERR_BAD_HINT;
       cudaStream_t cs;
       memcpy(&cs, bytes.data(), sizeof(cs));
+      // exec_queue_is_live (proj/src/proc_stream.cpp:17): a stream this
+      // library saw destroyed is rejected without touching the handle; a
+      // foreign stream is probed (the runtime cannot know its lifetime).
+      if (stream_registry_state((void*)cs) == 0) return MPIX_ERR_BAD_HINT;
       int dev = -1;
       if (cudaStreamGetDevice(cs, &dev) != cudaSuccess) {
         cudaGetLastError();

@@ -7,6 +7,7 @@
 #include <atomic>
 
 #include "mpix_testing.h"
+#include "mpix_internal.h"
 
 namespace {
 
@@ -193,19 +194,108 @@ __global__ void k_halo(float* u, int nx, int ny, int nz, int face, float* buf, i
   }
 }
 
-__global__ void k_stencil7(const float* __restrict__ u, float* __restrict__ out, int nx, int ny,
-                           int nz, float w0, float w1) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x + 1;
-  int y = blockIdx.y + 1;
-  int z = blockIdx.z + 1;
-  if (x > nx) return;
-  const uint64_t sx = 1, sy = nx + 2, sz = (uint64_t)(nx + 2) * (ny + 2);
-  uint64_t c = hidx(x, y, z, nx, ny);
+__device__ __forceinline__ float st7(float xm, float xp, float ym, float yp, float zm, float zp,
+                                     float c, float w0, float w1) {
   // explicit roundings (no FMA contraction): bit-identical to orc_stencil7
-  float s = __fadd_rn(u[c - sx], u[c + sx]);
-  s = __fadd_rn(s, __fadd_rn(u[c - sy], u[c + sy]));
-  s = __fadd_rn(s, __fadd_rn(u[c - sz], u[c + sz]));
-  out[c] = __fadd_rn(__fmul_rn(w0, u[c]), __fmul_rn(w1, s));
+  float s = __fadd_rn(xm, xp);
+  s = __fadd_rn(s, __fadd_rn(ym, yp));
+  s = __fadd_rn(s, __fadd_rn(zm, zp));
+  return __fadd_rn(__fmul_rn(w0, c), __fmul_rn(w1, s));
+}
+
+// 7-point update of the box [x0,x1]x[y0,y1]x[z0,z1] (1-based interior
+// coordinates). Each thread marches one (x, y) column through kZc planes
+// with the z neighbours in registers (u is read from HBM once per plane);
+// the x/y neighbours of the current plane come through L1 from the loads of
+// the neighbouring columns. Streaming stores keep the output out of L2's
+// way. Shape measured with tools/stencil_probe.cu.
+constexpr int kSbx = 32, kSby = 8, kSzc = 16;
+__global__ void __launch_bounds__(kSbx* kSby) k_stencil_box(const float* __restrict__ u,
+                                                           float* __restrict__ out, int nx, int ny,
+                                                           int x0, int x1, int y0, int y1, int z0,
+                                                           int z1, float w0, float w1) {
+  const int x = x0 + blockIdx.x * kSbx + threadIdx.x;
+  const int y = y0 + blockIdx.y * kSby + threadIdx.y;
+  const int zs = z0 + blockIdx.z * kSzc;
+  if (x > x1 || y > y1 || zs > z1) return;
+  const int ze = min(zs + kSzc - 1, z1);
+  const uint64_t sy = nx + 2, sz = (uint64_t)(nx + 2) * (ny + 2);
+  uint64_t c = hidx(x, y, zs, nx, ny);
+  float below = __ldg(u + c - sz), cen = __ldg(u + c), above = __ldg(u + c + sz);
+  for (int z = zs; z <= ze; ++z) {
+    const float nxt = z < ze ? __ldg(u + c + 2 * sz) : 0.f;
+    __stcs(out + c, st7(__ldg(u + c - 1), __ldg(u + c + 1), __ldg(u + c - sy), __ldg(u + c + sy),
+                        below, above, cen, w0, w1));
+    below = cen;
+    cen = above;
+    above = nxt;
+    c += sz;
+  }
+}
+
+// The boundary shell of an n^3 block (every point with a coordinate 1 or n:
+// the points whose update reads a halo), split disjointly into the z = 1 and
+// z = n planes, the y = 1 and y = n rows of the planes between, and the
+// x = 1 and x = n points of the rows between. Runs after the unpack.
+__global__ void k_stencil_shell(const float* __restrict__ u, float* __restrict__ out, int nx, int ny,
+                                int nz, float w0, float w1) {
+  const uint64_t pz = (uint64_t)nx * ny;                         // one z plane
+  const uint64_t nzi = nz > 2 ? (uint64_t)(nz - 2) : 0;          // planes between
+  const uint64_t ry = (uint64_t)nx;                              // one y row
+  const uint64_t nyi = ny > 2 ? (uint64_t)(ny - 2) : 0;          // rows between
+  const uint64_t n_z = nz > 1 ? 2 * pz : pz;
+  const uint64_t n_y = nzi * (ny > 1 ? 2 * ry : ry);
+  const uint64_t n_x = nzi * nyi * (nx > 1 ? 2 : 1);
+  const uint64_t total = n_z + n_y + n_x;
+  const uint64_t sy = nx + 2, sz = (uint64_t)(nx + 2) * (ny + 2);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int x, y, z;
+    if (i < n_z) {
+      const uint64_t k = i % pz;
+      z = i < pz ? 1 : nz;
+      x = 1 + (int)(k % nx);
+      y = 1 + (int)(k / nx);
+    } else if (i < n_z + n_y) {
+      const uint64_t j = i - n_z, per = ny > 1 ? 2 * ry : ry;
+      z = 2 + (int)(j / per);
+      const uint64_t k = j % per;
+      y = k < ry ? 1 : ny;
+      x = 1 + (int)(k % ry);
+    } else {
+      const uint64_t j = i - n_z - n_y, per = nx > 1 ? 2 : 1;
+      const uint64_t row = j / per;
+      z = 2 + (int)(row / nyi);
+      y = 2 + (int)(row % nyi);
+      x = (j % per) == 0 ? 1 : nx;
+    }
+    const uint64_t c = hidx(x, y, z, nx, ny);
+    out[c] = st7(u[c - 1], u[c + 1], u[c - sy], u[c + sy], u[c - sz], u[c + sz], u[c], w0, w1);
+  }
+}
+
+// All six faces in one launch (blockIdx.y = face): pack the interior
+// boundary layer into bufs[face], or unpack bufs[face] into the halo layer.
+struct Faces {
+  float* buf[6];
+};
+__global__ void k_halo6(float* u, int nx, int ny, int nz, Faces f, int pack) {
+  const int face = blockIdx.y;
+  int na, nb;
+  face_dims(face, nx, ny, nz, na, nb);
+  const uint64_t n = (uint64_t)na * nb;
+  float* buf = f.buf[face];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(i % na), b = (int)(i / na);
+    int x, y, z;
+    face_coord(face, a, b, pack ? 1 : 0, nx, ny, nz, x, y, z);
+    const uint64_t c = hidx(x, y, z, nx, ny);
+    if (pack)
+      buf[i] = u[c];
+    else
+      u[c] = buf[i];
+  }
 }
 
 int grid_for(uint64_t n, int threads) {
@@ -269,11 +359,13 @@ int MPIXT_Stream_create(int device, void** stream) {
   cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
   cudaSetDevice(prev);
   if (e != cudaSuccess) return 1;
+  mpix::stream_registry_note((void*)s, 1);
   *stream = (void*)s;
   return 0;
 }
 
 int MPIXT_Stream_destroy(void* stream) {
+  mpix::stream_registry_note(stream, 0);
   return cudaStreamDestroy((cudaStream_t)stream) == cudaSuccess ? 0 : 1;
 }
 
@@ -302,11 +394,43 @@ int MPIXT_Halo_unpack(float* u, int nx, int ny, int nz, int face, const float* b
   return done(cudaGetLastError());
 }
 
+int MPIXT_Stencil7_box(const float* u, float* out, int nx, int ny, int nz, int x0, int x1, int y0,
+                       int y1, int z0, int z1, float w0, float w1, void* stream) {
+  if (x0 < 1 || y0 < 1 || z0 < 1 || x1 > nx || y1 > ny || z1 > nz) return 103;
+  if (x1 < x0 || y1 < y0 || z1 < z0) return 0;  // empty box
+  dim3 grid((x1 - x0 + kSbx) / kSbx, (y1 - y0 + kSby) / kSby, (z1 - z0 + kSzc) / kSzc);
+  k_stencil_box<<<grid, dim3(kSbx, kSby), 0, (cudaStream_t)stream>>>(u, out, nx, ny, x0, x1, y0, y1,
+                                                                      z0, z1, w0, w1);
+  return done(cudaGetLastError());
+}
+
 int MPIXT_Stencil7(const float* u, float* out, int nx, int ny, int nz, float w0, float w1,
                    void* stream) {
-  dim3 block(128);
-  dim3 grid((nx + 127) / 128, ny, nz);
-  k_stencil7<<<grid, block, 0, (cudaStream_t)stream>>>(u, out, nx, ny, nz, w0, w1);
+  return MPIXT_Stencil7_box(u, out, nx, ny, nz, 1, nx, 1, ny, 1, nz, w0, w1, stream);
+}
+
+int MPIXT_Stencil7_shell(const float* u, float* out, int nx, int ny, int nz, float w0, float w1,
+                         void* stream) {
+  const uint64_t pts = 2ull * ((uint64_t)nx * ny + (uint64_t)nx * nz + (uint64_t)ny * nz);
+  k_stencil_shell<<<grid_for(pts, 256), 256, 0, (cudaStream_t)stream>>>(u, out, nx, ny, nz, w0, w1);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Halo_pack6(const float* u, int nx, int ny, int nz, float* const* bufs, void* stream) {
+  Faces f;
+  for (int d = 0; d < 6; ++d) f.buf[d] = bufs[d];
+  const int m = nx > ny ? (nx > nz ? nx : nz) : (ny > nz ? ny : nz);
+  const int gx = grid_for((uint64_t)m * m, 256) / 6 + 1;
+  k_halo6<<<dim3(gx, 6), 256, 0, (cudaStream_t)stream>>>(const_cast<float*>(u), nx, ny, nz, f, 1);
+  return done(cudaGetLastError());
+}
+
+int MPIXT_Halo_unpack6(float* u, int nx, int ny, int nz, float* const* bufs, void* stream) {
+  Faces f;
+  for (int d = 0; d < 6; ++d) f.buf[d] = bufs[d];
+  const int m = nx > ny ? (nx > nz ? nx : nz) : (ny > nz ? ny : nz);
+  const int gx = grid_for((uint64_t)m * m, 256) / 6 + 1;
+  k_halo6<<<dim3(gx, 6), 256, 0, (cudaStream_t)stream>>>(u, nx, ny, nz, f, 0);
   return done(cudaGetLastError());
 }
 
@@ -361,7 +485,8 @@ int MPIXT_Preload(void) {
   cudaFuncAttributes fa;
   const void* ks[] = {(const void*)k_fill_pattern, (const void*)k_checksum, (const void*)k_fill_values, (const void*)k_saxpy,
                       (const void*)k_delay,        (const void*)k_empty,    (const void*)k_fill_f32,
-                      (const void*)k_halo,         (const void*)k_stencil7, (const void*)k_iter_fill,
+                      (const void*)k_halo,         (const void*)k_stencil_box, (const void*)k_stencil_shell,
+                      (const void*)k_halo6, (const void*)k_iter_fill,
                       (const void*)k_iter_check,   (const void*)k_iter_bump};
   int rc = 0;
   for (const void* k : ks)

@@ -184,7 +184,11 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Empty_loop": (I, [I, P, P, P]),
         "MPIXT_Loopback": (I, [P, P, P, U64, I, P, P, P]),
         "MPIXT_Allreduce_loop": (I, [I, P, P, P, P, P, I, I, I, I, P, P]),
-        "MPIXT_Halo_steps": (I, [I, I, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P]),
+        "MPIXT_Halo_steps": (I, [I, I, I, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P]),
+        "MPIXT_Stencil7_box": (I, [P, P, I, I, I, I, I, I, I, I, I, C.c_float, C.c_float, P]),
+        "MPIXT_Stencil7_shell": (I, [P, P, I, I, I, C.c_float, C.c_float, P]),
+        "MPIXT_Halo_pack6": (I, [P, I, I, I, P, P]),
+        "MPIXT_Halo_unpack6": (I, [P, I, I, I, P, P]),
         "MPIXT_Stream_create": (I, [I, C.POINTER(P)]),
         "MPIXT_Stream_destroy": (I, [P]),
         "MPIXT_Reduce_only": (I, [I, I, P, P, I, I, I, I, P]),
@@ -804,6 +808,27 @@ class testing:
     def stencil7(u, out, nx, ny, nz, w0, w1, stream) -> None:
         check(lib().MPIXT_Stencil7(_ptr(u), _ptr(out), nx, ny, nz, w0, w1, _stream_handle(stream)))
 
+    @staticmethod
+    def stencil7_box(u, out, nx, ny, nz, box, w0, w1, stream) -> None:
+        """box = (x0, x1, y0, y1, z0, z1), 1-based inclusive."""
+        check(lib().MPIXT_Stencil7_box(_ptr(u), _ptr(out), nx, ny, nz, *box, w0, w1,
+                                       _stream_handle(stream)), "Stencil7_box")
+
+    @staticmethod
+    def stencil7_shell(u, out, nx, ny, nz, w0, w1, stream) -> None:
+        check(lib().MPIXT_Stencil7_shell(_ptr(u), _ptr(out), nx, ny, nz, w0, w1,
+                                         _stream_handle(stream)))
+
+    @staticmethod
+    def halo_pack6(u, nx, ny, nz, bufs, stream) -> None:
+        arr = (C.c_void_p * 6)(*[_ptr(b) for b in bufs])
+        check(lib().MPIXT_Halo_pack6(_ptr(u), nx, ny, nz, arr, _stream_handle(stream)))
+
+    @staticmethod
+    def halo_unpack6(u, nx, ny, nz, bufs, stream) -> None:
+        arr = (C.c_void_p * 6)(*[_ptr(b) for b in bufs])
+        check(lib().MPIXT_Halo_unpack6(_ptr(u), nx, ny, nz, arr, _stream_handle(stream)))
+
     # native drivers (csrc/mpix_drivers.cpp) -------------------------------
     @staticmethod
     def msgrate(comms, streams, sbufs, rbufs, devices, P: int, S: int, W: int, batches: int) -> dict:
@@ -870,10 +895,14 @@ class testing:
         check(lib().MPIXT_Copy_timing_read(C.byref(ms), C.byref(n), C.byref(b)))
         return ms.value, n.value, b.value
 
+    HALO_SEQ, HALO_PIPE, HALO_COMPUTE, HALO_EXCHANGE = 0, 1, 2, 3
+
     @staticmethod
-    def halo_steps(blocks, steps: int, devices):
+    def halo_steps(blocks, steps: int, devices, mode: int = 1):
         """Native cfg5 driver over 8 workloads.HaloStencil blocks (one per
-        rank); returns (device seconds, host seconds) for `steps` steps."""
+        rank); returns (device seconds, host seconds) for `steps` steps.
+        mode: HALO_SEQ / HALO_PIPE (interior overlapped with the exchange) /
+        HALO_COMPUTE (stencil only) / HALO_EXCHANGE (exchange only)."""
         assert len(blocks) == 8
         VP = C.c_void_p
         comms = (VP * 8)(*[b.comm.h for b in blocks])
@@ -885,9 +914,9 @@ class testing:
         rb = (VP * 48)(*[_ptr(b.rbuf[d]) for b in blocks for d in range(6)])
         ds, hs = C.c_double(), C.c_double()
         b0 = blocks[0]
-        check(lib().MPIXT_Halo_steps(b0.n, steps, comms, streams, devs, u, v, sb, rb,
+        check(lib().MPIXT_Halo_steps(b0.n, steps, mode, comms, streams, devs, u, v, sb, rb,
                                      b0.W0, b0.W1, C.byref(ds), C.byref(hs)), "Halo_steps")
-        if steps % 2:
+        if steps % 2 and mode != 3:
             for b in blocks:
                 b.u, b.v = b.v, b.u
         return ds.value, hs.value

@@ -4,7 +4,10 @@ bench.py (BASELINE.json configs 4 and 5):
 - `HaloStencil`: 3-D 7-point stencil on a 2x2x2 periodic decomposition. Each
   step packs the 6 faces, exchanges them with Isend/Irecv_enqueue +
   Waitall_enqueue, unpacks into the halos and runs the stencil, all in the
-  rank's CUDA stream (no host synchronisation between steps).
+  rank's CUDA stream (no host synchronisation between steps). Pipelined
+  (default): the interior [2, n-1]^3, which reads no halo, runs on a second
+  stream while the faces are in flight; the boundary shell runs after the
+  unpack.
 - `msgrate`: S single-stream comms per rank (the reference rejects enqueue on
   multiplex comms, proc_enqueue.cpp:24), ring neighbours, W outstanding
   8-byte Isend/Irecv_enqueue per stream, Waitall_enqueue per batch.
@@ -37,9 +40,11 @@ class HaloStencil:
 
     W0, W1 = 0.5, 1.0 / 12.0
 
-    def __init__(self, rank: int, n: int, stream, comm, device=0, torch=None):
+    def __init__(self, rank: int, n: int, stream, comm, device=0, torch=None, pipelined=True):
         import torch as _t
         self.t = torch or _t
+        self.pipelined = pipelined
+        self.s2 = mpix.testing.new_stream(device) if pipelined else None
         self.rank, self.n, self.stream, self.comm = rank, n, stream, comm
         shape = ((n + 2) * (n + 2) * (n + 2),)
         self.u = self.t.zeros(shape, dtype=self.t.float32, device=device)
@@ -49,8 +54,7 @@ class HaloStencil:
 
     def exchange(self):
         n, s = self.n, self.stream
-        for d in range(6):
-            mpix.testing.halo_pack(self.u, n, n, n, d, self.sbuf[d], s)
+        mpix.testing.halo_pack6(self.u, n, n, n, self.sbuf, s)
         reqs = []
         for d in range(6):  # halo d is filled by the neighbour across d, which sent its OPP(d) face
             reqs.append(self.comm.irecv_enqueue(self.rbuf[d], n * n, mpix.MPI_FLOAT,
@@ -59,12 +63,24 @@ class HaloStencil:
             reqs.append(self.comm.isend_enqueue(self.sbuf[d], n * n, mpix.MPI_FLOAT,
                                                 neighbour(self.rank, d), d))
         mpix.waitall_enqueue(reqs)
-        for d in range(6):
-            mpix.testing.halo_unpack(self.u, n, n, n, d, self.rbuf[d], s)
+        mpix.testing.halo_unpack6(self.u, n, n, n, self.rbuf, s)
 
     def step(self):
-        self.exchange()
-        mpix.testing.stencil7(self.u, self.v, self.n, self.n, self.n, self.W0, self.W1, self.stream)
+        n = self.n
+        if not self.pipelined:
+            self.exchange()
+            mpix.testing.stencil7(self.u, self.v, n, n, n, self.W0, self.W1, self.stream)
+        else:
+            ea = self.t.cuda.Event()
+            ea.record(self.stream)
+            self.s2.wait_event(ea)
+            mpix.testing.stencil7_box(self.u, self.v, n, n, n, (2, n - 1) * 3, self.W0, self.W1,
+                                      self.s2)
+            eb = self.t.cuda.Event()
+            eb.record(self.s2)
+            self.exchange()
+            mpix.testing.stencil7_shell(self.u, self.v, n, n, n, self.W0, self.W1, self.stream)
+            self.stream.wait_event(eb)
         self.u, self.v = self.v, self.u
 
 

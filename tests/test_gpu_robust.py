@@ -263,3 +263,24 @@ def test_comm_free_refuses_while_a_conventional_receive_is_pending():
         assert mpix.wait(r)["bytes"] == 16
         w.run_ranks(lambda q: comms[q].free())
         assert torch.equal(buf, src)
+
+
+def test_destroyed_stream_hint_is_bad_hint():
+    """A cudaStream_t hint naming a stream destroyed through this library is
+    BAD_HINT without dereferencing the handle — the reference's live-queue
+    registry (proj/src/exec_queue.cpp:100-103, checked at
+    proj/src/proc_stream.cpp:17); a live one is accepted."""
+    h = mpix.C.c_void_p()
+    assert mpix.lib().MPIXT_Stream_create(0, mpix.C.byref(h)) == 0
+    live = h.value
+
+    def hint(v):
+        info = mpix.Info()
+        info.set("type", "cudaStream_t")
+        info.set_hex("value", v.to_bytes(8, "little"))
+        return err(lambda: mpix.Stream(info).free())
+
+    with gpu_world(1):
+        assert hint(live) == "OK"
+        assert mpix.lib().MPIXT_Stream_destroy(mpix.C.c_void_p(live)) == 0
+        assert hint(live) == "BAD_HINT"

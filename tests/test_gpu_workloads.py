@@ -29,10 +29,14 @@ def global_step(g, w0, w1):
     return out[1:-1, 1:-1, 1:-1].copy()
 
 
+@pytest.mark.parametrize("pipelined", [False, True], ids=["seq", "pipe"])
 @pytest.mark.parametrize("native", [False, True], ids=["python", "native"])
-@pytest.mark.parametrize("n", [6, 17])
-def test_halo_stencil_matches_global_oracle(n, native):
-    """native: the same steps through the C++ driver (MPIXT_Halo_steps)."""
+@pytest.mark.parametrize("n", [2, 3, 6, 17, 40])
+def test_halo_stencil_matches_global_oracle(n, native, pipelined):
+    """native: the same steps through the C++ driver (MPIXT_Halo_steps).
+    pipelined: interior [2, n-1]^3 on a second stream during the exchange,
+    boundary shell after the unpack — must equal the sequential step bit for
+    bit (n = 2, 3: empty / one-point interior)."""
     P = 8
     N = 2 * n
     rng = np.random.default_rng(n)
@@ -40,7 +44,7 @@ def test_halo_stencil_matches_global_oracle(n, native):
     with gpu_world(P) as (w, ctx):
         blocks = []
         for r in range(P):
-            b = HaloStencil(r, n, ctx[r].stream, ctx[r].comm)
+            b = HaloStencil(r, n, ctx[r].stream, ctx[r].comm, pipelined=pipelined)
             cx, cy, cz = coords(r)
             pad = np.zeros((n + 2, n + 2, n + 2), dtype=np.float32)
             pad[1:-1, 1:-1, 1:-1] = g[cz * n:(cz + 1) * n, cy * n:(cy + 1) * n, cx * n:(cx + 1) * n]
@@ -49,7 +53,8 @@ def test_halo_stencil_matches_global_oracle(n, native):
         torch.cuda.synchronize()
         steps = 3
         if native:
-            mpix.testing.halo_steps(blocks, steps, [0] * P)
+            mpix.testing.halo_steps(blocks, steps, [0] * P,
+                                    mpix.testing.HALO_PIPE if pipelined else mpix.testing.HALO_SEQ)
         else:
             w.run_ranks(lambda r: [blocks[r].step() for _ in range(steps)])
         sync_all(ctx)
@@ -109,3 +114,32 @@ def test_msgrate_ring_all_messages_arrive():
             for k in range(S):
                 rb = bufs[r][k][1].cpu()
                 assert bool((rb[:, 0] == left).all()) and bool((rb[:, 1] == k).all()), (r, k)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 70])
+def test_stencil_box_plus_shell_is_the_whole_update(n):
+    """The interior box kernel and the shell kernel write disjoint points whose
+    union is the block's interior: together they equal orc_stencil7 on the
+    whole block, and the halo of out stays untouched."""
+    rng = np.random.default_rng(n)
+    N3 = (n + 2) ** 3
+    u_h = rng.uniform(-1, 1, N3).astype(np.float32)
+    exp = O.stencil7(u_h, n, n, n, HaloStencil.W0, HaloStencil.W1)
+    u = torch.from_numpy(u_h).to(0)
+    s = torch.cuda.current_stream()
+    for how in ("full", "split"):
+        out = torch.full((N3,), 7.0, dtype=torch.float32, device=0)
+        if how == "full":
+            mpix.testing.stencil7(u, out, n, n, n, HaloStencil.W0, HaloStencil.W1, s)
+        else:
+            mpix.testing.stencil7_box(u, out, n, n, n, (2, n - 1) * 3, HaloStencil.W0,
+                                      HaloStencil.W1, s)
+            mpix.testing.stencil7_shell(u, out, n, n, n, HaloStencil.W0, HaloStencil.W1, s)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().reshape(n + 2, n + 2, n + 2)
+        want = exp.reshape(n + 2, n + 2, n + 2).copy()
+        inner = (slice(1, -1),) * 3
+        assert np.array_equal(got[inner].view(np.uint32), want[inner].view(np.uint32)), how
+        halo = np.ones_like(got, dtype=bool)
+        halo[inner] = False
+        assert (got[halo] == 7.0).all(), how
