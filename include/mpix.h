@@ -126,6 +126,13 @@ typedef struct {
 /* A device-side protocol check failed (a descriptor another agent must not
  * have taken was taken). Sticky like MPIX_ERR_TIMEOUT. */
 #define MPIX_ERR_DEVICE 108
+/* A collective among ranks that share a GPU was enqueued while kernels of
+ * different streams of that GPU cannot run concurrently (kernel
+ * serialisation by a profiler or sanitizer; probed at MPIX_World_init, see
+ * MPIX_Device_coresident). Every rank's barrier would wait for a kernel that
+ * can only start after it, so the call fails at once instead of hanging until
+ * the watchdog. Not sticky. */
+#define MPIX_ERR_NOT_CORESIDENT 109
 
 /* Name of an error code, e.g. "NOT_ENQUEUE_COMM" (result.cpp:5-32). */
 const char *MPIX_Error_string(int code);
@@ -379,6 +386,11 @@ int MPIX_Rank_error(int rank, uint64_t *code);
  * watchdog (see MPIX_ERR_TIMEOUT). Work already enqueued is not waited for:
  * synchronise the stream first to check it. */
 int MPIX_Comm_check(MPI_Comm comm);
+/* 1 in *coresident when two spinning kernels of different streams of
+ * `device` run at the same time (probed with two one-thread kernels and a
+ * 200 ms bound), else 0 — e.g. under ncu's kernel serialisation. Ranks that
+ * share a GPU rely on it for every cross-rank wait. */
+int MPIX_Device_coresident(int device, int *coresident);
 /* Tracing (MPIX_TRACE=1 at MPIX_World_init): copies up to max_records
  * 128-byte per-operation records (struct TraceRec in csrc/mpix_internal.h:
  * op sequence, kind/mode/decision, bytes, key, clock64 stamps of the

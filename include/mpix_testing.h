@@ -34,6 +34,9 @@ int MPIXT_Delay(uint64_t ns, void *stream);
 /* A fresh non-blocking CUDA stream on `device` (not from torch's 32-stream
  * pool, which aliases streams beyond 32), and its destruction. */
 int MPIXT_Stream_create(int device, void **stream);
+/* The same with a stream priority (0 = default/lowest, negative = higher;
+ * clamped to the device's range). */
+int MPIXT_Stream_create_prio(int device, int priority, void **stream);
 int MPIXT_Stream_destroy(void *stream);
 /* One empty kernel (launch-floor measurement). */
 int MPIXT_Empty(void *stream);

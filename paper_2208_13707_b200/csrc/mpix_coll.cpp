@@ -146,6 +146,11 @@ int coll_enqueue(int kind, const void* sbuf, void* rbuf, int count, MPI_Datatype
   }
   bool sys = g_world->cfg.force_sys;
   for (int q = 0; q < P; ++q) sys |= rank_of(q).device != rs.device;
+  // every member waits for every other one: members sharing my GPU must be
+  // able to run concurrently (fail now instead of at the watchdog)
+  if (!rs.coresident && !g_world->mp)
+    for (int q = 0; q < P; ++q)
+      if (q != me && rank_of(q).device == rs.device) return MPIX_ERR_NOT_CORESIDENT;
   CK(cudaSetDevice(rs.device));
   if (!c->batch) c->batch = &batch_of(c->cu, rs.device);
   StreamBatch& b = *c->batch;

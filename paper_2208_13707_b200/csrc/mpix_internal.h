@@ -379,6 +379,9 @@ int launch_collective(const ARArgs& a, bool sys, uint64_t work_grid, cudaStream_
 uint64_t p2p_copy_grid(uint64_t bytes);
 uint64_t ar_reduce_grid(uint64_t work_bytes, int P);
 int preload_kernels();
+// 1 in *ok when two spinning kernels of different streams of `device` run
+// concurrently (mpix_kernels.cu); -1 on a CUDA error.
+int coresident_probe(int device, int* ok);
 // Registry of CUDA streams this library created (MPIXT_Stream_create) or saw
 // destroyed through it (MPIXT_Stream_destroy): the analogue of the
 // reference's live exec-queue registry (proj/src/exec_queue.cpp:82-103).

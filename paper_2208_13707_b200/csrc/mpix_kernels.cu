@@ -2039,6 +2039,56 @@ int launch_reduce_only(const uint64_t* sb, const uint64_t* rb, int P, int me, ui
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
+// Co-residency probe: can two spinning single-CTA kernels of different
+// streams of one device run at the same time? A waits (bounded) for a flag B
+// sets; B is launched after A. Under kernel serialisation (ncu's launch
+// capture, some sanitizer modes) A times out. Ranks sharing a GPU need
+// co-residency for every cross-rank wait of their collectives.
+__global__ void k_cores_wait(volatile uint64_t* f, uint64_t limit_ns) {
+  const uint64_t t0 = globaltimer();
+  while (f[0] == 0) {
+    if (globaltimer() - t0 > limit_ns) {
+      f[1] = 2;
+      return;
+    }
+    __nanosleep(256);
+  }
+  f[1] = 1;
+}
+__global__ void k_cores_set(volatile uint64_t* f) {
+  __threadfence();
+  f[0] = 1;
+}
+
+int coresident_probe(int device, int* ok) {
+  *ok = 0;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) return -1;
+  uint64_t* h = nullptr;
+  cudaStream_t a = nullptr, b = nullptr;
+  int rc = -1;
+  if (cudaHostAlloc((void**)&h, 64, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess &&
+      cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking) == cudaSuccess &&
+      cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking) == cudaSuccess) {
+    h[0] = h[1] = 0;
+    uint64_t* d = nullptr;
+    cudaHostGetDevicePointer((void**)&d, h, 0);
+    k_cores_wait<<<1, 1, 0, a>>>(d, 200ull * 1000 * 1000);
+    k_cores_set<<<1, 1, 0, b>>>(d);
+    if (cudaStreamSynchronize(a) == cudaSuccess && cudaStreamSynchronize(b) == cudaSuccess) {
+      *ok = ((volatile uint64_t*)h)[1] == 1;
+      rc = 0;
+    }
+  }
+  if (a) cudaStreamDestroy(a);
+  if (b) cudaStreamDestroy(b);
+  if (h) cudaFreeHost(h);
+  cudaGetLastError();
+  cudaSetDevice(prev);
+  return rc;
+}
+
 // Force-load every kernel of this module on the current device. Under CUDA
 // lazy loading the first launch of a kernel waits for the device while a
 // spinning handshake kernel may be waiting for exactly that launch (a peer's
@@ -2062,7 +2112,8 @@ int preload_kernels() {
       (const void*)k_gfin<true, 4, 8>, (const void*)k_gfin<false, 4, 8>,
       (const void*)k_gfin<true, 16, 32>, (const void*)k_gfin<false, 16, 32>,
       (const void*)k_gfin<true, kBatchOps, kBatchWaits>,
-      (const void*)k_gfin<false, kBatchOps, kBatchWaits>, (const void*)k_gcopy};
+      (const void*)k_gfin<false, kBatchOps, kBatchWaits>, (const void*)k_gcopy,
+      (const void*)k_cores_wait, (const void*)k_cores_set};
   for (const void* k : ks) {
     cudaError_t r = cudaFuncGetAttributes(&fa, k);
     if (r != cudaSuccess) e = r;

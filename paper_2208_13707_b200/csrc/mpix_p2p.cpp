@@ -689,6 +689,13 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
       // whose send is in this batch could wait in k_batch for the send's
       // push, which only the k_gcopy behind it performs — launch the send first
       flush_first |= gr && blocking && is_recv && peer == me && !b.ops.empty();
+      // a blocking receive may wait inside k_batch for a peer's push; that
+      // push can sit in the peer's own k_gcopy behind a k_batch whose blocking
+      // receive waits for MY deferred copy (head-to-head large Isend + Recv,
+      // found by tests/test_gpu_model_check.py): never let a blocking receive
+      // share a launch with a copy-grid operation
+      if (blocking && is_recv && !flush_first)
+        for (const BatchOp& o : b.ops) flush_first |= !o.inl;
       if (gr && !b.d_arrive) {
         uint32_t k = rs.arrive_next.fetch_add(1);
         if (k >= kArriveWords) return MPIX_ERR_NO_MEM;

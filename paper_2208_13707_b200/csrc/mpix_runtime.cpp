@@ -397,6 +397,7 @@ const char* MPIX_Error_string(int code) {
     case MPIX_ERR_NO_MEM: return "NO_MEM";
     case MPIX_ERR_TIMEOUT: return "TIMEOUT";
     case MPIX_ERR_DEVICE: return "DEVICE_PROTOCOL";
+    case MPIX_ERR_NOT_CORESIDENT: return "NOT_CORESIDENT";
     default: return "UNKNOWN";
   }
 }
@@ -451,6 +452,21 @@ static int world_build(World* w, int nranks, const int* devices, int ndev) {
     if (!rs->hosted) continue;
     int rc = rank_pool(*w, *rs);
     if (rc) return rc;
+  }
+  // Ranks of this process sharing a GPU: can their spinning kernels be
+  // co-resident? (one probe per device; processes time-slice instead)
+  if (!w->mp) {
+    std::map<int, int> probed;
+    for (auto& rs : w->ranks) {
+      if (rs->per_device < 2) continue;
+      auto it = probed.find(rs->device);
+      if (it == probed.end()) {
+        int ok = 0;
+        if (coresident_probe(rs->device, &ok) != 0) return MPIX_ERR_CUDA;
+        it = probed.emplace(rs->device, ok).first;
+      }
+      rs->coresident = it->second != 0;
+    }
   }
   // Bootstrap world communicator, ctx 0 (world.cpp:61-76). It carries no
   // stream, so enqueue on it is NOT_ENQUEUE_COMM.
@@ -948,6 +964,14 @@ int MPIX_Rank_error(int rank, uint64_t* code) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
   if (rank < 0 || rank >= g_world->n || !code) return MPIX_ERR_INVALID_RANK;
   *code = *reinterpret_cast<volatile uint64_t*>(g_world->ranks[rank]->h_err);
+  return MPI_SUCCESS;
+}
+
+int MPIX_Device_coresident(int device, int* coresident) {
+  if (!coresident) return MPIX_ERR_INVALID_ARG;
+  int ok = 0;
+  if (coresident_probe(device, &ok) != 0) return MPIX_ERR_CUDA;
+  *coresident = ok;
   return MPI_SUCCESS;
 }
 

@@ -141,6 +141,7 @@ struct RankState {
   int device = 0;
   int sms = 148;
   int per_device = 1;  // ranks sharing this GPU
+  bool coresident = true;  // their spinning kernels can run concurrently (probed)
   uint64_t* d_done = nullptr;
   std::atomic<uint64_t> req_next{0};
   OpRecord* d_rec = nullptr;

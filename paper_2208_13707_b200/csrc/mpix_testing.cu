@@ -351,12 +351,21 @@ int MPIXT_Delay(uint64_t ns, void* stream) {
 // creating more than 32 aliases them; aliased streams serialise ranks that
 // must run concurrently (a Waitall of one rank would block the operations of
 // another queued behind it).
-int MPIXT_Stream_create(int device, void** stream) {
+int MPIXT_Stream_create(int device, void** stream) { return MPIXT_Stream_create_prio(device, 0, stream); }
+
+// priority: 0 = default (the lowest); negative = higher, clamped to the
+// device's range (a communication stream whose handshake kernels should be
+// scheduled ahead of bulk compute on the same GPU).
+int MPIXT_Stream_create_prio(int device, int priority, void** stream) {
   int prev = 0;
   cudaGetDevice(&prev);
   if (cudaSetDevice(device) != cudaSuccess) return 1;
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (priority < greatest) priority = greatest;
+  if (priority > least) priority = least;
   cudaStream_t s = nullptr;
-  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  cudaError_t e = cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority);
   cudaSetDevice(prev);
   if (e != cudaSuccess) return 1;
   mpix::stream_registry_note((void*)s, 1);

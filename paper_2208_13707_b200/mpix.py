@@ -40,7 +40,7 @@ ERR_NAMES = [
 ERR = {n: i for i, n in enumerate(ERR_NAMES)}
 ERR.update({"CUDA_ERROR": 100, "NOT_INITIALIZED": 101, "UNSUPPORTED": 102,
             "INVALID_ARG": 103, "INVALID_TYPE": 104, "INVALID_OP": 105, "NO_MEM": 106,
-            "TIMEOUT": 107, "DEVICE_PROTOCOL": 108})
+            "TIMEOUT": 107, "DEVICE_PROTOCOL": 108, "NOT_CORESIDENT": 109})
 
 _TORCH_DT = {}
 
@@ -154,6 +154,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIX_Version": (C.c_char_p, []),
         "MPIX_Rank_error": (I, [I, C.POINTER(U64)]),
         "MPIX_Comm_check": (I, [P]),
+        "MPIX_Device_coresident": (I, [I, C.POINTER(I)]),
         "MPIX_Comm_region": (I, [P, C.POINTER(P), C.POINTER(U64)]),
         "MPIX_Trace_read": (I, [I, P, I, C.POINTER(I)]),
         "MPIXT_Copy_to_host": (I, [P, P, U64]),
@@ -190,6 +191,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Halo_pack6": (I, [P, I, I, I, P, P]),
         "MPIXT_Halo_unpack6": (I, [P, I, I, I, P, P]),
         "MPIXT_Stream_create": (I, [I, C.POINTER(P)]),
+        "MPIXT_Stream_create_prio": (I, [I, I, C.POINTER(P)]),
         "MPIXT_Stream_destroy": (I, [P]),
         "MPIXT_Reduce_only": (I, [I, I, P, P, I, I, I, I, P]),
         "MPIXT_Copy_timing": (I, [I]),
@@ -234,6 +236,14 @@ def rank_error(rank: int) -> int:
     v = C.c_uint64()
     check(lib().MPIX_Rank_error(rank, C.byref(v)))
     return v.value
+
+
+def device_coresident(device: int = 0) -> bool:
+    """MPIX_Device_coresident: can two spinning kernels of different streams
+    of `device` run concurrently (False under ncu's kernel serialisation)?"""
+    v = C.c_int()
+    check(lib().MPIX_Device_coresident(device, C.byref(v)), "MPIX_Device_coresident")
+    return bool(v.value)
 
 
 def trace_read(rank: int, max_records: int = 4096):
@@ -722,13 +732,14 @@ class MPWorld:
 # --- test/bench helper kernels (include/mpix_testing.h) ---------------------------
 class testing:
     @staticmethod
-    def new_stream(device: int = 0):
+    def new_stream(device: int = 0, priority: int = 0):
         """A fresh CUDA stream as a torch ExternalStream (torch.cuda.Stream()
         draws from a 32-entry pool per device and aliases beyond that; ranks
-        on aliased streams would be serialised)."""
+        on aliased streams would be serialised). priority < 0: higher than
+        the default (clamped to the device's range)."""
         import torch
         h = C.c_void_p()
-        check(lib().MPIXT_Stream_create(device, C.byref(h)), "MPIXT_Stream_create")
+        check(lib().MPIXT_Stream_create_prio(device, priority, C.byref(h)), "MPIXT_Stream_create")
         s = torch.cuda.ExternalStream(h.value, device=torch.device("cuda", device))
         _owned_streams.append(h.value)
         return s

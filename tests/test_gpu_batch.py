@@ -22,6 +22,10 @@ def rand_bytes(n, seed, device=0):
 @pytest.fixture(params=["1", "0"], ids=["batch", "nobatch"])
 def batch_env(request, monkeypatch):
     monkeypatch.setenv("MPIX_BATCH", request.param)
+    # launch counts below assume no held batch ages past the flusher's
+    # deadline while the Python loop enqueues (a progress guarantee that
+    # these tests never need)
+    monkeypatch.setenv("MPIX_FLUSH_US", "2000000")
     return request.param == "1"
 
 

@@ -51,6 +51,22 @@ __global__ void k_spin_set(uint64_t* peer, const uint64_t* mine, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(peer), "l"(v) : "memory");
 }
 __global__ void k_touch(int* p) { atomicAdd(p, 1); }
+__global__ void k_pdl_empty() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+static void launch_pdl(cudaStream_t s, int threads) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_pdl_empty);
+}
 __global__ void k_empty() {}
 
 static void wr(cudaStream_t s, uint64_t* f, uint64_t v) {
@@ -93,6 +109,12 @@ static double time_it(cudaStream_t s0, cudaStream_t s1, int mode, int n, uint64_
         wr(s0, f0, v);
         wt(s0, f0, v);
         break;
+      case 5:  // PDL chain of empty 32-thread kernels
+        launch_pdl(s0, 32);
+        break;
+      case 6:  // PDL chain of empty 512-thread kernels
+        launch_pdl(s0, 512);
+        break;
     }
   }
   cudaEventRecord(e1, s0);
@@ -104,6 +126,7 @@ static double time_it(cudaStream_t s0, cudaStream_t s1, int mode, int n, uint64_
 }
 
 int main(int argc, char** argv) {
+  setvbuf(stdout, nullptr, _IONBF, 0);
   const char* what = argc > 1 ? argv[1] : "lat";
   cudaSetDevice(0);
   cudaFree(0);
@@ -122,9 +145,12 @@ int main(int argc, char** argv) {
   cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
   if (!strcmp(what, "lat")) {
     const char* names[] = {"memop ping-pong (us per round trip)", "kernel ping-pong", "kernel set -> memop wait",
-                           "empty kernel", "memop write+wait (satisfied)"};
+                           "empty kernel", "memop write+wait (satisfied)",
+                           "PDL empty kernel x32", "PDL empty kernel x512"};
     uint64_t base = 0;
-    for (int mode = 0; mode < 5; ++mode) {
+    const int first = argc > 2 ? atoi(argv[2]) : 0;
+    for (int mode = first; mode < 7; ++mode) {
+      printf("mode %d ...\n", mode);
       cudaMemset(f, 0, 4096);
       cudaDeviceSynchronize();
       base = 0;
@@ -132,6 +158,7 @@ int main(int argc, char** argv) {
       base += 100;
       double us = time_it(s0, s1, mode, 2000, f, base);
       printf("%-40s %8.3f us\n", names[mode], us);
+      fflush(stdout);
     }
     return 0;
   }

@@ -99,6 +99,121 @@ __global__ void __launch_bounds__(BX* BY) k_zsmem(const float* __restrict__ u, f
   }
 }
 
+// D: warp = 32 consecutive x; each thread marches R consecutive y rows:
+// x neighbours by shuffle (edge lanes load), inner y neighbours from the
+// registers of the rows above/below, only rows y0-1 and y0+R loaded.
+template <int BY, int R, int ZC>
+__global__ void __launch_bounds__(32 * BY) k_zrows(const float* __restrict__ u, float* __restrict__ out,
+                                                  int nx, int ny, int x0, int x1, int y0, int y1,
+                                                  int z0, int z1, float w0, float w1) {
+  const int lane = threadIdx.x;
+  const int x = x0 + blockIdx.x * 32 + lane;
+  const int yb = y0 + (blockIdx.y * BY + threadIdx.y) * R;
+  const int zs = z0 + blockIdx.z * ZC;
+  if (yb > y1 || zs > z1) return;  // whole warp exits together (yb per warp)
+  const bool in = x <= x1;
+  const int xc = min(x, nx + 1);
+  const int ze = min(zs + ZC - 1, z1);
+  const uint64_t sy = nx + 2, sz = (uint64_t)(nx + 2) * (ny + 2);
+  uint64_t c = hidx(xc, yb, zs, nx, ny);
+  float bl[R], ce[R], ab[R], nx_[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int yy = min(yb + k, ny + 1);
+    const uint64_t ck = c + (uint64_t)(yy - yb) * sy;
+    bl[k] = __ldg(u + ck - sz);
+    ce[k] = __ldg(u + ck);
+    ab[k] = __ldg(u + ck + sz);
+  }
+  for (int z = zs; z <= ze; ++z) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int yy = min(yb + k, ny + 1);
+      nx_[k] = z < ze ? __ldg(u + c + (uint64_t)(yy - yb) * sy + 2 * sz) : 0.f;
+    }
+    const float ylo = __ldg(u + c - sy);
+    const int ytop = min(yb + R, ny + 1);
+    const float yhi = __ldg(u + c + (uint64_t)(ytop - yb) * sy);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      float xm = __shfl_up_sync(0xffffffffu, ce[k], 1);
+      float xp = __shfl_down_sync(0xffffffffu, ce[k], 1);
+      const uint64_t ck = c + (uint64_t)k * sy;
+      if (lane == 0) xm = __ldg(u + ck - 1);
+      if (lane == 31 || x == x1) xp = __ldg(u + ck + 1);
+      const float ym = k == 0 ? ylo : ce[k - 1];
+      const float yp = k == R - 1 ? yhi : ce[k + 1];
+      if (in && yb + k <= y1) __stcs(out + ck, st7(xm, xp, ym, yp, bl[k], ab[k], ce[k], w0, w1));
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      bl[k] = ce[k];
+      ce[k] = ab[k];
+      ab[k] = nx_[k];
+    }
+    c += sz;
+  }
+}
+
+// E: the same z-march but the output goes to a dense, 128-B aligned n^3
+// array (timing only: tells whether the misaligned halo-layout stores cost)
+template <int BX, int BY, int ZC>
+__global__ void __launch_bounds__(BX* BY) k_zmarch_dense(const float* __restrict__ u, float* __restrict__ out,
+                                                        int nx, int ny, int nz, float w0, float w1) {
+  const int x = 1 + blockIdx.x * BX + threadIdx.x;
+  const int y = 1 + blockIdx.y * BY + threadIdx.y;
+  const int zs = 1 + blockIdx.z * ZC;
+  if (x > nx || y > ny || zs > nz) return;
+  const int ze = min(zs + ZC - 1, nz);
+  const uint64_t sy = nx + 2, sz = (uint64_t)(nx + 2) * (ny + 2);
+  uint64_t c = hidx(x, y, zs, nx, ny);
+  uint64_t o = ((uint64_t)(zs - 1) * ny + (y - 1)) * nx + (x - 1);
+  float below = __ldg(u + c - sz), cen = __ldg(u + c), above = __ldg(u + c + sz);
+  for (int z = zs; z <= ze; ++z) {
+    const float nxt = z < ze ? __ldg(u + c + 2 * sz) : 0.f;
+    __stcs(out + o, st7(__ldg(u + c - 1), __ldg(u + c + 1), __ldg(u + c - sy), __ldg(u + c + sy), below,
+                        above, cen, w0, w1));
+    below = cen;
+    cen = above;
+    above = nxt;
+    c += sz;
+    o += (uint64_t)nx * ny;
+  }
+}
+// F: interior copy in the halo layout (same misaligned rows, no stencil)
+__global__ void k_rowcopy(const float* __restrict__ u, float* __restrict__ out, int nx, int ny, int nz) {
+  const int x = 1 + blockIdx.x * 32 + threadIdx.x;
+  const int y = 1 + blockIdx.y * 8 + threadIdx.y;
+  if (x > nx || y > ny) return;
+  for (int z = 1 + blockIdx.z * 16; z <= min(nz, 16 + blockIdx.z * 16); ++z) {
+    const uint64_t c = hidx(x, y, z, nx, ny);
+    __stcs(out + c, __ldg(u + c));
+  }
+}
+// G: plain stores instead of streaming stores
+template <int BX, int BY, int ZC>
+__global__ void __launch_bounds__(BX* BY) k_zmarch_st(const float* __restrict__ u, float* __restrict__ out,
+                                                     int nx, int ny, int x0, int x1, int y0, int y1,
+                                                     int z0, int z1, float w0, float w1) {
+  const int x = x0 + blockIdx.x * BX + threadIdx.x;
+  const int y = y0 + blockIdx.y * BY + threadIdx.y;
+  const int zs = z0 + blockIdx.z * ZC;
+  if (x > x1 || y > y1 || zs > z1) return;
+  const int ze = min(zs + ZC - 1, z1);
+  const uint64_t sy = nx + 2, sz = (uint64_t)(nx + 2) * (ny + 2);
+  uint64_t c = hidx(x, y, zs, nx, ny);
+  float below = __ldg(u + c - sz), cen = __ldg(u + c), above = __ldg(u + c + sz);
+  for (int z = zs; z <= ze; ++z) {
+    const float nxt = z < ze ? __ldg(u + c + 2 * sz) : 0.f;
+    out[c] = st7(__ldg(u + c - 1), __ldg(u + c + 1), __ldg(u + c - sy), __ldg(u + c + sy), below, above,
+                 cen, w0, w1);
+    below = cen;
+    cen = above;
+    above = nxt;
+    c += sz;
+  }
+}
+
 __global__ void k_fill(float* u, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t h = (uint32_t)i * 2654435761u;
@@ -166,6 +281,25 @@ int main(int argc, char** argv) {
   });
   ZM(32, 4, 8) ZM(32, 4, 16) ZM(32, 8, 16) ZM(32, 8, 32) ZM(64, 4, 16) ZM(64, 4, 32) ZM(128, 2, 16)
   ZM(128, 2, 64) ZM(32, 16, 64) ZM(64, 8, 64)
+#define ZR(BY, R, ZC)                                                                                      \
+  run("zrows 32x" #BY " R" #R " z" #ZC, [&] {                                                              \
+    k_zrows<BY, R, ZC><<<dim3((n + 31) / 32, (n + BY * R - 1) / (BY * R), (n + ZC - 1) / ZC), dim3(32, BY)>>>( \
+        u, b, n, n, 1, n, 1, n, 1, n, w0, w1);                                                              \
+  });
+  ZR(4, 2, 16) ZR(4, 4, 16) ZR(8, 2, 16) ZR(8, 4, 16) ZR(4, 8, 16) ZR(8, 4, 32) ZR(4, 4, 64) ZR(2, 8, 32)
+  ZR(8, 2, 8) ZR(16, 2, 16)
+  run("zmarch dense-out 32x8 z16 (timing)", [&] {
+    k_zmarch_dense<32, 8, 16><<<dim3((n + 31) / 32, (n + 7) / 8, (n + 15) / 16), dim3(32, 8)>>>(u, b, n, n, n, w0, w1);
+  });
+  run("rowcopy halo layout (timing)", [&] {
+    k_rowcopy<<<dim3((n + 31) / 32, (n + 7) / 8, (n + 15) / 16), dim3(32, 8)>>>(u, b, n, n, n);
+  });
+  run("zmarch plain-st 32x8 z16", [&] {
+    k_zmarch_st<32, 8, 16><<<dim3((n + 31) / 32, (n + 7) / 8, (n + 15) / 16), dim3(32, 8)>>>(u, b, n, n, 1, n, 1, n, 1, n, w0, w1);
+  });
+  run("zmarch plain-st 32x8 z8", [&] {
+    k_zmarch_st<32, 8, 8><<<dim3((n + 31) / 32, (n + 7) / 8, (n + 7) / 8), dim3(32, 8)>>>(u, b, n, n, 1, n, 1, n, 1, n, w0, w1);
+  });
   ZS(32, 4, 16) ZS(32, 8, 16) ZS(32, 8, 32) ZS(64, 4, 32) ZS(64, 8, 64) ZS(128, 4, 32)
   // plain copy of the same bytes (roofline sanity)
   run("memcpy d2d (n^3*4)", [&] { cudaMemcpyAsync(b, u, (uint64_t)n * n * n * 4, cudaMemcpyDeviceToDevice); });
