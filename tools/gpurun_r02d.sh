@@ -1,0 +1,12 @@
+# round 2, call d (fresh container): smoke (plain + under ncu), full GPU suite, bench N=1, ncu evidence
+set -x
+O=gpurun_out/r02d
+mkdir -p $O
+export CUDA_MODULE_LOADING=EAGER
+nvidia-smi > $O/nvidia_smi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; echo "rc=$?" >> $O/smoke.txt
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/smoke_ncu.csv python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke_ncu.txt 2>&1; echo "rc=$?" >> $O/smoke_ncu.txt
+timeout 2400 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > $O/pytest.txt 2>&1; echo "rc=$?" >> $O/pytest.txt
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "rc=$?" >> $O/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err; echo "rc=$?" >> $O/bench_ref.err
+timeout 1200 bash tools/profile_round.sh $O/prof > $O/prof.log 2>&1
