@@ -37,6 +37,14 @@ METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 MiB = 1 << 20
 
 
+_T0 = time.time()
+
+
+def log(msg):
+    """Progress on stderr (locates a stall when a run is cut off)."""
+    print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -205,6 +213,16 @@ def cpu_reference_configs():
     t = R.ref_msgrate(8, 4, 64, 100, C.byref(msgs))
     out["cfg4_msgrate_8B"] = {"ranks": 8, "streams_per_rank": 4, "window": 64, "batches": 100,
                               "msgs_per_s": msgs.value / t, "threads": 8 + 8 * 4}
+    # paper Fig. 3: the reference's own lock-regime bench (bench.cpp:118-235),
+    # 2 ranks x T threads, 8-B messages, window 64, 6400 messages per thread
+    f3 = {}
+    for mode, name in ((0, "global"), (1, "pervci"), (2, "stream")):
+        f3[name] = {}
+        for T in (1, 2, 4, 8):
+            m = C.c_double()
+            e = R.ref_fig3(mode, T, 64, 6400, C.byref(m))
+            f3[name][str(T)] = m.value if e > 0 else None
+    out["fig3_lock_regimes_msgs_per_s"] = f3
     return out
 
 
@@ -681,6 +699,7 @@ def bench_world(args):
         ctx[r] = (s, ms, c)
 
     w.run_ranks(setup)
+    log('buffers (> L2: every step streams from HBM)')
     # buffers (> L2: every step streams from HBM)
     src, dst = {}, {}
     for r in range(P):
@@ -716,6 +735,7 @@ def bench_world(args):
         for d in set(dev):
             torch.cuda.synchronize(d)
 
+    log('correctness of the measured path (same inputs as the timed lo')
     # correctness of the measured path (same inputs as the timed loop)
     step()
     sync()
@@ -727,6 +747,7 @@ def bench_world(args):
     for _ in range(args.warmup):
         step()
     sync()
+    log('soak so that the clock sampler sees the step under load (~0.5')
     # soak so that the clock sampler sees the step under load (~0.5 s)
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < 0.5:
@@ -734,6 +755,7 @@ def bench_world(args):
             step()
         sync()
 
+    log('---- timed region: K steps, events on every stream, max over ')
     # ---- timed region: K steps, events on every stream, max over GPUs ----
     starts = {r: torch.cuda.Event(enable_timing=True) for r in range(P)}
     ends = {r: torch.cuda.Event(enable_timing=True) for r in range(P)}
@@ -752,6 +774,7 @@ def bench_world(args):
     t_step = ms / 1e3 / args.steps
     value = S * len(pairs) / t_step / 1e9
 
+    log('dominant kernel: the copy grid (k_gcopy), timed with CUDA eve')
     # dominant kernel: the copy grid (k_gcopy), timed with CUDA events the
     # runtime records around each launch on the launching stream
     # (MPIXT_Copy_timing; only grids that copied are counted), over K more
@@ -765,6 +788,7 @@ def bench_world(args):
     k_ms = tot_ms / max(ncopy, 1)
     k_bytes = moved / max(ncopy, 1)  # message bytes one copying grid moved
 
+    log('roofline of the dominant kernel (the copy grid that moves the')
     # roofline of the dominant kernel (the copy grid that moves the payload)
     if P == 1:
         alg_bytes = 2 * k_bytes  # read + write of the message on one GPU
@@ -794,6 +818,7 @@ def bench_world(args):
                  "step_note": "whole step (all launches: post, decide, copy, complete, wait) "
                               "against the same roofline"})
 
+    log('---- e2e through the C ABI with host buffers ----')
     # ---- e2e through the C ABI with host buffers ----
     e2e = e2e_pass(args, mpix, torch, ctx, pairs, src, dst, S)
 
@@ -898,6 +923,7 @@ def extras(args, mpix, torch, w, ctx):
     big = torch.empty(1 << 30, dtype=torch.uint8, device=0)
     big2 = torch.empty(1 << 30, dtype=torch.uint8, device=0)
 
+    log('launch floor: back-to-back empty kernels in one stream (nativ')
     # launch floor: back-to-back empty kernels in one stream (native loop)
     mpix.testing.empty_loop(50, s0)
     dev, host = mpix.testing.empty_loop(2000, s0)
@@ -905,6 +931,7 @@ def extras(args, mpix, torch, w, ctx):
     out["launch_floor_us"] = t_empty * 1e6
     out["launch_floor_host_us"] = host / 2000 * 1e6
 
+    log('loopback sweep (Isend/Irecv/Waitall on one stream, native loo')
     # loopback sweep (Isend/Irecv/Waitall on one stream, native loop)
     sweep = {}
     for sz in [8, 4096, 65536, 1 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30]:
@@ -916,6 +943,7 @@ def extras(args, mpix, torch, w, ctx):
                           "hbm_frac": 2 * sz / t / 1e9 / peaks().get("hbm_gbs", 6650.0)}
     out["loopback_sweep"] = sweep
 
+    log('in-stream latency: producer -> Send_enqueue -> Recv_enqueue -')
     # in-stream latency: producer -> Send_enqueue -> Recv_enqueue -> consumer
     # (8 B self message, one stream, native driver so the host runs ahead)
     prod = torch.zeros(2, dtype=torch.float32, device=0)
@@ -989,6 +1017,7 @@ def extras_multirank(args, mpix, torch):
         for s, _, _ in ctx.values():
             s.synchronize()
 
+    log('cfg2 latency: blocking Send/Recv_enqueue ping-pong between 2 ')
     # cfg2 latency: blocking Send/Recv_enqueue ping-pong between 2 ranks
     # (both on GPU 0 unless 2 GPUs are visible), half round trip
     w, ctx = world(2)
@@ -1007,6 +1036,7 @@ def extras_multirank(args, mpix, torch):
     w.finalize()
     out["pingpong_2ranks"] = {"gpus": len({ctx[0][2], ctx[1][2]}), **pp}
 
+    log('cfg3: Allreduce_enqueue 256 MiB fp32 and bf16 at P = 1, 2, 4,')
     # cfg3: Allreduce_enqueue 256 MiB fp32 and bf16 at P = 1, 2, 4, 8
     ar = {}
     for P in (1, 2, 4, 8):
@@ -1051,6 +1081,7 @@ def extras_multirank(args, mpix, torch):
         w.finalize()
     out["allreduce_256MiB"] = ar
 
+    log('the other enqueued collectives at P = 8 (ranks share the visi')
     # the other enqueued collectives at P = 8 (ranks share the visible GPUs),
     # 256 MiB per rank of fp32: bcast of 256 MiB, allgather of 32 MiB blocks,
     # reduce_scatter_block of 32 MiB blocks (256 MiB input per rank)
@@ -1095,8 +1126,10 @@ def extras_multirank(args, mpix, torch):
     w.finalize()
     out["collectives_P8"] = cres
 
+    log('cfg5: 3-D halo stencil, 2x2x2 periodic, 512^3 fp32 per rank')
     # cfg5: 3-D halo stencil, 2x2x2 periodic, 512^3 fp32 per rank
     n = 512  # BASELINE cfg5: 512^3 fp32 per rank (8 ranks share the visible GPUs)
+    log('communication streams above the default priority: the exchang')
     # communication streams above the default priority: the exchange's
     # handshake and copy kernels are scheduled ahead of the interior stencil
     # CTAs (on the default-priority second stream) they overlap with
@@ -1116,10 +1149,12 @@ def extras_multirank(args, mpix, torch):
         halo[f"{name}_step_ms"] = d / steps * 1e3
     t_seq, t_pipe = halo["seq_step_ms"], halo["pipe_step_ms"]
     t_comp, t_x = halo["compute_step_ms"], halo["exchange_step_ms"]
+    log('stencil roofline: every rank reads u once and writes its n^3 ')
     # stencil roofline: every rank reads u once and writes its n^3 interior once
     sb = 8 * 2 * n ** 3 * 4
     halo["stencil_hbm_GBps"] = sb / (t_comp / 1e3) / 1e9 / max(1, ndev)
     halo["stencil_frac_of_hbm"] = halo["stencil_hbm_GBps"] / peaks().get("hbm_gbs", 6650.0)
+    log('exposed communication and overlap efficiency (SURVEY.md §8(d)')
     # exposed communication and overlap efficiency:
     # the share of the exchange hidden behind the stencil
     halo["exposed_comm_ms_seq"] = t_seq - t_comp
@@ -1129,6 +1164,7 @@ def extras_multirank(args, mpix, torch):
     del blocks
     w.finalize()
 
+    log('cfg4: 8 ranks x 4 stream comms, ring, 8-byte messages, window')
     # cfg4: 8 ranks x 4 stream comms, ring, 8-byte messages, window 64
     P, S, W, B = 8, 4, 64, 50
     devs = [r % ndev for r in range(P)]
@@ -1143,6 +1179,7 @@ def extras_multirank(args, mpix, torch):
     w.run_ranks(setup)
     bufs = [[(torch.zeros(2, dtype=torch.int32, device=devs[r]),
               torch.zeros((W, 2), dtype=torch.int32, device=devs[r])) for _ in range(S)] for r in range(P)]
+    log('host-bound (enqueue threads): warm up twice, report the media')
     # host-bound (enqueue threads): warm up twice, report the median of 3 runs
     msgrate(w, ctxs, S, W, 1, bufs)
     for _ in range(2):
@@ -1157,6 +1194,7 @@ def extras_multirank(args, mpix, torch):
                          "launches_per_window": "1 coalesced k_batch (2W = 128 operations + the Waitall)"}
     w.finalize()
 
+    log('the same under the dynamic (wildcard-capable) matching engine')
     # the same under the dynamic (wildcard-capable) matching engine
     prev = os.environ.get("MPIX_MATCHING")
     os.environ["MPIX_MATCHING"] = "dynamic"
@@ -1176,6 +1214,19 @@ def extras_multirank(args, mpix, torch):
         else:
             os.environ["MPIX_MATCHING"] = prev
 
+    log('paper Fig. 3: lock regimes over conventional p2p (2 ranks x T threads)')
+    from paper_2208_13707_b200.workloads import fig3
+    f3 = {}
+    for regime, name in ((0, "global"), (1, "pervci"), (2, "stream")):
+        f3[name] = {}
+        for T in (1, 2, 4, 8):
+            fig3(T, W=64, batches=5, regime=regime, torch=torch)  # warm-up
+            f3[name][str(T)] = fig3(T, W=64, batches=50, regime=regime, torch=torch)["msgs_per_s"]
+    out["fig3_lock_regimes_msgs_per_s"] = {
+        "rates": f3, "messages_per_thread": 64 * 50, "bytes": 8,
+        "driver": "native threads over the C ABI (MPIXT_Fig3), conventional MPI_Isend/Irecv/Waitall "
+                  "+ credit, host wall clock as the reference (bench.cpp:200-223)"}
+    log('CUDA-Graph capture: the same latency-bound patterns enqueued ')
     # CUDA-Graph capture: the same latency-bound patterns enqueued eagerly
     # from Python vs captured once and replayed (graph-capturable comms)
     from paper_2208_13707_b200.workloads import graph_latency
@@ -1184,6 +1235,9 @@ def extras_multirank(args, mpix, torch):
 
 
 def main():
+    # a stalled run prints every thread's stack (stderr) instead of dying silently
+    import faulthandler
+    faulthandler.dump_traceback_later(240, repeat=True, file=sys.stderr)
     args = parse()
     if args.impl == "reference":
         run_reference(args)

@@ -92,6 +92,16 @@ int MPIXT_Preload(void);
  * of event time. */
 int MPIXT_Msgrate(int P, int S, int W, int batches, MPI_Comm *comms, void **streams, void **sbufs,
                   void **rbufs, int *devices, double *host_s, double *dev_s);
+/* The reference's lock-regime message-rate bench (paper Fig. 3,
+ * proj/src/bench.cpp:118-235) over conventional p2p: 2 ranks x T threads,
+ * windows of W MPI_Isend / MPI_Irecv + MPI_Waitall + a 1-byte credit.
+ * comms/bufs: [r * T + t]; bufs hold W slots of max(bytes, 1) + 1 byte. */
+int MPIXT_Fig3(int T, int W, int batches, int bytes, MPI_Comm *comms, void **bufs, int *devices,
+               double *elapsed_s, long *messages);
+/* The world's host exclusion regime (MPIX_HOST_EXCLUSION at init):
+ * 0 global lock, 1 per communicator, 2 serial contexts lock-free. Call with
+ * no operation in flight. Returns the previous regime in *prev. */
+int MPIXT_Set_exclusion(int regime, int *prev);
 /* Blocking ping-pong of `bytes` between ranks 0 (c0, s0) and 1 (c1, s1):
  * Send+Recv / Recv+Send, `iters` round trips; *dev_s = event time on s0. */
 int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void *b0, void *b1, uint64_t bytes, int iters,

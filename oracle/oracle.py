@@ -112,6 +112,8 @@ def ref():
         L.ref_allreduce.argtypes = [I, U64, I, I, P, P, I]
         L.ref_msgrate.restype = D
         L.ref_msgrate.argtypes = [I, I, I, I, C.POINTER(U64)]
+        L.ref_fig3.restype = D
+        L.ref_fig3.argtypes = [I, I, I, I, C.POINTER(D)]
         _ref = L
     return _ref
 

@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "streamix/bench.hpp"
 #include "streamix/exec_queue.hpp"
 #include "streamix/info.hpp"
 #include "streamix/oracle.hpp"
@@ -513,6 +514,26 @@ double ref_msgrate(int P, int S, int W, int batches, uint64_t* messages) {
   for (auto& s : st)
     for (auto* q : s.q) exec_queue_destroy(q);
   return t;
+}
+
+// The reference's own lock-regime message-rate bench (paper Fig. 3,
+// proj/src/bench.cpp:118-235), called unmodified: mode 0 global_lock,
+// 1 per_vci_implicit, 2 stream_explicit; 8-B messages. Returns elapsed s
+// (-1 on failure) and the reference's msgs/s.
+double ref_fig3(int mode, int threads, int window, int iters, double* msgs_per_s) {
+  streamix::bench::BenchConfig cfg;
+  cfg.mode = mode == 0 ? streamix::bench::Mode::global_lock
+                       : (mode == 1 ? streamix::bench::Mode::per_vci_implicit
+                                    : streamix::bench::Mode::stream_explicit);
+  cfg.threads = threads;
+  cfg.msg_bytes = 8;
+  cfg.window = window;
+  cfg.iters = iters;
+  cfg.warmup = window;
+  auto r = streamix::bench::run_msgrate(cfg);
+  if (!r.ok()) return -1.0;
+  *msgs_per_s = r->msgs_per_s;
+  return r->elapsed_s;
 }
 
 }  // extern "C"

@@ -63,6 +63,33 @@ def build(force=False, verbose=False):
     return LIB
 
 
+def build_tsan(verbose=False):
+    """libmpix_tsan.so: the same sources with the host code built under
+    ThreadSanitizer (-fsanitize=thread), for tools/sanitize.sh (load it with
+    MPIX_LIB_PATH and LD_PRELOAD=libtsan.so). Not used by the product."""
+    out = os.path.join(HERE, "libmpix_tsan.so")
+    odir = os.path.join(HERE, "_obj_tsan")
+    os.makedirs(odir, exist_ok=True)
+    common = ["-O1", "-g", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fsanitize=thread",
+              "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+    objs, cmds = [], []
+    for src in SOURCES:
+        obj = os.path.join(odir, src + ".o")
+        cmds.append([nvcc(), ARCH, *common, "-c", os.path.join(CSRC, src), "-o", obj])
+        objs.append(obj)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c), cmds)):
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
+    subprocess.run([nvcc(), ARCH, "-shared", "-o", out, *objs, "-lpthread", "-Xcompiler", "-fsanitize=thread",
+                    "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map")], check=True)
+    return out
+
+
 if __name__ == "__main__":
+    if "--tsan" in sys.argv:
+        print(build_tsan())
+        sys.exit(0)
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)

@@ -93,6 +93,62 @@ int MPIXT_Msgrate(int P, int S, int W, int batches, MPI_Comm* comms, void** stre
   return err.load();
 }
 
+// The reference's lock-regime message-rate bench (paper Fig. 3,
+// proj/src/bench.cpp:118-235: sender_loop / receiver_loop): two ranks, T
+// driver threads each, thread t of rank 0 streams W conventional MPI_Isend of
+// `bytes` to thread t of rank 1 over their own communicator, MPI_Waitall, then
+// waits for a 1-byte credit (MPI_Recv) that rank 1 returns after its W
+// MPI_Irecv + MPI_Waitall (tag 0 data, tag 1 credit). The regime is the
+// world's host exclusion (MPIXT_Set_exclusion). bufs[r * T + t] holds W
+// message slots plus one credit byte; *elapsed_s = last stop - first start
+// over all threads (host clock, as the reference); *messages = T * W *
+// batches (counted on the receive side).
+int MPIXT_Fig3(int T, int W, int batches, int bytes, MPI_Comm* comms, void** bufs, int* devices,
+               double* elapsed_s, long* messages) {
+  if (T < 1 || W < 1 || W > 4096 || batches < 1 || bytes < 0) return MPIX_ERR_INVALID_ARG;
+  std::atomic<int> err{0};
+  Spin go(2 * T);
+  std::vector<double> t_start(2 * T), t_stop(2 * T);
+  const uint64_t slot = bytes > 0 ? (uint64_t)bytes : 1;
+  auto body = [&](int r, int t) {
+    cudaSetDevice(devices[r]);
+    MPIX_Rank_bind(r);
+    MPI_Comm c = comms[r * T + t];
+    uint8_t* b = static_cast<uint8_t*>(bufs[r * T + t]);
+    uint8_t* credit = b + slot * W;
+    std::vector<MPI_Request> reqs(W);
+    auto round = [&]() -> int {
+      int rc = 0;
+      if (r == 0) {
+        for (int i = 0; i < W && !rc; ++i) rc = MPI_Isend(b, bytes, MPI_BYTE, 1, 0, c, &reqs[i]);
+        if (!rc) rc = MPI_Waitall(W, reqs.data(), MPI_STATUSES_IGNORE);
+        if (!rc) rc = MPI_Recv(credit, 1, MPI_BYTE, 1, 1, c, MPI_STATUS_IGNORE);
+      } else {
+        for (int i = 0; i < W && !rc; ++i) rc = MPI_Irecv(b + slot * i, bytes, MPI_BYTE, 0, 0, c, &reqs[i]);
+        if (!rc) rc = MPI_Waitall(W, reqs.data(), MPI_STATUSES_IGNORE);
+        if (!rc) rc = MPI_Send(credit, 1, MPI_BYTE, 0, 1, c);
+      }
+      return rc;
+    };
+    int rc = round();  // warm-up window
+    if (rc) err.store(rc);
+    go.arrive_and_wait();
+    t_start[r * T + t] = now_s();
+    for (int k = 0; k < batches && !rc && !err.load(); ++k) rc = round();
+    if (rc) err.store(rc);
+    t_stop[r * T + t] = now_s();
+  };
+  std::vector<std::thread> th;
+  for (int r = 0; r < 2; ++r)
+    for (int t = 0; t < T; ++t) th.emplace_back(body, r, t);
+  for (auto& x : th) x.join();
+  const double t0 = *std::min_element(t_start.begin(), t_start.end());
+  const double t1 = *std::max_element(t_stop.begin(), t_stop.end());
+  if (elapsed_s) *elapsed_s = t1 - t0;
+  if (messages) *messages = (long)T * W * batches;
+  return err.load();
+}
+
 int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void* b0, void* b1, uint64_t bytes, int iters,
                    void* s0, void* s1, int dev0, int dev1, double* dev_s, double* host_s) {
   if (iters < 1) return MPIX_ERR_INVALID_ARG;

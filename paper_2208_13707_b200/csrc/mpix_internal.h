@@ -38,6 +38,22 @@ constexpr uint64_t kStatusOff = kDoneWords * 8;
 constexpr uint64_t kTruncBit = 1ull << 63;
 
 enum : uint64_t { ST_FREE = 0, ST_POSTED = 1, ST_TAKEN = 2 };
+// State bit of a posted send descriptor whose payload travels inside it as
+// flag-in-data words (sends of <= kLLBytes). Scans match
+// (state & ~ST_LL) == ST_POSTED.
+constexpr uint64_t ST_LL = 0x10;
+constexpr uint64_t kLLBytes = 16;
+// An LL word: 4 payload bytes | flag << 32, flag = 0x80000000 | (pseq &
+// 0x7fffffff). A reader that sees the flag of the post's own pseq in every
+// word holds that post's payload, whatever order the words landed in; no
+// stale word carries it (the slot's previous occupant was pseq - R, and
+// descriptor fields of other posts never have bit 63 set).
+__host__ __device__ inline uint32_t ll_flag(uint64_t pseq) {
+  return 0x80000000u | (uint32_t)(pseq & 0x7fffffffu);
+}
+__host__ __device__ inline uint64_t ll_word(uint32_t data, uint32_t flag) {
+  return ((uint64_t)flag << 32) | data;
+}
 // Codes a kernel stores in the rank's watchdog word before giving up
 // (the host turns any of them into the sticky MPIX_ERR_TIMEOUT / _DEVICE).
 enum : uint64_t { ERRW_WAIT_SLOT = 1, ERRW_WAIT_DONE = 2, ERRW_WAIT_COLL = 3, ERRW_PROTOCOL = 4 };
@@ -195,6 +211,8 @@ struct P2PArgs {
   uint64_t* err_word;     // per-rank error word (watchdog)
   uint64_t spin_limit_ns; // 0 = wait forever
   TraceRec* trace;        // MPIX_TRACE: this op's trace record, else null
+  uint64_t trace_seq;     // its host sequence number (the record's head)
+  int ll;                 // MPIX_LL: LL sends (<= kLLBytes) + polling blocking receives
   int early_trigger;      // large blocking receive: let the copy grid launch before
                           // waiting for the sender (only when the grid is small)
   // dynamic matching (dyn = 1): pseq is the receive ticket on the receive
@@ -277,8 +295,9 @@ struct BatchOp {
   // receive zeroes its completion word before posting.
   uint8_t gflags;
   uint16_t gp, gt;
+  uint8_t ll;             // P2PArgs::ll
 };
-static_assert(sizeof(BatchOp) == 200, "BatchOp packing");
+static_assert(sizeof(BatchOp) <= 208, "BatchOp packing");
 
 constexpr int kBatchOps = 128;    // operations per coalesced launch (27.7 KB of parameters)
 constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch

@@ -126,8 +126,10 @@ __device__ __noinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_
 
 __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+// Phase stamps (globaltimer ns): one time base for the kernels of every
+// rank, so two ranks' phases can be lined up.
 __device__ __forceinline__ void trace_t(TraceRec* tr, int k) {
-  if (tr) tr->t[k] = clock64();
+  if (tr) tr->t[k] = globaltimer();
 }
 
 // ---------------------------------------------------------------------------
@@ -138,7 +140,7 @@ constexpr int kCopyUnroll = 4;  // 64-KiB tiles (tools/copyshape.cu)
 constexpr uint64_t kTileVec = (uint64_t)kCopyThreads * kCopyUnroll;  // 16-B vectors per tile
 
 // Whole-CTA copy of n bytes (k_proto inline path and the rare staged push).
-__device__ void cta_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
+__device__ __noinline__ void cta_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
   if (n == 0 || dst == src) return;
   const uint64_t t = threadIdx.x, nt = blockDim.x;
   uint64_t mis = (uint64_t)dst & 15;
@@ -203,7 +205,7 @@ __device__ __forceinline__ void tile_copy(uint8_t* dst, const uint8_t* src, uint
 // style (the state word carries the pair sequence, so it never repeats).
 // ---------------------------------------------------------------------------
 struct Snap {
-  uint64_t state, key, addr, bytes, done_addr, done_val;
+  uint64_t state, key, addr, bytes, done_addr, done_val, p0;  // p0: an LL post's 4th word
 };
 
 template <bool SYS>
@@ -216,8 +218,11 @@ __device__ __forceinline__ void ld_pair(const SlotDesc* s, uint64_t& st, uint64_
 
 constexpr int kMaxScanPerLane = 8;  // R <= 256
 
+// Not inlined: the first scan, the poll loop and the rescan share one copy
+// of this code, so a rescan runs from a warm instruction cache (a kernel
+// launch on a cold SM otherwise waits on instruction fetch).
 template <bool SYS>
-__device__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
+__device__ __noinline__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
   using M = Scope<SYS>;
   const int lane = threadIdx.x & 31;
   // Issue every (state, key) load of this lane before looking at any.
@@ -229,32 +234,34 @@ __device__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
     ky[k] = 0;
     if (i < R) ld_pair<SYS>(&ring[i], st[k], ky[k]);
   }
+  uint32_t hits = 0;  // bit k: slot k * 32 + lane is posted with my key
 #pragma unroll
-  for (int k = 0; k < kMaxScanPerLane; ++k) {
-    if (k * 32 >= R) break;
-    int i = k * 32 + lane;
-    bool hit = i < R && (st[k] & 0xff) == ST_POSTED && ky[k] == key;
-    unsigned m = __ballot_sync(0xffffffffu, hit);
+  for (int k = 0; k < kMaxScanPerLane; ++k)
+    if (k * 32 + lane < R && (st[k] & ~ST_LL & 0xff) == ST_POSTED && ky[k] == key) hits |= 1u << k;
+#pragma unroll 1
+  for (int k = 0; k < kMaxScanPerLane && k * 32 < R; ++k) {
+    unsigned m = __ballot_sync(0xffffffffu, (hits >> k) & 1u);
     while (m) {
       int src = __ffs(m) - 1;
       m &= m - 1;
       int ok = 0;
       Snap sn = {};
       if (lane == src) {
-        SlotDesc* s = &ring[i];
+        SlotDesc* s = &ring[k * 32 + lane];
         sn.state = M::ld_acq(&s->state);
         sn.key = M::ld_rlx(&s->key);
         sn.addr = M::ld_rlx(&s->addr);
         sn.bytes = M::ld_rlx(&s->bytes);
         sn.done_addr = M::ld_rlx(&s->done_addr);
         sn.done_val = M::ld_rlx(&s->done_val);
+        sn.p0 = M::ld_rlx(&s->pad[0]);
         // No re-validation: a state moves POSTED(pseq) -> TAKEN -> FREE ->
         // POSTED(pseq + R) only, and the fields change only with a new post,
         // so they belong to this post as long as the state does — which the
         // snapshot's user either proves by CAS on exactly sn.state (taking a
         // send descriptor) or owns (a receive descriptor only its one
         // matching sender reads).
-        ok = ((sn.state & 0xff) == ST_POSTED) && sn.key == key;
+        ok = ((sn.state & ~ST_LL & 0xff) == ST_POSTED) && sn.key == key;
       }
       ok = __shfl_sync(0xffffffffu, ok, src);
       if (ok) {
@@ -264,6 +271,7 @@ __device__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
         out->bytes = __shfl_sync(0xffffffffu, sn.bytes, src);
         out->done_addr = __shfl_sync(0xffffffffu, sn.done_addr, src);
         out->done_val = __shfl_sync(0xffffffffu, sn.done_val, src);
+        out->p0 = __shfl_sync(0xffffffffu, sn.p0, src);
         return k * 32 + src;
       }
     }
@@ -850,24 +858,151 @@ __device__ void decide_paired(const P2PArgs& a, Decision& dc) {
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// Flag-in-data (LL) small sends and polling blocking receives
+// ---------------------------------------------------------------------------
+// Payload bytes (<= kLLBytes) into four 32-bit words: byte loads, all in
+// flight together (no read past the user's buffer).
+__device__ __forceinline__ void ll_load(const uint8_t* src, uint64_t n, uint32_t w[4]) {
+  uint8_t b[kLLBytes];
+#pragma unroll
+  for (int i = 0; i < (int)kLLBytes; ++i) b[i] = i < (int)n ? src[i] : 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    w[k] = (uint32_t)b[4 * k] | ((uint32_t)b[4 * k + 1] << 8) | ((uint32_t)b[4 * k + 2] << 16) |
+           ((uint32_t)b[4 * k + 3] << 24);
+}
+
+// Post an LL send descriptor (lane 0): five flag-in-data words and the key,
+// then the state, all relaxed — a reader validates the words by their flags,
+// and a stale key never matches (keys are unique per pair), so nothing has
+// to be ordered before the state store.
+template <bool SYS>
+__device__ void ll_post(const P2PArgs& a, const uint32_t w[4]) {
+  using M = Scope<SYS>;
+  SlotDesc* d = &a.post_ring[(int)(a.pseq % (uint64_t)a.R)];
+  const uint32_t f = ll_flag(a.pseq);
+  M::st_rlx(&d->addr, ll_word(w[0], f));
+  M::st_rlx(&d->done_addr, ll_word(w[1], f));
+  M::st_rlx(&d->done_val, ll_word(w[2], f));
+  M::st_rlx(&d->pad[0], ll_word(w[3], f));
+  M::st_rlx(&d->bytes, ll_word((uint32_t)a.bytes, f));
+  M::st_rlx(&d->key, a.key);
+  M::st_rlx(&d->state, st_word(a.pseq, ST_POSTED | ST_LL));
+}
+
+// Read an LL send descriptor's words (lane 0) until every flag is its post's.
+// Returns the payload length, or -1 on watchdog expiry.
+template <bool SYS>
+__device__ int64_t ll_read(const SlotDesc* s, const Snap& sn, uint32_t w[4], const P2PArgs& a) {
+  using M = Scope<SYS>;
+  const uint32_t f = ll_flag(sn.state >> 8);
+  const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
+  // the scan's snapshot first: usually every word has landed already
+  uint64_t w0 = sn.addr, w1 = sn.done_addr, w2 = sn.done_val, w3 = sn.p0, wl = sn.bytes;
+  for (;;) {
+    if ((uint32_t)(w0 >> 32) == f && (uint32_t)(w1 >> 32) == f && (uint32_t)(w2 >> 32) == f &&
+        (uint32_t)(w3 >> 32) == f && (uint32_t)(wl >> 32) == f) {
+      w[0] = (uint32_t)w0;
+      w[1] = (uint32_t)w1;
+      w[2] = (uint32_t)w2;
+      w[3] = (uint32_t)w3;
+      return (int64_t)(uint32_t)wl;
+    }
+    __nanosleep(32);
+    w0 = M::ld_rlx(&s->addr);
+    w1 = M::ld_rlx(&s->done_addr);
+    w2 = M::ld_rlx(&s->done_val);
+    w3 = M::ld_rlx(&s->pad[0]);
+    wl = M::ld_rlx(&s->bytes);
+    if (a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
+      if (a.err_word) ScopeSys::st_rlx(a.err_word, ERRW_WAIT_SLOT);
+      return -1;
+    }
+  }
+}
+
+// Complete my receive from an LL send descriptor (lane 0; the descriptor is
+// mine: taken by CAS, or never contended): payload and status, my post slot
+// consumed (and my posted descriptor retracted if I had posted one), my
+// completion word, then the sender's free-mirror (it may reuse its slot).
+template <bool SYS>
+__device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const uint32_t w[4],
+                            uint64_t len, bool posted) {
+  using M = Scope<SYS>;
+  const uint64_t n = umin(len, a.bytes);  // truncation: endpoint.cpp:17
+  for (uint64_t i = 0; i < n; ++i) a.buf[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+  if (a.my_done) {
+    uint8_t* d = reinterpret_cast<uint8_t*>(a.my_done);
+    ScopeGpu::st_rlx(reinterpret_cast<uint64_t*>(d + kStatusOff), n | (len > a.bytes ? kTruncBit : 0));
+    ScopeGpu::st_rlx(reinterpret_cast<uint64_t*>(d + 2 * kStatusOff),
+                     ((uint64_t)(a.peer & 0xffffff) << 40) | (((uint64_t)(a.sidx + 2) & 0xff) << 32) |
+                         (uint32_t)(sn.key >> 32));
+  }
+  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  if (posted) M::st_rlx(&a.post_ring[slot].state, st_word(a.pseq, ST_FREE));  // retract
+  ScopeGpu::st_rlx(&a.post_mirror[slot], a.pseq + 1);  // consumed either way (local)
+  // my completion: read only by this rank (its waits, the host after a
+  // synchronisation), so device scope orders the payload and status before it
+  if (a.my_done) ScopeGpu::st_rel(a.my_done, a.my_gen);
+  M::st_rlx(&a.scan_mirror[j], (sn.state >> 8) + 1);
+}
+
+// A blocking receive (static matching) never posts a descriptor: no sender
+// waits for one (eager and staged sends complete on their own, an Isend
+// leaves its descriptor), so it polls its scan ring until the send with its
+// key is there and takes it as the second arriver — no Dekker fence on the
+// receive side. Warp 0; returns the slot or -1 on watchdog expiry.
+template <bool SYS>
+__device__ int poll_scan(const P2PArgs& a, Snap* sn) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
+  unsigned ns = 32;
+  for (;;) {
+    const int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, sn);
+    if (j >= 0) return j;
+    int expired = 0;
+    if (lane == 0 && a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
+      if (a.err_word) ScopeSys::st_rlx(a.err_word, ERRW_WAIT_DONE);
+      expired = 1;
+    }
+    if (__shfl_sync(0xffffffffu, expired, 0)) return -1;
+    __nanosleep(ns);
+    if (ns < 64) ns <<= 1;
+  }
+}
+
 // The handshake (whole CTA calls; warp 0 works, the CTA copies eager
 // payloads). On return dc holds ACT_NONE / ACT_COPY / ACT_STAGE.
-template <bool SYS>
+// TINY: the lean instantiation of k_batch_tiny (no staged sends, no trace):
+// less code to fetch into a cold SM's instruction cache.
+template <bool SYS, bool TINY = false>
 __device__ void decide(const P2PArgs& a, Decision& dc) {
   using M = Scope<SYS>;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   __shared__ int s_phase;  // 0 decided, 1 eager copy then post, 2 posted, 3 claim staging
+  // LL: a small send's payload travels in its descriptor; a blocking
+  // receive polls instead of posting
+  const bool ll_send = a.ll && !a.is_recv && a.bytes <= kLLBytes && a.mode != MODE_STAGED;
+  const bool poll_recv = a.ll && a.is_recv && a.blocking;
+  __shared__ uint32_t s_pay[4];  // an LL send's payload (lane 0)
+  TraceRec* const trace = TINY ? nullptr : a.trace;
   if (warp == 0) {
     // the free-mirror of my post slot, loaded alongside the ring scan (one
-    // round trip instead of two in steady state, pseq >= R)
+    // round trip instead of two in steady state, pseq >= R); an LL send's
+    // payload loads are in flight with them too
     uint64_t pre = 0;
+    uint32_t pay[4] = {0, 0, 0, 0};
     if (lane == 0 && a.pseq >= (uint64_t)a.R)
-      pre = M::ld_acq(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)]);
+      pre = ll_send ? M::ld_rlx(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)])
+                    : M::ld_acq(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)]);
+    if (lane == 0 && ll_send) ll_load(a.buf, a.bytes, pay);
     Snap sn;
     int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
+    if (poll_recv && j < 0) j = poll_scan<SYS>(a, &sn);
     if (lane == 0) {
-      trace_t(a.trace, 1);
+      trace_t(trace, 1);
       dc.wait_own = 0;
       dc.now = 0;
       dc.fin.clear();
@@ -880,12 +1015,21 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
         if (j >= 0) {
           // receive already posted: push (my slot is skipped, but only after
           // its previous occupant retired, so its mirror stays monotonic)
-          if (wait_post_slot<SYS>(a, pre)) send_win(a, dc, j, sn, false, a.buf);
-        } else if (a.mode == MODE_STAGED) {
+          // (an LL send pushes the payload it already holds, s_pay below)
+          if (wait_post_slot<SYS>(a, pre))
+            send_win(a, dc, j, sn, false, ll_send ? reinterpret_cast<const uint8_t*>(s_pay) : a.buf);
+        } else if (!TINY && a.mode == MODE_STAGED) {
           dc.action = ACT_STAGE;
           if (!dc.stage_ptr) s_phase = 3;
         } else if (wait_post_slot<SYS>(a, pre)) {
-          if (a.mode == MODE_EAGER) {
+          if (ll_send) {
+            // payload captured: my Isend is complete; the Dekker fence and
+            // rescan follow the post (off the receiver's critical path)
+            ll_post<SYS>(a, pay);
+            if (a.my_done) ScopeGpu::st_rlx(a.my_done, a.my_gen);
+            M::fence_sc();
+            s_phase = 2;
+          } else if (a.mode == MODE_EAGER) {
             s_phase = 1;
           } else {  // MODE_ISEND: publish the user buffer
             post_desc<SYS>(a, (uint64_t)a.buf, a.bytes, (uint64_t)a.my_done, a.my_gen, false);
@@ -894,27 +1038,41 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
         }
       } else {
         if (j >= 0) {
-          uint64_t want = st_word(sn.state >> 8, ST_POSTED);
+          // I have not posted, so no one else may take this descriptor (its
+          // sender takes its own post only after finding my posted receive):
+          // no CAS
           if (!wait_post_slot<SYS>(a, pre)) {
             // watchdog: leave the send descriptor for nobody
-          } else if (M::cas(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN)) == want) {
+          } else if (sn.state & ST_LL) {
+            M::st_rlx(&a.scan_ring[j].state, st_word(sn.state >> 8, ST_TAKEN));
+            uint32_t w[4];
+            const int64_t len = ll_read<SYS>(&a.scan_ring[j], sn, w, a);
+            if (len >= 0) ll_complete<SYS>(a, j, sn, w, (uint64_t)len, false);
+          } else {
+            M::st_rlx(&a.scan_ring[j].state, st_word(sn.state >> 8, ST_TAKEN));
             recv_win(a, dc, j, sn, false);
-          } else if (a.err_word) {
-            ScopeSys::st_rlx(a.err_word, ERRW_PROTOCOL);  // nobody else may take it
           }
-        } else if (wait_post_slot<SYS>(a, pre)) {
+        } else if (!poll_recv && wait_post_slot<SYS>(a, pre)) {
           post_desc<SYS>(a, (uint64_t)a.buf, a.bytes, (uint64_t)a.my_done, a.my_gen, false);
           s_phase = 2;
         }
       }
+      if (ll_send) {
+        s_pay[0] = pay[0];
+        s_pay[1] = pay[1];
+        s_pay[2] = pay[2];
+        s_pay[3] = pay[3];
+      }
     }
     __syncwarp();
-    if (s_phase == 3 && !claim_stage_slot<SYS>(a, dc) && lane == 0) dc.action = ACT_NONE;
-    __syncwarp();
-    if (lane == 0 && s_phase == 3) s_phase = 0;
+    if (!TINY) {
+      if (s_phase == 3 && !claim_stage_slot<SYS>(a, dc) && lane == 0) dc.action = ACT_NONE;
+      __syncwarp();
+      if (lane == 0 && s_phase == 3) s_phase = 0;
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) trace_t(a.trace, 2);
+  if (threadIdx.x == 0) trace_t(trace, 2);
   int phase = s_phase;
   if (phase == 1) {
     // Eager: payload into the receiver's eager slot (peer stores).
@@ -933,20 +1091,27 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     if (lane == 0 && j >= 0) {
       if (!a.is_recv) {
         const int slot = (int)(a.pseq % (uint64_t)a.R);
-        uint64_t want = st_word(a.pseq, ST_POSTED);
+        uint64_t want = st_word(a.pseq, ll_send ? (ST_POSTED | ST_LL) : ST_POSTED);
         if (M::cas(&a.post_ring[slot].state, want, st_word(a.pseq, ST_TAKEN)) == want)
-          send_win(a, dc, j, sn, true, a.buf);
+          send_win(a, dc, j, sn, true, ll_send ? reinterpret_cast<const uint8_t*>(s_pay) : a.buf);
       } else {
-        uint64_t want = st_word(sn.state >> 8, ST_POSTED);
-        if (M::cas(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN)) == want)
-          recv_win(a, dc, j, sn, true);
+        const uint64_t want = sn.state;
+        if (M::cas(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN)) == want) {
+          if (sn.state & ST_LL) {
+            uint32_t w[4];
+            const int64_t len = ll_read<SYS>(&a.scan_ring[j], sn, w, a);
+            if (len >= 0) ll_complete<SYS>(a, j, sn, w, (uint64_t)len, true);
+          } else {
+            recv_win(a, dc, j, sn, true);
+          }
+        }
       }
     }
     if (lane == 0 && dc.action == ACT_NONE && a.is_recv && a.blocking) dc.wait_own = 1;
     __syncwarp();
   }
   __syncthreads();
-  if (threadIdx.x == 0) trace_t(a.trace, 3);
+  if (threadIdx.x == 0) trace_t(trace, 3);
 }
 
 // Publish a staged blocking send and race for its descriptor (whole CTA).
@@ -989,11 +1154,32 @@ __device__ void stage_publish(const P2PArgs& a, Decision& dc) {
 // The whole handshake of one operation (one CTA). INLINE: the copy and the
 // completion stores happen here too; otherwise the decision goes to the op
 // record for k_copy / k_fin.
-template <bool SYS, bool INLINE>
+template <bool SYS, bool INLINE, bool TINY = false>
 __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
+  static_assert(!TINY || INLINE, "tiny operations are inline");
+  if (TINY) {  // static matching, inline, no staging, no graph counters, no trace
+    decide<SYS, true>(a, s_dc);
+    if (s_dc.action == ACT_COPY) {
+      cta_copy(reinterpret_cast<uint8_t*>(s_dc.dst), reinterpret_cast<const uint8_t*>(s_dc.src),
+               s_dc.bytes);
+      __syncthreads();
+      if (threadIdx.x == 0) s_dc.fin.run<SYS>();
+    } else if (threadIdx.x == 0 && s_dc.wait_own) {
+      spin_ge<SYS>(a.my_done, a.my_gen, a.err_word, a.spin_limit_ns, ERRW_WAIT_DONE);
+    }
+    return;
+  }
   if (a.trace && threadIdx.x == 0) {
+    // the record's head is written here, not by a host copy: a copy node
+    // between two operation kernels would distort the gaps being measured
     a.trace->g0 = globaltimer();
-    a.trace->t[0] = clock64();
+    a.trace->t[0] = a.trace->g0;
+    a.trace->seq = a.trace_seq;
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    a.trace->pad[0] = sm;
+    a.trace->bytes = a.bytes;
+    a.trace->key = a.key;
   }
   if (a.greset) {  // captured blocking receive: its completion word is reused every replay
     if (threadIdx.x == 0) {
@@ -1196,6 +1382,7 @@ __device__ void load_op(const BatchOp& o, uint64_t spin_limit_ns, P2PArgs& a) {
   a.spin_limit_ns = spin_limit_ns;
   a.trace = nullptr;
   a.early_trigger = o.early;
+  a.ll = o.ll;
   a.dyn = o.dyn;
   a.P = o.P;
   a.me = o.me;
@@ -1285,6 +1472,25 @@ __global__ void __launch_bounds__(kThreads) k_batch(const BatchArgs<NOPS, NWAIT>
     }
   }
   graph_advance(b);
+}
+
+// The lean k_batch: every operation inline, static matching,
+// no staged send, no graph counters — the common small-message window. One
+// CTA per operation plus the closing wait, as k_batch; its code is a fraction
+// of k_batch's, so a launch on a cold SM fetches far fewer instructions.
+template <bool SYS, int NOPS, int NWAIT>
+__global__ void __launch_bounds__(kThreads) k_batch_tiny(const BatchArgs<NOPS, NWAIT> b) {
+  __shared__ Decision s_dc;
+  __shared__ P2PArgs a;
+  pdl_wait();
+  pdl_trigger();  // no grouped copy behind me: the next head kernel may park
+  if ((int)blockIdx.x < b.n) {
+    if (threadIdx.x == 0) load_op(b.ops[blockIdx.x], b.spin_limit_ns, a);
+    __syncthreads();
+    proto_body<SYS, true, true>(a, s_dc);
+  } else {
+    wait_all<SYS>(b.w, b.nwait, b.err_word, b.spin_limit_ns);
+  }
 }
 
 // Grouped copy (PDL behind k_batch): CTA t finds its operation in the tile
@@ -1910,6 +2116,16 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   if (g.m == 0) {  // inline operations only: one launch, the wait included
     const int grid = head_ctas + (nwait > 0 ? 1 : 0);
     b.early = 1;
+    bool tiny = !arrive && b.n_static == n;
+    for (int i = 0; i < n && tiny; ++i) {
+      const BatchOp& o = b.ops[i];
+      tiny = !o.paired && !(o.gflags & G_ON) && !(!o.is_recv && o.mode == MODE_STAGED);
+    }
+    if (tiny) {
+      cudaError_t e = sys ? launch_head(k_batch_tiny<true, NOPS, NWAIT>, grid, kThreads, s, b)
+                          : launch_head(k_batch_tiny<false, NOPS, NWAIT>, grid, kThreads, s, b);
+      return e == cudaSuccess ? 1 : -1;
+    }
     cudaError_t e = sys ? launch_head(k_batch<true, NOPS, NWAIT>, grid, kThreads, s, b)
                         : launch_head(k_batch<false, NOPS, NWAIT>, grid, kThreads, s, b);
     return e == cudaSuccess ? 1 : -1;
@@ -2113,7 +2329,12 @@ int preload_kernels() {
       (const void*)k_gfin<true, 16, 32>, (const void*)k_gfin<false, 16, 32>,
       (const void*)k_gfin<true, kBatchOps, kBatchWaits>,
       (const void*)k_gfin<false, kBatchOps, kBatchWaits>, (const void*)k_gcopy,
-      (const void*)k_cores_wait, (const void*)k_cores_set};
+      (const void*)k_cores_wait, (const void*)k_cores_set,
+      (const void*)k_batch_tiny<true, 4, 8>, (const void*)k_batch_tiny<false, 4, 8>,
+      (const void*)k_batch_tiny<true, 16, 32>, (const void*)k_batch_tiny<false, 16, 32>,
+      (const void*)k_batch_tiny<true, 64, kBatchWaits>, (const void*)k_batch_tiny<false, 64, kBatchWaits>,
+      (const void*)k_batch_tiny<true, kBatchOps, kBatchWaits>,
+      (const void*)k_batch_tiny<false, kBatchOps, kBatchWaits>};
   for (const void* k : ks) {
     cudaError_t r = cudaFuncGetAttributes(&fa, k);
     if (r != cudaSuccess) e = r;

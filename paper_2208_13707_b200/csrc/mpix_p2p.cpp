@@ -5,6 +5,9 @@
 #include "mpix_state.h"
 
 #include <chrono>
+#include <cstdio>
+#include <functional>
+#include <thread>
 
 namespace mpix {
 
@@ -220,6 +223,7 @@ BatchOp pack_op(const P2PArgs& a, bool inl) {
   o.mode = (uint8_t)a.mode;
   o.blocking = (uint8_t)a.blocking;
   o.inl = inl ? 1 : 0;
+  o.ll = (uint8_t)a.ll;
   return o;
 }
 
@@ -399,9 +403,62 @@ int check_p2p_args(const mpix_comm_s* c, int count, int peer, int tag, bool recv
 // The stream conventional operations of comm c run on: the rank's internal
 // stream, or — graph-capturable comm, whose device counters must be read
 // and advanced in one stream order — the comm's own stream.
-cudaStream_t conv_stream(const mpix_comm_s* c) {
-  return c->graph && c->cu ? c->cu : rank_of(c->rank).p2p;
+cudaStream_t conv_stream(mpix_comm_s* c) {
+  if (c->graph && c->cu) return c->cu;
+  RankState& rs = rank_of(c->rank);
+  // MPIX_HOST_EXCLUSION=global: one internal stream per rank (the single
+  // progress context of the reference's global lock regime); otherwise one
+  // per communicator, so threads on different comms never queue behind each
+  // other's blocking operations (the per-VCI regime)
+  if (g_world->cfg.excl == 0) return rs.p2p;
+  std::call_once(c->conv_once, [&] {
+    {
+      std::lock_guard<std::mutex> pl(rs.conv_pool_mu);
+      if (!rs.conv_pool.empty()) {
+        c->conv_cu = rs.conv_pool.back();
+        rs.conv_pool.pop_back();
+        return;
+      }
+    }
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(rs.device);
+    if (cudaStreamCreateWithFlags(&c->conv_cu, cudaStreamNonBlocking) != cudaSuccess) c->conv_cu = nullptr;
+    if (prev >= 0) cudaSetDevice(prev);
+  });
+  return c->conv_cu ? c->conv_cu : rs.p2p;
 }
+
+// The host exclusion of one p2p call (Config::excl; EndpointGuard,
+// proj/include/streamix/fabric.hpp:17-61): the process-wide lock, the
+// communicator's lock, or — a serial-context communicator under the serial
+// regime — nothing (with the optional owner trap).
+struct CommGuard {
+  std::unique_lock<std::mutex> lk;
+  std::atomic<uint64_t>* owner = nullptr;
+  CommGuard(mpix_comm_s* c) {
+    const Config& cfg = g_world->cfg;
+    if (cfg.excl == 0) {
+      lk = std::unique_lock<std::mutex>(g_world->global_mu);
+    } else if (cfg.excl == 2 && c->serial_ctx) {
+      if (cfg.serial_check) {
+        const uint64_t me = (uint64_t)std::hash<std::thread::id>()(std::this_thread::get_id()) | 1;
+        uint64_t prev = c->owner.exchange(me);
+        if (prev != 0 && prev != me) {
+          std::fprintf(stderr, "mpix: concurrent entry into a serial-context communicator "
+                               "(MPIX_HOST_EXCLUSION=serial contract violated)\n");
+          std::abort();
+        }
+        owner = &c->owner;
+      }
+    } else {
+      lk = std::unique_lock<std::mutex>(c->mu);
+    }
+  }
+  ~CommGuard() {
+    if (owner) owner->store(0);
+  }
+};
 
 // Conventional p2p (Proc::isend/irecv, proc_p2p.cpp:96-113) on GPU buffers:
 // executed on the rank's internal stream, launched at once (no batching:
@@ -493,7 +550,7 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   }
   if (capturing && !is_recv && blocking && bytes > L.E && bytes > w.cfg.stage_chunk)
     return MPIX_ERR_UNSUPPORTED;  // host staging buffers are reclaimed by the host
-  std::lock_guard<std::mutex> clk(c->mu);
+  CommGuard clk(c);
 
   P2PArgs a = {};
   a.is_recv = is_recv;
@@ -540,6 +597,8 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   a.tag = tag;    // -1 = ANY_TAG (receives, dynamic matching)
   a.sidx = how.sidx;  // multiplex stream indices (-2 none)
   a.didx = how.didx;
+  // flag-in-data small sends and polling blocking receives (static matching)
+  a.ll = w.cfg.ll && !dyn ? 1 : 0;
   if (dyn) {
     a.dyn = 1;
     a.P = sh.P;
@@ -602,11 +661,7 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   if (rs.d_trace && !gr) {
     uint64_t n = rs.trace_next.fetch_add(1);
     a.trace = rs.d_trace + (n % kTraceRecs);
-    TraceRec head = {};
-    head.seq = n + 1;
-    head.bytes = bytes;
-    head.key = a.key;
-    CK(cudaMemcpyAsync(a.trace, &head, 32, cudaMemcpyHostToDevice, s));
+    a.trace_seq = n + 1;
   }
   bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
   bool post_only = false;
@@ -818,6 +873,8 @@ int waitall_enqueue(int n, MPI_Request* reqs, MPI_Status* statuses) {
     }
   }
   // The wait closes the stream's batch: one launch for the window.
+  std::unique_lock<std::mutex> glk;  // MPIX_HOST_EXCLUSION=global
+  if (g_world->cfg.excl == 0) glk = std::unique_lock<std::mutex>(g_world->global_mu);
   StreamBatch& b = batch_of(s0, dev0);
   std::lock_guard<std::mutex> lk(b.mu);
   if (flush_locked(b, s0, we.data(), n, sys, rank_of(items[0].rank).d_err) < 0) return MPIX_ERR_CUDA;
@@ -890,6 +947,10 @@ int host_waitall(int n, MPI_Request* reqs, MPI_Status* statuses) {
     CK(cudaSetDevice(rs0.device));
     StreamBatch& b = batch_of(s, rs0.device);
     {
+      // the global regime's lock covers the launch, not the synchronisation
+      // below (another thread's send may be what this wait needs)
+      std::unique_lock<std::mutex> glk;
+      if (g_world->cfg.excl == 0) glk = std::unique_lock<std::mutex>(g_world->global_mu);
       std::lock_guard<std::mutex> lk(b.mu);
       if (flush_locked(b, s, we.data(), (int)we.size(), sys, rs0.d_err) < 0) return MPIX_ERR_CUDA;
     }

@@ -334,6 +334,7 @@ int create_comm(mpix_comm_s* par, const std::vector<mpix_stream_s*>& streams, bo
   c->enqueue_ok = !multiplex && streams.size() == 1 && streams[0] &&
                   streams[0]->kind == mpix_stream_s::cuda;
   c->cu = c->enqueue_ok ? streams[0]->cu : nullptr;
+  c->serial_ctx = !multiplex && streams.size() == 1 && streams[0];
   c->send_pseq.assign(P, 0);
   c->recv_pseq.assign(P, 0);
   // graph-capturable: this rank's choice alone (the device counters count
@@ -632,6 +633,8 @@ int MPIX_World_finalize(void) {
     cudaFreeHost(rs->h_err);
     cudaStreamDestroy(rs->aux);
     cudaStreamDestroy(rs->p2p);
+    for (cudaStream_t cs : rs->conv_pool) cudaStreamDestroy(cs);
+    rs->conv_pool.clear();
     cudaFreeHost(rs->h_stage);
     if (rs->pool) cudaMemPoolDestroy(rs->pool);
   }
@@ -732,6 +735,10 @@ int MPI_Comm_free(MPI_Comm* comm) {  // proc_comm.cpp:178-194
       std::lock_guard<std::mutex> lk(w.comms_mu);
       w.all_comms.erase(std::remove(w.all_comms.begin(), w.all_comms.end(), c), w.all_comms.end());
     }
+    if (c->conv_cu) {
+      std::lock_guard<std::mutex> pl(rs.conv_pool_mu);
+      rs.conv_pool.push_back(c->conv_cu);
+    }
     delete c;
     *comm = MPI_COMM_NULL;
     return MPI_SUCCESS;
@@ -752,9 +759,10 @@ int MPI_Comm_free(MPI_Comm* comm) {  // proc_comm.cpp:178-194
   CollMsg m;
   m.p0 = ev;
   auto v = c->sh->rv.exchange(P, c->rank, c->rv_seq++, m);
+  if ((int)v.size() != P) return MPIX_ERR_TIMEOUT;  // a member never arrived
   for (int q = 0; q < P; ++q) CK(cudaStreamWaitEvent(rs.aux, (cudaEvent_t)v[q].p0, 0));
   // Nobody destroys an event before all members have enqueued their waits.
-  c->sh->rv.exchange(P, c->rank, c->rv_seq++, CollMsg{});
+  if ((int)c->sh->rv.exchange(P, c->rank, c->rv_seq++, CollMsg{}).size() != P) return MPIX_ERR_TIMEOUT;
   CK(cudaEventDestroy(ev));
   uint8_t* region = c->sh->base[c->rank];
   if (region) CK(cudaFreeAsync(region, rs.aux));
@@ -765,6 +773,10 @@ int MPI_Comm_free(MPI_Comm* comm) {  // proc_comm.cpp:178-194
   {
     std::lock_guard<std::mutex> lk(w.comms_mu);
     w.all_comms.erase(std::remove(w.all_comms.begin(), w.all_comms.end(), c), w.all_comms.end());
+  }
+  if (c->conv_cu) {  // after the region release was ordered behind it
+    std::lock_guard<std::mutex> pl(rs.conv_pool_mu);
+    rs.conv_pool.push_back(c->conv_cu);
   }
   delete c;
   *comm = MPI_COMM_NULL;
@@ -964,6 +976,14 @@ int MPIX_Rank_error(int rank, uint64_t* code) {
   if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
   if (rank < 0 || rank >= g_world->n || !code) return MPIX_ERR_INVALID_RANK;
   *code = *reinterpret_cast<volatile uint64_t*>(g_world->ranks[rank]->h_err);
+  return MPI_SUCCESS;
+}
+
+int MPIXT_Set_exclusion(int regime, int* prev) {
+  if (!g_world) return MPIX_ERR_NOT_INITIALIZED;
+  if (regime < 0 || regime > 2) return MPIX_ERR_INVALID_ARG;
+  if (prev) *prev = g_world->cfg.excl;
+  g_world->cfg.excl = regime;
   return MPI_SUCCESS;
 }
 

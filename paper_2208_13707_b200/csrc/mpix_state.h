@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <map>
@@ -45,6 +46,16 @@ struct Config {
   int stage_slots = 64;              // MPIX_STAGE_SLOTS: device staging arena slots per rank
   uint64_t stage_chunk = 4ull << 20; // MPIX_STAGE_CHUNK: bytes per arena slot
   bool graph = false;                // MPIX_GRAPH=1: every enqueue comm is graph-capturable
+  bool ll = true;                    // MPIX_LL=0: no flag-in-data sends, blocking receives post
+  // MPIX_HOST_EXCLUSION (the reference's lock regimes, bench.hpp:13-16,
+  // fabric.hpp:17-61): 0 "global" — one process-wide lock around every p2p
+  // call and one internal stream per rank for conventional operations;
+  // 1 "comm" (default) — a lock per communicator, an internal stream per
+  // communicator; 2 "serial" — a communicator bound to one MPIX stream is a
+  // serial context: no lock on its path (MPIX_SERIAL_CHECK=1 traps
+  // concurrent entry, as the reference's debug owner check does)
+  int excl = 1;
+  bool serial_check = false;
   uint64_t flush_ns = 100000;        // MPIX_FLUSH_US: a held batch older than this is launched by
                                      // the flusher thread (progress guarantee); 0 = no flusher
 
@@ -73,6 +84,12 @@ struct Config {
     c.stage_chunk = (geti("MPIX_STAGE_CHUNK", c.stage_chunk) + 255) & ~255ull;
     c.graph = geti("MPIX_GRAPH", 0) != 0;
     c.flush_ns = geti("MPIX_FLUSH_US", 100) * 1000ull;
+    c.ll = geti("MPIX_LL", 1) != 0;
+    if (const char* x = std::getenv("MPIX_HOST_EXCLUSION")) {
+      const std::string v(x);
+      c.excl = (v == "global" || v == "0") ? 0 : (v == "serial" || v == "stream" || v == "2") ? 2 : 1;
+    }
+    c.serial_check = geti("MPIX_SERIAL_CHECK", 0) != 0;
     return c;
   }
 };
@@ -115,10 +132,20 @@ class Rendezvous {
     Round& r = rounds_[seq];
     if (r.vals.empty()) r.vals.resize(P);
     r.vals[rank] = std::move(m);
-    if (++r.arrived == P)
+    if (++r.arrived == P) {
       cv_.notify_all();
-    else
-      cv_.wait(lk, [&] { return r.arrived == P; });
+    } else {
+      // a member that never arrives (it failed before this collective step)
+      // must not hang the others: they give up after MPIX_RENDEZVOUS_MS
+      static const uint64_t limit_ms = [] {
+        const char* v = std::getenv("MPIX_RENDEZVOUS_MS");
+        return v && *v ? std::strtoull(v, nullptr, 10) : 120000ull;
+      }();
+      if (!cv_.wait_for(lk, std::chrono::milliseconds(limit_ms), [&] { return r.arrived == P; })) {
+        --r.arrived;
+        return {};
+      }
+    }
     std::vector<CollMsg> out = r.vals;
     if (++r.left == P) rounds_.erase(seq);
     return out;
@@ -141,6 +168,10 @@ struct RankState {
   int device = 0;
   int sms = 148;
   int per_device = 1;  // ranks sharing this GPU
+  // internal streams of freed communicators, reused by new ones (a stream
+  // handle stays valid while its StreamBatch entry exists)
+  std::vector<cudaStream_t> conv_pool;
+  std::mutex conv_pool_mu;
   bool coresident = true;  // their spinning kernels can run concurrently (probed)
   uint64_t* d_done = nullptr;
   std::atomic<uint64_t> req_next{0};
@@ -298,6 +329,14 @@ struct mpix_comm_s {
   // Streams other than cu this member launched on (conventional and
   // multiplex p2p): MPI_Comm_free orders the region release after them.
   std::vector<cudaStream_t> side_streams;
+  // A single-stream communicator (MPIX_Stream_comm_create with a stream):
+  // a serial context — lock-free under MPIX_HOST_EXCLUSION=serial.
+  bool serial_ctx = false;
+  // Its conventional operations' internal stream (host exclusion comm /
+  // serial), created on first use; and the owner trap of the serial regime.
+  cudaStream_t conv_cu = nullptr;
+  std::once_flag conv_once;
+  std::atomic<uint64_t> owner{0};
 };
 
 namespace mpix {
@@ -321,6 +360,7 @@ struct World {
   uint32_t next_ctx = 1;
   std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<>> retired;
   std::mutex comms_mu;
+  std::mutex global_mu;  // MPIX_HOST_EXCLUSION=global: the one critical section
   std::vector<mpix_comm_s*> all_comms;
   // Flusher thread (progress guarantee for held batches, mpix_p2p.cpp)
   std::thread flusher;

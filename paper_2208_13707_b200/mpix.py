@@ -19,7 +19,8 @@ import threading
 from typing import Callable, List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpix.so")
+# MPIX_LIB_PATH: an instrumented build (tools/sanitize.sh, libmpix_tsan.so)
+LIB_PATH = os.environ.get("MPIX_LIB_PATH") or os.path.join(_HERE, "libmpix.so")
 
 # --- constants (include/mpix.h) ---------------------------------------------
 MPI_SUCCESS = 0
@@ -178,6 +179,8 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Launch_count": (U64, []),
         "MPIXT_Preload": (I, []),
         "MPIXT_Msgrate": (I, [I, I, I, I, P, P, P, P, P, P, P]),
+        "MPIXT_Fig3": (I, [I, I, I, I, P, P, P, P, P]),
+        "MPIXT_Set_exclusion": (I, [I, P]),
         "MPIXT_Pingpong": (I, [P, P, P, P, U64, I, P, P, I, I, P, P]),
         "MPIXT_Pingpong_side": (I, [P, P, U64, I, I, I, P, P]),
         "MPIXT_Selfchain": (I, [P, P, P, I, I, P, P, P]),
@@ -257,7 +260,8 @@ def trace_read(rank: int, max_records: int = 4096):
         f = struct.unpack_from("<16Q", buf.raw, 128 * i)
         out.append({"seq": f[0], "is_recv": f[1] & 15, "mode": (f[1] >> 4) & 15,
                     "inline": (f[1] >> 8) & 15, "action": (f[1] >> 12) & 15, "bytes": f[2],
-                    "key": f[3], "t": list(f[4:10]), "g0": f[10], "g1": f[11]})
+                    "key": f[3], "t": list(f[4:10]), "g0": f[10], "g1": f[11],
+                    "gt": list(f[12:16])})
     return out
 
 
@@ -855,6 +859,26 @@ class testing:
         msgs = P * S * W * batches
         return {"messages": msgs, "enqueue_s": hs[0], "host_s": hs[1], "device_s": ds.value,
                 "msgs_per_s": msgs / max(ds.value, hs[1])}
+
+    @staticmethod
+    def fig3(comms, bufs, devices, T: int, W: int, batches: int, nbytes: int) -> dict:
+        """The reference's lock-regime message-rate bench (Fig. 3) over
+        conventional p2p, under the world's current host exclusion."""
+        CA = (C.c_void_p * (2 * T))(*[c.h for c in comms])
+        BA = (C.c_void_p * (2 * T))(*[_ptr(b) for b in bufs])
+        DV = (C.c_int * 2)(*devices)
+        el = C.c_double()
+        n = C.c_long()
+        check(lib().MPIXT_Fig3(T, W, batches, nbytes, CA, BA, DV, C.byref(el), C.byref(n)), "Fig3")
+        return {"threads": T, "window": W, "messages": n.value, "elapsed_s": el.value,
+                "msgs_per_s": n.value / max(el.value, 1e-9)}
+
+    @staticmethod
+    def set_exclusion(regime: int) -> int:
+        """0 global lock, 1 per communicator, 2 serial contexts (lock-free)."""
+        prev = C.c_int()
+        check(lib().MPIXT_Set_exclusion(regime, C.byref(prev)), "Set_exclusion")
+        return prev.value
 
     @staticmethod
     def pingpong(c0, c1, b0, b1, nbytes: int, iters: int, s0, s1, dev0: int = 0, dev1: int = 0):

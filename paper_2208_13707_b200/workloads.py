@@ -8,6 +8,10 @@ bench.py (BASELINE.json configs 4 and 5):
   (default): the interior [2, n-1]^3, which reads no halo, runs on a second
   stream while the faces are in flight; the boundary shell runs after the
   unpack.
+- `fig3`: the reference's lock-regime message-rate bench (paper Fig. 3,
+  proj/src/bench.cpp:118-235) over conventional p2p on GPU buffers: 2 ranks x
+  T host threads, each pair on its own communicator, under one of the three
+  host exclusion regimes (global lock / per communicator / serial context).
 - `msgrate`: S single-stream comms per rank (the reference rejects enqueue on
   multiplex comms, proc_enqueue.cpp:24), ring neighbours, W outstanding
   8-byte Isend/Irecv_enqueue per stream, Waitall_enqueue per batch.
@@ -101,6 +105,51 @@ def msgrate(world, ctxs, S: int, W: int, batches: int, bufs) -> dict:
             sb.append(bufs[r][k][0])
             rb.append(bufs[r][k][1])
     return mpix.testing.msgrate(comms, streams, sb, rb, devs, P, S, W, batches)
+
+
+REGIMES = {0: "global", 1: "pervci", 2: "stream"}  # the reference's mode names (bench.cpp:102-108)
+
+
+def fig3(T: int, W: int = 64, batches: int = 100, nbytes: int = 8, regime: int = 1,
+         device: int = 0, torch=None) -> dict:
+    """Paper Fig. 3 on the GPU path: regime 0 ("global") runs every p2p call
+    under one process-wide lock with one internal stream per rank; 1
+    ("pervci", the reference's per_vci_implicit) a lock and an internal stream
+    per communicator; 2 ("stream", stream_explicit) gives each thread an
+    explicit MPIX stream whose communicator is a lock-free serial context.
+    Comms for regimes 0/1 are created on MPIX_STREAM_NULL, as the reference
+    does (bench.cpp:157-171). Driven by native threads (MPIXT_Fig3)."""
+    if torch is None:
+        import torch
+    w = mpix.World(2, [device, device])
+    try:
+        mpix.testing.set_exclusion(regime)
+        comms = {0: [], 1: []}
+        streams = {0: [], 1: []}
+
+        def setup(r):
+            for _ in range(T):
+                st = mpix.Stream() if regime == 2 else None
+                streams[r].append(st)
+                comms[r].append(w.comm(r).stream_comm_create(st))
+
+        w.run_ranks(setup)
+        slot = max(nbytes, 1)
+        bufs = [torch.zeros(slot * W + 1, dtype=torch.uint8, device=device) for _ in range(2 * T)]
+        out = mpix.testing.fig3(comms[0] + comms[1], bufs, [device, device], T, W, batches, nbytes)
+        out["regime"] = REGIMES[regime]
+
+        def teardown(r):
+            for c in comms[r]:
+                c.free()
+            for st in streams[r]:
+                if st is not None:
+                    st.free()
+
+        w.run_ranks(teardown)
+        return out
+    finally:
+        w.finalize()
 
 
 def graph_latency(G: int = 64, R: int = 20) -> dict:

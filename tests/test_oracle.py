@@ -235,3 +235,16 @@ def test_model_check_enumeration_and_matching_follow_the_reference_matcher():
                     s = int(pairs[r][i])
                     sr, si = s >> 16, s & 0xFFFF
                     assert exp[(r, comm, where[r][i])] == (sr, comm, where[sr][si])
+
+
+def test_reference_fig3_runs_every_regime():
+    """The reference's own lock-regime bench (bench.cpp:118-235) through
+    oracle/_ref: the CPU baseline bench.py reports beside MPIXT_Fig3."""
+    import ctypes as C
+    R = O.ref()
+    if R is None:
+        pytest.skip("reference library not built")
+    for mode in (0, 1, 2):
+        m = C.c_double()
+        assert R.ref_fig3(mode, 2, 16, 320, C.byref(m)) > 0
+        assert m.value > 0

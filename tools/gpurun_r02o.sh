@@ -1,0 +1,9 @@
+# round 2, call o: fig3 regimes + full GPU suite + sanitizers + bench x2
+O=gpurun_out/r02o
+mkdir -p $O
+export CUDA_MODULE_LOADING=EAGER
+timeout 300 python -m pytest tests/test_gpu_fig3.py -q -x --timeout 120 -p no:cacheprovider > $O/pytest_fig3.txt 2>&1; echo "rc=$?" >> $O/pytest_fig3.txt
+timeout 1800 python -m pytest tests -m gpu -q -x --timeout 200 -p no:cacheprovider > $O/pytest.txt 2>&1; echo "rc=$?" >> $O/pytest.txt
+timeout 900 env MPIX_SPIN_TIMEOUT_MS=30000 python bench.py > $O/bench.json 2> $O/bench.err; echo "rc=$?" >> $O/bench.err
+timeout 900 env MPIX_SPIN_TIMEOUT_MS=30000 python bench.py > $O/bench2.json 2> $O/bench2.err; echo "rc=$?" >> $O/bench2.err
+timeout 1500 bash tools/sanitize.sh $O/sanitize > $O/sanitize.log 2>&1

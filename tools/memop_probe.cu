@@ -51,6 +51,38 @@ __global__ void k_spin_set(uint64_t* peer, const uint64_t* mine, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(peer), "l"(v) : "memory");
 }
 __global__ void k_touch(int* p) { atomicAdd(p, 1); }
+// PDL variants: wait for the previous grid, let the next one launch at once
+__global__ void k_set_spin_pdl(uint64_t* peer, const uint64_t* mine, uint64_t v) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(peer), "l"(v) : "memory");
+  uint64_t x;
+  do {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(mine) : "memory");
+  } while (x < v);
+}
+__global__ void k_spin_set_pdl(uint64_t* peer, const uint64_t* mine, uint64_t v) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  uint64_t x;
+  do {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(mine) : "memory");
+  } while (x < v);
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(peer), "l"(v) : "memory");
+}
+template <typename K>
+static void launch_pdl2(cudaStream_t s, K k, uint64_t* a, const uint64_t* b, uint64_t v) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, a, b, v);
+}
 __global__ void k_pdl_empty() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
@@ -115,6 +147,10 @@ static double time_it(cudaStream_t s0, cudaStream_t s1, int mode, int n, uint64_
       case 6:  // PDL chain of empty 512-thread kernels
         launch_pdl(s0, 512);
         break;
+      case 7:  // kernel ping-pong, PDL launches (each kernel pre-launched behind the previous)
+        launch_pdl2(s0, k_set_spin_pdl, f1, f0, v);
+        launch_pdl2(s1, k_spin_set_pdl, f0, f1, v);
+        break;
     }
   }
   cudaEventRecord(e1, s0);
@@ -146,10 +182,10 @@ int main(int argc, char** argv) {
   if (!strcmp(what, "lat")) {
     const char* names[] = {"memop ping-pong (us per round trip)", "kernel ping-pong", "kernel set -> memop wait",
                            "empty kernel", "memop write+wait (satisfied)",
-                           "PDL empty kernel x32", "PDL empty kernel x512"};
+                           "PDL empty kernel x32", "PDL empty kernel x512", "kernel ping-pong, PDL"};
     uint64_t base = 0;
     const int first = argc > 2 ? atoi(argv[2]) : 0;
-    for (int mode = first; mode < 7; ++mode) {
+    for (int mode = first; mode < 8; ++mode) {
       printf("mode %d ...\n", mode);
       cudaMemset(f, 0, 4096);
       cudaDeviceSynchronize();

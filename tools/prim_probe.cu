@@ -1,0 +1,524 @@
+// prim_probe.cu — device-side cost of the handshake primitives on one GPU:
+// dependent strong loads (L2 round trip), fences, CAS, release stores, and a
+// cold vs warm pass over a large straight-line code body (instruction fetch).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/prim_probe tools/prim_probe.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+__device__ __forceinline__ uint64_t gt() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint64_t ldg(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t lds(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// out[k]: ns per op for k = 0 chain.gpu, 1 chain.sys, 2 fence.sc.gpu, 3 fence.sc.sys,
+// 4 fence.acq_rel.gpu, 5 cas.gpu, 6 cas.sys, 7 st.release.gpu+ld, 8 clock MHz estimate
+__global__ void k_prims(uint64_t* a, uint64_t* out, int n) {
+  if (threadIdx.x != 0) return;
+  uint64_t t0, t1, x = 0;
+  {  // first touches from this SM: a fresh 2-MiB page each (TLB), then the same line again
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    uint64_t* far = a + 4096 + (uint64_t)(sm % 8) * (1ull << 18);  // 2 MiB apart
+    t0 = gt();
+    x = ldg(far);
+    t1 = gt();
+    uint64_t y = ldg(far + 1 + x);
+    uint64_t t2 = gt();
+    out[13] = t1 - t0;
+    out[14] = t2 - t1;
+    out[15] = sm + y;
+  }
+  // pointer chase over a[0..] (a[i] = (i+1)%64)
+  t0 = gt();
+  for (int i = 0; i < n; ++i) x = ldg(a + x);
+  t1 = gt();
+  out[0] = (t1 - t0) * 1000 / n;
+  t0 = gt();
+  for (int i = 0; i < n; ++i) x = lds(a + x);
+  t1 = gt();
+  out[1] = (t1 - t0) * 1000 / n;
+  t0 = gt();
+  for (int i = 0; i < n; ++i) {
+    a[128 + (i & 7)] = x;
+    asm volatile("fence.sc.gpu;" ::: "memory");
+  }
+  t1 = gt();
+  out[2] = (t1 - t0) * 1000 / n;
+  t0 = gt();
+  for (int i = 0; i < n; ++i) {
+    a[128 + (i & 7)] = x;
+    asm volatile("fence.sc.sys;" ::: "memory");
+  }
+  t1 = gt();
+  out[3] = (t1 - t0) * 1000 / n;
+  t0 = gt();
+  for (int i = 0; i < n; ++i) {
+    a[128 + (i & 7)] = x;
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  t1 = gt();
+  out[4] = (t1 - t0) * 1000 / n;
+  uint64_t v = 0;
+  t0 = gt();
+  for (int i = 0; i < n; ++i)
+    asm volatile("atom.acq_rel.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(v) : "l"(a + 200), "l"(v), "l"(v + 1) : "memory");
+  t1 = gt();
+  out[5] = (t1 - t0) * 1000 / n;
+  t0 = gt();
+  for (int i = 0; i < n; ++i)
+    asm volatile("atom.acq_rel.sys.global.cas.b64 %0, [%1], %2, %3;" : "=l"(v) : "l"(a + 200), "l"(v), "l"(v + 1) : "memory");
+  t1 = gt();
+  out[6] = (t1 - t0) * 1000 / n;
+  t0 = gt();
+  for (int i = 0; i < n; ++i) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a + 256), "l"(x) : "memory");
+    x = ldg(a + (x & 63));
+  }
+  t1 = gt();
+  out[7] = (t1 - t0) * 1000 / n;
+  long long c0 = clock64();
+  t0 = gt();
+  while (gt() - t0 < 20000) {
+  }
+  long long c1 = clock64();
+  t1 = gt();
+  out[8] = (uint64_t)(c1 - c0) * 1000 / (t1 - t0);
+  out[9] = x + v;
+}
+
+// Large straight-line body: cold pass then warm pass over the same code.
+#define B4(k) acc = acc * 1664525u + (k); acc ^= acc >> 7; acc += (k) * 3u; acc ^= acc << 5;
+#define B16(k) B4(k) B4(k + 1) B4(k + 2) B4(k + 3)
+#define B64(k) B16(k) B16(k + 4) B16(k + 8) B16(k + 12)
+#define B256(k) B64(k) B64(k + 16) B64(k + 32) B64(k + 48)
+__device__ __noinline__ uint32_t body(uint32_t acc) {
+  B256(1) B256(101) B256(201) B256(301) B256(401) B256(501) B256(601) B256(701)
+  return acc;
+}
+__global__ void k_icache(uint64_t* out, uint32_t seed) {
+  if (threadIdx.x != 0) return;
+  uint64_t t0 = gt();
+  uint32_t a = body(seed);
+  uint64_t t1 = gt();
+  a = body(a);
+  uint64_t t2 = gt();
+  out[10] = t1 - t0;
+  out[11] = t2 - t1;
+  out[12] = a;
+}
+
+// Kernel-parameter (constant bank) first-access latency: a 1 KiB parameter
+// struct, read field by field with each read's address depending on the last.
+struct Big {
+  uint64_t v[128];
+};
+__global__ void k_params(const Big p, uint64_t* out) {
+  if (threadIdx.x != 0) return;
+  uint64_t t0 = gt();
+  uint64_t x = p.v[0];
+  uint64_t t1 = gt() + (x & 0);
+  uint64_t y = p.v[(x & 7) + 1];  // same 64-B line
+  uint64_t t2 = gt() + (y & 0);
+  uint64_t z = p.v[(y & 7) + 16];  // another line
+  uint64_t t3 = gt() + (z & 0);
+  uint64_t w = p.v[(z & 7) + 96];  // far line
+  uint64_t t4 = gt() + (w & 0);
+  out[0] = t1 - t0;
+  out[1] = t2 - t1;
+  out[2] = t3 - t2;
+  out[3] = t4 - t3;
+  out[4] = x + y + z + w;
+}
+
+// The ring scan alone: one warp, 4 x 16-B relaxed loads per lane over a
+// 128-slot ring of 64-B descriptors (8 KiB), then a ballot — as warp_scan.
+__global__ void k_scan(const uint64_t* ring, uint64_t* out, int iters) {
+  const int lane = threadIdx.x & 31;
+  uint64_t acc = 0, tsum = 0;
+  for (int it = 0; it < iters; ++it) {
+    uint64_t t0 = gt();
+    uint64_t st[4], ky[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(st[k]), "=l"(ky[k]) : "l"(ring + 8 * (k * 32 + lane)) : "memory");
+    unsigned m = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m |= __ballot_sync(0xffffffffu, st[k] == 12345 && ky[k] == 7);
+    acc += m;
+    uint64_t t1 = gt();
+    tsum += t1 - t0;
+  }
+  if (lane == 0) {
+    out[0] = tsum / iters;
+    out[1] = acc;
+  }
+}
+
+// Branchy code for the instruction-cache test: 256 switch cases visited in a
+// scrambled order (the sequential prefetcher cannot follow).
+__device__ __noinline__ uint32_t branchy(const uint8_t* order, uint32_t x) {
+  for (int i = 0; i < 256; ++i) {
+    switch (order[i]) {
+      case 0: x = x * 3u + 0u; x ^= x >> 1; x += 17u; x ^= x << 1; x = x * 1u + 0u; break;
+      case 1: x = x * 5u + 7919u; x ^= x >> 2; x += 48u; x ^= x << 2; x = x * 5u + 1u; break;
+      case 2: x = x * 7u + 15838u; x ^= x >> 3; x += 79u; x ^= x << 3; x = x * 9u + 2u; break;
+      case 3: x = x * 9u + 23757u; x ^= x >> 4; x += 110u; x ^= x << 4; x = x * 13u + 3u; break;
+      case 4: x = x * 11u + 31676u; x ^= x >> 5; x += 141u; x ^= x << 5; x = x * 17u + 4u; break;
+      case 5: x = x * 13u + 39595u; x ^= x >> 6; x += 172u; x ^= x << 6; x = x * 21u + 5u; break;
+      case 6: x = x * 15u + 47514u; x ^= x >> 7; x += 203u; x ^= x << 7; x = x * 25u + 6u; break;
+      case 7: x = x * 17u + 55433u; x ^= x >> 8; x += 234u; x ^= x << 1; x = x * 29u + 7u; break;
+      case 8: x = x * 19u + 63352u; x ^= x >> 9; x += 265u; x ^= x << 2; x = x * 33u + 8u; break;
+      case 9: x = x * 21u + 71271u; x ^= x >> 10; x += 296u; x ^= x << 3; x = x * 37u + 9u; break;
+      case 10: x = x * 23u + 79190u; x ^= x >> 11; x += 327u; x ^= x << 4; x = x * 41u + 10u; break;
+      case 11: x = x * 25u + 87109u; x ^= x >> 12; x += 358u; x ^= x << 5; x = x * 45u + 11u; break;
+      case 12: x = x * 27u + 95028u; x ^= x >> 13; x += 389u; x ^= x << 6; x = x * 49u + 12u; break;
+      case 13: x = x * 29u + 102947u; x ^= x >> 1; x += 420u; x ^= x << 7; x = x * 53u + 13u; break;
+      case 14: x = x * 31u + 110866u; x ^= x >> 2; x += 451u; x ^= x << 1; x = x * 57u + 14u; break;
+      case 15: x = x * 33u + 118785u; x ^= x >> 3; x += 482u; x ^= x << 2; x = x * 61u + 15u; break;
+      case 16: x = x * 35u + 126704u; x ^= x >> 4; x += 513u; x ^= x << 3; x = x * 65u + 16u; break;
+      case 17: x = x * 37u + 134623u; x ^= x >> 5; x += 544u; x ^= x << 4; x = x * 69u + 17u; break;
+      case 18: x = x * 39u + 142542u; x ^= x >> 6; x += 575u; x ^= x << 5; x = x * 73u + 18u; break;
+      case 19: x = x * 41u + 150461u; x ^= x >> 7; x += 606u; x ^= x << 6; x = x * 77u + 19u; break;
+      case 20: x = x * 43u + 158380u; x ^= x >> 8; x += 637u; x ^= x << 7; x = x * 81u + 20u; break;
+      case 21: x = x * 45u + 166299u; x ^= x >> 9; x += 668u; x ^= x << 1; x = x * 85u + 21u; break;
+      case 22: x = x * 47u + 174218u; x ^= x >> 10; x += 699u; x ^= x << 2; x = x * 89u + 22u; break;
+      case 23: x = x * 49u + 182137u; x ^= x >> 11; x += 730u; x ^= x << 3; x = x * 93u + 23u; break;
+      case 24: x = x * 51u + 190056u; x ^= x >> 12; x += 761u; x ^= x << 4; x = x * 97u + 24u; break;
+      case 25: x = x * 53u + 197975u; x ^= x >> 13; x += 792u; x ^= x << 5; x = x * 101u + 25u; break;
+      case 26: x = x * 55u + 205894u; x ^= x >> 1; x += 823u; x ^= x << 6; x = x * 105u + 26u; break;
+      case 27: x = x * 57u + 213813u; x ^= x >> 2; x += 854u; x ^= x << 7; x = x * 109u + 27u; break;
+      case 28: x = x * 59u + 221732u; x ^= x >> 3; x += 885u; x ^= x << 1; x = x * 113u + 28u; break;
+      case 29: x = x * 61u + 229651u; x ^= x >> 4; x += 916u; x ^= x << 2; x = x * 117u + 29u; break;
+      case 30: x = x * 63u + 237570u; x ^= x >> 5; x += 947u; x ^= x << 3; x = x * 121u + 30u; break;
+      case 31: x = x * 65u + 245489u; x ^= x >> 6; x += 978u; x ^= x << 4; x = x * 125u + 31u; break;
+      case 32: x = x * 67u + 253408u; x ^= x >> 7; x += 1009u; x ^= x << 5; x = x * 129u + 32u; break;
+      case 33: x = x * 69u + 261327u; x ^= x >> 8; x += 1040u; x ^= x << 6; x = x * 133u + 33u; break;
+      case 34: x = x * 71u + 269246u; x ^= x >> 9; x += 1071u; x ^= x << 7; x = x * 137u + 34u; break;
+      case 35: x = x * 73u + 277165u; x ^= x >> 10; x += 1102u; x ^= x << 1; x = x * 141u + 35u; break;
+      case 36: x = x * 75u + 285084u; x ^= x >> 11; x += 1133u; x ^= x << 2; x = x * 145u + 36u; break;
+      case 37: x = x * 77u + 293003u; x ^= x >> 12; x += 1164u; x ^= x << 3; x = x * 149u + 37u; break;
+      case 38: x = x * 79u + 300922u; x ^= x >> 13; x += 1195u; x ^= x << 4; x = x * 153u + 38u; break;
+      case 39: x = x * 81u + 308841u; x ^= x >> 1; x += 1226u; x ^= x << 5; x = x * 157u + 39u; break;
+      case 40: x = x * 83u + 316760u; x ^= x >> 2; x += 1257u; x ^= x << 6; x = x * 161u + 40u; break;
+      case 41: x = x * 85u + 324679u; x ^= x >> 3; x += 1288u; x ^= x << 7; x = x * 165u + 41u; break;
+      case 42: x = x * 87u + 332598u; x ^= x >> 4; x += 1319u; x ^= x << 1; x = x * 169u + 42u; break;
+      case 43: x = x * 89u + 340517u; x ^= x >> 5; x += 1350u; x ^= x << 2; x = x * 173u + 43u; break;
+      case 44: x = x * 91u + 348436u; x ^= x >> 6; x += 1381u; x ^= x << 3; x = x * 177u + 44u; break;
+      case 45: x = x * 93u + 356355u; x ^= x >> 7; x += 1412u; x ^= x << 4; x = x * 181u + 45u; break;
+      case 46: x = x * 95u + 364274u; x ^= x >> 8; x += 1443u; x ^= x << 5; x = x * 185u + 46u; break;
+      case 47: x = x * 97u + 372193u; x ^= x >> 9; x += 1474u; x ^= x << 6; x = x * 189u + 47u; break;
+      case 48: x = x * 99u + 380112u; x ^= x >> 10; x += 1505u; x ^= x << 7; x = x * 193u + 48u; break;
+      case 49: x = x * 101u + 388031u; x ^= x >> 11; x += 1536u; x ^= x << 1; x = x * 197u + 49u; break;
+      case 50: x = x * 103u + 395950u; x ^= x >> 12; x += 1567u; x ^= x << 2; x = x * 201u + 50u; break;
+      case 51: x = x * 105u + 403869u; x ^= x >> 13; x += 1598u; x ^= x << 3; x = x * 205u + 51u; break;
+      case 52: x = x * 107u + 411788u; x ^= x >> 1; x += 1629u; x ^= x << 4; x = x * 209u + 52u; break;
+      case 53: x = x * 109u + 419707u; x ^= x >> 2; x += 1660u; x ^= x << 5; x = x * 213u + 53u; break;
+      case 54: x = x * 111u + 427626u; x ^= x >> 3; x += 1691u; x ^= x << 6; x = x * 217u + 54u; break;
+      case 55: x = x * 113u + 435545u; x ^= x >> 4; x += 1722u; x ^= x << 7; x = x * 221u + 55u; break;
+      case 56: x = x * 115u + 443464u; x ^= x >> 5; x += 1753u; x ^= x << 1; x = x * 225u + 56u; break;
+      case 57: x = x * 117u + 451383u; x ^= x >> 6; x += 1784u; x ^= x << 2; x = x * 229u + 57u; break;
+      case 58: x = x * 119u + 459302u; x ^= x >> 7; x += 1815u; x ^= x << 3; x = x * 233u + 58u; break;
+      case 59: x = x * 121u + 467221u; x ^= x >> 8; x += 1846u; x ^= x << 4; x = x * 237u + 59u; break;
+      case 60: x = x * 123u + 475140u; x ^= x >> 9; x += 1877u; x ^= x << 5; x = x * 241u + 60u; break;
+      case 61: x = x * 125u + 483059u; x ^= x >> 10; x += 1908u; x ^= x << 6; x = x * 245u + 61u; break;
+      case 62: x = x * 127u + 490978u; x ^= x >> 11; x += 1939u; x ^= x << 7; x = x * 249u + 62u; break;
+      case 63: x = x * 129u + 498897u; x ^= x >> 12; x += 1970u; x ^= x << 1; x = x * 253u + 63u; break;
+      case 64: x = x * 131u + 506816u; x ^= x >> 13; x += 2001u; x ^= x << 2; x = x * 257u + 64u; break;
+      case 65: x = x * 133u + 514735u; x ^= x >> 1; x += 2032u; x ^= x << 3; x = x * 261u + 65u; break;
+      case 66: x = x * 135u + 522654u; x ^= x >> 2; x += 2063u; x ^= x << 4; x = x * 265u + 66u; break;
+      case 67: x = x * 137u + 530573u; x ^= x >> 3; x += 2094u; x ^= x << 5; x = x * 269u + 67u; break;
+      case 68: x = x * 139u + 538492u; x ^= x >> 4; x += 2125u; x ^= x << 6; x = x * 273u + 68u; break;
+      case 69: x = x * 141u + 546411u; x ^= x >> 5; x += 2156u; x ^= x << 7; x = x * 277u + 69u; break;
+      case 70: x = x * 143u + 554330u; x ^= x >> 6; x += 2187u; x ^= x << 1; x = x * 281u + 70u; break;
+      case 71: x = x * 145u + 562249u; x ^= x >> 7; x += 2218u; x ^= x << 2; x = x * 285u + 71u; break;
+      case 72: x = x * 147u + 570168u; x ^= x >> 8; x += 2249u; x ^= x << 3; x = x * 289u + 72u; break;
+      case 73: x = x * 149u + 578087u; x ^= x >> 9; x += 2280u; x ^= x << 4; x = x * 293u + 73u; break;
+      case 74: x = x * 151u + 586006u; x ^= x >> 10; x += 2311u; x ^= x << 5; x = x * 297u + 74u; break;
+      case 75: x = x * 153u + 593925u; x ^= x >> 11; x += 2342u; x ^= x << 6; x = x * 301u + 75u; break;
+      case 76: x = x * 155u + 601844u; x ^= x >> 12; x += 2373u; x ^= x << 7; x = x * 305u + 76u; break;
+      case 77: x = x * 157u + 609763u; x ^= x >> 13; x += 2404u; x ^= x << 1; x = x * 309u + 77u; break;
+      case 78: x = x * 159u + 617682u; x ^= x >> 1; x += 2435u; x ^= x << 2; x = x * 313u + 78u; break;
+      case 79: x = x * 161u + 625601u; x ^= x >> 2; x += 2466u; x ^= x << 3; x = x * 317u + 79u; break;
+      case 80: x = x * 163u + 633520u; x ^= x >> 3; x += 2497u; x ^= x << 4; x = x * 321u + 80u; break;
+      case 81: x = x * 165u + 641439u; x ^= x >> 4; x += 2528u; x ^= x << 5; x = x * 325u + 81u; break;
+      case 82: x = x * 167u + 649358u; x ^= x >> 5; x += 2559u; x ^= x << 6; x = x * 329u + 82u; break;
+      case 83: x = x * 169u + 657277u; x ^= x >> 6; x += 2590u; x ^= x << 7; x = x * 333u + 83u; break;
+      case 84: x = x * 171u + 665196u; x ^= x >> 7; x += 2621u; x ^= x << 1; x = x * 337u + 84u; break;
+      case 85: x = x * 173u + 673115u; x ^= x >> 8; x += 2652u; x ^= x << 2; x = x * 341u + 85u; break;
+      case 86: x = x * 175u + 681034u; x ^= x >> 9; x += 2683u; x ^= x << 3; x = x * 345u + 86u; break;
+      case 87: x = x * 177u + 688953u; x ^= x >> 10; x += 2714u; x ^= x << 4; x = x * 349u + 87u; break;
+      case 88: x = x * 179u + 696872u; x ^= x >> 11; x += 2745u; x ^= x << 5; x = x * 353u + 88u; break;
+      case 89: x = x * 181u + 704791u; x ^= x >> 12; x += 2776u; x ^= x << 6; x = x * 357u + 89u; break;
+      case 90: x = x * 183u + 712710u; x ^= x >> 13; x += 2807u; x ^= x << 7; x = x * 361u + 90u; break;
+      case 91: x = x * 185u + 720629u; x ^= x >> 1; x += 2838u; x ^= x << 1; x = x * 365u + 91u; break;
+      case 92: x = x * 187u + 728548u; x ^= x >> 2; x += 2869u; x ^= x << 2; x = x * 369u + 92u; break;
+      case 93: x = x * 189u + 736467u; x ^= x >> 3; x += 2900u; x ^= x << 3; x = x * 373u + 93u; break;
+      case 94: x = x * 191u + 744386u; x ^= x >> 4; x += 2931u; x ^= x << 4; x = x * 377u + 94u; break;
+      case 95: x = x * 193u + 752305u; x ^= x >> 5; x += 2962u; x ^= x << 5; x = x * 381u + 95u; break;
+      case 96: x = x * 195u + 760224u; x ^= x >> 6; x += 2993u; x ^= x << 6; x = x * 385u + 96u; break;
+      case 97: x = x * 197u + 768143u; x ^= x >> 7; x += 3024u; x ^= x << 7; x = x * 389u + 97u; break;
+      case 98: x = x * 199u + 776062u; x ^= x >> 8; x += 3055u; x ^= x << 1; x = x * 393u + 98u; break;
+      case 99: x = x * 201u + 783981u; x ^= x >> 9; x += 3086u; x ^= x << 2; x = x * 397u + 99u; break;
+      case 100: x = x * 203u + 791900u; x ^= x >> 10; x += 3117u; x ^= x << 3; x = x * 401u + 100u; break;
+      case 101: x = x * 205u + 799819u; x ^= x >> 11; x += 3148u; x ^= x << 4; x = x * 405u + 101u; break;
+      case 102: x = x * 207u + 807738u; x ^= x >> 12; x += 3179u; x ^= x << 5; x = x * 409u + 102u; break;
+      case 103: x = x * 209u + 815657u; x ^= x >> 13; x += 3210u; x ^= x << 6; x = x * 413u + 103u; break;
+      case 104: x = x * 211u + 823576u; x ^= x >> 1; x += 3241u; x ^= x << 7; x = x * 417u + 104u; break;
+      case 105: x = x * 213u + 831495u; x ^= x >> 2; x += 3272u; x ^= x << 1; x = x * 421u + 105u; break;
+      case 106: x = x * 215u + 839414u; x ^= x >> 3; x += 3303u; x ^= x << 2; x = x * 425u + 106u; break;
+      case 107: x = x * 217u + 847333u; x ^= x >> 4; x += 3334u; x ^= x << 3; x = x * 429u + 107u; break;
+      case 108: x = x * 219u + 855252u; x ^= x >> 5; x += 3365u; x ^= x << 4; x = x * 433u + 108u; break;
+      case 109: x = x * 221u + 863171u; x ^= x >> 6; x += 3396u; x ^= x << 5; x = x * 437u + 109u; break;
+      case 110: x = x * 223u + 871090u; x ^= x >> 7; x += 3427u; x ^= x << 6; x = x * 441u + 110u; break;
+      case 111: x = x * 225u + 879009u; x ^= x >> 8; x += 3458u; x ^= x << 7; x = x * 445u + 111u; break;
+      case 112: x = x * 227u + 886928u; x ^= x >> 9; x += 3489u; x ^= x << 1; x = x * 449u + 112u; break;
+      case 113: x = x * 229u + 894847u; x ^= x >> 10; x += 3520u; x ^= x << 2; x = x * 453u + 113u; break;
+      case 114: x = x * 231u + 902766u; x ^= x >> 11; x += 3551u; x ^= x << 3; x = x * 457u + 114u; break;
+      case 115: x = x * 233u + 910685u; x ^= x >> 12; x += 3582u; x ^= x << 4; x = x * 461u + 115u; break;
+      case 116: x = x * 235u + 918604u; x ^= x >> 13; x += 3613u; x ^= x << 5; x = x * 465u + 116u; break;
+      case 117: x = x * 237u + 926523u; x ^= x >> 1; x += 3644u; x ^= x << 6; x = x * 469u + 117u; break;
+      case 118: x = x * 239u + 934442u; x ^= x >> 2; x += 3675u; x ^= x << 7; x = x * 473u + 118u; break;
+      case 119: x = x * 241u + 942361u; x ^= x >> 3; x += 3706u; x ^= x << 1; x = x * 477u + 119u; break;
+      case 120: x = x * 243u + 950280u; x ^= x >> 4; x += 3737u; x ^= x << 2; x = x * 481u + 120u; break;
+      case 121: x = x * 245u + 958199u; x ^= x >> 5; x += 3768u; x ^= x << 3; x = x * 485u + 121u; break;
+      case 122: x = x * 247u + 966118u; x ^= x >> 6; x += 3799u; x ^= x << 4; x = x * 489u + 122u; break;
+      case 123: x = x * 249u + 974037u; x ^= x >> 7; x += 3830u; x ^= x << 5; x = x * 493u + 123u; break;
+      case 124: x = x * 251u + 981956u; x ^= x >> 8; x += 3861u; x ^= x << 6; x = x * 497u + 124u; break;
+      case 125: x = x * 253u + 989875u; x ^= x >> 9; x += 3892u; x ^= x << 7; x = x * 501u + 125u; break;
+      case 126: x = x * 255u + 997794u; x ^= x >> 10; x += 3923u; x ^= x << 1; x = x * 505u + 126u; break;
+      case 127: x = x * 257u + 5710u; x ^= x >> 11; x += 3954u; x ^= x << 2; x = x * 509u + 127u; break;
+      case 128: x = x * 259u + 13629u; x ^= x >> 12; x += 3985u; x ^= x << 3; x = x * 513u + 128u; break;
+      case 129: x = x * 261u + 21548u; x ^= x >> 13; x += 4016u; x ^= x << 4; x = x * 517u + 129u; break;
+      case 130: x = x * 263u + 29467u; x ^= x >> 1; x += 4047u; x ^= x << 5; x = x * 521u + 130u; break;
+      case 131: x = x * 265u + 37386u; x ^= x >> 2; x += 4078u; x ^= x << 6; x = x * 525u + 131u; break;
+      case 132: x = x * 267u + 45305u; x ^= x >> 3; x += 4109u; x ^= x << 7; x = x * 529u + 132u; break;
+      case 133: x = x * 269u + 53224u; x ^= x >> 4; x += 4140u; x ^= x << 1; x = x * 533u + 133u; break;
+      case 134: x = x * 271u + 61143u; x ^= x >> 5; x += 4171u; x ^= x << 2; x = x * 537u + 134u; break;
+      case 135: x = x * 273u + 69062u; x ^= x >> 6; x += 4202u; x ^= x << 3; x = x * 541u + 135u; break;
+      case 136: x = x * 275u + 76981u; x ^= x >> 7; x += 4233u; x ^= x << 4; x = x * 545u + 136u; break;
+      case 137: x = x * 277u + 84900u; x ^= x >> 8; x += 4264u; x ^= x << 5; x = x * 549u + 137u; break;
+      case 138: x = x * 279u + 92819u; x ^= x >> 9; x += 4295u; x ^= x << 6; x = x * 553u + 138u; break;
+      case 139: x = x * 281u + 100738u; x ^= x >> 10; x += 4326u; x ^= x << 7; x = x * 557u + 139u; break;
+      case 140: x = x * 283u + 108657u; x ^= x >> 11; x += 4357u; x ^= x << 1; x = x * 561u + 140u; break;
+      case 141: x = x * 285u + 116576u; x ^= x >> 12; x += 4388u; x ^= x << 2; x = x * 565u + 141u; break;
+      case 142: x = x * 287u + 124495u; x ^= x >> 13; x += 4419u; x ^= x << 3; x = x * 569u + 142u; break;
+      case 143: x = x * 289u + 132414u; x ^= x >> 1; x += 4450u; x ^= x << 4; x = x * 573u + 143u; break;
+      case 144: x = x * 291u + 140333u; x ^= x >> 2; x += 4481u; x ^= x << 5; x = x * 577u + 144u; break;
+      case 145: x = x * 293u + 148252u; x ^= x >> 3; x += 4512u; x ^= x << 6; x = x * 581u + 145u; break;
+      case 146: x = x * 295u + 156171u; x ^= x >> 4; x += 4543u; x ^= x << 7; x = x * 585u + 146u; break;
+      case 147: x = x * 297u + 164090u; x ^= x >> 5; x += 4574u; x ^= x << 1; x = x * 589u + 147u; break;
+      case 148: x = x * 299u + 172009u; x ^= x >> 6; x += 4605u; x ^= x << 2; x = x * 593u + 148u; break;
+      case 149: x = x * 301u + 179928u; x ^= x >> 7; x += 4636u; x ^= x << 3; x = x * 597u + 149u; break;
+      case 150: x = x * 303u + 187847u; x ^= x >> 8; x += 4667u; x ^= x << 4; x = x * 601u + 150u; break;
+      case 151: x = x * 305u + 195766u; x ^= x >> 9; x += 4698u; x ^= x << 5; x = x * 605u + 151u; break;
+      case 152: x = x * 307u + 203685u; x ^= x >> 10; x += 4729u; x ^= x << 6; x = x * 609u + 152u; break;
+      case 153: x = x * 309u + 211604u; x ^= x >> 11; x += 4760u; x ^= x << 7; x = x * 613u + 153u; break;
+      case 154: x = x * 311u + 219523u; x ^= x >> 12; x += 4791u; x ^= x << 1; x = x * 617u + 154u; break;
+      case 155: x = x * 313u + 227442u; x ^= x >> 13; x += 4822u; x ^= x << 2; x = x * 621u + 155u; break;
+      case 156: x = x * 315u + 235361u; x ^= x >> 1; x += 4853u; x ^= x << 3; x = x * 625u + 156u; break;
+      case 157: x = x * 317u + 243280u; x ^= x >> 2; x += 4884u; x ^= x << 4; x = x * 629u + 157u; break;
+      case 158: x = x * 319u + 251199u; x ^= x >> 3; x += 4915u; x ^= x << 5; x = x * 633u + 158u; break;
+      case 159: x = x * 321u + 259118u; x ^= x >> 4; x += 4946u; x ^= x << 6; x = x * 637u + 159u; break;
+      case 160: x = x * 323u + 267037u; x ^= x >> 5; x += 4977u; x ^= x << 7; x = x * 641u + 160u; break;
+      case 161: x = x * 325u + 274956u; x ^= x >> 6; x += 5008u; x ^= x << 1; x = x * 645u + 161u; break;
+      case 162: x = x * 327u + 282875u; x ^= x >> 7; x += 5039u; x ^= x << 2; x = x * 649u + 162u; break;
+      case 163: x = x * 329u + 290794u; x ^= x >> 8; x += 5070u; x ^= x << 3; x = x * 653u + 163u; break;
+      case 164: x = x * 331u + 298713u; x ^= x >> 9; x += 5101u; x ^= x << 4; x = x * 657u + 164u; break;
+      case 165: x = x * 333u + 306632u; x ^= x >> 10; x += 5132u; x ^= x << 5; x = x * 661u + 165u; break;
+      case 166: x = x * 335u + 314551u; x ^= x >> 11; x += 5163u; x ^= x << 6; x = x * 665u + 166u; break;
+      case 167: x = x * 337u + 322470u; x ^= x >> 12; x += 5194u; x ^= x << 7; x = x * 669u + 167u; break;
+      case 168: x = x * 339u + 330389u; x ^= x >> 13; x += 5225u; x ^= x << 1; x = x * 673u + 168u; break;
+      case 169: x = x * 341u + 338308u; x ^= x >> 1; x += 5256u; x ^= x << 2; x = x * 677u + 169u; break;
+      case 170: x = x * 343u + 346227u; x ^= x >> 2; x += 5287u; x ^= x << 3; x = x * 681u + 170u; break;
+      case 171: x = x * 345u + 354146u; x ^= x >> 3; x += 5318u; x ^= x << 4; x = x * 685u + 171u; break;
+      case 172: x = x * 347u + 362065u; x ^= x >> 4; x += 5349u; x ^= x << 5; x = x * 689u + 172u; break;
+      case 173: x = x * 349u + 369984u; x ^= x >> 5; x += 5380u; x ^= x << 6; x = x * 693u + 173u; break;
+      case 174: x = x * 351u + 377903u; x ^= x >> 6; x += 5411u; x ^= x << 7; x = x * 697u + 174u; break;
+      case 175: x = x * 353u + 385822u; x ^= x >> 7; x += 5442u; x ^= x << 1; x = x * 701u + 175u; break;
+      case 176: x = x * 355u + 393741u; x ^= x >> 8; x += 5473u; x ^= x << 2; x = x * 705u + 176u; break;
+      case 177: x = x * 357u + 401660u; x ^= x >> 9; x += 5504u; x ^= x << 3; x = x * 709u + 177u; break;
+      case 178: x = x * 359u + 409579u; x ^= x >> 10; x += 5535u; x ^= x << 4; x = x * 713u + 178u; break;
+      case 179: x = x * 361u + 417498u; x ^= x >> 11; x += 5566u; x ^= x << 5; x = x * 717u + 179u; break;
+      case 180: x = x * 363u + 425417u; x ^= x >> 12; x += 5597u; x ^= x << 6; x = x * 721u + 180u; break;
+      case 181: x = x * 365u + 433336u; x ^= x >> 13; x += 5628u; x ^= x << 7; x = x * 725u + 181u; break;
+      case 182: x = x * 367u + 441255u; x ^= x >> 1; x += 5659u; x ^= x << 1; x = x * 729u + 182u; break;
+      case 183: x = x * 369u + 449174u; x ^= x >> 2; x += 5690u; x ^= x << 2; x = x * 733u + 183u; break;
+      case 184: x = x * 371u + 457093u; x ^= x >> 3; x += 5721u; x ^= x << 3; x = x * 737u + 184u; break;
+      case 185: x = x * 373u + 465012u; x ^= x >> 4; x += 5752u; x ^= x << 4; x = x * 741u + 185u; break;
+      case 186: x = x * 375u + 472931u; x ^= x >> 5; x += 5783u; x ^= x << 5; x = x * 745u + 186u; break;
+      case 187: x = x * 377u + 480850u; x ^= x >> 6; x += 5814u; x ^= x << 6; x = x * 749u + 187u; break;
+      case 188: x = x * 379u + 488769u; x ^= x >> 7; x += 5845u; x ^= x << 7; x = x * 753u + 188u; break;
+      case 189: x = x * 381u + 496688u; x ^= x >> 8; x += 5876u; x ^= x << 1; x = x * 757u + 189u; break;
+      case 190: x = x * 383u + 504607u; x ^= x >> 9; x += 5907u; x ^= x << 2; x = x * 761u + 190u; break;
+      case 191: x = x * 385u + 512526u; x ^= x >> 10; x += 5938u; x ^= x << 3; x = x * 765u + 191u; break;
+      case 192: x = x * 387u + 520445u; x ^= x >> 11; x += 5969u; x ^= x << 4; x = x * 769u + 192u; break;
+      case 193: x = x * 389u + 528364u; x ^= x >> 12; x += 6000u; x ^= x << 5; x = x * 773u + 193u; break;
+      case 194: x = x * 391u + 536283u; x ^= x >> 13; x += 6031u; x ^= x << 6; x = x * 777u + 194u; break;
+      case 195: x = x * 393u + 544202u; x ^= x >> 1; x += 6062u; x ^= x << 7; x = x * 781u + 195u; break;
+      case 196: x = x * 395u + 552121u; x ^= x >> 2; x += 6093u; x ^= x << 1; x = x * 785u + 196u; break;
+      case 197: x = x * 397u + 560040u; x ^= x >> 3; x += 6124u; x ^= x << 2; x = x * 789u + 197u; break;
+      case 198: x = x * 399u + 567959u; x ^= x >> 4; x += 6155u; x ^= x << 3; x = x * 793u + 198u; break;
+      case 199: x = x * 401u + 575878u; x ^= x >> 5; x += 6186u; x ^= x << 4; x = x * 797u + 199u; break;
+      case 200: x = x * 403u + 583797u; x ^= x >> 6; x += 6217u; x ^= x << 5; x = x * 801u + 200u; break;
+      case 201: x = x * 405u + 591716u; x ^= x >> 7; x += 6248u; x ^= x << 6; x = x * 805u + 201u; break;
+      case 202: x = x * 407u + 599635u; x ^= x >> 8; x += 6279u; x ^= x << 7; x = x * 809u + 202u; break;
+      case 203: x = x * 409u + 607554u; x ^= x >> 9; x += 6310u; x ^= x << 1; x = x * 813u + 203u; break;
+      case 204: x = x * 411u + 615473u; x ^= x >> 10; x += 6341u; x ^= x << 2; x = x * 817u + 204u; break;
+      case 205: x = x * 413u + 623392u; x ^= x >> 11; x += 6372u; x ^= x << 3; x = x * 821u + 205u; break;
+      case 206: x = x * 415u + 631311u; x ^= x >> 12; x += 6403u; x ^= x << 4; x = x * 825u + 206u; break;
+      case 207: x = x * 417u + 639230u; x ^= x >> 13; x += 6434u; x ^= x << 5; x = x * 829u + 207u; break;
+      case 208: x = x * 419u + 647149u; x ^= x >> 1; x += 6465u; x ^= x << 6; x = x * 833u + 208u; break;
+      case 209: x = x * 421u + 655068u; x ^= x >> 2; x += 6496u; x ^= x << 7; x = x * 837u + 209u; break;
+      case 210: x = x * 423u + 662987u; x ^= x >> 3; x += 6527u; x ^= x << 1; x = x * 841u + 210u; break;
+      case 211: x = x * 425u + 670906u; x ^= x >> 4; x += 6558u; x ^= x << 2; x = x * 845u + 211u; break;
+      case 212: x = x * 427u + 678825u; x ^= x >> 5; x += 6589u; x ^= x << 3; x = x * 849u + 212u; break;
+      case 213: x = x * 429u + 686744u; x ^= x >> 6; x += 6620u; x ^= x << 4; x = x * 853u + 213u; break;
+      case 214: x = x * 431u + 694663u; x ^= x >> 7; x += 6651u; x ^= x << 5; x = x * 857u + 214u; break;
+      case 215: x = x * 433u + 702582u; x ^= x >> 8; x += 6682u; x ^= x << 6; x = x * 861u + 215u; break;
+      case 216: x = x * 435u + 710501u; x ^= x >> 9; x += 6713u; x ^= x << 7; x = x * 865u + 216u; break;
+      case 217: x = x * 437u + 718420u; x ^= x >> 10; x += 6744u; x ^= x << 1; x = x * 869u + 217u; break;
+      case 218: x = x * 439u + 726339u; x ^= x >> 11; x += 6775u; x ^= x << 2; x = x * 873u + 218u; break;
+      case 219: x = x * 441u + 734258u; x ^= x >> 12; x += 6806u; x ^= x << 3; x = x * 877u + 219u; break;
+      case 220: x = x * 443u + 742177u; x ^= x >> 13; x += 6837u; x ^= x << 4; x = x * 881u + 220u; break;
+      case 221: x = x * 445u + 750096u; x ^= x >> 1; x += 6868u; x ^= x << 5; x = x * 885u + 221u; break;
+      case 222: x = x * 447u + 758015u; x ^= x >> 2; x += 6899u; x ^= x << 6; x = x * 889u + 222u; break;
+      case 223: x = x * 449u + 765934u; x ^= x >> 3; x += 6930u; x ^= x << 7; x = x * 893u + 223u; break;
+      case 224: x = x * 451u + 773853u; x ^= x >> 4; x += 6961u; x ^= x << 1; x = x * 897u + 224u; break;
+      case 225: x = x * 453u + 781772u; x ^= x >> 5; x += 6992u; x ^= x << 2; x = x * 901u + 225u; break;
+      case 226: x = x * 455u + 789691u; x ^= x >> 6; x += 7023u; x ^= x << 3; x = x * 905u + 226u; break;
+      case 227: x = x * 457u + 797610u; x ^= x >> 7; x += 7054u; x ^= x << 4; x = x * 909u + 227u; break;
+      case 228: x = x * 459u + 805529u; x ^= x >> 8; x += 7085u; x ^= x << 5; x = x * 913u + 228u; break;
+      case 229: x = x * 461u + 813448u; x ^= x >> 9; x += 7116u; x ^= x << 6; x = x * 917u + 229u; break;
+      case 230: x = x * 463u + 821367u; x ^= x >> 10; x += 7147u; x ^= x << 7; x = x * 921u + 230u; break;
+      case 231: x = x * 465u + 829286u; x ^= x >> 11; x += 7178u; x ^= x << 1; x = x * 925u + 231u; break;
+      case 232: x = x * 467u + 837205u; x ^= x >> 12; x += 7209u; x ^= x << 2; x = x * 929u + 232u; break;
+      case 233: x = x * 469u + 845124u; x ^= x >> 13; x += 7240u; x ^= x << 3; x = x * 933u + 233u; break;
+      case 234: x = x * 471u + 853043u; x ^= x >> 1; x += 7271u; x ^= x << 4; x = x * 937u + 234u; break;
+      case 235: x = x * 473u + 860962u; x ^= x >> 2; x += 7302u; x ^= x << 5; x = x * 941u + 235u; break;
+      case 236: x = x * 475u + 868881u; x ^= x >> 3; x += 7333u; x ^= x << 6; x = x * 945u + 236u; break;
+      case 237: x = x * 477u + 876800u; x ^= x >> 4; x += 7364u; x ^= x << 7; x = x * 949u + 237u; break;
+      case 238: x = x * 479u + 884719u; x ^= x >> 5; x += 7395u; x ^= x << 1; x = x * 953u + 238u; break;
+      case 239: x = x * 481u + 892638u; x ^= x >> 6; x += 7426u; x ^= x << 2; x = x * 957u + 239u; break;
+      case 240: x = x * 483u + 900557u; x ^= x >> 7; x += 7457u; x ^= x << 3; x = x * 961u + 240u; break;
+      case 241: x = x * 485u + 908476u; x ^= x >> 8; x += 7488u; x ^= x << 4; x = x * 965u + 241u; break;
+      case 242: x = x * 487u + 916395u; x ^= x >> 9; x += 7519u; x ^= x << 5; x = x * 969u + 242u; break;
+      case 243: x = x * 489u + 924314u; x ^= x >> 10; x += 7550u; x ^= x << 6; x = x * 973u + 243u; break;
+      case 244: x = x * 491u + 932233u; x ^= x >> 11; x += 7581u; x ^= x << 7; x = x * 977u + 244u; break;
+      case 245: x = x * 493u + 940152u; x ^= x >> 12; x += 7612u; x ^= x << 1; x = x * 981u + 245u; break;
+      case 246: x = x * 495u + 948071u; x ^= x >> 13; x += 7643u; x ^= x << 2; x = x * 985u + 246u; break;
+      case 247: x = x * 497u + 955990u; x ^= x >> 1; x += 7674u; x ^= x << 3; x = x * 989u + 247u; break;
+      case 248: x = x * 499u + 963909u; x ^= x >> 2; x += 7705u; x ^= x << 4; x = x * 993u + 248u; break;
+      case 249: x = x * 501u + 971828u; x ^= x >> 3; x += 7736u; x ^= x << 5; x = x * 997u + 249u; break;
+      case 250: x = x * 503u + 979747u; x ^= x >> 4; x += 7767u; x ^= x << 6; x = x * 1001u + 250u; break;
+      case 251: x = x * 505u + 987666u; x ^= x >> 5; x += 7798u; x ^= x << 7; x = x * 1005u + 251u; break;
+      case 252: x = x * 507u + 995585u; x ^= x >> 6; x += 7829u; x ^= x << 1; x = x * 1009u + 252u; break;
+      case 253: x = x * 509u + 3501u; x ^= x >> 7; x += 7860u; x ^= x << 2; x = x * 1013u + 253u; break;
+      case 254: x = x * 511u + 11420u; x ^= x >> 8; x += 7891u; x ^= x << 3; x = x * 1017u + 254u; break;
+      case 255: x = x * 513u + 19339u; x ^= x >> 9; x += 7922u; x ^= x << 4; x = x * 1021u + 255u; break;
+    }
+  }
+  return x;
+}
+__global__ void k_branchy(const uint8_t* order, uint64_t* out, int slot) {
+  if (threadIdx.x != 0) return;
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  uint64_t t0 = gt();
+  uint32_t x = branchy(order, 1);
+  uint64_t t1 = gt() + (x & 0);
+  x = branchy(order, x);
+  uint64_t t2 = gt() + (x & 0);
+  out[20 + 3 * slot] = t1 - t0;
+  out[21 + 3 * slot] = t2 - t1;
+  out[22 + 3 * slot] = sm + ((uint64_t)x << 32);
+}
+
+__global__ void k_sleep(uint64_t* out) {
+  if (threadIdx.x != 0) return;
+  const unsigned ds[4] = {0, 32, 64, 256};
+  for (int k = 0; k < 4; ++k) {
+    uint64_t t0 = gt();
+    for (int i = 0; i < 100; ++i) __nanosleep(ds[k]);
+    uint64_t t1 = gt();
+    out[40 + k] = (t1 - t0) / 100;
+  }
+}
+
+int main() {
+  uint64_t *a, *out, h[16];
+  cudaMalloc(&a, 64ull << 20);
+  cudaMalloc(&out, 256);
+  uint64_t init[64];
+  for (int i = 0; i < 64; ++i) init[i] = (i + 1) % 64;
+  cudaMemset(a, 0, 64ull << 20);
+  cudaMemcpy(a, init, sizeof(init), cudaMemcpyHostToDevice);
+  const char* names[] = {"dep load .gpu (ps->ns/1000)", "dep load .sys", "st+fence.sc.gpu", "st+fence.sc.sys",
+                         "st+fence.acq_rel.gpu", "cas.acq_rel.gpu", "cas.acq_rel.sys", "st.release.gpu + dep load",
+                         "SM clock MHz"};
+  for (int rep = 0; rep < 6; ++rep) {
+    k_prims<<<1, 32>>>(a, out, 200);
+    k_icache<<<1, 32>>>(out, rep);
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("rep %d:\n", rep);
+    for (int k = 0; k < 8; ++k) printf("  %-30s %8.1f ns\n", names[k], h[k] / 1000.0);
+    printf("  %-30s %8.0f\n", names[8], (double)h[8]);
+    printf("  first load on a fresh page %llu ns, next line same page %llu ns (sm %llu)\n",
+           (unsigned long long)h[13], (unsigned long long)h[14], (unsigned long long)h[15]);
+    printf("  icache: 8K-instruction body cold %llu ns, warm %llu ns\n", (unsigned long long)h[10],
+           (unsigned long long)h[11]);
+  }
+  for (int rep = 0; rep < 3; ++rep) {
+    k_scan<<<1, 32>>>(a + 8192, out, 1);
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    uint64_t first = h[0];
+    k_scan<<<1, 32>>>(a + 8192, out, 100);
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("ring scan (4 x v2 loads/lane + ballots): first launch %llu ns, steady %llu ns\n",
+           (unsigned long long)first, (unsigned long long)h[0]);
+  }
+  {
+    uint8_t ord[256];
+    for (int i = 0; i < 256; ++i) ord[i] = (uint8_t)((i * 97 + 13) & 255);
+    uint8_t* d_ord;
+    cudaMalloc(&d_ord, 256);
+    cudaMemcpy(d_ord, ord, 256, cudaMemcpyHostToDevice);
+    uint64_t* o2;
+    cudaMalloc(&o2, 8 * 64);
+    for (int l = 0; l < 4; ++l) k_branchy<<<1, 32>>>(d_ord, o2, l);
+    uint64_t hh[64];
+    cudaMemcpy(hh, o2, sizeof(hh), cudaMemcpyDeviceToHost);
+    for (int l = 0; l < 4; ++l)
+      printf("branchy 256 cases: launch %d (sm %llu) first pass %llu ns, second pass %llu ns\n", l,
+             (unsigned long long)(hh[22 + 3 * l] & 0xffffffff), (unsigned long long)hh[20 + 3 * l],
+             (unsigned long long)hh[21 + 3 * l]);
+  }
+  {
+    uint64_t* o3;
+    cudaMalloc(&o3, 8 * 64);
+    k_sleep<<<1, 32>>>(o3);
+    uint64_t hh[64];
+    cudaMemcpy(hh, o3, sizeof(hh), cudaMemcpyDeviceToHost);
+    printf("nanosleep(0/32/64/256) takes %llu / %llu / %llu / %llu ns\n", (unsigned long long)hh[40],
+           (unsigned long long)hh[41], (unsigned long long)hh[42], (unsigned long long)hh[43]);
+  }
+  Big b = {};
+  for (int rep = 0; rep < 4; ++rep) {
+    k_params<<<1, 32>>>(b, out);
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("param first access %llu ns, same line %llu, new line %llu, far line %llu\n",
+           (unsigned long long)h[0], (unsigned long long)h[1], (unsigned long long)h[2], (unsigned long long)h[3]);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}

@@ -15,7 +15,7 @@ torch.cuda.synchronize()
 recs = mpix.trace_read(0)[20:]
 for kind in (0, 1):
     rs = [r for r in recs if r["is_recv"] == kind]
-    d = lambda a, b: st.median((r["t"][b] - r["t"][a]) / 1.95 for r in rs if r["t"][b] and r["t"][a])
+    d = lambda a, b: st.median((r["t"][b] - r["t"][a]) for r in rs if r["t"][b] and r["t"][a])
     ph = ["scan1", "post", "rescan/cas", "copy", "fin"]
     out = {}
     for k in range(1, 6):
