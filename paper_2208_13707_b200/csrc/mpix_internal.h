@@ -42,18 +42,22 @@ enum : uint64_t { ST_FREE = 0, ST_POSTED = 1, ST_TAKEN = 2 };
 // flag-in-data words (sends of <= kLLBytes). Scans match
 // (state & ~ST_LL) == ST_POSTED.
 constexpr uint64_t ST_LL = 0x10;
-constexpr uint64_t kLLBytes = 16;
+constexpr uint64_t kLLBytes = 12;
 // An LL word: 4 payload bytes | flag << 32, flag = 0x80000000 | (pseq &
 // 0x7fffffff). A reader that sees the flag of the post's own pseq in every
 // word holds that post's payload, whatever order the words landed in; no
 // stale word carries it (the slot's previous occupant was pseq - R, and
-// descriptor fields of other posts never have bit 63 set).
+// descriptor fields of other posts never have bit 63 set). The sender's
+// completion word and value (< 2^48) travel with a 16-bit check of the same
+// kind in their top bits (ll_chk).
 __host__ __device__ inline uint32_t ll_flag(uint64_t pseq) {
   return 0x80000000u | (uint32_t)(pseq & 0x7fffffffu);
 }
 __host__ __device__ inline uint64_t ll_word(uint32_t data, uint32_t flag) {
   return ((uint64_t)flag << 32) | data;
 }
+__host__ __device__ inline uint64_t ll_chk(uint64_t pseq) { return (0x8000ull | (pseq & 0x7fffull)) << 48; }
+constexpr uint64_t kLLPtrMask = (1ull << 48) - 1;
 // Codes a kernel stores in the rank's watchdog word before giving up
 // (the host turns any of them into the sticky MPIX_ERR_TIMEOUT / _DEVICE).
 enum : uint64_t { ERRW_WAIT_SLOT = 1, ERRW_WAIT_DONE = 2, ERRW_WAIT_COLL = 3, ERRW_PROTOCOL = 4 };
@@ -236,6 +240,10 @@ struct P2PArgs {
 // griddepcontrol.wait) while a blocking receive waits for its sender; larger
 // ones launch after it, so a parked grid never fills the GPU.
 constexpr uint64_t kEarlyTriggerTiles = 64;
+// A head kernel (k_batch) of at most this many CTAs lets the stream's next
+// head kernel launch early (programmatic dependent launch); larger ones
+// trigger at exit.
+constexpr int kEarlyHeadCtas = 8;
 
 struct WaitEntry {
   uint64_t* flag;

@@ -205,7 +205,7 @@ __device__ __forceinline__ void tile_copy(uint8_t* dst, const uint8_t* src, uint
 // style (the state word carries the pair sequence, so it never repeats).
 // ---------------------------------------------------------------------------
 struct Snap {
-  uint64_t state, key, addr, bytes, done_addr, done_val, p0;  // p0: an LL post's 4th word
+  uint64_t state, key, addr, bytes, done_addr, done_val, p0, p1;  // p0, p1: an LL post's words
 };
 
 template <bool SYS>
@@ -255,6 +255,7 @@ __device__ __noinline__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap*
         sn.done_addr = M::ld_rlx(&s->done_addr);
         sn.done_val = M::ld_rlx(&s->done_val);
         sn.p0 = M::ld_rlx(&s->pad[0]);
+        sn.p1 = M::ld_rlx(&s->pad[1]);
         // No re-validation: a state moves POSTED(pseq) -> TAKEN -> FREE ->
         // POSTED(pseq + R) only, and the fields change only with a new post,
         // so they belong to this post as long as the state does — which the
@@ -272,6 +273,7 @@ __device__ __noinline__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap*
         out->done_addr = __shfl_sync(0xffffffffu, sn.done_addr, src);
         out->done_val = __shfl_sync(0xffffffffu, sn.done_val, src);
         out->p0 = __shfl_sync(0xffffffffu, sn.p0, src);
+        out->p1 = __shfl_sync(0xffffffffu, sn.p1, src);
         return k * 32 + src;
       }
     }
@@ -861,80 +863,97 @@ __device__ void decide_paired(const P2PArgs& a, Decision& dc) {
 // ---------------------------------------------------------------------------
 // Flag-in-data (LL) small sends and polling blocking receives
 // ---------------------------------------------------------------------------
-// Payload bytes (<= kLLBytes) into four 32-bit words: byte loads, all in
+// Payload bytes (<= kLLBytes) into three 32-bit words: byte loads, all in
 // flight together (no read past the user's buffer).
-__device__ __forceinline__ void ll_load(const uint8_t* src, uint64_t n, uint32_t w[4]) {
+__device__ __forceinline__ void ll_load(const uint8_t* src, uint64_t n, uint32_t w[3]) {
   uint8_t b[kLLBytes];
 #pragma unroll
   for (int i = 0; i < (int)kLLBytes; ++i) b[i] = i < (int)n ? src[i] : 0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < 3; ++k)
     w[k] = (uint32_t)b[4 * k] | ((uint32_t)b[4 * k + 1] << 8) | ((uint32_t)b[4 * k + 2] << 16) |
            ((uint32_t)b[4 * k + 3] << 24);
 }
 
-// Post an LL send descriptor (lane 0): five flag-in-data words and the key,
-// then the state, all relaxed — a reader validates the words by their flags,
-// and a stale key never matches (keys are unique per pair), so nothing has
-// to be ordered before the state store.
+// Post an LL send descriptor (lane 0): three payload words and the length as
+// LL words, the sender's completion word/value check-tagged (ll_chk), the key,
+// then the state — all relaxed: a reader validates every word by its flag or
+// check, and a stale key never matches (keys are unique per pair), so nothing
+// has to be ordered before the state store. Like an Isend's descriptor, the
+// post completes the sender's request only when a receiver consumes it (the
+// windows of a stream stay flow-controlled by their receivers).
 template <bool SYS>
-__device__ void ll_post(const P2PArgs& a, const uint32_t w[4]) {
+__device__ void ll_post(const P2PArgs& a, const uint32_t w[3]) {
   using M = Scope<SYS>;
   SlotDesc* d = &a.post_ring[(int)(a.pseq % (uint64_t)a.R)];
   const uint32_t f = ll_flag(a.pseq);
+  const uint64_t chk = ll_chk(a.pseq);
   M::st_rlx(&d->addr, ll_word(w[0], f));
-  M::st_rlx(&d->done_addr, ll_word(w[1], f));
-  M::st_rlx(&d->done_val, ll_word(w[2], f));
-  M::st_rlx(&d->pad[0], ll_word(w[3], f));
+  M::st_rlx(&d->pad[0], ll_word(w[1], f));
+  M::st_rlx(&d->pad[1], ll_word(w[2], f));
   M::st_rlx(&d->bytes, ll_word((uint32_t)a.bytes, f));
+  M::st_rlx(&d->done_addr, ((uint64_t)a.my_done & kLLPtrMask) | chk);
+  M::st_rlx(&d->done_val, (a.my_done ? (a.my_gen & kLLPtrMask) : 0) | chk);
   M::st_rlx(&d->key, a.key);
   M::st_rlx(&d->state, st_word(a.pseq, ST_POSTED | ST_LL));
 }
 
-// Read an LL send descriptor's words (lane 0) until every flag is its post's.
-// Returns the payload length, or -1 on watchdog expiry.
+struct LLMsg {
+  uint32_t w[3];
+  uint64_t len;
+  uint64_t* sdone;  // the sender's completion word (null: a blocking send)
+  uint64_t sgen;
+};
+
+// Read an LL send descriptor's words (lane 0) until every flag and check is
+// its post's (the scan's snapshot first: usually everything has landed).
+// Returns false on watchdog expiry.
 template <bool SYS>
-__device__ int64_t ll_read(const SlotDesc* s, const Snap& sn, uint32_t w[4], const P2PArgs& a) {
+__device__ bool ll_read(const SlotDesc* s, const Snap& sn, LLMsg& m, const P2PArgs& a) {
   using M = Scope<SYS>;
-  const uint32_t f = ll_flag(sn.state >> 8);
+  const uint64_t pseq = sn.state >> 8;
+  const uint32_t f = ll_flag(pseq);
+  const uint64_t chk = ll_chk(pseq);
   const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
-  // the scan's snapshot first: usually every word has landed already
-  uint64_t w0 = sn.addr, w1 = sn.done_addr, w2 = sn.done_val, w3 = sn.p0, wl = sn.bytes;
+  uint64_t w0 = sn.addr, w1 = sn.p0, w2 = sn.p1, wl = sn.bytes, da = sn.done_addr, dv = sn.done_val;
   for (;;) {
     if ((uint32_t)(w0 >> 32) == f && (uint32_t)(w1 >> 32) == f && (uint32_t)(w2 >> 32) == f &&
-        (uint32_t)(w3 >> 32) == f && (uint32_t)(wl >> 32) == f) {
-      w[0] = (uint32_t)w0;
-      w[1] = (uint32_t)w1;
-      w[2] = (uint32_t)w2;
-      w[3] = (uint32_t)w3;
-      return (int64_t)(uint32_t)wl;
+        (uint32_t)(wl >> 32) == f && (da & ~kLLPtrMask) == chk && (dv & ~kLLPtrMask) == chk) {
+      m.w[0] = (uint32_t)w0;
+      m.w[1] = (uint32_t)w1;
+      m.w[2] = (uint32_t)w2;
+      m.len = (uint32_t)wl;
+      m.sdone = reinterpret_cast<uint64_t*>(da & kLLPtrMask);
+      m.sgen = dv & kLLPtrMask;
+      return true;
     }
     __nanosleep(32);
-    w0 = M::ld_rlx(&s->addr);
-    w1 = M::ld_rlx(&s->done_addr);
-    w2 = M::ld_rlx(&s->done_val);
-    w3 = M::ld_rlx(&s->pad[0]);
-    wl = M::ld_rlx(&s->bytes);
     if (a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
       if (a.err_word) ScopeSys::st_rlx(a.err_word, ERRW_WAIT_SLOT);
-      return -1;
+      return false;
     }
+    w0 = M::ld_rlx(&s->addr);
+    w1 = M::ld_rlx(&s->pad[0]);
+    w2 = M::ld_rlx(&s->pad[1]);
+    wl = M::ld_rlx(&s->bytes);
+    da = M::ld_rlx(&s->done_addr);
+    dv = M::ld_rlx(&s->done_val);
   }
 }
 
 // Complete my receive from an LL send descriptor (lane 0; the descriptor is
 // mine: taken by CAS, or never contended): payload and status, my post slot
 // consumed (and my posted descriptor retracted if I had posted one), my
-// completion word, then the sender's free-mirror (it may reuse its slot).
+// completion word, then the sender's free-mirror (it may reuse its slot) and
+// its completion word.
 template <bool SYS>
-__device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const uint32_t w[4],
-                            uint64_t len, bool posted) {
+__device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const LLMsg& m, bool posted) {
   using M = Scope<SYS>;
-  const uint64_t n = umin(len, a.bytes);  // truncation: endpoint.cpp:17
-  for (uint64_t i = 0; i < n; ++i) a.buf[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+  const uint64_t n = umin(m.len, a.bytes);  // truncation: endpoint.cpp:17
+  for (uint64_t i = 0; i < n; ++i) a.buf[i] = (uint8_t)(m.w[i >> 2] >> (8 * (i & 3)));
   if (a.my_done) {
     uint8_t* d = reinterpret_cast<uint8_t*>(a.my_done);
-    ScopeGpu::st_rlx(reinterpret_cast<uint64_t*>(d + kStatusOff), n | (len > a.bytes ? kTruncBit : 0));
+    ScopeGpu::st_rlx(reinterpret_cast<uint64_t*>(d + kStatusOff), n | (m.len > a.bytes ? kTruncBit : 0));
     ScopeGpu::st_rlx(reinterpret_cast<uint64_t*>(d + 2 * kStatusOff),
                      ((uint64_t)(a.peer & 0xffffff) << 40) | (((uint64_t)(a.sidx + 2) & 0xff) << 32) |
                          (uint32_t)(sn.key >> 32));
@@ -946,6 +965,7 @@ __device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const uint3
   // synchronisation), so device scope orders the payload and status before it
   if (a.my_done) ScopeGpu::st_rel(a.my_done, a.my_gen);
   M::st_rlx(&a.scan_mirror[j], (sn.state >> 8) + 1);
+  if (m.sdone) M::st_rlx(m.sdone, m.sgen);
 }
 
 // A blocking receive (static matching) never posts a descriptor: no sender
@@ -986,14 +1006,14 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   // receive polls instead of posting
   const bool ll_send = a.ll && !a.is_recv && a.bytes <= kLLBytes && a.mode != MODE_STAGED;
   const bool poll_recv = a.ll && a.is_recv && a.blocking;
-  __shared__ uint32_t s_pay[4];  // an LL send's payload (lane 0)
+  __shared__ uint32_t s_pay[3];  // an LL send's payload (lane 0)
   TraceRec* const trace = TINY ? nullptr : a.trace;
   if (warp == 0) {
     // the free-mirror of my post slot, loaded alongside the ring scan (one
     // round trip instead of two in steady state, pseq >= R); an LL send's
     // payload loads are in flight with them too
     uint64_t pre = 0;
-    uint32_t pay[4] = {0, 0, 0, 0};
+    uint32_t pay[3] = {0, 0, 0};
     if (lane == 0 && a.pseq >= (uint64_t)a.R)
       pre = ll_send ? M::ld_rlx(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)])
                     : M::ld_acq(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)]);
@@ -1023,10 +1043,9 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
           if (!dc.stage_ptr) s_phase = 3;
         } else if (wait_post_slot<SYS>(a, pre)) {
           if (ll_send) {
-            // payload captured: my Isend is complete; the Dekker fence and
-            // rescan follow the post (off the receiver's critical path)
+            // the Dekker fence and rescan follow the post (off the
+            // receiver's critical path)
             ll_post<SYS>(a, pay);
-            if (a.my_done) ScopeGpu::st_rlx(a.my_done, a.my_gen);
             M::fence_sc();
             s_phase = 2;
           } else if (a.mode == MODE_EAGER) {
@@ -1045,9 +1064,8 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
             // watchdog: leave the send descriptor for nobody
           } else if (sn.state & ST_LL) {
             M::st_rlx(&a.scan_ring[j].state, st_word(sn.state >> 8, ST_TAKEN));
-            uint32_t w[4];
-            const int64_t len = ll_read<SYS>(&a.scan_ring[j], sn, w, a);
-            if (len >= 0) ll_complete<SYS>(a, j, sn, w, (uint64_t)len, false);
+            LLMsg m;
+            if (ll_read<SYS>(&a.scan_ring[j], sn, m, a)) ll_complete<SYS>(a, j, sn, m, false);
           } else {
             M::st_rlx(&a.scan_ring[j].state, st_word(sn.state >> 8, ST_TAKEN));
             recv_win(a, dc, j, sn, false);
@@ -1061,14 +1079,15 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
         s_pay[0] = pay[0];
         s_pay[1] = pay[1];
         s_pay[2] = pay[2];
-        s_pay[3] = pay[3];
       }
     }
     __syncwarp();
     if (!TINY) {
-      if (s_phase == 3 && !claim_stage_slot<SYS>(a, dc) && lane == 0) dc.action = ACT_NONE;
+      const int ph = s_phase;  // every lane reads before lane 0 may rewrite it
       __syncwarp();
-      if (lane == 0 && s_phase == 3) s_phase = 0;
+      if (ph == 3 && !claim_stage_slot<SYS>(a, dc) && lane == 0) dc.action = ACT_NONE;
+      __syncwarp();
+      if (lane == 0 && ph == 3) s_phase = 0;
     }
   }
   __syncthreads();
@@ -1088,7 +1107,8 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     // send descriptor's state word (second arriver copies).
     Snap sn;
     int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
-    if (lane == 0 && j >= 0) {
+    if (lane == 0) {
+     if (j >= 0) {
       if (!a.is_recv) {
         const int slot = (int)(a.pseq % (uint64_t)a.R);
         uint64_t want = st_word(a.pseq, ll_send ? (ST_POSTED | ST_LL) : ST_POSTED);
@@ -1098,16 +1118,17 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
         const uint64_t want = sn.state;
         if (M::cas(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN)) == want) {
           if (sn.state & ST_LL) {
-            uint32_t w[4];
-            const int64_t len = ll_read<SYS>(&a.scan_ring[j], sn, w, a);
-            if (len >= 0) ll_complete<SYS>(a, j, sn, w, (uint64_t)len, true);
+            LLMsg m;
+            if (ll_read<SYS>(&a.scan_ring[j], sn, m, a)) ll_complete<SYS>(a, j, sn, m, true);
           } else {
             recv_win(a, dc, j, sn, true);
           }
         }
       }
+     }
+     // (lane 0 only: the other lanes never touch the shared decision)
+     if (dc.action == ACT_NONE && a.is_recv && a.blocking) dc.wait_own = 1;
     }
-    if (lane == 0 && dc.action == ACT_NONE && a.is_recv && a.blocking) dc.wait_own = 1;
     __syncwarp();
   }
   __syncthreads();
@@ -1483,7 +1504,7 @@ __global__ void __launch_bounds__(kThreads) k_batch_tiny(const BatchArgs<NOPS, N
   __shared__ Decision s_dc;
   __shared__ P2PArgs a;
   pdl_wait();
-  pdl_trigger();  // no grouped copy behind me: the next head kernel may park
+  if (b.early) pdl_trigger();  // small grid, no grouped copy behind me: the next head kernel may park
   if ((int)blockIdx.x < b.n) {
     if (threadIdx.x == 0) load_op(b.ops[blockIdx.x], b.spin_limit_ns, a);
     __syncthreads();
@@ -2115,7 +2136,11 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   for (int i = 0; i < n; ++i) b.ops[i].early = tiles <= kEarlyTriggerTiles;
   if (g.m == 0) {  // inline operations only: one launch, the wait included
     const int grid = head_ctas + (nwait > 0 ? 1 : 0);
-    b.early = 1;
+    // let the stream's next head kernel launch (and park at
+    // griddepcontrol.wait) early only behind a small grid: a parked
+    // window-sized grid would hold SMs the peers' operations need while this
+    // one's wait spins
+    b.early = grid <= kEarlyHeadCtas ? 1 : 0;
     bool tiny = !arrive && b.n_static == n;
     for (int i = 0; i < n && tiny; ++i) {
       const BatchOp& o = b.ops[i];

@@ -406,11 +406,12 @@ int check_p2p_args(const mpix_comm_s* c, int count, int peer, int tag, bool recv
 cudaStream_t conv_stream(mpix_comm_s* c) {
   if (c->graph && c->cu) return c->cu;
   RankState& rs = rank_of(c->rank);
-  // MPIX_HOST_EXCLUSION=global: one internal stream per rank (the single
-  // progress context of the reference's global lock regime); otherwise one
-  // per communicator, so threads on different comms never queue behind each
-  // other's blocking operations (the per-VCI regime)
-  if (g_world->cfg.excl == 0) return rs.p2p;
+  // One internal stream per communicator (every host exclusion regime: the
+  // regimes differ in host locking only): threads on different comms never
+  // queue behind each other's blocking operations — with one stream per
+  // rank, a blocking MPI_Recv kernel of one thread would stall the operations
+  // its peer is waiting for (a cross-rank deadlock the reference's global
+  // progress does not have)
   std::call_once(c->conv_once, [&] {
     {
       std::lock_guard<std::mutex> pl(rs.conv_pool_mu);

@@ -56,6 +56,7 @@ def body(r):
             bad.append(("blocking", r, n))
     x = torch.full((4099,), float(r + 1), device=0)
     y = torch.zeros(4099, device=0)
+    torch.cuda.synchronize()  # torch fills on its own stream; ours does not wait for it
     if P == 1 or mpix.device_coresident(0):
         c.allreduce_enqueue(x, y, 4099, mpix.MPI_FLOAT)
         s.synchronize()
@@ -66,5 +67,5 @@ def body(r):
 
 w.run_ranks(body)
 w.finalize()
-print("sanitize cases:", "ok" if not bad else bad)
+print("sanitize cases:", "ok" if not bad else bad, "lib", mpix.LIB_PATH)
 sys.exit(1 if bad else 0)
