@@ -686,7 +686,18 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
     a.opid = op;
   }
   if (!c->batch && !how.conventional) c->batch = &batch_of(s, rs.device);
-  StreamBatch& b = how.conventional ? batch_of(s, rs.device) : *c->batch;
+  // the batch of a conventional operation's stream: the comm's internal
+  // stream's is looked up once (no process-wide lock per operation)
+  StreamBatch* bp = c->batch;
+  if (how.conventional) {
+    if (s == c->conv_cu) {
+      if (!c->conv_batch) c->conv_batch = &batch_of(s, rs.device);
+      bp = c->conv_batch;
+    } else {
+      bp = &batch_of(s, rs.device);
+    }
+  }
+  StreamBatch& b = *bp;
   std::lock_guard<std::mutex> lk(b.mu);
   if ((w.cfg.batch || gr) && !a.trace) {
     // Join the stream's batch; a blocking operation closes it (it must have
@@ -778,7 +789,10 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
     }
     // a blocking operation closes the batch; conventional operations are
     // launched at once
-    if (blocking || how.conventional || !w.cfg.batch) {
+    // conventional operations are held like enqueued ones (MPIX_CONV_BATCH,
+    // default on): launched by the thread's next ordering call on that
+    // stream (a blocking operation or a wait) or, failing one, by the flusher
+    if (blocking || (how.conventional && !w.cfg.conv_batch) || !w.cfg.batch) {
       if (flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
     } else if (!b.ops.empty()) {
       batch_note_held(b);  // the flusher launches it if no ordering call comes

@@ -47,6 +47,7 @@ struct Config {
   uint64_t stage_chunk = 4ull << 20; // MPIX_STAGE_CHUNK: bytes per arena slot
   bool graph = false;                // MPIX_GRAPH=1: every enqueue comm is graph-capturable
   bool ll = true;                    // MPIX_LL=0: no flag-in-data sends, blocking receives post
+  bool conv_batch = true;            // MPIX_CONV_BATCH=0: conventional p2p launches at once
   // MPIX_HOST_EXCLUSION (the reference's lock regimes, bench.hpp:13-16,
   // fabric.hpp:17-61): 0 "global" — one process-wide lock around every p2p
   // call and one internal stream per rank for conventional operations;
@@ -85,6 +86,7 @@ struct Config {
     c.graph = geti("MPIX_GRAPH", 0) != 0;
     c.flush_ns = geti("MPIX_FLUSH_US", 100) * 1000ull;
     c.ll = geti("MPIX_LL", 1) != 0;
+    c.conv_batch = geti("MPIX_CONV_BATCH", 1) != 0;
     if (const char* x = std::getenv("MPIX_HOST_EXCLUSION")) {
       const std::string v(x);
       c.excl = (v == "global" || v == "0") ? 0 : (v == "serial" || v == "stream" || v == "2") ? 2 : 1;
@@ -335,6 +337,7 @@ struct mpix_comm_s {
   // Its conventional operations' internal stream (host exclusion comm /
   // serial), created on first use; and the owner trap of the serial regime.
   cudaStream_t conv_cu = nullptr;
+  mpix::StreamBatch* conv_batch = nullptr;  // its StreamBatch (looked up once)
   std::once_flag conv_once;
   std::atomic<uint64_t> owner{0};
 };
