@@ -106,6 +106,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // Spin until *p >= target. Returns false on watchdog expiry after recording
 // `code` in the rank's host-mapped error word (the kernel then exits rather
 // than hanging the GPU).
+// Polls with relaxed loads (an acquire load invalidates the SM's L1 on every
+// poll — the stacks and cached reads of every CTA on the SM with it) and
+// orders what follows with one acquire load once the value is there.
 template <bool SYS>
 __device__ __noinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_t* err_word,
                                      uint64_t limit_ns, uint64_t code) {
@@ -113,7 +116,7 @@ __device__ __noinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_
   if (M::ld_acq(p) >= target) return true;
   uint64_t t0 = limit_ns ? globaltimer() : 0;
   unsigned ns = 32;
-  while (M::ld_acq(p) < target) {
+  while (M::ld_rlx(p) < target) {
     __nanosleep(ns);
     if (ns < 64) ns <<= 1;  // short cap: the poll's own round trip dominates (256: +0.3-0.5 us latency)
     if (limit_ns && globaltimer() - t0 > limit_ns) {
@@ -121,6 +124,7 @@ __device__ __noinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_
       return false;
     }
   }
+  (void)M::ld_acq(p);  // acquire: what the writer released is visible from here
   return true;
 }
 
@@ -140,7 +144,7 @@ constexpr int kCopyUnroll = 4;  // 64-KiB tiles (tools/copyshape.cu)
 constexpr uint64_t kTileVec = (uint64_t)kCopyThreads * kCopyUnroll;  // 16-B vectors per tile
 
 // Whole-CTA copy of n bytes (k_proto inline path and the rare staged push).
-__device__ __noinline__ void cta_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
+__device__ void cta_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
   if (n == 0 || dst == src) return;
   const uint64_t t = threadIdx.x, nt = blockDim.x;
   uint64_t mis = (uint64_t)dst & 15;
@@ -218,11 +222,10 @@ __device__ __forceinline__ void ld_pair(const SlotDesc* s, uint64_t& st, uint64_
 
 constexpr int kMaxScanPerLane = 8;  // R <= 256
 
-// Not inlined: the first scan, the poll loop and the rescan share one copy
-// of this code, so a rescan runs from a warm instruction cache (a kernel
-// launch on a cold SM otherwise waits on instruction fetch).
+// Inlined: the snapshot stays in registers (a call would pass it through
+// the stack, i.e. local memory, which every acquire's L1 invalidation evicts).
 template <bool SYS>
-__device__ __noinline__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
+__device__ __forceinline__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap* out) {
   using M = Scope<SYS>;
   const int lane = threadIdx.x & 31;
   // Issue every (state, key) load of this lane before looking at any.
@@ -248,7 +251,13 @@ __device__ __noinline__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Snap*
       Snap sn = {};
       if (lane == src) {
         SlotDesc* s = &ring[k * 32 + lane];
-        sn.state = M::ld_acq(&s->state);
+        // an LL post validates its own words (flags), so the scan's relaxed
+        // state suffices; any other post's fields are read behind an acquire
+        uint64_t stk = 0;
+#pragma unroll
+        for (int kk = 0; kk < kMaxScanPerLane; ++kk)
+          if (kk == k) stk = st[kk];
+        sn.state = (stk & ST_LL) ? stk : M::ld_acq(&s->state);
         sn.key = M::ld_rlx(&s->key);
         sn.addr = M::ld_rlx(&s->addr);
         sn.bytes = M::ld_rlx(&s->bytes);
@@ -717,7 +726,7 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
       got = spin_ge<SYS>(D.next_rpost, a.pseq, a.err_word, a.spin_limit_ns, ERRW_WAIT_SLOT);
       if (got) {
         const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
-        while ((M::ld_acq(&D.pq[qslot].state) & 0xff) == ST_POSTED) {
+        while ((M::ld_rlx(&D.pq[qslot].state) & 0xff) == ST_POSTED) {
           __nanosleep(128);
           if (a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
             if (a.err_word) ScopeSys::st_rlx(a.err_word, ERRW_WAIT_SLOT);
@@ -1014,9 +1023,9 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     // payload loads are in flight with them too
     uint64_t pre = 0;
     uint32_t pay[3] = {0, 0, 0};
-    if (lane == 0 && a.pseq >= (uint64_t)a.R)
-      pre = ll_send ? M::ld_rlx(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)])
-                    : M::ld_acq(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)]);
+    // (relaxed: the slot's previous occupant is done with it once its mirror
+    // moved; nothing read here depends on data the mirror publishes)
+    if (lane == 0 && a.pseq >= (uint64_t)a.R) pre = M::ld_rlx(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)]);
     if (lane == 0 && ll_send) ll_load(a.buf, a.bytes, pay);
     Snap sn;
     int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
