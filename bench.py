@@ -1036,6 +1036,55 @@ def extras_multirank(args, mpix, torch):
     w.finalize()
     out["pingpong_2ranks"] = {"gpus": len({ctx[0][2], ctx[1][2]}), **pp}
 
+    log('unpaired exchange: 2 ranks, 256 MiB each way, device handshake')
+    # The headline's self-messages are host-paired (no descriptors, DESIGN.md
+    # §3); this is the cross-rank device handshake (post, scan, second
+    # arriver's copy grid, completion) on the same 256 MiB, both directions at
+    # once: Isend + Irecv + Waitall_enqueue per rank and step.
+    w, ctx = world(2)
+    S = 256 << 20
+    xs = [torch.empty(S, dtype=torch.uint8, device=ctx[r][2]) for r in range(2)]
+    xd = [torch.empty(S, dtype=torch.uint8, device=ctx[r][2]) for r in range(2)]
+    for r in range(2):
+        xs[r].fill_(r + 1)
+    torch.cuda.synchronize()
+
+    def xstep(r):
+        c = ctx[r][1]
+        q1 = c.irecv_enqueue(xd[r], S, mpix.MPI_BYTE, 1 - r, 9)
+        q2 = c.isend_enqueue(xs[r], S, mpix.MPI_BYTE, 1 - r, 9)
+        mpix.waitall_enqueue([q1, q2])
+
+    for _ in range(3):
+        w.run_ranks(xstep)
+    sync_all(ctx)
+    K = 10
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
+    mpix.testing.copy_timing(True)
+    for r in range(2):
+        ev[r][0].record(ctx[r][0])
+    for _ in range(K):
+        w.run_ranks(xstep)
+    for r in range(2):
+        ev[r][1].record(ctx[r][0])
+    sync_all(ctx)
+    mpix.testing.copy_timing(False)
+    cms, cn, cb = mpix.testing.copy_timing_read()
+    t = max(ev[r][0].elapsed_time(ev[r][1]) for r in range(2)) / 1e3 / K
+    ok = bool(int(xd[0][0]) == 2 and int(xd[1][-1]) == 1)
+    gpus = len({ctx[0][2], ctx[1][2]})
+    ach = cb / (cms / 1e3) / 1e9 if cms > 0 else None
+    out["exchange_256MiB_2ranks_unpaired"] = {
+        "gpus": gpus, "step_us": t * 1e6, "GBps_per_direction": S / t / 1e9,
+        "GBps_both": 2 * S / t / 1e9,
+        "copy_grids": {"timed": cn, "bytes": cb, "ms": cms, "achieved_GBps": ach,
+                       "note": "the grids that copied (second arrivers'); on one GPU each copy moves "
+                               "2 x S of HBM traffic"},
+        "hbm_frac_step": (4 * S / t / 1e9) / peaks().get("hbm_gbs", 6650.0) if gpus == 1 else None,
+        "check": ok}
+    del xs, xd
+    w.finalize()
+
     log('cfg3: Allreduce_enqueue 256 MiB fp32 and bf16 at P = 1, 2, 4,')
     # cfg3: Allreduce_enqueue 256 MiB fp32 and bf16 at P = 1, 2, 4, 8
     ar = {}
