@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <utility>
 
 #include "mpix_internal.h"
@@ -129,6 +130,13 @@ __device__ __noinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_
 }
 
 __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// Ring slot of a pair sequence. A 64-bit modulo is a software division
+// (a call of ~150 cycles, and the handshake needs several per operation);
+// the default ring sizes are powers of two, so it is a mask.
+__device__ __forceinline__ int ring_slot(uint64_t pseq, int R) {
+  return (R & (R - 1)) == 0 ? (int)(pseq & (uint64_t)(R - 1)) : (int)(pseq % (uint64_t)R);
+}
 
 // Phase stamps (globaltimer ns): one time base for the kernels of every
 // rank, so two ranks' phases can be lined up.
@@ -347,7 +355,7 @@ template <bool SYS>
 __device__ void post_desc(const P2PArgs& a, uint64_t addr, uint64_t bytes, uint64_t done_addr,
                           uint64_t done_val, bool others_wrote) {
   using M = Scope<SYS>;
-  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  const int slot = ring_slot(a.pseq, a.R);
   SlotDesc* d = &a.post_ring[slot];
   M::st_rlx(&d->key, a.key);
   M::st_rlx(&d->addr, addr);
@@ -364,7 +372,7 @@ __device__ void post_desc(const P2PArgs& a, uint64_t addr, uint64_t bytes, uint6
 
 template <bool SYS>
 __device__ bool wait_post_slot(const P2PArgs& a, uint64_t prefetched = 0) {
-  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  const int slot = ring_slot(a.pseq, a.R);
   uint64_t need = a.pseq >= (uint64_t)a.R ? a.pseq - a.R + 1 : 0;
   if (need == 0 || prefetched >= need) return true;
   return spin_ge<SYS>(&a.post_mirror[slot], need, a.err_word, a.spin_limit_ns, ERRW_WAIT_SLOT);
@@ -374,7 +382,7 @@ __device__ bool wait_post_slot(const P2PArgs& a, uint64_t prefetched = 0) {
 __device__ void send_win(const P2PArgs& a, Decision& dc, int j, const Snap& r, bool posted,
                          const uint8_t* src) {
   const uint64_t rpseq = r.state >> 8;
-  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  const int slot = ring_slot(a.pseq, a.R);
   dc.action = ACT_COPY;
   dc.src = (uint64_t)src;
   dc.dst = r.addr;
@@ -396,7 +404,7 @@ __device__ void send_win(const P2PArgs& a, Decision& dc, int j, const Snap& r, b
 // Receiver wins (send descriptor already TAKEN by me): pull.
 __device__ void recv_win(const P2PArgs& a, Decision& dc, int j, const Snap& s, bool posted) {
   const uint64_t spseq = s.state >> 8;
-  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  const int slot = ring_slot(a.pseq, a.R);
   dc.action = ACT_COPY;
   dc.src = s.addr;
   dc.dst = (uint64_t)a.buf;
@@ -570,7 +578,7 @@ __device__ int dyn_scan_sends(const P2PArgs& a, uint8_t* my_base, const RegionLa
   }
   warp_argmin(best, best_idx);
   if (best == ~0ull) return -1;
-  *slot_out = best_idx % a.R;
+  *slot_out = best_idx % a.R;  // (32-bit, once per dynamic scan)
   return best_idx / a.R;
 }
 
@@ -621,7 +629,7 @@ __device__ void dyn_send_take(const P2PArgs& a, Decision& dc, SlotDesc* pq, int 
   const uint64_t done_addr = M::ld_rlx(&e->done_addr), done_val = M::ld_rlx(&e->done_val);
   M::st_rlx(&e->state, st_word(st >> 8, ST_TAKEN));
   M::st_rlx(&D.next_spost[a.me], a.pseq + 1);
-  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  const int slot = ring_slot(a.pseq, a.R);
   dc.action = ACT_COPY;
   dc.src = (uint64_t)src;
   dc.dst = addr;
@@ -642,7 +650,7 @@ template <bool SYS>
 __device__ void dyn_send_post(const P2PArgs& a, const Dom& D, uint64_t addr, uint64_t done_addr,
                               uint64_t done_val, bool eager) {
   using M = Scope<SYS>;
-  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  const int slot = ring_slot(a.pseq, a.R);
   SlotDesc* d = &a.post_ring[slot];
   const uint64_t arr = M::ld_rlx(D.arrival);
   M::st_rlx(D.arrival, arr + 1);
@@ -685,7 +693,7 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
     }
     __syncthreads();
     if (s_stage == 1) {  // eager: payload into my slot of the receiver's eager ring first
-      const int slot = (int)(a.pseq % (uint64_t)a.R);
+      const int slot = ring_slot(a.pseq, a.R);
       cta_copy(a.eager_ring + (uint64_t)slot * a.E, a.buf, a.bytes);
       __syncthreads();  // published by the unlock's release (after the CTA barrier)
     }
@@ -701,7 +709,7 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
           } else if (a.mode == MODE_STAGED) {
             dc.action = ACT_STAGE;  // ticket kept until the staged copy is published
           } else {
-            const int slot = (int)(a.pseq % (uint64_t)a.R);
+            const int slot = ring_slot(a.pseq, a.R);
             const uint64_t addr = a.mode == MODE_EAGER ? (uint64_t)(a.eager_ring + (uint64_t)slot * a.E)
                                                        : (uint64_t)a.buf;
             if (a.mode == MODE_EAGER) dyn_send_post<SYS>(a, D, addr, 0, 0, true);
@@ -719,7 +727,7 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
     }
   } else if (warp == 0) {
     const Dom D = dom_at(my_base, L);
-    const int qslot = (int)(a.pseq % (uint64_t)a.R);
+    const int qslot = ring_slot(a.pseq, a.R);
     int got = 0;
     if (lane == 0) {
       // my receive ticket, my PQ slot no longer POSTED, then the lock
@@ -847,8 +855,8 @@ __device__ void decide_paired(const P2PArgs& a, Decision& dc) {
     dc.stage_ptr = nullptr;
     dc.stage_done = nullptr;
     dc.stage_gen = 0;
-    const int rslot = (int)(a.pseq % (uint64_t)a.R);
-    const int sslot = (int)(a.pair_pseq % (uint64_t)a.R);
+    const int rslot = ring_slot(a.pseq, a.R);
+    const int sslot = ring_slot(a.pair_pseq, a.R);
     const uint64_t rneed = a.pseq >= (uint64_t)a.R ? a.pseq - a.R + 1 : 0;
     const uint64_t sneed = a.pair_pseq >= (uint64_t)a.R ? a.pair_pseq - a.R + 1 : 0;
     if ((rneed == 0 || spin_ge<SYS>(&a.post_mirror[rslot], rneed, a.err_word, a.spin_limit_ns,
@@ -876,8 +884,19 @@ __device__ void decide_paired(const P2PArgs& a, Decision& dc) {
 // flight together (no read past the user's buffer).
 __device__ __forceinline__ void ll_load(const uint8_t* src, uint64_t n, uint32_t w[3]) {
   uint8_t b[kLLBytes];
+  if (n == 0) {
 #pragma unroll
-  for (int i = 0; i < (int)kLLBytes; ++i) b[i] = i < (int)n ? src[i] : 0;
+    for (int i = 0; i < (int)kLLBytes; ++i) b[i] = 0;
+  } else {
+    // branch-free: every load is issued before any result is used (a
+    // conditional load per byte compiled to a chain of dependent round
+    // trips); bytes past n re-read the last byte and are masked below
+    uint8_t v[kLLBytes];
+#pragma unroll
+    for (int i = 0; i < (int)kLLBytes; ++i) v[i] = __ldcg(src + (i < (int)n ? i : (int)n - 1));
+#pragma unroll
+    for (int i = 0; i < (int)kLLBytes; ++i) b[i] = i < (int)n ? v[i] : 0;
+  }
 #pragma unroll
   for (int k = 0; k < 3; ++k)
     w[k] = (uint32_t)b[4 * k] | ((uint32_t)b[4 * k + 1] << 8) | ((uint32_t)b[4 * k + 2] << 16) |
@@ -894,7 +913,7 @@ __device__ __forceinline__ void ll_load(const uint8_t* src, uint64_t n, uint32_t
 template <bool SYS>
 __device__ void ll_post(const P2PArgs& a, const uint32_t w[3]) {
   using M = Scope<SYS>;
-  SlotDesc* d = &a.post_ring[(int)(a.pseq % (uint64_t)a.R)];
+  SlotDesc* d = &a.post_ring[ring_slot(a.pseq, a.R)];
   const uint32_t f = ll_flag(a.pseq);
   const uint64_t chk = ll_chk(a.pseq);
   M::st_rlx(&d->addr, ll_word(w[0], f));
@@ -967,7 +986,7 @@ __device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const LLMsg
                      ((uint64_t)(a.peer & 0xffffff) << 40) | (((uint64_t)(a.sidx + 2) & 0xff) << 32) |
                          (uint32_t)(sn.key >> 32));
   }
-  const int slot = (int)(a.pseq % (uint64_t)a.R);
+  const int slot = ring_slot(a.pseq, a.R);
   if (posted) M::st_rlx(&a.post_ring[slot].state, st_word(a.pseq, ST_FREE));  // retract
   ScopeGpu::st_rlx(&a.post_mirror[slot], a.pseq + 1);  // consumed either way (local)
   // my completion: read only by this rank (its waits, the host after a
@@ -1025,7 +1044,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     uint32_t pay[3] = {0, 0, 0};
     // (relaxed: the slot's previous occupant is done with it once its mirror
     // moved; nothing read here depends on data the mirror publishes)
-    if (lane == 0 && a.pseq >= (uint64_t)a.R) pre = M::ld_rlx(&a.post_mirror[(int)(a.pseq % (uint64_t)a.R)]);
+    if (lane == 0 && a.pseq >= (uint64_t)a.R) pre = M::ld_rlx(&a.post_mirror[ring_slot(a.pseq, a.R)]);
     if (lane == 0 && ll_send) ll_load(a.buf, a.bytes, pay);
     Snap sn;
     int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
@@ -1104,7 +1123,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   int phase = s_phase;
   if (phase == 1) {
     // Eager: payload into the receiver's eager slot (peer stores).
-    const int slot = (int)(a.pseq % (uint64_t)a.R);
+    const int slot = ring_slot(a.pseq, a.R);
     cta_copy(a.eager_ring + (uint64_t)slot * a.E, a.buf, a.bytes);
     __syncthreads();
     if (threadIdx.x == 0)
@@ -1119,7 +1138,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     if (lane == 0) {
      if (j >= 0) {
       if (!a.is_recv) {
-        const int slot = (int)(a.pseq % (uint64_t)a.R);
+        const int slot = ring_slot(a.pseq, a.R);
         uint64_t want = st_word(a.pseq, ll_send ? (ST_POSTED | ST_LL) : ST_POSTED);
         if (M::cas(&a.post_ring[slot].state, want, st_word(a.pseq, ST_TAKEN)) == want)
           send_win(a, dc, j, sn, true, ll_send ? reinterpret_cast<const uint8_t*>(s_pay) : a.buf);
@@ -1163,7 +1182,7 @@ __device__ void stage_publish(const P2PArgs& a, Decision& dc) {
       Snap sn;
       int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
       if (threadIdx.x == 0 && j >= 0) {
-        const int slot = (int)(a.pseq % (uint64_t)a.R);
+        const int slot = ring_slot(a.pseq, a.R);
         uint64_t want = st_word(a.pseq, ST_POSTED);
         if (M::cas(&a.post_ring[slot].state, want, st_word(a.pseq, ST_TAKEN)) == want) {
           send_win(a, dc, j, sn, true, dc.stage_ptr);
@@ -2040,6 +2059,15 @@ __global__ void __launch_bounds__(32) k_ar_exit(const ARArgs a) {
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStream_t s,
                               Args&&... args) {
+  // MPIX_PDL=0: plain launches (A/B of programmatic dependent launch)
+  static const bool pdl = [] {
+    const char* v = std::getenv("MPIX_PDL");
+    return !(v && v[0] == '0');
+  }();
+  if (!pdl) {
+    k<<<grid, block, 0, s>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);

@@ -456,6 +456,311 @@ __global__ void k_sleep(uint64_t* out) {
   }
 }
 
+// The ring scan inside a 512-thread CTA (warp 0 scans, the other warps wait
+// at a barrier) over a pool allocation, as the handshake kernels do; cycles.
+__global__ void __launch_bounds__(512) k_scan512(const uint64_t* ring, uint64_t* out, int iters) {
+  const int lane = threadIdx.x & 31;
+  __shared__ uint64_t s_acc;
+  uint64_t cyc = 0;
+  for (int it = 0; it < iters; ++it) {
+    if (threadIdx.x < 32) {
+      long long c0 = clock64();
+      uint64_t st[4], ky[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(st[k]), "=l"(ky[k]) : "l"(ring + 8 * (k * 32 + lane)) : "memory");
+      unsigned m = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) m |= __ballot_sync(0xffffffffu, st[k] == 12345 && ky[k] == 7);
+      long long c1 = clock64();
+      cyc += (uint64_t)(c1 - c0) + (m & 0);
+      if (lane == 0) s_acc = m;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[50] = cyc / iters;
+    out[51] = s_acc;
+  }
+}
+
+// Instruction-cache residency across launches: two kernels of ~3 K branchy
+// instructions each (different code), launched back to back on one SM; the
+// first pass of each launch pays for whatever instruction lines are cold.
+template <unsigned V>
+__device__ __noinline__ uint32_t branchy_v(const uint8_t* order, uint32_t x) {
+  for (int i = 0; i < 256; ++i) {
+    switch (order[i]) {
+      case 0: x = x * 3u + V + 0u; x ^= x >> 1; x += 17u; x ^= x << 1; x = x * 1u + 0u; break;
+      case 1: x = x * 5u + V + 7919u; x ^= x >> 2; x += 48u; x ^= x << 2; x = x * 5u + 1u; break;
+      case 2: x = x * 7u + V + 15838u; x ^= x >> 3; x += 79u; x ^= x << 3; x = x * 9u + 2u; break;
+      case 3: x = x * 9u + V + 23757u; x ^= x >> 4; x += 110u; x ^= x << 4; x = x * 13u + 3u; break;
+      case 4: x = x * 11u + V + 31676u; x ^= x >> 5; x += 141u; x ^= x << 5; x = x * 17u + 4u; break;
+      case 5: x = x * 13u + V + 39595u; x ^= x >> 6; x += 172u; x ^= x << 6; x = x * 21u + 5u; break;
+      case 6: x = x * 15u + V + 47514u; x ^= x >> 7; x += 203u; x ^= x << 7; x = x * 25u + 6u; break;
+      case 7: x = x * 17u + V + 55433u; x ^= x >> 8; x += 234u; x ^= x << 1; x = x * 29u + 7u; break;
+      case 8: x = x * 19u + V + 63352u; x ^= x >> 9; x += 265u; x ^= x << 2; x = x * 33u + 8u; break;
+      case 9: x = x * 21u + V + 71271u; x ^= x >> 10; x += 296u; x ^= x << 3; x = x * 37u + 9u; break;
+      case 10: x = x * 23u + V + 79190u; x ^= x >> 11; x += 327u; x ^= x << 4; x = x * 41u + 10u; break;
+      case 11: x = x * 25u + V + 87109u; x ^= x >> 12; x += 358u; x ^= x << 5; x = x * 45u + 11u; break;
+      case 12: x = x * 27u + V + 95028u; x ^= x >> 13; x += 389u; x ^= x << 6; x = x * 49u + 12u; break;
+      case 13: x = x * 29u + V + 102947u; x ^= x >> 1; x += 420u; x ^= x << 7; x = x * 53u + 13u; break;
+      case 14: x = x * 31u + V + 110866u; x ^= x >> 2; x += 451u; x ^= x << 1; x = x * 57u + 14u; break;
+      case 15: x = x * 33u + V + 118785u; x ^= x >> 3; x += 482u; x ^= x << 2; x = x * 61u + 15u; break;
+      case 16: x = x * 35u + V + 126704u; x ^= x >> 4; x += 513u; x ^= x << 3; x = x * 65u + 16u; break;
+      case 17: x = x * 37u + V + 134623u; x ^= x >> 5; x += 544u; x ^= x << 4; x = x * 69u + 17u; break;
+      case 18: x = x * 39u + V + 142542u; x ^= x >> 6; x += 575u; x ^= x << 5; x = x * 73u + 18u; break;
+      case 19: x = x * 41u + V + 150461u; x ^= x >> 7; x += 606u; x ^= x << 6; x = x * 77u + 19u; break;
+      case 20: x = x * 43u + V + 158380u; x ^= x >> 8; x += 637u; x ^= x << 7; x = x * 81u + 20u; break;
+      case 21: x = x * 45u + V + 166299u; x ^= x >> 9; x += 668u; x ^= x << 1; x = x * 85u + 21u; break;
+      case 22: x = x * 47u + V + 174218u; x ^= x >> 10; x += 699u; x ^= x << 2; x = x * 89u + 22u; break;
+      case 23: x = x * 49u + V + 182137u; x ^= x >> 11; x += 730u; x ^= x << 3; x = x * 93u + 23u; break;
+      case 24: x = x * 51u + V + 190056u; x ^= x >> 12; x += 761u; x ^= x << 4; x = x * 97u + 24u; break;
+      case 25: x = x * 53u + V + 197975u; x ^= x >> 13; x += 792u; x ^= x << 5; x = x * 101u + 25u; break;
+      case 26: x = x * 55u + V + 205894u; x ^= x >> 1; x += 823u; x ^= x << 6; x = x * 105u + 26u; break;
+      case 27: x = x * 57u + V + 213813u; x ^= x >> 2; x += 854u; x ^= x << 7; x = x * 109u + 27u; break;
+      case 28: x = x * 59u + V + 221732u; x ^= x >> 3; x += 885u; x ^= x << 1; x = x * 113u + 28u; break;
+      case 29: x = x * 61u + V + 229651u; x ^= x >> 4; x += 916u; x ^= x << 2; x = x * 117u + 29u; break;
+      case 30: x = x * 63u + V + 237570u; x ^= x >> 5; x += 947u; x ^= x << 3; x = x * 121u + 30u; break;
+      case 31: x = x * 65u + V + 245489u; x ^= x >> 6; x += 978u; x ^= x << 4; x = x * 125u + 31u; break;
+      case 32: x = x * 67u + V + 253408u; x ^= x >> 7; x += 1009u; x ^= x << 5; x = x * 129u + 32u; break;
+      case 33: x = x * 69u + V + 261327u; x ^= x >> 8; x += 1040u; x ^= x << 6; x = x * 133u + 33u; break;
+      case 34: x = x * 71u + V + 269246u; x ^= x >> 9; x += 1071u; x ^= x << 7; x = x * 137u + 34u; break;
+      case 35: x = x * 73u + V + 277165u; x ^= x >> 10; x += 1102u; x ^= x << 1; x = x * 141u + 35u; break;
+      case 36: x = x * 75u + V + 285084u; x ^= x >> 11; x += 1133u; x ^= x << 2; x = x * 145u + 36u; break;
+      case 37: x = x * 77u + V + 293003u; x ^= x >> 12; x += 1164u; x ^= x << 3; x = x * 149u + 37u; break;
+      case 38: x = x * 79u + V + 300922u; x ^= x >> 13; x += 1195u; x ^= x << 4; x = x * 153u + 38u; break;
+      case 39: x = x * 81u + V + 308841u; x ^= x >> 1; x += 1226u; x ^= x << 5; x = x * 157u + 39u; break;
+      case 40: x = x * 83u + V + 316760u; x ^= x >> 2; x += 1257u; x ^= x << 6; x = x * 161u + 40u; break;
+      case 41: x = x * 85u + V + 324679u; x ^= x >> 3; x += 1288u; x ^= x << 7; x = x * 165u + 41u; break;
+      case 42: x = x * 87u + V + 332598u; x ^= x >> 4; x += 1319u; x ^= x << 1; x = x * 169u + 42u; break;
+      case 43: x = x * 89u + V + 340517u; x ^= x >> 5; x += 1350u; x ^= x << 2; x = x * 173u + 43u; break;
+      case 44: x = x * 91u + V + 348436u; x ^= x >> 6; x += 1381u; x ^= x << 3; x = x * 177u + 44u; break;
+      case 45: x = x * 93u + V + 356355u; x ^= x >> 7; x += 1412u; x ^= x << 4; x = x * 181u + 45u; break;
+      case 46: x = x * 95u + V + 364274u; x ^= x >> 8; x += 1443u; x ^= x << 5; x = x * 185u + 46u; break;
+      case 47: x = x * 97u + V + 372193u; x ^= x >> 9; x += 1474u; x ^= x << 6; x = x * 189u + 47u; break;
+      case 48: x = x * 99u + V + 380112u; x ^= x >> 10; x += 1505u; x ^= x << 7; x = x * 193u + 48u; break;
+      case 49: x = x * 101u + V + 388031u; x ^= x >> 11; x += 1536u; x ^= x << 1; x = x * 197u + 49u; break;
+      case 50: x = x * 103u + V + 395950u; x ^= x >> 12; x += 1567u; x ^= x << 2; x = x * 201u + 50u; break;
+      case 51: x = x * 105u + V + 403869u; x ^= x >> 13; x += 1598u; x ^= x << 3; x = x * 205u + 51u; break;
+      case 52: x = x * 107u + V + 411788u; x ^= x >> 1; x += 1629u; x ^= x << 4; x = x * 209u + 52u; break;
+      case 53: x = x * 109u + V + 419707u; x ^= x >> 2; x += 1660u; x ^= x << 5; x = x * 213u + 53u; break;
+      case 54: x = x * 111u + V + 427626u; x ^= x >> 3; x += 1691u; x ^= x << 6; x = x * 217u + 54u; break;
+      case 55: x = x * 113u + V + 435545u; x ^= x >> 4; x += 1722u; x ^= x << 7; x = x * 221u + 55u; break;
+      case 56: x = x * 115u + V + 443464u; x ^= x >> 5; x += 1753u; x ^= x << 1; x = x * 225u + 56u; break;
+      case 57: x = x * 117u + V + 451383u; x ^= x >> 6; x += 1784u; x ^= x << 2; x = x * 229u + 57u; break;
+      case 58: x = x * 119u + V + 459302u; x ^= x >> 7; x += 1815u; x ^= x << 3; x = x * 233u + 58u; break;
+      case 59: x = x * 121u + V + 467221u; x ^= x >> 8; x += 1846u; x ^= x << 4; x = x * 237u + 59u; break;
+      case 60: x = x * 123u + V + 475140u; x ^= x >> 9; x += 1877u; x ^= x << 5; x = x * 241u + 60u; break;
+      case 61: x = x * 125u + V + 483059u; x ^= x >> 10; x += 1908u; x ^= x << 6; x = x * 245u + 61u; break;
+      case 62: x = x * 127u + V + 490978u; x ^= x >> 11; x += 1939u; x ^= x << 7; x = x * 249u + 62u; break;
+      case 63: x = x * 129u + V + 498897u; x ^= x >> 12; x += 1970u; x ^= x << 1; x = x * 253u + 63u; break;
+      case 64: x = x * 131u + V + 506816u; x ^= x >> 13; x += 2001u; x ^= x << 2; x = x * 257u + 64u; break;
+      case 65: x = x * 133u + V + 514735u; x ^= x >> 1; x += 2032u; x ^= x << 3; x = x * 261u + 65u; break;
+      case 66: x = x * 135u + V + 522654u; x ^= x >> 2; x += 2063u; x ^= x << 4; x = x * 265u + 66u; break;
+      case 67: x = x * 137u + V + 530573u; x ^= x >> 3; x += 2094u; x ^= x << 5; x = x * 269u + 67u; break;
+      case 68: x = x * 139u + V + 538492u; x ^= x >> 4; x += 2125u; x ^= x << 6; x = x * 273u + 68u; break;
+      case 69: x = x * 141u + V + 546411u; x ^= x >> 5; x += 2156u; x ^= x << 7; x = x * 277u + 69u; break;
+      case 70: x = x * 143u + V + 554330u; x ^= x >> 6; x += 2187u; x ^= x << 1; x = x * 281u + 70u; break;
+      case 71: x = x * 145u + V + 562249u; x ^= x >> 7; x += 2218u; x ^= x << 2; x = x * 285u + 71u; break;
+      case 72: x = x * 147u + V + 570168u; x ^= x >> 8; x += 2249u; x ^= x << 3; x = x * 289u + 72u; break;
+      case 73: x = x * 149u + V + 578087u; x ^= x >> 9; x += 2280u; x ^= x << 4; x = x * 293u + 73u; break;
+      case 74: x = x * 151u + V + 586006u; x ^= x >> 10; x += 2311u; x ^= x << 5; x = x * 297u + 74u; break;
+      case 75: x = x * 153u + V + 593925u; x ^= x >> 11; x += 2342u; x ^= x << 6; x = x * 301u + 75u; break;
+      case 76: x = x * 155u + V + 601844u; x ^= x >> 12; x += 2373u; x ^= x << 7; x = x * 305u + 76u; break;
+      case 77: x = x * 157u + V + 609763u; x ^= x >> 13; x += 2404u; x ^= x << 1; x = x * 309u + 77u; break;
+      case 78: x = x * 159u + V + 617682u; x ^= x >> 1; x += 2435u; x ^= x << 2; x = x * 313u + 78u; break;
+      case 79: x = x * 161u + V + 625601u; x ^= x >> 2; x += 2466u; x ^= x << 3; x = x * 317u + 79u; break;
+      case 80: x = x * 163u + V + 633520u; x ^= x >> 3; x += 2497u; x ^= x << 4; x = x * 321u + 80u; break;
+      case 81: x = x * 165u + V + 641439u; x ^= x >> 4; x += 2528u; x ^= x << 5; x = x * 325u + 81u; break;
+      case 82: x = x * 167u + V + 649358u; x ^= x >> 5; x += 2559u; x ^= x << 6; x = x * 329u + 82u; break;
+      case 83: x = x * 169u + V + 657277u; x ^= x >> 6; x += 2590u; x ^= x << 7; x = x * 333u + 83u; break;
+      case 84: x = x * 171u + V + 665196u; x ^= x >> 7; x += 2621u; x ^= x << 1; x = x * 337u + 84u; break;
+      case 85: x = x * 173u + V + 673115u; x ^= x >> 8; x += 2652u; x ^= x << 2; x = x * 341u + 85u; break;
+      case 86: x = x * 175u + V + 681034u; x ^= x >> 9; x += 2683u; x ^= x << 3; x = x * 345u + 86u; break;
+      case 87: x = x * 177u + V + 688953u; x ^= x >> 10; x += 2714u; x ^= x << 4; x = x * 349u + 87u; break;
+      case 88: x = x * 179u + V + 696872u; x ^= x >> 11; x += 2745u; x ^= x << 5; x = x * 353u + 88u; break;
+      case 89: x = x * 181u + V + 704791u; x ^= x >> 12; x += 2776u; x ^= x << 6; x = x * 357u + 89u; break;
+      case 90: x = x * 183u + V + 712710u; x ^= x >> 13; x += 2807u; x ^= x << 7; x = x * 361u + 90u; break;
+      case 91: x = x * 185u + V + 720629u; x ^= x >> 1; x += 2838u; x ^= x << 1; x = x * 365u + 91u; break;
+      case 92: x = x * 187u + V + 728548u; x ^= x >> 2; x += 2869u; x ^= x << 2; x = x * 369u + 92u; break;
+      case 93: x = x * 189u + V + 736467u; x ^= x >> 3; x += 2900u; x ^= x << 3; x = x * 373u + 93u; break;
+      case 94: x = x * 191u + V + 744386u; x ^= x >> 4; x += 2931u; x ^= x << 4; x = x * 377u + 94u; break;
+      case 95: x = x * 193u + V + 752305u; x ^= x >> 5; x += 2962u; x ^= x << 5; x = x * 381u + 95u; break;
+      case 96: x = x * 195u + V + 760224u; x ^= x >> 6; x += 2993u; x ^= x << 6; x = x * 385u + 96u; break;
+      case 97: x = x * 197u + V + 768143u; x ^= x >> 7; x += 3024u; x ^= x << 7; x = x * 389u + 97u; break;
+      case 98: x = x * 199u + V + 776062u; x ^= x >> 8; x += 3055u; x ^= x << 1; x = x * 393u + 98u; break;
+      case 99: x = x * 201u + V + 783981u; x ^= x >> 9; x += 3086u; x ^= x << 2; x = x * 397u + 99u; break;
+      case 100: x = x * 203u + V + 791900u; x ^= x >> 10; x += 3117u; x ^= x << 3; x = x * 401u + 100u; break;
+      case 101: x = x * 205u + V + 799819u; x ^= x >> 11; x += 3148u; x ^= x << 4; x = x * 405u + 101u; break;
+      case 102: x = x * 207u + V + 807738u; x ^= x >> 12; x += 3179u; x ^= x << 5; x = x * 409u + 102u; break;
+      case 103: x = x * 209u + V + 815657u; x ^= x >> 13; x += 3210u; x ^= x << 6; x = x * 413u + 103u; break;
+      case 104: x = x * 211u + V + 823576u; x ^= x >> 1; x += 3241u; x ^= x << 7; x = x * 417u + 104u; break;
+      case 105: x = x * 213u + V + 831495u; x ^= x >> 2; x += 3272u; x ^= x << 1; x = x * 421u + 105u; break;
+      case 106: x = x * 215u + V + 839414u; x ^= x >> 3; x += 3303u; x ^= x << 2; x = x * 425u + 106u; break;
+      case 107: x = x * 217u + V + 847333u; x ^= x >> 4; x += 3334u; x ^= x << 3; x = x * 429u + 107u; break;
+      case 108: x = x * 219u + V + 855252u; x ^= x >> 5; x += 3365u; x ^= x << 4; x = x * 433u + 108u; break;
+      case 109: x = x * 221u + V + 863171u; x ^= x >> 6; x += 3396u; x ^= x << 5; x = x * 437u + 109u; break;
+      case 110: x = x * 223u + V + 871090u; x ^= x >> 7; x += 3427u; x ^= x << 6; x = x * 441u + 110u; break;
+      case 111: x = x * 225u + V + 879009u; x ^= x >> 8; x += 3458u; x ^= x << 7; x = x * 445u + 111u; break;
+      case 112: x = x * 227u + V + 886928u; x ^= x >> 9; x += 3489u; x ^= x << 1; x = x * 449u + 112u; break;
+      case 113: x = x * 229u + V + 894847u; x ^= x >> 10; x += 3520u; x ^= x << 2; x = x * 453u + 113u; break;
+      case 114: x = x * 231u + V + 902766u; x ^= x >> 11; x += 3551u; x ^= x << 3; x = x * 457u + 114u; break;
+      case 115: x = x * 233u + V + 910685u; x ^= x >> 12; x += 3582u; x ^= x << 4; x = x * 461u + 115u; break;
+      case 116: x = x * 235u + V + 918604u; x ^= x >> 13; x += 3613u; x ^= x << 5; x = x * 465u + 116u; break;
+      case 117: x = x * 237u + V + 926523u; x ^= x >> 1; x += 3644u; x ^= x << 6; x = x * 469u + 117u; break;
+      case 118: x = x * 239u + V + 934442u; x ^= x >> 2; x += 3675u; x ^= x << 7; x = x * 473u + 118u; break;
+      case 119: x = x * 241u + V + 942361u; x ^= x >> 3; x += 3706u; x ^= x << 1; x = x * 477u + 119u; break;
+      case 120: x = x * 243u + V + 950280u; x ^= x >> 4; x += 3737u; x ^= x << 2; x = x * 481u + 120u; break;
+      case 121: x = x * 245u + V + 958199u; x ^= x >> 5; x += 3768u; x ^= x << 3; x = x * 485u + 121u; break;
+      case 122: x = x * 247u + V + 966118u; x ^= x >> 6; x += 3799u; x ^= x << 4; x = x * 489u + 122u; break;
+      case 123: x = x * 249u + V + 974037u; x ^= x >> 7; x += 3830u; x ^= x << 5; x = x * 493u + 123u; break;
+      case 124: x = x * 251u + V + 981956u; x ^= x >> 8; x += 3861u; x ^= x << 6; x = x * 497u + 124u; break;
+      case 125: x = x * 253u + V + 989875u; x ^= x >> 9; x += 3892u; x ^= x << 7; x = x * 501u + 125u; break;
+      case 126: x = x * 255u + V + 997794u; x ^= x >> 10; x += 3923u; x ^= x << 1; x = x * 505u + 126u; break;
+      case 127: x = x * 257u + V + 5710u; x ^= x >> 11; x += 3954u; x ^= x << 2; x = x * 509u + 127u; break;
+      case 128: x = x * 259u + V + 13629u; x ^= x >> 12; x += 3985u; x ^= x << 3; x = x * 513u + 128u; break;
+      case 129: x = x * 261u + V + 21548u; x ^= x >> 13; x += 4016u; x ^= x << 4; x = x * 517u + 129u; break;
+      case 130: x = x * 263u + V + 29467u; x ^= x >> 1; x += 4047u; x ^= x << 5; x = x * 521u + 130u; break;
+      case 131: x = x * 265u + V + 37386u; x ^= x >> 2; x += 4078u; x ^= x << 6; x = x * 525u + 131u; break;
+      case 132: x = x * 267u + V + 45305u; x ^= x >> 3; x += 4109u; x ^= x << 7; x = x * 529u + 132u; break;
+      case 133: x = x * 269u + V + 53224u; x ^= x >> 4; x += 4140u; x ^= x << 1; x = x * 533u + 133u; break;
+      case 134: x = x * 271u + V + 61143u; x ^= x >> 5; x += 4171u; x ^= x << 2; x = x * 537u + 134u; break;
+      case 135: x = x * 273u + V + 69062u; x ^= x >> 6; x += 4202u; x ^= x << 3; x = x * 541u + 135u; break;
+      case 136: x = x * 275u + V + 76981u; x ^= x >> 7; x += 4233u; x ^= x << 4; x = x * 545u + 136u; break;
+      case 137: x = x * 277u + V + 84900u; x ^= x >> 8; x += 4264u; x ^= x << 5; x = x * 549u + 137u; break;
+      case 138: x = x * 279u + V + 92819u; x ^= x >> 9; x += 4295u; x ^= x << 6; x = x * 553u + 138u; break;
+      case 139: x = x * 281u + V + 100738u; x ^= x >> 10; x += 4326u; x ^= x << 7; x = x * 557u + 139u; break;
+      case 140: x = x * 283u + V + 108657u; x ^= x >> 11; x += 4357u; x ^= x << 1; x = x * 561u + 140u; break;
+      case 141: x = x * 285u + V + 116576u; x ^= x >> 12; x += 4388u; x ^= x << 2; x = x * 565u + 141u; break;
+      case 142: x = x * 287u + V + 124495u; x ^= x >> 13; x += 4419u; x ^= x << 3; x = x * 569u + 142u; break;
+      case 143: x = x * 289u + V + 132414u; x ^= x >> 1; x += 4450u; x ^= x << 4; x = x * 573u + 143u; break;
+      case 144: x = x * 291u + V + 140333u; x ^= x >> 2; x += 4481u; x ^= x << 5; x = x * 577u + 144u; break;
+      case 145: x = x * 293u + V + 148252u; x ^= x >> 3; x += 4512u; x ^= x << 6; x = x * 581u + 145u; break;
+      case 146: x = x * 295u + V + 156171u; x ^= x >> 4; x += 4543u; x ^= x << 7; x = x * 585u + 146u; break;
+      case 147: x = x * 297u + V + 164090u; x ^= x >> 5; x += 4574u; x ^= x << 1; x = x * 589u + 147u; break;
+      case 148: x = x * 299u + V + 172009u; x ^= x >> 6; x += 4605u; x ^= x << 2; x = x * 593u + 148u; break;
+      case 149: x = x * 301u + V + 179928u; x ^= x >> 7; x += 4636u; x ^= x << 3; x = x * 597u + 149u; break;
+      case 150: x = x * 303u + V + 187847u; x ^= x >> 8; x += 4667u; x ^= x << 4; x = x * 601u + 150u; break;
+      case 151: x = x * 305u + V + 195766u; x ^= x >> 9; x += 4698u; x ^= x << 5; x = x * 605u + 151u; break;
+      case 152: x = x * 307u + V + 203685u; x ^= x >> 10; x += 4729u; x ^= x << 6; x = x * 609u + 152u; break;
+      case 153: x = x * 309u + V + 211604u; x ^= x >> 11; x += 4760u; x ^= x << 7; x = x * 613u + 153u; break;
+      case 154: x = x * 311u + V + 219523u; x ^= x >> 12; x += 4791u; x ^= x << 1; x = x * 617u + 154u; break;
+      case 155: x = x * 313u + V + 227442u; x ^= x >> 13; x += 4822u; x ^= x << 2; x = x * 621u + 155u; break;
+      case 156: x = x * 315u + V + 235361u; x ^= x >> 1; x += 4853u; x ^= x << 3; x = x * 625u + 156u; break;
+      case 157: x = x * 317u + V + 243280u; x ^= x >> 2; x += 4884u; x ^= x << 4; x = x * 629u + 157u; break;
+      case 158: x = x * 319u + V + 251199u; x ^= x >> 3; x += 4915u; x ^= x << 5; x = x * 633u + 158u; break;
+      case 159: x = x * 321u + V + 259118u; x ^= x >> 4; x += 4946u; x ^= x << 6; x = x * 637u + 159u; break;
+      case 160: x = x * 323u + V + 267037u; x ^= x >> 5; x += 4977u; x ^= x << 7; x = x * 641u + 160u; break;
+      case 161: x = x * 325u + V + 274956u; x ^= x >> 6; x += 5008u; x ^= x << 1; x = x * 645u + 161u; break;
+      case 162: x = x * 327u + V + 282875u; x ^= x >> 7; x += 5039u; x ^= x << 2; x = x * 649u + 162u; break;
+      case 163: x = x * 329u + V + 290794u; x ^= x >> 8; x += 5070u; x ^= x << 3; x = x * 653u + 163u; break;
+      case 164: x = x * 331u + V + 298713u; x ^= x >> 9; x += 5101u; x ^= x << 4; x = x * 657u + 164u; break;
+      case 165: x = x * 333u + V + 306632u; x ^= x >> 10; x += 5132u; x ^= x << 5; x = x * 661u + 165u; break;
+      case 166: x = x * 335u + V + 314551u; x ^= x >> 11; x += 5163u; x ^= x << 6; x = x * 665u + 166u; break;
+      case 167: x = x * 337u + V + 322470u; x ^= x >> 12; x += 5194u; x ^= x << 7; x = x * 669u + 167u; break;
+      case 168: x = x * 339u + V + 330389u; x ^= x >> 13; x += 5225u; x ^= x << 1; x = x * 673u + 168u; break;
+      case 169: x = x * 341u + V + 338308u; x ^= x >> 1; x += 5256u; x ^= x << 2; x = x * 677u + 169u; break;
+      case 170: x = x * 343u + V + 346227u; x ^= x >> 2; x += 5287u; x ^= x << 3; x = x * 681u + 170u; break;
+      case 171: x = x * 345u + V + 354146u; x ^= x >> 3; x += 5318u; x ^= x << 4; x = x * 685u + 171u; break;
+      case 172: x = x * 347u + V + 362065u; x ^= x >> 4; x += 5349u; x ^= x << 5; x = x * 689u + 172u; break;
+      case 173: x = x * 349u + V + 369984u; x ^= x >> 5; x += 5380u; x ^= x << 6; x = x * 693u + 173u; break;
+      case 174: x = x * 351u + V + 377903u; x ^= x >> 6; x += 5411u; x ^= x << 7; x = x * 697u + 174u; break;
+      case 175: x = x * 353u + V + 385822u; x ^= x >> 7; x += 5442u; x ^= x << 1; x = x * 701u + 175u; break;
+      case 176: x = x * 355u + V + 393741u; x ^= x >> 8; x += 5473u; x ^= x << 2; x = x * 705u + 176u; break;
+      case 177: x = x * 357u + V + 401660u; x ^= x >> 9; x += 5504u; x ^= x << 3; x = x * 709u + 177u; break;
+      case 178: x = x * 359u + V + 409579u; x ^= x >> 10; x += 5535u; x ^= x << 4; x = x * 713u + 178u; break;
+      case 179: x = x * 361u + V + 417498u; x ^= x >> 11; x += 5566u; x ^= x << 5; x = x * 717u + 179u; break;
+      case 180: x = x * 363u + V + 425417u; x ^= x >> 12; x += 5597u; x ^= x << 6; x = x * 721u + 180u; break;
+      case 181: x = x * 365u + V + 433336u; x ^= x >> 13; x += 5628u; x ^= x << 7; x = x * 725u + 181u; break;
+      case 182: x = x * 367u + V + 441255u; x ^= x >> 1; x += 5659u; x ^= x << 1; x = x * 729u + 182u; break;
+      case 183: x = x * 369u + V + 449174u; x ^= x >> 2; x += 5690u; x ^= x << 2; x = x * 733u + 183u; break;
+      case 184: x = x * 371u + V + 457093u; x ^= x >> 3; x += 5721u; x ^= x << 3; x = x * 737u + 184u; break;
+      case 185: x = x * 373u + V + 465012u; x ^= x >> 4; x += 5752u; x ^= x << 4; x = x * 741u + 185u; break;
+      case 186: x = x * 375u + V + 472931u; x ^= x >> 5; x += 5783u; x ^= x << 5; x = x * 745u + 186u; break;
+      case 187: x = x * 377u + V + 480850u; x ^= x >> 6; x += 5814u; x ^= x << 6; x = x * 749u + 187u; break;
+      case 188: x = x * 379u + V + 488769u; x ^= x >> 7; x += 5845u; x ^= x << 7; x = x * 753u + 188u; break;
+      case 189: x = x * 381u + V + 496688u; x ^= x >> 8; x += 5876u; x ^= x << 1; x = x * 757u + 189u; break;
+      case 190: x = x * 383u + V + 504607u; x ^= x >> 9; x += 5907u; x ^= x << 2; x = x * 761u + 190u; break;
+      case 191: x = x * 385u + V + 512526u; x ^= x >> 10; x += 5938u; x ^= x << 3; x = x * 765u + 191u; break;
+      case 192: x = x * 387u + V + 520445u; x ^= x >> 11; x += 5969u; x ^= x << 4; x = x * 769u + 192u; break;
+      case 193: x = x * 389u + V + 528364u; x ^= x >> 12; x += 6000u; x ^= x << 5; x = x * 773u + 193u; break;
+      case 194: x = x * 391u + V + 536283u; x ^= x >> 13; x += 6031u; x ^= x << 6; x = x * 777u + 194u; break;
+      case 195: x = x * 393u + V + 544202u; x ^= x >> 1; x += 6062u; x ^= x << 7; x = x * 781u + 195u; break;
+      case 196: x = x * 395u + V + 552121u; x ^= x >> 2; x += 6093u; x ^= x << 1; x = x * 785u + 196u; break;
+      case 197: x = x * 397u + V + 560040u; x ^= x >> 3; x += 6124u; x ^= x << 2; x = x * 789u + 197u; break;
+      case 198: x = x * 399u + V + 567959u; x ^= x >> 4; x += 6155u; x ^= x << 3; x = x * 793u + 198u; break;
+      case 199: x = x * 401u + V + 575878u; x ^= x >> 5; x += 6186u; x ^= x << 4; x = x * 797u + 199u; break;
+      case 200: x = x * 403u + V + 583797u; x ^= x >> 6; x += 6217u; x ^= x << 5; x = x * 801u + 200u; break;
+      case 201: x = x * 405u + V + 591716u; x ^= x >> 7; x += 6248u; x ^= x << 6; x = x * 805u + 201u; break;
+      case 202: x = x * 407u + V + 599635u; x ^= x >> 8; x += 6279u; x ^= x << 7; x = x * 809u + 202u; break;
+      case 203: x = x * 409u + V + 607554u; x ^= x >> 9; x += 6310u; x ^= x << 1; x = x * 813u + 203u; break;
+      case 204: x = x * 411u + V + 615473u; x ^= x >> 10; x += 6341u; x ^= x << 2; x = x * 817u + 204u; break;
+      case 205: x = x * 413u + V + 623392u; x ^= x >> 11; x += 6372u; x ^= x << 3; x = x * 821u + 205u; break;
+      case 206: x = x * 415u + V + 631311u; x ^= x >> 12; x += 6403u; x ^= x << 4; x = x * 825u + 206u; break;
+      case 207: x = x * 417u + V + 639230u; x ^= x >> 13; x += 6434u; x ^= x << 5; x = x * 829u + 207u; break;
+      case 208: x = x * 419u + V + 647149u; x ^= x >> 1; x += 6465u; x ^= x << 6; x = x * 833u + 208u; break;
+      case 209: x = x * 421u + V + 655068u; x ^= x >> 2; x += 6496u; x ^= x << 7; x = x * 837u + 209u; break;
+      case 210: x = x * 423u + V + 662987u; x ^= x >> 3; x += 6527u; x ^= x << 1; x = x * 841u + 210u; break;
+      case 211: x = x * 425u + V + 670906u; x ^= x >> 4; x += 6558u; x ^= x << 2; x = x * 845u + 211u; break;
+      case 212: x = x * 427u + V + 678825u; x ^= x >> 5; x += 6589u; x ^= x << 3; x = x * 849u + 212u; break;
+      case 213: x = x * 429u + V + 686744u; x ^= x >> 6; x += 6620u; x ^= x << 4; x = x * 853u + 213u; break;
+      case 214: x = x * 431u + V + 694663u; x ^= x >> 7; x += 6651u; x ^= x << 5; x = x * 857u + 214u; break;
+      case 215: x = x * 433u + V + 702582u; x ^= x >> 8; x += 6682u; x ^= x << 6; x = x * 861u + 215u; break;
+      case 216: x = x * 435u + V + 710501u; x ^= x >> 9; x += 6713u; x ^= x << 7; x = x * 865u + 216u; break;
+      case 217: x = x * 437u + V + 718420u; x ^= x >> 10; x += 6744u; x ^= x << 1; x = x * 869u + 217u; break;
+      case 218: x = x * 439u + V + 726339u; x ^= x >> 11; x += 6775u; x ^= x << 2; x = x * 873u + 218u; break;
+      case 219: x = x * 441u + V + 734258u; x ^= x >> 12; x += 6806u; x ^= x << 3; x = x * 877u + 219u; break;
+      case 220: x = x * 443u + V + 742177u; x ^= x >> 13; x += 6837u; x ^= x << 4; x = x * 881u + 220u; break;
+      case 221: x = x * 445u + V + 750096u; x ^= x >> 1; x += 6868u; x ^= x << 5; x = x * 885u + 221u; break;
+      case 222: x = x * 447u + V + 758015u; x ^= x >> 2; x += 6899u; x ^= x << 6; x = x * 889u + 222u; break;
+      case 223: x = x * 449u + V + 765934u; x ^= x >> 3; x += 6930u; x ^= x << 7; x = x * 893u + 223u; break;
+      case 224: x = x * 451u + V + 773853u; x ^= x >> 4; x += 6961u; x ^= x << 1; x = x * 897u + 224u; break;
+      case 225: x = x * 453u + V + 781772u; x ^= x >> 5; x += 6992u; x ^= x << 2; x = x * 901u + 225u; break;
+      case 226: x = x * 455u + V + 789691u; x ^= x >> 6; x += 7023u; x ^= x << 3; x = x * 905u + 226u; break;
+      case 227: x = x * 457u + V + 797610u; x ^= x >> 7; x += 7054u; x ^= x << 4; x = x * 909u + 227u; break;
+      case 228: x = x * 459u + V + 805529u; x ^= x >> 8; x += 7085u; x ^= x << 5; x = x * 913u + 228u; break;
+      case 229: x = x * 461u + V + 813448u; x ^= x >> 9; x += 7116u; x ^= x << 6; x = x * 917u + 229u; break;
+      case 230: x = x * 463u + V + 821367u; x ^= x >> 10; x += 7147u; x ^= x << 7; x = x * 921u + 230u; break;
+      case 231: x = x * 465u + V + 829286u; x ^= x >> 11; x += 7178u; x ^= x << 1; x = x * 925u + 231u; break;
+      case 232: x = x * 467u + V + 837205u; x ^= x >> 12; x += 7209u; x ^= x << 2; x = x * 929u + 232u; break;
+      case 233: x = x * 469u + V + 845124u; x ^= x >> 13; x += 7240u; x ^= x << 3; x = x * 933u + 233u; break;
+      case 234: x = x * 471u + V + 853043u; x ^= x >> 1; x += 7271u; x ^= x << 4; x = x * 937u + 234u; break;
+      case 235: x = x * 473u + V + 860962u; x ^= x >> 2; x += 7302u; x ^= x << 5; x = x * 941u + 235u; break;
+      case 236: x = x * 475u + V + 868881u; x ^= x >> 3; x += 7333u; x ^= x << 6; x = x * 945u + 236u; break;
+      case 237: x = x * 477u + V + 876800u; x ^= x >> 4; x += 7364u; x ^= x << 7; x = x * 949u + 237u; break;
+      case 238: x = x * 479u + V + 884719u; x ^= x >> 5; x += 7395u; x ^= x << 1; x = x * 953u + 238u; break;
+      case 239: x = x * 481u + V + 892638u; x ^= x >> 6; x += 7426u; x ^= x << 2; x = x * 957u + 239u; break;
+      case 240: x = x * 483u + V + 900557u; x ^= x >> 7; x += 7457u; x ^= x << 3; x = x * 961u + 240u; break;
+      case 241: x = x * 485u + V + 908476u; x ^= x >> 8; x += 7488u; x ^= x << 4; x = x * 965u + 241u; break;
+      case 242: x = x * 487u + V + 916395u; x ^= x >> 9; x += 7519u; x ^= x << 5; x = x * 969u + 242u; break;
+      case 243: x = x * 489u + V + 924314u; x ^= x >> 10; x += 7550u; x ^= x << 6; x = x * 973u + 243u; break;
+      case 244: x = x * 491u + V + 932233u; x ^= x >> 11; x += 7581u; x ^= x << 7; x = x * 977u + 244u; break;
+      case 245: x = x * 493u + V + 940152u; x ^= x >> 12; x += 7612u; x ^= x << 1; x = x * 981u + 245u; break;
+      case 246: x = x * 495u + V + 948071u; x ^= x >> 13; x += 7643u; x ^= x << 2; x = x * 985u + 246u; break;
+      case 247: x = x * 497u + V + 955990u; x ^= x >> 1; x += 7674u; x ^= x << 3; x = x * 989u + 247u; break;
+      case 248: x = x * 499u + V + 963909u; x ^= x >> 2; x += 7705u; x ^= x << 4; x = x * 993u + 248u; break;
+      case 249: x = x * 501u + V + 971828u; x ^= x >> 3; x += 7736u; x ^= x << 5; x = x * 997u + 249u; break;
+      case 250: x = x * 503u + V + 979747u; x ^= x >> 4; x += 7767u; x ^= x << 6; x = x * 1001u + 250u; break;
+      case 251: x = x * 505u + V + 987666u; x ^= x >> 5; x += 7798u; x ^= x << 7; x = x * 1005u + 251u; break;
+      case 252: x = x * 507u + V + 995585u; x ^= x >> 6; x += 7829u; x ^= x << 1; x = x * 1009u + 252u; break;
+      case 253: x = x * 509u + V + 3501u; x ^= x >> 7; x += 7860u; x ^= x << 2; x = x * 1013u + 253u; break;
+      case 254: x = x * 511u + V + 11420u; x ^= x >> 8; x += 7891u; x ^= x << 3; x = x * 1017u + 254u; break;
+      case 255: x = x * 513u + V + 19339u; x ^= x >> 9; x += 7922u; x ^= x << 4; x = x * 1021u + 255u; break;
+    }
+  }
+  return x;
+}
+template <unsigned V>
+__global__ void k_branchy_v(const uint8_t* order, uint64_t* out, int slot) {
+  if (threadIdx.x != 0) return;
+  long long c0 = clock64();
+  uint32_t x = branchy_v<V>(order, 1);
+  long long c1 = clock64();
+  out[slot] = (uint64_t)(c1 - c0);
+  out[slot + 32] = x;
+}
+
 int main() {
   uint64_t *a, *out, h[16];
   cudaMalloc(&a, 64ull << 20);
@@ -512,6 +817,57 @@ int main() {
     cudaMemcpy(hh, o3, sizeof(hh), cudaMemcpyDeviceToHost);
     printf("nanosleep(0/32/64/256) takes %llu / %llu / %llu / %llu ns\n", (unsigned long long)hh[40],
            (unsigned long long)hh[41], (unsigned long long)hh[42], (unsigned long long)hh[43]);
+  }
+  {
+    cudaMemPool_t pool;
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = 0;
+    cudaMemPoolCreate(&pool, &props);
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    uint64_t* pr;
+    cudaMallocFromPoolAsync((void**)&pr, 1 << 20, pool, st);
+    cudaMemsetAsync(pr, 0, 1 << 20, st);
+    cudaStreamSynchronize(st);
+    uint64_t* o4;
+    cudaMalloc(&o4, 8 * 64);
+    uint64_t hh[64];
+    for (int rep = 0; rep < 3; ++rep) {
+      k_scan512<<<1, 512, 0, st>>>(pr, o4, 1);
+      cudaMemcpy(hh, o4, sizeof(hh), cudaMemcpyDeviceToHost);
+      uint64_t first = hh[50];
+      k_scan512<<<1, 512, 0, st>>>(pr, o4, 100);
+      cudaMemcpy(hh, o4, sizeof(hh), cudaMemcpyDeviceToHost);
+      printf("scan in a 512-thread CTA over pool memory: first launch %llu cycles, steady %llu cycles\n",
+             (unsigned long long)first, (unsigned long long)hh[50]);
+      k_scan512<<<1, 512, 0, st>>>(a + 8192, o4, 1);
+      cudaMemcpy(hh, o4, sizeof(hh), cudaMemcpyDeviceToHost);
+      printf("scan in a 512-thread CTA over cudaMalloc memory: first launch %llu cycles\n", (unsigned long long)hh[50]);
+    }
+  }
+  {
+    uint8_t ord[256];
+    for (int i = 0; i < 256; ++i) ord[i] = (uint8_t)((i * 97 + 13) & 255);
+    uint8_t* d_ord;
+    cudaMalloc(&d_ord, 256);
+    cudaMemcpy(d_ord, ord, 256, cudaMemcpyHostToDevice);
+    uint64_t* o5;
+    cudaMalloc(&o5, 8 * 64);
+    uint64_t hh[64];
+    // A A A A (warm), then A B A B (alternating)
+    for (int i = 0; i < 4; ++i) k_branchy_v<1><<<1, 32>>>(d_ord, o5, i);
+    for (int i = 4; i < 12; ++i) {
+      if (i & 1) k_branchy_v<2><<<1, 32>>>(d_ord, o5, i);
+      else k_branchy_v<1><<<1, 32>>>(d_ord, o5, i);
+    }
+    cudaMemcpy(hh, o5, sizeof(hh), cudaMemcpyDeviceToHost);
+    printf("icache across launches (cycles per 256-case pass): A A A A:");
+    for (int i = 0; i < 4; ++i) printf(" %llu", (unsigned long long)hh[i]);
+    printf(" | A B A B ...:");
+    for (int i = 4; i < 12; ++i) printf(" %llu", (unsigned long long)hh[i]);
+    printf("\n");
   }
   Big b = {};
   for (int rep = 0; rep < 4; ++rep) {
