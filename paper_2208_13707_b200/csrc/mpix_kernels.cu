@@ -990,8 +990,13 @@ __device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const LLMsg
   if (posted) M::st_rlx(&a.post_ring[slot].state, st_word(a.pseq, ST_FREE));  // retract
   ScopeGpu::st_rlx(&a.post_mirror[slot], a.pseq + 1);  // consumed either way (local)
   // my completion: read only by this rank (its waits, the host after a
-  // synchronisation), so device scope orders the payload and status before it
-  if (a.my_done) ScopeGpu::st_rel(a.my_done, a.my_gen);
+  // synchronisation), so device scope orders the payload and status before
+  // it; a blocking receive completes in its own kernel, whose end publishes
+  // everything to later stream work and to the host (no fence)
+  if (a.my_done) {
+    if (a.blocking) ScopeGpu::st_rlx(a.my_done, a.my_gen);
+    else ScopeGpu::st_rel(a.my_done, a.my_gen);
+  }
   M::st_rlx(&a.scan_mirror[j], (sn.state >> 8) + 1);
   if (m.sdone) M::st_rlx(m.sdone, m.sgen);
 }
@@ -1047,7 +1052,10 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
     if (lane == 0 && a.pseq >= (uint64_t)a.R) pre = M::ld_rlx(&a.post_mirror[ring_slot(a.pseq, a.R)]);
     if (lane == 0 && ll_send) ll_load(a.buf, a.bytes, pay);
     Snap sn;
-    int j = warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
+    // An LL send posts first and scans after its fence (phase 2: the same
+    // Dekker race, resolved by the CAS on its LL state word): its post
+    // reaches the receiver one round trip earlier than scan-then-post.
+    int j = ll_send ? -1 : warp_scan<SYS>(a.scan_ring, a.R, a.key, &sn);
     if (poll_recv && j < 0) j = poll_scan<SYS>(a, &sn);
     if (lane == 0) {
       trace_t(trace, 1);

@@ -666,11 +666,13 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
   }
   bool inl = bytes <= w.cfg.inline_bytes || (!is_recv && a.mode == MODE_EAGER);
   bool post_only = false;
-  if (!inl && !blocking && peer == me && !dyn && !how.conventional && !gr) {
+  if (!blocking && peer == me && !dyn && !how.conventional && !gr) {
     // Self-message whose counterpart has not been enqueued yet: it can only
     // be enqueued later on this same stream (an enqueue comm has one stream),
     // so it runs after this operation, which therefore only posts and never
-    // copies: one small launch instead of proto + copy grid + fin.
+    // copies: one small launch instead of proto + copy grid + fin. Small
+    // ones too: if the counterpart joins the same batch, the host pairs them
+    // (one copy, no descriptors, no Dekker race between two CTAs).
     const auto& other = is_recv ? c->send_tagseq : c->recv_tagseq;
     auto it = other.find(tagseq_key(me, tag));
     if (it == other.end() || it->second <= tseq) inl = post_only = true;
