@@ -32,6 +32,6 @@ print(f"samples {allv}; barrier {tot['barrier']}; non-barrier {allv - tot['barri
 for k, v in tot.most_common():
     if v and k != "barrier":
         print(f"  {k:20s} {v:6d}  {v / max(1, allv - tot['barrier']):.0%}")
-items.sort(reverse=True)
+items.sort(key=lambda t: (t[0], t[1]), reverse=True)
 for it in items[:top]:
     print(it[0], it[1], it[2], it[3], it[4])
