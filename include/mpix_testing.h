@@ -102,6 +102,12 @@ int MPIXT_Fig3(int T, int W, int batches, int bytes, MPI_Comm *comms, void **buf
  * 0 global lock, 1 per communicator, 2 serial contexts lock-free. Call with
  * no operation in flight. Returns the previous regime in *prev. */
 int MPIXT_Set_exclusion(int regime, int *prev);
+/* Bidirectional exchange of `bytes` between ranks 0 and 1: per step each
+ * rank enqueues Irecv + Isend + Waitall (one host thread per rank);
+ * *dev_s = max over the two streams of event time for `iters` steps. */
+int MPIXT_Exchange(MPI_Comm c0, MPI_Comm c1, void *s0buf, void *r0buf, void *s1buf, void *r1buf,
+                   uint64_t bytes, int iters, void *st0, void *st1, int dev0, int dev1,
+                   double *dev_s);
 /* Blocking ping-pong of `bytes` between ranks 0 (c0, s0) and 1 (c1, s1):
  * Send+Recv / Recv+Send, `iters` round trips; *dev_s = event time on s0. */
 int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void *b0, void *b1, uint64_t bytes, int iters,

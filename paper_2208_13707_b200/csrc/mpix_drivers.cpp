@@ -149,6 +149,59 @@ int MPIXT_Fig3(int T, int W, int batches, int bytes, MPI_Comm* comms, void** buf
   return err.load();
 }
 
+// Bidirectional exchange between ranks 0 and 1 (one host thread each):
+// per step Irecv_enqueue + Isend_enqueue of `bytes` + Waitall_enqueue, the
+// cross-rank device handshake on both messages. *dev_s = max over the two
+// streams of event time for `iters` steps.
+int MPIXT_Exchange(MPI_Comm c0, MPI_Comm c1, void* s0buf, void* r0buf, void* s1buf, void* r1buf,
+                   uint64_t bytes, int iters, void* st0, void* st1, int dev0, int dev1,
+                   double* dev_s) {
+  if (iters < 1) return MPIX_ERR_INVALID_ARG;
+  cudaEvent_t ev[2][2];
+  for (int r = 0; r < 2; ++r) {
+    cudaSetDevice(r ? dev1 : dev0);
+    if (cudaEventCreate(&ev[r][0]) != cudaSuccess || cudaEventCreate(&ev[r][1]) != cudaSuccess)
+      return MPIX_ERR_CUDA;
+  }
+  std::atomic<int> err{0};
+  Spin go(2);
+  const int count = (int)bytes;
+  auto side = [&](int r) {
+    cudaSetDevice(r ? dev1 : dev0);
+    MPIX_Rank_bind(r);
+    MPI_Comm c = r ? c1 : c0;
+    void* sb = r ? s1buf : s0buf;
+    void* rb = r ? r1buf : r0buf;
+    cudaStream_t s = (cudaStream_t)(r ? st1 : st0);
+    cudaEventRecord(ev[r][0], s);
+    go.arrive_and_wait();
+    for (int i = 0; i < iters && !err.load(); ++i) {
+      MPI_Request q[2];
+      int rc = MPIX_Irecv_enqueue(rb, count, MPI_BYTE, 1 - r, 9, c, &q[0]);
+      rc |= MPIX_Isend_enqueue(sb, count, MPI_BYTE, 1 - r, 9, c, &q[1]);
+      rc |= MPIX_Waitall_enqueue(2, q, MPI_STATUSES_IGNORE);
+      if (rc) err.store(rc);
+    }
+    cudaEventRecord(ev[r][1], s);
+  };
+  std::thread t(side, 1);
+  side(0);
+  t.join();
+  float mx = 0;
+  for (int r = 0; r < 2; ++r) {
+    cudaSetDevice(r ? dev1 : dev0);
+    cudaEventSynchronize(ev[r][1]);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[r][0], ev[r][1]);
+    mx = std::max(mx, ms);
+    cudaEventDestroy(ev[r][0]);
+    cudaEventDestroy(ev[r][1]);
+  }
+  cudaSetDevice(dev0);
+  if (dev_s) *dev_s = mx / 1e3;
+  return err.load();
+}
+
 int MPIXT_Pingpong(MPI_Comm c0, MPI_Comm c1, void* b0, void* b1, uint64_t bytes, int iters,
                    void* s0, void* s1, int dev0, int dev1, double* dev_s, double* host_s) {
   if (iters < 1) return MPIX_ERR_INVALID_ARG;

@@ -180,6 +180,7 @@ def _declare(L: C.CDLL) -> None:
         "MPIXT_Preload": (I, []),
         "MPIXT_Msgrate": (I, [I, I, I, I, P, P, P, P, P, P, P]),
         "MPIXT_Fig3": (I, [I, I, I, I, P, P, P, P, P]),
+        "MPIXT_Exchange": (I, [P, P, P, P, P, P, U64, I, P, P, I, I, P]),
         "MPIXT_Set_exclusion": (I, [I, P]),
         "MPIXT_Pingpong": (I, [P, P, P, P, U64, I, P, P, I, I, P, P]),
         "MPIXT_Pingpong_side": (I, [P, P, U64, I, I, I, P, P]),
@@ -872,6 +873,17 @@ class testing:
         check(lib().MPIXT_Fig3(T, W, batches, nbytes, CA, BA, DV, C.byref(el), C.byref(n)), "Fig3")
         return {"threads": T, "window": W, "messages": n.value, "elapsed_s": el.value,
                 "msgs_per_s": n.value / max(el.value, 1e-9)}
+
+    @staticmethod
+    def exchange(c0, c1, s0, r0, s1, r1, nbytes: int, iters: int, st0, st1, dev0: int = 0,
+                 dev1: int = 0) -> float:
+        """Bidirectional Isend/Irecv/Waitall_enqueue exchange between ranks 0
+        and 1 (native threads); returns device seconds for `iters` steps."""
+        ds = C.c_double()
+        check(lib().MPIXT_Exchange(c0.h, c1.h, _ptr(s0), _ptr(r0), _ptr(s1), _ptr(r1), nbytes, iters,
+                                   _stream_handle(st0), _stream_handle(st1), dev0, dev1,
+                                   C.byref(ds)), "Exchange")
+        return ds.value
 
     @staticmethod
     def set_exclusion(regime: int) -> int:
