@@ -80,6 +80,11 @@ namespace mpix {
                    : "memory");                                                                   \
       return o;                                                                                   \
     }                                                                                             \
+    static __device__ __forceinline__ uint64_t exch(uint64_t* p, uint64_t v) {                  \
+      uint64_t o;                                                                                 \
+      asm volatile("atom.relaxed." SC ".global.exch.b64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(v) : "memory"); \
+      return o;                                                                                   \
+    }                                                                                             \
     static __device__ __forceinline__ void fence_sc() { asm volatile("fence.sc." SC ";" ::: "memory"); } \
     static __device__ __forceinline__ void fence_ar() {                                           \
       asm volatile("fence.acq_rel." SC ";" ::: "memory");                                        \
@@ -975,7 +980,8 @@ __device__ bool ll_read(const SlotDesc* s, const Snap& sn, LLMsg& m, const P2PAr
 // completion word, then the sender's free-mirror (it may reuse its slot) and
 // its completion word.
 template <bool SYS>
-__device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const LLMsg& m, bool posted) {
+__device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const LLMsg& m, bool posted,
+                            uint64_t gate = 0) {
   using M = Scope<SYS>;
   const uint64_t n = umin(m.len, a.bytes);  // truncation: endpoint.cpp:17
   for (uint64_t i = 0; i < n; ++i) a.buf[i] = (uint8_t)(m.w[i >> 2] >> (8 * (i & 3)));
@@ -997,6 +1003,10 @@ __device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const LLMsg
     if (a.blocking) ScopeGpu::st_rlx(a.my_done, a.my_gen);
     else ScopeGpu::st_rel(a.my_done, a.my_gen);
   }
+  // `gate`: the result of the atomic that took the slot (first-scan take);
+  // branching on it makes the free-mirror wait until that atomic has been
+  // performed, so the TAKEN state can never land after the sender's next post
+  if (gate == ~0ull) return;
   M::st_rlx(&a.scan_mirror[j], (sn.state >> 8) + 1);
   if (m.sdone) M::st_rlx(m.sdone, m.sgen);
 }
@@ -1099,9 +1109,12 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
           if (!wait_post_slot<SYS>(a, pre)) {
             // watchdog: leave the send descriptor for nobody
           } else if (sn.state & ST_LL) {
-            M::st_rlx(&a.scan_ring[j].state, st_word(sn.state >> 8, ST_TAKEN));
+            // TAKEN by an atomic exchange (no competitor: a plain store would
+            // do, but it could land after the free-mirror below); its round
+            // trip overlaps the payload and status stores
+            const uint64_t old = M::exch(&a.scan_ring[j].state, st_word(sn.state >> 8, ST_TAKEN));
             LLMsg m;
-            if (ll_read<SYS>(&a.scan_ring[j], sn, m, a)) ll_complete<SYS>(a, j, sn, m, false);
+            if (ll_read<SYS>(&a.scan_ring[j], sn, m, a)) ll_complete<SYS>(a, j, sn, m, false, old);
           } else {
             M::st_rlx(&a.scan_ring[j].state, st_word(sn.state >> 8, ST_TAKEN));
             recv_win(a, dc, j, sn, false);
