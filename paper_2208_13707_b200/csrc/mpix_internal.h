@@ -234,6 +234,7 @@ struct P2PArgs {
   uint64_t* pair_mirror;
   uint64_t pair_pseq;
   int greset;             // captured blocking receive: zero my_done before posting
+  int mate_skip;          // a device-matched send: its receive does the paired copy
 };
 
 // Copy grids up to this many CTAs may be launched (and park at
@@ -304,8 +305,13 @@ struct BatchOp {
   uint8_t gflags;
   uint16_t gp, gt;
   uint8_t ll;             // P2PArgs::ll
+  // graph-capturable comm: the index in this launch of the operation the
+  // host expects to match this self-message (-1 none); the kernels compare
+  // both absolute keys (device counters) and, if equal, the receive does
+  // the paired copy and the send stands down
+  int16_t mate;
 };
-static_assert(sizeof(BatchOp) <= 208, "BatchOp packing");
+static_assert(sizeof(BatchOp) <= 216, "BatchOp packing");
 
 constexpr int kBatchOps = 128;    // operations per coalesced launch (27.7 KB of parameters)
 constexpr int kBatchWaits = 128;  // wait entries carried by the closing launch

@@ -1251,6 +1251,12 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
     a.trace->bytes = a.bytes;
     a.trace->key = a.key;
   }
+  if (a.mate_skip) {  // a device-matched send: its receive copies and completes it
+    if (!INLINE && threadIdx.x == 0) a.rec->action = ACT_NONE;
+    __syncthreads();
+    if (!INLINE) pdl_trigger();
+    return;
+  }
   if (a.greset) {  // captured blocking receive: its completion word is reused every replay
     if (threadIdx.x == 0) {
       *reinterpret_cast<volatile uint64_t*>(a.my_done) = 0;
@@ -1453,6 +1459,7 @@ __device__ void load_op(const BatchOp& o, uint64_t spin_limit_ns, P2PArgs& a) {
   a.trace = nullptr;
   a.early_trigger = o.early;
   a.ll = o.ll;
+  a.mate_skip = 0;
   a.dyn = o.dyn;
   a.P = o.P;
   a.me = o.me;
@@ -1461,6 +1468,34 @@ __device__ void load_op(const BatchOp& o, uint64_t spin_limit_ns, P2PArgs& a) {
   a.sidx = o.sidx;
   a.didx = o.didx;
   a.bases = o.bases;
+}
+
+// A graph-capturable self-message and its host-expected counterpart in the
+// same launch (BatchOp::mate): both CTAs read the same device counters, so
+// both reach the same verdict. Equal absolute keys: the receive takes the
+// paired path (one copy, both completions, both ring slots consumed) and the
+// send stands down; otherwise each runs the two-sided protocol.
+__device__ void mate_match(const BatchOp& m, P2PArgs& a) {
+  if (!(m.gflags & G_ON)) return;
+  const volatile uint64_t* g = m.bases;
+  const uint64_t mpseq = g[m.gp] + m.pseq;
+  const uint32_t t = (uint32_t)g[m.gt] + (uint32_t)m.key;
+  const uint64_t mkey = (m.key & 0xffffffff00000000ull) | t;
+  if (mkey != a.key) return;
+  if (a.is_recv) {
+    a.paired = 1;
+    a.pair_src = m.buf;
+    a.pair_bytes = m.bytes;
+    a.pair_done = m.my_done;
+    a.pair_gen = m.my_gen;
+    a.pair_mirror = m.post_mirror;
+    a.pair_pseq = mpseq;
+    a.staging = nullptr;
+    a.stage_done = nullptr;
+    a.stage_gen = 0;
+  } else {
+    a.mate_skip = 1;
+  }
 }
 
 template <bool SYS>
@@ -1506,7 +1541,10 @@ __global__ void __launch_bounds__(kThreads) k_batch(const BatchArgs<NOPS, NWAIT>
   __shared__ P2PArgs a;
   if ((int)blockIdx.x < b.n_static) {
     const BatchOp& o = b.ops[blockIdx.x];
-    if (threadIdx.x == 0) load_op(o, b.spin_limit_ns, a);
+    if (threadIdx.x == 0) {
+      load_op(o, b.spin_limit_ns, a);
+      if (o.mate >= 0) mate_match(b.ops[o.mate], a);
+    }
     __syncthreads();
     if (o.inl) proto_body<SYS, true>(a, s_dc);
     else proto_body<SYS, false>(a, s_dc);  // decision -> op record; triggers k_gcopy
@@ -2157,9 +2195,17 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
   // static-matching operations first (one CTA each), then the dynamic ones
   // (one sequential CTA), keeping batch order within each group
   int k = 0;
-  for (int i = 0; i < n; ++i)
-    if (!ops[i].dyn) b.ops[k++] = ops[i];
+  int newidx[NOPS];
+  for (int i = 0; i < n; ++i) {
+    newidx[i] = -1;
+    if (!ops[i].dyn) {
+      newidx[i] = k;
+      b.ops[k++] = ops[i];
+    }
+  }
   b.n_static = k;
+  for (int i = 0; i < k; ++i)  // mates refer to positions in this launch
+    if (b.ops[i].mate >= 0) b.ops[i].mate = (int16_t)newidx[b.ops[i].mate];
   // Dynamic receives, then dynamic sends, batch order in each — unless a
   // blocking receive closes the batch: it may wait in k_batch for a push
   // that its send, had it run second in the other CTA, would leave to the

@@ -67,6 +67,7 @@ int flush_locked(StreamBatch& b, cudaStream_t s, const WaitEntry* w, int nwait, 
     b.ops.clear();
     b.first_large_pseq.clear();
     b.post_only.clear();
+    b.gmates.clear();
     b.grel.clear();
     wi += m;
   } while (wi < nwait);
@@ -224,6 +225,7 @@ BatchOp pack_op(const P2PArgs& a, bool inl) {
   o.blocking = (uint8_t)a.blocking;
   o.inl = inl ? 1 : 0;
   o.ll = (uint8_t)a.ll;
+  o.mate = -1;
   return o;
 }
 
@@ -777,7 +779,24 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
       if (b.ops.empty()) b.err_word = rs.d_err;
       if (!inl && a.post_mirror) b.first_large_pseq.emplace(a.post_mirror, a.pseq);
       if (post_only) b.post_only.push_back({c, a.key, b.ops.size(), (bool)is_recv});
+      // graph-capturable self-message: remember it, or mate it with the
+      // opposite operation of the same (relative) key already in this batch
+      int mate = -1;
+      if (gr && peer == me && !blocking && inl) {
+        for (size_t k = 0; k < b.gmates.size() && mate < 0; ++k) {
+          const auto& gm = b.gmates[k];
+          if (gm.comm == c && gm.key == a.key && gm.is_recv != is_recv) {
+            mate = (int)gm.idx;
+            b.gmates.erase(b.gmates.begin() + k);
+          }
+        }
+        if (mate < 0) b.gmates.push_back({c, a.key, b.ops.size(), (bool)is_recv});
+      }
       b.ops.push_back(pack_op(a, inl));
+      if (mate >= 0) {
+        b.ops.back().mate = (int16_t)mate;
+        b.ops[mate].mate = (int16_t)(b.ops.size() - 1);
+      }
       if (gr) {
         BatchOp& o = b.ops.back();
         o.bases = c->d_gseq;

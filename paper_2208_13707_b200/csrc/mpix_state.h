@@ -275,6 +275,9 @@ struct StreamBatch {
     bool is_recv;
   };
   std::vector<PostOnly> post_only;
+  // - graph-capturable comms: self-message operations whose counterpart may
+  //   join this batch (matched on the device)
+  std::vector<PostOnly> gmates;
   // graph-capturable comms: operations of this batch per device counter so
   // far (the next operation's relative sequence), and the arrival word of
   // the final launch, which advances the counters

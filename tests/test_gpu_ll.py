@@ -165,3 +165,44 @@ def test_held_conventional_isend_progresses():
         w.run_ranks(body)
         assert torch.equal(dst, src)
         assert out["t"] < 5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [8, 4096])
+def test_graph_comm_device_matched_self_messages_and_fallback(n):
+    """Graph-capturable comm (sequences in device counters): a self Isend +
+    Irecv in one launch are matched on the device (the receive copies, the
+    send stands down). An earlier unmatched Isend on the same tag puts the
+    send and receive counters out of step, so the next launch's host-expected
+    pair does not match on the device and both take the two-sided protocol:
+    the receive gets the earlier send, as static matching requires."""
+    w = mpix.World(1, [0])
+    try:
+        s = mpix.testing.new_stream(0)
+        c = w.comm(0).stream_comm_create(mpix.Stream.from_cuda(s, mpix_graph="1"))
+        A, B, C = pattern(n, 31), pattern(n, 32), pattern(n, 33)
+        X, Y, Z = [torch.zeros(n, dtype=torch.uint8, device=0) for _ in range(3)]
+        tmp = torch.zeros(16, dtype=torch.uint8, device=0)
+        torch.cuda.synchronize()
+        # matched pair in one launch
+        q1 = c.isend_enqueue(C, n, mpix.MPI_BYTE, 0, 4)
+        q2 = c.irecv_enqueue(Z, n, mpix.MPI_BYTE, 0, 4)
+        mpix.waitall_enqueue([q1, q2])
+        # an unmatched Isend on tag 5, launched (a blocking self send/recv on
+        # another tag closes the batches)
+        qa = c.isend_enqueue(A, n, mpix.MPI_BYTE, 0, 5)
+        c.send_enqueue(tmp, 8, mpix.MPI_BYTE, 0, 99)
+        c.recv_enqueue(tmp, 8, mpix.MPI_BYTE, 0, 99)
+        # host-expected pair, counters out of step: the receive takes A
+        qb = c.isend_enqueue(B, n, mpix.MPI_BYTE, 0, 5)
+        qx = c.irecv_enqueue(X, n, mpix.MPI_BYTE, 0, 5)
+        mpix.waitall_enqueue([qx])
+        qy = c.irecv_enqueue(Y, n, mpix.MPI_BYTE, 0, 5)
+        mpix.waitall_enqueue([qa, qb, qy])
+        s.synchronize()
+        assert torch.equal(Z, C)
+        assert torch.equal(X, A) and torch.equal(Y, B)
+        assert mpix.rank_error(0) == 0
+    finally:
+        torch.cuda.synchronize()
+        w.finalize()
