@@ -1,5 +1,5 @@
 # N>1 launch paths on the 1-GPU box (--share-gpus validation, not measurements)
-O=gpurun_out/r02s
+O=gpurun_out/r02s2
 mkdir -p $O
 export CUDA_MODULE_LOADING=EAGER
 for N in 2 4; do
