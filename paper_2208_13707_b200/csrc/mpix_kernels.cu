@@ -1601,6 +1601,20 @@ __global__ void __launch_bounds__(kThreads) k_batch_tiny(const BatchArgs<NOPS, N
   }
 }
 
+// One operation, no wait (a blocking small send or receive: the ping-pong
+// case): the operation is the kernel parameter itself, so its fields are
+// read at compile-time offsets instead of through a run-time array index.
+template <bool SYS>
+__global__ void __launch_bounds__(kThreads) k_op1(const BatchOp o, const uint64_t spin_limit_ns) {
+  __shared__ Decision s_dc;
+  __shared__ P2PArgs a;
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) load_op(o, spin_limit_ns, a);
+  __syncthreads();
+  proto_body<SYS, true, true>(a, s_dc);
+}
+
 // Grouped copy (PDL behind k_batch): CTA t finds its operation in the tile
 // prefix table and streams one tile of it.
 __global__ void __launch_bounds__(kCopyThreads, 2) k_gcopy(const GCopyArgs g) {
@@ -2250,6 +2264,15 @@ static int launch_batch_t(const BatchOp* ops, int n, const WaitEntry* w, int nwa
       const BatchOp& o = b.ops[i];
       tiny = !o.paired && !(o.gflags & G_ON) && !(!o.is_recv && o.mode == MODE_STAGED);
     }
+    static const bool op1 = [] {
+      const char* v = std::getenv("MPIX_OP1");
+      return !(v && v[0] == '0');
+    }();
+    if (tiny && op1 && n == 1 && nwait == 0 && !arrive) {
+      cudaError_t e = sys ? launch_head(k_op1<true>, 1, kThreads, s, b.ops[0], spin_limit_ns)
+                          : launch_head(k_op1<false>, 1, kThreads, s, b.ops[0], spin_limit_ns);
+      return e == cudaSuccess ? 1 : -1;
+    }
     if (tiny) {
       cudaError_t e = sys ? launch_head(k_batch_tiny<true, NOPS, NWAIT>, grid, kThreads, s, b)
                           : launch_head(k_batch_tiny<false, NOPS, NWAIT>, grid, kThreads, s, b);
@@ -2459,6 +2482,7 @@ int preload_kernels() {
       (const void*)k_gfin<true, kBatchOps, kBatchWaits>,
       (const void*)k_gfin<false, kBatchOps, kBatchWaits>, (const void*)k_gcopy,
       (const void*)k_cores_wait, (const void*)k_cores_set,
+      (const void*)k_op1<true>, (const void*)k_op1<false>,
       (const void*)k_batch_tiny<true, 4, 8>, (const void*)k_batch_tiny<false, 4, 8>,
       (const void*)k_batch_tiny<true, 16, 32>, (const void*)k_batch_tiny<false, 16, 32>,
       (const void*)k_batch_tiny<true, 64, kBatchWaits>, (const void*)k_batch_tiny<false, 64, kBatchWaits>,
