@@ -624,7 +624,13 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
 
   const bool sys = w.cfg.force_sys ||
                    (dyn ? c->any_remote : rank_of(peer).device != rs.device);
-  CK(cudaSetDevice(rs.device));
+  // the rank's device is made current only before a CUDA call: a held
+  // (batched) operation makes none, and cudaSetDevice is ~1/4 of its host cost
+  bool dev_set = false;
+  auto ensure_dev = [&]() -> bool {
+    if (!dev_set) dev_set = cudaSetDevice(rs.device) == cudaSuccess;
+    return dev_set;
+  };
   cudaStream_t s = how.stream;
   Ticket t{};
   if (!blocking || is_recv) {
@@ -657,6 +663,7 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
       a.arena_slots = (uint32_t)w.cfg.stage_slots;
       a.arena_chunk = w.cfg.stage_chunk;
     } else {
+      if (!ensure_dev()) return MPIX_ERR_CUDA;
       int rc2 = acquire_staging(rs, bytes, s, &a.staging, &a.stage_done, &a.stage_gen);
       if (rc2) return rc2;
     }
@@ -773,7 +780,7 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
         b.d_arrive = rs.d_arrive + k;
       }
       if (flush_first) {
-        if (flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
+        if (!ensure_dev() || flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
         if (gr) relative();
       }
       if (b.ops.empty()) b.err_word = rs.d_err;
@@ -814,11 +821,12 @@ int p2p_post(mpix_comm_s* c, void* buf, int count, MPI_Datatype dt, int peer, in
     // default on): launched by the thread's next ordering call on that
     // stream (a blocking operation or a wait) or, failing one, by the flusher
     if (blocking || (how.conventional && !w.cfg.conv_batch) || !w.cfg.batch) {
-      if (flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
+      if (!ensure_dev() || flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
     } else if (!b.ops.empty()) {
       batch_note_held(b);  // the flusher launches it if no ordering call comes
     }
   } else {
+    if (!ensure_dev()) return MPIX_ERR_CUDA;
     if (!b.ops.empty() && flush_locked(b, s, nullptr, 0, false, nullptr) < 0) return MPIX_ERR_CUDA;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (!inl && g_copy_timing.on.load()) {
