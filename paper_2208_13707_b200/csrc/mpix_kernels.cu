@@ -136,6 +136,8 @@ __device__ __noinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_
 
 __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+constexpr uint64_t kPollMaxBytes = 65536;  // blocking receives up to this capacity poll (§3c)
+
 // Ring slot of a pair sequence. A 64-bit modulo is a software division
 // (a call of ~150 cycles, and the handshake needs several per operation);
 // the default ring sizes are powers of two, so it is a mask.
@@ -1048,7 +1050,13 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   // LL: a small send's payload travels in its descriptor; a blocking
   // receive polls instead of posting
   const bool ll_send = a.ll && !a.is_recv && a.bytes <= kLLBytes && a.mode != MODE_STAGED;
-  const bool poll_recv = a.ll && a.is_recv && a.blocking;
+  // (only receives of at most kPollMaxBytes: a larger one posts, as in round
+  // 1, so that a large blocking send finds it and pushes straight into the
+  // receive buffer instead of staging its payload first — an extra copy
+  // grid and three more launches: 1 MiB ping-pong 16.8 -> 23.3 us when every
+  // blocking receive polled; up to 64 KiB polling wins, the receiver's post
+  // fences cost more than the sender's staging copy)
+  const bool poll_recv = a.ll && a.is_recv && a.blocking && a.bytes <= kPollMaxBytes;
   __shared__ uint32_t s_pay[3];  // an LL send's payload (lane 0)
   TraceRec* const trace = TINY ? nullptr : a.trace;
   if (warp == 0) {

@@ -21,7 +21,7 @@ def setup(r):
 
 w.run_ranks(setup)
 out = {}
-for nb in (8, 4096, 65536):
+for nb in (8, 4096, 65536, 1 << 20):
     b0 = torch.zeros(max(nb, 16), dtype=torch.uint8, device=0)
     b1 = torch.zeros(max(nb, 16), dtype=torch.uint8, device=0)
     mpix.testing.pingpong(ctx[0][1], ctx[1][1], b0, b1, nb, 20, ctx[0][0], ctx[1][0])
