@@ -121,3 +121,26 @@ def test_kernels_are_sm100a_sass():
     """The library carries sm_100a SASS for the runtime kernels (no PTX JIT)."""
     out = subprocess.run(["cuobjdump", "--list-elf", mpix.LIB_PATH], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_integration_c_example_compiles_and_links(tmp_path):
+    """INTEGRATION.md's C example (Listing 2 against include/mpix.h)
+    compiles for sm_100a and links against libmpix.so: the documented
+    drop-in stays valid."""
+    import shutil
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(nvcc) and not shutil.which("nvcc"):
+        pytest.skip("nvcc not available")
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    m = re.search(r"## C example.*?```c\n(.*?)```", doc, flags=re.S)
+    assert m, "C example block missing"
+    src = tmp_path / "app.cu"
+    src.write_text("__global__ void saxpy(int n, float a, const float* x, float* y) {\n"
+                   "  int i = blockIdx.x * blockDim.x + threadIdx.x;\n"
+                   "  if (i < n) y[i] = a * x[i] + y[i];\n}\n" + m.group(1) +
+                   "\nint main() { int devs[2] = {0, 1}; return MPIX_World_init(2, devs) ? 1 : 0; }\n")
+    libdir = os.path.dirname(mpix.LIB_PATH)
+    r = subprocess.run([nvcc, "-gencode=arch=compute_100a,code=sm_100a", "-I" + os.path.join(ROOT, "include"),
+                        str(src), "-o", str(tmp_path / "app"), "-L" + libdir, "-l:libmpix.so"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
