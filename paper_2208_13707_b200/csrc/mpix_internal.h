@@ -42,6 +42,9 @@ enum : uint64_t { ST_FREE = 0, ST_POSTED = 1, ST_TAKEN = 2 };
 // flag-in-data words (sends of <= kLLBytes). Scans match
 // (state & ~ST_LL) == ST_POSTED.
 constexpr uint64_t ST_LL = 0x10;
+// With ST_LL: the payload is in the sender's eager slot as LL words (4
+// bytes + the post's flag each) — an eager send of 13 B .. E.
+constexpr uint64_t ST_LLE = 0x20;
 constexpr uint64_t kLLBytes = 12;
 // An LL word: 4 payload bytes | flag << 32, flag = 0x80000000 | (pseq &
 // 0x7fffffff). A reader that sees the flag of the post's own pseq in every
@@ -140,8 +143,9 @@ struct RegionLayout {
     return (gseq() + 8ull * (2ull * P + 1 + kGraphTagCounters) + 255) & ~255ull;
   }
   // eager payload ring of messages q -> me
+  // an eager slot holds E payload bytes, or E bytes as LL words (2E)
   __host__ __device__ uint64_t eager(int q) const {
-    return eager_base() + (uint64_t)q * R * E;
+    return eager_base() + (uint64_t)q * R * 2 * E;
   }
   __host__ __device__ uint64_t total() const { return eager(P); }
 };
@@ -164,7 +168,7 @@ struct alignas(64) OpRecord {
   uint64_t stat_addr, stat_bytes, stat_srctag; // status of the completed receive (kStatusOff)
 };
 
-enum : uint64_t { ACT_NONE = 0, ACT_COPY = 1, ACT_STAGE = 2 };
+enum : uint64_t { ACT_NONE = 0, ACT_COPY = 1, ACT_STAGE = 2, ACT_LLE = 3 };
 
 // Per-op trace record (MPIX_TRACE=1), written by the op's kernels.
 // t[]: clock64 stamps of k_proto phases: 0 start, 1 first scan done,

@@ -255,7 +255,7 @@ __device__ __forceinline__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Sn
   uint32_t hits = 0;  // bit k: slot k * 32 + lane is posted with my key
 #pragma unroll
   for (int k = 0; k < kMaxScanPerLane; ++k)
-    if (k * 32 + lane < R && (st[k] & ~ST_LL & 0xff) == ST_POSTED && ky[k] == key) hits |= 1u << k;
+    if (k * 32 + lane < R && (st[k] & ~(ST_LL | ST_LLE) & 0xff) == ST_POSTED && ky[k] == key) hits |= 1u << k;
 #pragma unroll 1
   for (int k = 0; k < kMaxScanPerLane && k * 32 < R; ++k) {
     unsigned m = __ballot_sync(0xffffffffu, (hits >> k) & 1u);
@@ -286,7 +286,7 @@ __device__ __forceinline__ int warp_scan(SlotDesc* ring, int R, uint64_t key, Sn
         // snapshot's user either proves by CAS on exactly sn.state (taking a
         // send descriptor) or owns (a receive descriptor only its one
         // matching sender reads).
-        ok = ((sn.state & ~ST_LL & 0xff) == ST_POSTED) && sn.key == key;
+        ok = ((sn.state & ~(ST_LL | ST_LLE) & 0xff) == ST_POSTED) && sn.key == key;
       }
       ok = __shfl_sync(0xffffffffu, ok, src);
       if (ok) {
@@ -356,6 +356,11 @@ struct Decision {
   uint8_t* stage_ptr;
   uint64_t* stage_done;
   uint64_t stage_gen;
+  // ACT_LLE: a taken LL-eager send (src = its eager slot of LL words, dst =
+  // my buffer, bytes = what I keep); completed by the CTA after the copy
+  uint64_t lle_len, lle_spseq, lle_key, lle_gate, lle_sgen;
+  uint64_t* lle_sdone;
+  int lle_j, lle_posted;
 };
 
 template <bool SYS>
@@ -701,7 +706,7 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
     __syncthreads();
     if (s_stage == 1) {  // eager: payload into my slot of the receiver's eager ring first
       const int slot = ring_slot(a.pseq, a.R);
-      cta_copy(a.eager_ring + (uint64_t)slot * a.E, a.buf, a.bytes);
+      cta_copy(a.eager_ring + (uint64_t)slot * 2 * a.E, a.buf, a.bytes);
       __syncthreads();  // published by the unlock's release (after the CTA barrier)
     }
     if (warp == 0 && s_stage != 0) {
@@ -717,7 +722,7 @@ __device__ void decide_dyn(const P2PArgs& a, Decision& dc) {
             dc.action = ACT_STAGE;  // ticket kept until the staged copy is published
           } else {
             const int slot = ring_slot(a.pseq, a.R);
-            const uint64_t addr = a.mode == MODE_EAGER ? (uint64_t)(a.eager_ring + (uint64_t)slot * a.E)
+            const uint64_t addr = a.mode == MODE_EAGER ? (uint64_t)(a.eager_ring + (uint64_t)slot * 2 * a.E)
                                                        : (uint64_t)a.buf;
             if (a.mode == MODE_EAGER) dyn_send_post<SYS>(a, D, addr, 0, 0, true);
             else dyn_send_post<SYS>(a, D, addr, (uint64_t)a.my_done, a.my_gen, false);
@@ -1013,6 +1018,142 @@ __device__ void ll_complete(const P2PArgs& a, int j, const Snap& sn, const LLMsg
   if (m.sdone) M::st_rlx(m.sdone, m.sgen);
 }
 
+// LL-eager: an eager send of 13 B .. E writes its payload
+// into its eager slot as LL words (4 bytes + the post's flag each; the slot
+// holds 2E bytes) and posts an LL-style descriptor — the whole CTA stores,
+// nothing orders them (every word carries the flag), thread 0 then does the
+// Dekker fence. The descriptor's addr holds the slot with a check like the
+// completion words (a stale addr must not send the reader elsewhere).
+template <bool SYS>
+__device__ void lle_post(const P2PArgs& a) {  // whole CTA
+  using M = Scope<SYS>;
+  const int slot = ring_slot(a.pseq, a.R);
+  uint64_t* w = reinterpret_cast<uint64_t*>(a.eager_ring + (uint64_t)slot * 2 * a.E);
+  const uint32_t f = ll_flag(a.pseq);
+  const uint64_t n = a.bytes, nw = (n + 3) / 4;
+  for (uint64_t i = threadIdx.x; i < nw; i += blockDim.x) {
+    uint32_t d = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint64_t k = 4 * i + b;
+      if (k < n) d |= (uint32_t)a.buf[k] << (8 * b);
+    }
+    M::st_rlx(&w[i], ll_word(d, f));
+  }
+  if (threadIdx.x == 0) {
+    SlotDesc* d = &a.post_ring[slot];
+    const uint64_t chk = ll_chk(a.pseq);
+    M::st_rlx(&d->addr, ((uint64_t)w & kLLPtrMask) | chk);
+    M::st_rlx(&d->pad[0], ll_word(0, f));
+    M::st_rlx(&d->pad[1], ll_word(0, f));
+    M::st_rlx(&d->bytes, ll_word((uint32_t)n, f));
+    M::st_rlx(&d->done_addr, ((uint64_t)a.my_done & kLLPtrMask) | chk);
+    M::st_rlx(&d->done_val, (a.my_done ? (a.my_gen & kLLPtrMask) : 0) | chk);
+    M::st_rlx(&d->key, a.key);
+    M::st_rlx(&d->state, st_word(a.pseq, ST_POSTED | ST_LL | ST_LLE));
+    M::fence_sc();
+  }
+}
+
+// Take an LL-eager descriptor (lane 0; taken already by CAS or exchange):
+// validate its words, record what the CTA copies and completes (ACT_LLE).
+// Returns false on watchdog expiry.
+template <bool SYS>
+__device__ bool lle_take(const P2PArgs& a, Decision& dc, int j, const Snap& sn, bool posted,
+                         uint64_t gate) {
+  using M = Scope<SYS>;
+  const SlotDesc* s = &a.scan_ring[j];
+  const uint64_t pseq = sn.state >> 8;
+  const uint32_t f = ll_flag(pseq);
+  const uint64_t chk = ll_chk(pseq);
+  const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
+  uint64_t ad = sn.addr, w1 = sn.p0, w2 = sn.p1, wl = sn.bytes, da = sn.done_addr, dv = sn.done_val;
+  while (!((ad & ~kLLPtrMask) == chk && (uint32_t)(w1 >> 32) == f && (uint32_t)(w2 >> 32) == f &&
+           (uint32_t)(wl >> 32) == f && (da & ~kLLPtrMask) == chk && (dv & ~kLLPtrMask) == chk)) {
+    __nanosleep(32);
+    if (a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
+      if (a.err_word) ScopeSys::st_rlx(a.err_word, ERRW_WAIT_SLOT);
+      return false;
+    }
+    ad = M::ld_rlx(&s->addr);
+    w1 = M::ld_rlx(&s->pad[0]);
+    w2 = M::ld_rlx(&s->pad[1]);
+    wl = M::ld_rlx(&s->bytes);
+    da = M::ld_rlx(&s->done_addr);
+    dv = M::ld_rlx(&s->done_val);
+  }
+  const uint64_t len = (uint32_t)wl;
+  dc.action = ACT_LLE;
+  dc.src = ad & kLLPtrMask;
+  dc.dst = (uint64_t)a.buf;
+  dc.bytes = umin(len, a.bytes);  // truncation: endpoint.cpp:17
+  dc.lle_len = len;
+  dc.lle_spseq = pseq;
+  dc.lle_key = sn.key;
+  dc.lle_gate = gate;
+  dc.lle_sdone = reinterpret_cast<uint64_t*>(da & kLLPtrMask);
+  dc.lle_sgen = dv & kLLPtrMask;
+  dc.lle_j = j;
+  dc.lle_posted = posted ? 1 : 0;
+  return true;
+}
+
+// The CTA copies the LL words of a taken LL-eager send into my buffer (each
+// word re-read until its flag is the post's), then thread 0 completes as
+// ll_complete does.
+template <bool SYS>
+__device__ void lle_finish(const P2PArgs& a, Decision& dc) {  // whole CTA
+  using M = Scope<SYS>;
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(dc.src);
+  const uint32_t f = ll_flag(dc.lle_spseq);
+  const uint64_t n = dc.bytes, nw = (n + 3) / 4;
+  uint8_t* out = reinterpret_cast<uint8_t*>(dc.dst);
+  const uint64_t t0 = a.spin_limit_ns ? globaltimer() : 0;
+  for (uint64_t i = threadIdx.x; i < nw; i += blockDim.x) {
+    uint64_t v = M::ld_rlx(&w[i]);
+    while ((uint32_t)(v >> 32) != f) {
+      __nanosleep(32);
+      if (a.spin_limit_ns && globaltimer() - t0 > a.spin_limit_ns) {
+        if (a.err_word) ScopeSys::st_rlx(a.err_word, ERRW_WAIT_SLOT);
+        break;
+      }
+      v = M::ld_rlx(&w[i]);
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint64_t k = 4 * i + b;
+      if (k < n) out[k] = (uint8_t)(v >> (8 * b));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (a.my_done) {
+      uint8_t* d = reinterpret_cast<uint8_t*>(a.my_done);
+      ScopeGpu::st_rlx(reinterpret_cast<uint64_t*>(d + kStatusOff),
+                       n | (dc.lle_len > a.bytes ? kTruncBit : 0));
+      ScopeGpu::st_rlx(reinterpret_cast<uint64_t*>(d + 2 * kStatusOff),
+                       ((uint64_t)(a.peer & 0xffffff) << 40) | (((uint64_t)(a.sidx + 2) & 0xff) << 32) |
+                           (uint32_t)(dc.lle_key >> 32));
+    }
+    const int slot = ring_slot(a.pseq, a.R);
+    if (dc.lle_posted) M::st_rlx(&a.post_ring[slot].state, st_word(a.pseq, ST_FREE));  // retract
+    ScopeGpu::st_rlx(&a.post_mirror[slot], a.pseq + 1);
+    if (a.my_done) {
+      if (a.blocking) ScopeGpu::st_rlx(a.my_done, a.my_gen);
+      else ScopeGpu::st_rel(a.my_done, a.my_gen);
+    }
+    // the payload loads have returned (their bytes are stored, barrier
+    // above) and the slot is TAKEN (gate: the exchange has been performed)
+    // before the sender may reuse it
+    if (dc.lle_gate != ~0ull) {
+      M::st_rlx(&a.scan_mirror[dc.lle_j], dc.lle_spseq + 1);
+      if (dc.lle_sdone) M::st_rlx(dc.lle_sdone, dc.lle_sgen);
+    }
+    dc.action = ACT_NONE;
+  }
+  __syncthreads();
+}
+
 // A blocking receive (static matching) never posts a descriptor: no sender
 // waits for one (eager and staged sends complete on their own, an Isend
 // leaves its descriptor), so it polls its scan ring until the send with its
@@ -1057,6 +1198,7 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   // blocking receive polled; up to 64 KiB polling wins, the receiver's post
   // fences cost more than the sender's staging copy)
   const bool poll_recv = a.ll && a.is_recv && a.blocking && a.bytes <= kPollMaxBytes;
+  const bool lle_send = a.ll && !a.is_recv && a.mode == MODE_EAGER && a.bytes > kLLBytes && a.bytes <= a.E;
   __shared__ uint32_t s_pay[3];  // an LL send's payload (lane 0)
   TraceRec* const trace = TINY ? nullptr : a.trace;
   if (warp == 0) {
@@ -1102,6 +1244,8 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
             ll_post<SYS>(a, pay);
             M::fence_sc();
             s_phase = 2;
+          } else if (lle_send) {
+            s_phase = 5;  // LL-eager post by the whole CTA, then the rescan
           } else if (a.mode == MODE_EAGER) {
             s_phase = 1;
           } else {  // MODE_ISEND: publish the user buffer
@@ -1116,6 +1260,9 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
           // no CAS
           if (!wait_post_slot<SYS>(a, pre)) {
             // watchdog: leave the send descriptor for nobody
+          } else if (sn.state & ST_LLE) {
+            const uint64_t old = M::exch(&a.scan_ring[j].state, st_word(sn.state >> 8, ST_TAKEN));
+            lle_take<SYS>(a, dc, j, sn, false, old);
           } else if (sn.state & ST_LL) {
             // TAKEN by an atomic exchange (no competitor: a plain store would
             // do, but it could land after the free-mirror below); its round
@@ -1150,13 +1297,17 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   __syncthreads();
   if (threadIdx.x == 0) trace_t(trace, 2);
   int phase = s_phase;
+  if (phase == 5) {
+    lle_post<SYS>(a);
+    phase = 2;
+  }
   if (phase == 1) {
     // Eager: payload into the receiver's eager slot (peer stores).
     const int slot = ring_slot(a.pseq, a.R);
-    cta_copy(a.eager_ring + (uint64_t)slot * a.E, a.buf, a.bytes);
+    cta_copy(a.eager_ring + (uint64_t)slot * 2 * a.E, a.buf, a.bytes);
     __syncthreads();
     if (threadIdx.x == 0)
-      post_desc<SYS>(a, (uint64_t)(a.eager_ring + (uint64_t)slot * a.E), a.bytes, 0, 0, true);
+      post_desc<SYS>(a, (uint64_t)(a.eager_ring + (uint64_t)slot * 2 * a.E), a.bytes, 0, 0, true);
     phase = 2;
   }
   if (phase == 2 && warp == 0) {
@@ -1168,13 +1319,16 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
      if (j >= 0) {
       if (!a.is_recv) {
         const int slot = ring_slot(a.pseq, a.R);
-        uint64_t want = st_word(a.pseq, ll_send ? (ST_POSTED | ST_LL) : ST_POSTED);
+        uint64_t want = st_word(a.pseq, ll_send ? (ST_POSTED | ST_LL)
+                                        : (lle_send ? (ST_POSTED | ST_LL | ST_LLE) : ST_POSTED));
         if (M::cas(&a.post_ring[slot].state, want, st_word(a.pseq, ST_TAKEN)) == want)
           send_win(a, dc, j, sn, true, ll_send ? reinterpret_cast<const uint8_t*>(s_pay) : a.buf);
       } else {
         const uint64_t want = sn.state;
         if (M::cas(&a.scan_ring[j].state, want, st_word(sn.state >> 8, ST_TAKEN)) == want) {
-          if (sn.state & ST_LL) {
+          if (sn.state & ST_LLE) {
+            lle_take<SYS>(a, dc, j, sn, true, 0);
+          } else if (sn.state & ST_LL) {
             LLMsg m;
             if (ll_read<SYS>(&a.scan_ring[j], sn, m, a)) ll_complete<SYS>(a, j, sn, m, true);
           } else {
@@ -1237,7 +1391,9 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
   static_assert(!TINY || INLINE, "tiny operations are inline");
   if (TINY) {  // static matching, inline, no staging, no graph counters, no trace
     decide<SYS, true>(a, s_dc);
-    if (s_dc.action == ACT_COPY) {
+    if (s_dc.action == ACT_LLE) {
+      lle_finish<SYS>(a, s_dc);
+    } else if (s_dc.action == ACT_COPY) {
       cta_copy(reinterpret_cast<uint8_t*>(s_dc.dst), reinterpret_cast<const uint8_t*>(s_dc.src),
                s_dc.bytes);
       __syncthreads();
@@ -1278,6 +1434,13 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
   if (a.trace && threadIdx.x == 0)
     a.trace->info = (uint64_t)a.is_recv | ((uint64_t)a.mode << 4) | ((uint64_t)INLINE << 8) |
                     (s_dc.action << 12);
+  if (!INLINE && s_dc.action == ACT_LLE) {
+    lle_finish<SYS>(a, s_dc);
+    if (threadIdx.x == 0) a.rec->action = ACT_NONE;  // nothing for the copy grid / k_fin
+    __syncthreads();
+    pdl_trigger();
+    return;
+  }
   if (!INLINE && s_dc.now) {
     cta_copy(reinterpret_cast<uint8_t*>(s_dc.dst), reinterpret_cast<const uint8_t*>(s_dc.src),
              s_dc.bytes);
@@ -1324,7 +1487,10 @@ __device__ __forceinline__ void proto_body(const P2PArgs& a, Decision& s_dc) {
     pdl_trigger();
     return;
   }
-  if (s_dc.action == ACT_COPY) {
+  if (s_dc.action == ACT_LLE) {
+    lle_finish<SYS>(a, s_dc);
+    if (threadIdx.x == 0 && a.trace) a.trace->g1 = globaltimer();
+  } else if (s_dc.action == ACT_COPY) {
     cta_copy(reinterpret_cast<uint8_t*>(s_dc.dst), reinterpret_cast<const uint8_t*>(s_dc.src),
              s_dc.bytes);
     __syncthreads();
