@@ -1,6 +1,6 @@
 # final evidence: suite + stress + bench + smoke (tools/gpurun/gpurun_r02w.sh), probes, ncu
 bash tools/gpurun/gpurun_r02w.sh
-O=gpurun_out/r02w7
+O=gpurun_out/r02w8
 export CUDA_MODULE_LOADING=EAGER
 timeout 120 python tools/pingpong_probe.py > $O/pp.txt 2>&1
 timeout 120 env MPIX_FORCE_SYS=1 python tools/pingpong_probe.py >> $O/pp.txt 2>&1

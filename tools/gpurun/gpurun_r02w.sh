@@ -1,5 +1,5 @@
 # relaxed polling + register snapshots: full suite, stress modes, bench
-O=gpurun_out/r02w7
+O=gpurun_out/r02w8
 mkdir -p $O
 export CUDA_MODULE_LOADING=EAGER
 timeout 1800 python -m pytest tests -m gpu -q --timeout 200 -p no:cacheprovider > $O/pytest.txt 2>&1; echo "rc=$?" >> $O/pytest.txt
