@@ -1198,7 +1198,10 @@ __device__ void decide(const P2PArgs& a, Decision& dc) {
   // blocking receive polled; up to 64 KiB polling wins, the receiver's post
   // fences cost more than the sender's staging copy)
   const bool poll_recv = a.ll && a.is_recv && a.blocking && a.bytes <= kPollMaxBytes;
-  const bool lle_send = a.ll && !a.is_recv && a.mode == MODE_EAGER && a.bytes > kLLBytes && a.bytes <= a.E;
+  // (an Isend too: its descriptor carries its completion word, signalled by
+  // the receiver that consumes it, as for any Isend)
+  const bool lle_send = a.ll && !a.is_recv && (a.mode == MODE_EAGER || a.mode == MODE_ISEND) &&
+                        a.bytes > kLLBytes && a.bytes <= a.E;
   __shared__ uint32_t s_pay[3];  // an LL send's payload (lane 0)
   TraceRec* const trace = TINY ? nullptr : a.trace;
   if (warp == 0) {

@@ -1,5 +1,5 @@
 # LL-eager: the full suite twice + stress modes
-O=gpurun_out/r02rr
+O=gpurun_out/r02rr2
 mkdir -p $O
 export CUDA_MODULE_LOADING=EAGER
 for i in 1 2; do
